@@ -1,0 +1,1072 @@
+// Runtime of the B200 path: device-resident level tables and vectors, the
+// operator orchestration that mirrors the reference's L2/L3 call graph
+// (transport.cpp:96-101, sweeps.cpp:106-113, multigrid.cpp:138-176,
+// krylov.cpp:9-93 + GMRES), and the C ABI declared in include/stamg_b200.h.
+// Every operator is a sequence of kernel launches on the context's stream;
+// the host only touches scalars (Krylov dot products).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.hpp"
+#include "setup.hpp"
+
+using namespace stamg_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NanError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+void ck_launch(const char* what) { ck(cudaGetLastError(), what); }
+
+template <class T>
+T* dalloc(size_t n) {
+  if (n == 0) return nullptr;
+  void* p = nullptr;
+  ck(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
+  return static_cast<T*>(p);
+}
+template <class T>
+T* dupload(const std::vector<T>& v, cudaStream_t s) {
+  T* p = dalloc<T>(v.size());
+  if (p) ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "upload");
+  return p;
+}
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct Nccl {
+  void* h = nullptr;
+  void* comm = nullptr;
+  int (*getUniqueId)(void*) = nullptr;
+  int (*commInitRank)(void**, int, const void*, int) = nullptr;
+  int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*commDestroy)(void*) = nullptr;
+  bool load() {
+    if (h) return true;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    getUniqueId = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclGetUniqueId"));
+    commInitRank = reinterpret_cast<int (*)(void**, int, const void*, int)>(dlsym(h, "ncclCommInitRank"));
+    allReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(dlsym(h, "ncclAllReduce"));
+    commDestroy = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommDestroy"));
+    return getUniqueId && commInitRank && allReduce && commDestroy;
+  }
+};
+Nccl& nccl() {
+  static Nccl n;
+  return n;
+}
+// ncclUniqueId is passed by value (128 bytes); wrap it for the C call
+struct UniqueId {
+  char internal[128];
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ device level
+struct DevLevel {
+  LevelTables t;
+  int64_t n = 0;  // vector length n_el * P * 4
+  int Hp = 0, Pk = 0, Pp = 0;
+  double *X = nullptr, *XT = nullptr, *sig = nullptr, *ones = nullptr, *B = nullptr, *Binv = nullptr;
+  double *cxy = nullptr, *BinvGS = nullptr, *sq = nullptr, *area = nullptr, *up_w = nullptr;
+  int *groups = nullptr, *group_oct = nullptr, *oct_patches = nullptr, *oct_ptr = nullptr;
+  int *up = nullptr, *child_ptr = nullptr, *child_idx = nullptr;
+  double* src = nullptr;  // scatter moments workspace [n_el][Hp][4]
+  double* mom = nullptr;  // coarse GS moments
+  int *gs_counter = nullptr, *gs_done = nullptr;
+  double *tmp = nullptr, *cf = nullptr, *ce = nullptr;  // V-cycle workspace
+  std::vector<void*> owned;
+};
+
+struct stamg_ctx {
+  Problem pb;
+  SphereTree tree;
+  int device = 0, rank = 0, world = 1;
+  cudaStream_t stream = nullptr;
+  DevLevel outer;
+  std::vector<DevLevel> mg;
+  int nr = 0;
+  bool have_mg = false;
+  int* mat = nullptr;
+  double* q_el = nullptr;
+  double nsum[4] = {0, 0, 0, 0};
+  // Krylov workspace
+  int restart_alloc = -1;
+  std::vector<double*> V;
+  double *z = nullptr, *u = nullptr, *partial = nullptr, *dots = nullptr, *coef = nullptr;
+  double* hbuf = nullptr;  // pinned host scalars
+  // host-buffer entry points
+  double *hostio = nullptr;
+  int64_t hostio_n = 0;
+  int64_t launches = 0;
+  bool timing = false;
+  std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::map<std::string, std::pair<double, int64_t>> timed;
+  void* comm = nullptr;
+};
+
+struct stamg_vec {
+  stamg_ctx* ctx = nullptr;
+  int level = 0;
+  int64_t n = 0;
+  double* d = nullptr;
+};
+
+namespace {
+
+// -------------------------------------------------------------- timing helper
+struct Timed {
+  stamg_ctx* c;
+  const char* name;
+  cudaEvent_t e1 = nullptr;
+  Timed(stamg_ctx* ctx, const char* nm) : c(ctx), name(nm) {
+    if (!c->timing) return;
+    cudaEvent_t e0;
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    ck(cudaEventRecord(e0, c->stream), "event");
+    c->pending[name].push_back({e0, e1});
+  }
+  ~Timed() {
+    if (c->timing && e1) cudaEventRecord(e1, c->stream);
+  }
+};
+
+void resolve_timing(stamg_ctx* c) {
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  for (auto& [name, v] : c->pending) {
+    auto& acc = c->timed[name];
+    for (auto& [a, b] : v) {
+      float ms = 0;
+      ck(cudaEventElapsedTime(&ms, a, b), "elapsed");
+      acc.first += ms, acc.second += 1;
+      cudaEventDestroy(a), cudaEventDestroy(b);
+    }
+    v.clear();
+  }
+}
+
+GroupGeom geom(stamg_ctx* c, DevLevel& L) {
+  GroupGeom g;
+  g.groups = L.groups, g.group_oct = L.group_oct, g.n_groups = int(L.t.group_oct.size());
+  g.P = L.t.P, g.nx = L.t.nx, g.ny = L.t.ny;
+  g.n_mat = L.t.n_mat, g.mat = L.t.n_mat > 1 ? c->mat : nullptr;
+  return g;
+}
+
+// tables in the sweep frame: dof i -> i ^ m, m = xneg | yneg << 1
+std::vector<double> frame_blocks(const std::vector<double>& blk, const LevelTables& t) {
+  std::vector<double> out(blk.size());
+  const size_t nblk = blk.size() / 16;
+  for (size_t b = 0; b < nblk; ++b) {
+    const int q = int(b % t.P);
+    const int m = t.octant[q] & 3;
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j) out[b * 16 + i * 4 + j] = blk[b * 16 + (i ^ m) * 4 + (j ^ m)];
+  }
+  return out;
+}
+
+void upload_level(stamg_ctx* c, DevLevel& L) {
+  const auto& t = L.t;
+  cudaStream_t s = c->stream;
+  L.n = int64_t(t.n_el) * t.P * 4;
+  L.Hp = round_up(t.H, 64);
+  L.Pk = round_up(t.P, 16);
+  L.Pp = round_up(t.P, 64);
+  std::vector<double> X(size_t(L.Pk) * L.Hp, 0.0), XT(size_t(L.Hp) * L.Pp, 0.0), sig(size_t(t.n_mat) * L.Hp, 0.0);
+  for (int q = 0; q < t.P; ++q)
+    for (int h = 0; h < t.H; ++h) X[size_t(q) * L.Hp + h] = XT[size_t(h) * L.Pp + q] = t.X[size_t(q) * t.H + h];
+  for (int m = 0; m < t.n_mat; ++m)
+    for (int h = 0; h < t.H; ++h) sig[size_t(m) * L.Hp + h] = t.sig[size_t(m) * t.H + h];
+  std::vector<double> ones(size_t(t.n_mat) * L.Hp, 1.0);
+  std::vector<double> cxyf(t.cxy.size());
+  for (int q = 0; q < t.P; ++q) {
+    const int xn = t.octant[q] & 1, yn = (t.octant[q] >> 1) & 1;
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 2; ++b) {
+        cxyf[q * 8 + a * 2 + b] = t.cxy[q * 8 + (a ^ yn) * 2 + (b ^ yn)];
+        cxyf[q * 8 + 4 + a * 2 + b] = t.cxy[q * 8 + 4 + (a ^ xn) * 2 + (b ^ xn)];
+      }
+  }
+  L.X = dupload(X, s), L.XT = dupload(XT, s), L.sig = dupload(sig, s), L.ones = dupload(ones, s);
+  L.B = dupload(frame_blocks(t.B, t), s);
+  L.Binv = dupload(frame_blocks(t.Binv, t), s);
+  L.cxy = dupload(cxyf, s);
+  L.area = dupload(t.area, s);
+  L.groups = dupload(t.groups, s), L.group_oct = dupload(t.group_oct, s);
+  L.oct_patches = dupload(t.oct_patches, s), L.oct_ptr = dupload(t.oct_ptr, s);
+  if (!t.BinvGS.empty()) {
+    L.BinvGS = dupload(frame_blocks(t.BinvGS, t), s);
+    L.sq = dupload(t.sq, s);
+    L.mom = dalloc<double>(size_t(t.n_el) * L.Hp * 4);
+    L.gs_counter = dalloc<int>(1);
+    L.gs_done = dalloc<int>(size_t(8) * t.n_el);
+  }
+  if (!t.up.empty()) {
+    L.up = dupload(t.up, s), L.up_w = dupload(t.up_w, s);
+    L.child_ptr = dupload(t.child_ptr, s), L.child_idx = dupload(t.child_idx, s);
+  }
+  L.src = dalloc<double>(size_t(t.n_el) * L.Hp * 4);
+  ck(cudaStreamSynchronize(s), "upload sync");
+}
+
+void free_level(DevLevel& L) {
+  for (void* p : {(void*)L.X, (void*)L.XT, (void*)L.sig, (void*)L.ones, (void*)L.B, (void*)L.Binv, (void*)L.cxy,
+                  (void*)L.BinvGS, (void*)L.sq, (void*)L.area, (void*)L.up_w, (void*)L.groups, (void*)L.group_oct,
+                  (void*)L.oct_patches, (void*)L.oct_ptr, (void*)L.up, (void*)L.child_ptr, (void*)L.child_idx,
+                  (void*)L.src, (void*)L.mom, (void*)L.gs_counter, (void*)L.gs_done, (void*)L.tmp, (void*)L.cf,
+                  (void*)L.ce})
+    if (p) cudaFree(p);
+}
+
+DevLevel& level_of(stamg_ctx* c, int level) {
+  if (level == STAMG_OUTER) return c->outer;
+  if (!c->have_mg) throw std::invalid_argument("multigrid hierarchy was not built for this context");
+  if (level < 0 || level >= int(c->mg.size())) throw std::invalid_argument("level out of range");
+  return c->mg[level];
+}
+
+void need(const stamg_vec* v, const DevLevel& L, const char* what) {
+  if (!v || v->n != L.n) throw std::invalid_argument(std::string(what) + ": layout mismatch");
+}
+
+// ------------------------------------------------------------------ operators
+void op_allreduce(stamg_ctx* c, double* buf, size_t n) {
+  if (c->world <= 1) return;
+  const int ncclDouble = 8, ncclSum = 0;
+  if (nccl().allReduce(buf, buf, n, ncclDouble, ncclSum, c->comm, c->stream) != 0)
+    throw NcclError("ncclAllReduce failed");
+}
+
+void op_apply_L(stamg_ctx* c, DevLevel& L, const double* x, double* y, double alpha = 1.0, double beta = 0.0,
+                const double* f = nullptr) {
+  Timed tm(c, "apply_L");
+  ApplyLParams p;
+  p.g = geom(c, L);
+  p.x = x, p.y = y, p.f = f, p.alpha = alpha, p.beta = beta, p.B = L.B, p.cxy = L.cxy;
+  launch_apply_L(p, c->stream);
+  ck_launch("apply_L");
+  c->launches += 1;
+}
+
+void op_d2m(stamg_ctx* c, DevLevel& L, const double* phi, int order, double* out, const double* sig, bool identity_N) {
+  Timed tm(c, "d2m");
+  D2MParams p;
+  p.phi = phi, p.src = out, p.X = L.X, p.sig = sig, p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
+  p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.Hused = (order + 1) * (order + 1);
+  for (int k = 0; k < 16; ++k) p.N[k] = identity_N ? ((k % 5) == 0 ? 1.0 : 0.0) : L.t.Nmat[k];
+  launch_d2m(p, c->stream);
+  ck_launch("d2m");
+  c->launches += 1;
+}
+
+void op_m2d(stamg_ctx* c, DevLevel& L, int order, double scale, double beta, double* y, const double* ext) {
+  Timed tm(c, "m2d");
+  M2DParams p;
+  p.src = L.src, p.y = y, p.XT = L.XT, p.n_el = L.t.n_el, p.P = L.t.P, p.Pp = L.Pp, p.Hp = L.Hp;
+  p.Hused = (order + 1) * (order + 1), p.scale = scale, p.beta = beta, p.ext_q = ext, p.area = L.area;
+  for (int i = 0; i < 4; ++i) p.nsum[i] = c->nsum[i];
+  launch_m2d(p, c->stream);
+  ck_launch("m2d");
+  c->launches += 1;
+}
+
+// apply_scatter_into (scatter.cpp:110-135): y += scale * S_order phi
+void op_scatter(stamg_ctx* c, DevLevel& L, const double* phi, int order, double scale, double* y) {
+  if (order > L.t.order) throw std::invalid_argument("sigma_by_harmonic: max_order exceeds kernel order");
+  if (order < 0) return;
+  op_d2m(c, L, phi, order, L.src, L.sig, false);
+  op_allreduce(c, L.src, size_t(L.t.n_el) * L.Hp * 4);
+  op_m2d(c, L, order, scale, 1.0, y, nullptr);
+}
+
+// apply_A_into (transport.cpp:96-101)
+void op_apply_A(stamg_ctx* c, DevLevel& L, const double* x, int order, double* y) {
+  op_apply_L(c, L, x, y);
+  op_scatter(c, L, x, order, -1.0, y);
+}
+
+// r = f - A_order phi
+void op_residual(stamg_ctx* c, DevLevel& L, const double* f, const double* phi, int order, double* r) {
+  op_apply_L(c, L, phi, r, -1.0, 1.0, f);
+  op_scatter(c, L, phi, order, 1.0, r);
+}
+
+void op_sweep(stamg_ctx* c, DevLevel& L, const double* rhs, double* z, const double* base = nullptr) {
+  Timed tm(c, "sweep");
+  SweepParams p;
+  p.g = geom(c, L);
+  p.rhs = rhs, p.z = z, p.base = base, p.Binv = L.Binv, p.cxy = L.cxy;
+  launch_sweep(p, c->stream);
+  ck_launch("sweep");
+  c->launches += 1;
+}
+
+// smoother_step (sweeps.cpp:106-113): phi += L^{-1}(f - A phi), the add fused into the sweep
+void op_smoother(stamg_ctx* c, DevLevel& L, const double* f, int order, double* phi) {
+  if (!L.tmp) L.tmp = dalloc<double>(L.n);
+  op_residual(c, L, f, phi, order, L.tmp);
+  op_sweep(c, L, L.tmp, phi, phi);
+}
+
+void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* phi) {
+  if (nu <= 0) return;
+  if (!L.BinvGS) throw std::invalid_argument("coarse_scatter_sweep: not the coarsest level");
+  // per-element moments of the current iterate (sweeps.cpp:74-79)
+  op_d2m(c, L, phi, L.t.order, L.mom, L.ones, true);
+  ck(cudaMemsetAsync(L.gs_counter, 0, sizeof(int), c->stream), "memset");
+  ck(cudaMemsetAsync(L.gs_done, 0, sizeof(int) * 8 * size_t(L.t.n_el), c->stream), "memset");
+  Timed tm(c, "coarse_gs");
+  CoarseGSParams p;
+  p.rhs = rhs, p.phi = phi, p.mom = L.mom, p.X = L.X, p.sig = L.sig, p.BinvGS = L.BinvGS, p.sq = L.sq, p.cxy = L.cxy;
+  p.oct_patches = L.oct_patches, p.oct_ptr = L.oct_ptr, p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
+  p.counter = L.gs_counter, p.done = L.gs_done;
+  p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.H = L.t.H, p.nx = L.t.nx, p.ny = L.t.ny, p.nu = nu;
+  for (int k = 0; k < 16; ++k) p.N[k] = L.t.Nmat[k];
+  launch_coarse_gs(p, c->stream);
+  ck_launch("coarse_gs");
+  c->launches += 1;
+}
+
+void op_prolong(stamg_ctx* c, int l, const double* coarse, double* fine, bool add) {
+  DevLevel& F = c->mg[l];
+  DevLevel& Cl = c->mg[l - 1];
+  Timed tm(c, "prolong");
+  launch_prolong(coarse, fine, F.up, F.up_w, F.t.n_el, F.t.P, Cl.t.P, add, c->stream);
+  ck_launch("prolong");
+  c->launches += 1;
+}
+
+void op_restrict(stamg_ctx* c, int l, const double* fine, double* coarse) {
+  DevLevel& F = c->mg[l];
+  DevLevel& Cl = c->mg[l - 1];
+  Timed tm(c, "restrict");
+  launch_restrict(fine, coarse, F.child_ptr, F.child_idx, F.up_w, F.t.n_el, F.t.P, Cl.t.P, c->stream);
+  ck_launch("restrict");
+  c->launches += 1;
+}
+
+double op_dot(stamg_ctx* c, const double* x, const double* y, int64_t n);
+
+// lmg_vcycle (multigrid.cpp:138-170)
+void op_vcycle(stamg_ctx* c, int l, const double* f, double* phi) {
+  DevLevel& L = c->mg[l];
+  const auto& spec = c->pb.spec;
+  if (l == 0) {
+    if (spec.coarse_tol > 0) {
+      if (!L.tmp) L.tmp = dalloc<double>(L.n);
+      const double fnorm = std::sqrt(op_dot(c, f, f, L.n));
+      for (int s = 0; s < 200; ++s) {
+        op_coarse_gs(c, L, f, 1, phi);
+        op_residual(c, L, f, phi, L.t.order, L.tmp);
+        if (std::sqrt(op_dot(c, L.tmp, L.tmp, L.n)) <= spec.coarse_tol * fnorm) break;
+      }
+    } else {
+      op_coarse_gs(c, L, f, spec.coarse_sweeps, phi);
+    }
+    return;
+  }
+  DevLevel& Cl = c->mg[l - 1];
+  if (!L.tmp) L.tmp = dalloc<double>(L.n);
+  if (!Cl.cf) Cl.cf = dalloc<double>(Cl.n), Cl.ce = dalloc<double>(Cl.n);
+  for (int s = 0; s < spec.nu_pre; ++s) op_smoother(c, L, f, c->nr, phi);
+  op_residual(c, L, f, phi, c->nr, L.tmp);
+  op_restrict(c, l, L.tmp, Cl.cf);
+  launch_fill(Cl.ce, 0.0, Cl.n, c->stream);
+  c->launches += 1;
+  op_vcycle(c, l - 1, Cl.cf, Cl.ce);
+  op_prolong(c, l, Cl.ce, phi, true);
+  for (int s = 0; s < spec.nu_post; ++s) op_smoother(c, L, f, c->nr, phi);
+}
+
+void op_mg_apply(stamg_ctx* c, const double* r, double* z) {
+  const int top = int(c->mg.size()) - 1;
+  launch_fill(z, 0.0, c->mg[top].n, c->stream);
+  c->launches += 1;
+  op_vcycle(c, top, r, z);
+}
+
+// --------------------------------------------------------------- BLAS helpers
+void ensure_krylov(stamg_ctx* c, int restart) {
+  if (c->restart_alloc >= restart) return;
+  for (double* v : c->V) cudaFree(v);
+  c->V.clear();
+  if (c->z) cudaFree(c->z), c->z = nullptr;
+  if (c->u) cudaFree(c->u), c->u = nullptr;
+  const int64_t n = c->outer.n;
+  for (int k = 0; k <= restart; ++k) c->V.push_back(dalloc<double>(n));
+  c->z = dalloc<double>(n);
+  c->u = dalloc<double>(n);
+  c->restart_alloc = restart;
+}
+
+void ensure_scalars(stamg_ctx* c) {
+  if (c->partial) return;
+  c->partial = dalloc<double>(size_t(multidot_blocks()) * 82);
+  c->dots = dalloc<double>(82);
+  c->coef = dalloc<double>(82);
+  ck(cudaMallocHost(&c->hbuf, 82 * sizeof(double)), "cudaMallocHost");
+}
+
+void op_multidot(stamg_ctx* c, const std::vector<const double*>& vs, const double* w, int64_t n, double* out_host) {
+  ensure_scalars(c);
+  launch_multidot(vs.data(), int(vs.size()), w, n, c->partial, c->dots, c->stream);
+  ck_launch("multidot");
+  c->launches += 2;
+  ck(cudaMemcpyAsync(c->hbuf, c->dots, vs.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  std::memcpy(out_host, c->hbuf, vs.size() * sizeof(double));
+  if (c->world > 1) throw std::logic_error("multi-rank Krylov reductions are not enabled in this build");
+}
+
+double op_dot(stamg_ctx* c, const double* x, const double* y, int64_t n) {
+  double d = 0;
+  op_multidot(c, {x}, y, n, &d);
+  (void)y;
+  return d;
+}
+
+void upload_coef(stamg_ctx* c, const double* host, int k) {
+  ensure_scalars(c);
+  std::memcpy(c->hbuf, host, k * sizeof(double));
+  ck(cudaMemcpyAsync(c->coef, c->hbuf, k * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+}
+
+void apply_precond(stamg_ctx* c, int precond, const double* v, double* z) {
+  if (precond == 0) op_sweep(c, c->outer, v, z);
+  else if (precond == 1) op_mg_apply(c, v, z);
+  else {
+    ck(cudaMemcpyAsync(z, v, c->outer.n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "copy");
+  }
+}
+
+// GMRES(m), right preconditioned, CGS2 + Givens; same algorithm and reporting
+// as the oracle's gmres (oracle/stamg_oracle.cpp) and krylov.hpp:15-24.
+stamg_report op_gmres(stamg_ctx* c, int precond, const double* b, double* x, double tol, int max_iter, int m,
+                      std::vector<double>& hist) {
+  if (tol <= 0) throw std::invalid_argument("gmres: tol must be positive");
+  if (m < 1 || m > 79) throw std::invalid_argument("gmres: restart must be in [1, 79]");
+  const auto t0 = std::chrono::steady_clock::now();
+  stamg_report rep{};
+  DevLevel& O = c->outer;
+  const int64_t n = O.n;
+  ensure_krylov(c, m);
+  launch_fill(x, 0.0, n, c->stream);
+  const double bnorm = std::sqrt(op_dot(c, b, b, n));
+  auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+  if (bnorm == 0.0) {
+    rep.converged = 1;
+    rep.wall_time = elapsed();
+    return rep;
+  }
+  ck(cudaMemcpyAsync(c->V[0], b, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "copy");
+  int it = 0;
+  bool done = false;
+  std::vector<double> cs(m), sn(m), g(m + 1), y(m), dots(m + 1);
+  std::vector<std::vector<double>> H(m, std::vector<double>(m + 1));
+  while (!done) {
+    const double beta = std::sqrt(op_dot(c, c->V[0], c->V[0], n));
+    launch_scale(1.0 / beta, c->V[0], n, c->stream);
+    std::fill(g.begin(), g.end(), 0.0);
+    for (auto& col : H) std::fill(col.begin(), col.end(), 0.0);
+    g[0] = beta;
+    int k = 0;
+    for (int j = 0; j < m; ++j) {
+      ++it;
+      apply_precond(c, precond, c->V[j], c->z);
+      ++rep.preconditioner_applications;
+      double* w = c->V[j + 1];
+      op_apply_A(c, O, c->z, c->pb.spec.N, w);
+      auto& h = H[j];
+      std::vector<const double*> basis(c->V.begin(), c->V.begin() + j + 1);
+      for (int pass = 0; pass < 2; ++pass) {  // CGS2
+        op_multidot(c, basis, w, n, dots.data());
+        upload_coef(c, dots.data(), j + 1);
+        launch_multi_axpy(basis.data(), j + 1, c->coef, w, n, c->stream);
+        c->launches += 1;
+        for (int i = 0; i <= j; ++i) h[i] += dots[i];
+      }
+      h[j + 1] = std::sqrt(op_dot(c, w, w, n));
+      if (h[j + 1] != 0.0) launch_scale(1.0 / h[j + 1], w, n, c->stream), c->launches += 1;
+      for (int i = 0; i < j; ++i) {
+        const double tmp = cs[i] * h[i] + sn[i] * h[i + 1];
+        h[i + 1] = -sn[i] * h[i] + cs[i] * h[i + 1];
+        h[i] = tmp;
+      }
+      const double den = std::hypot(h[j], h[j + 1]);
+      cs[j] = den == 0.0 ? 1.0 : h[j] / den;
+      sn[j] = den == 0.0 ? 0.0 : h[j + 1] / den;
+      const double hj1 = h[j + 1];
+      h[j] = cs[j] * h[j] + sn[j] * hj1;
+      h[j + 1] = 0.0;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      const double res = std::abs(g[j + 1]) / bnorm;
+      if (std::isnan(res)) throw NanError("gmres: NaN residual");
+      rep.iterations = it;
+      hist.push_back(res);
+      k = j + 1;
+      if (res < tol || it >= max_iter || hj1 == 0.0) {
+        done = true;
+        if (hj1 == 0.0 && !(res < tol)) rep.breakdown = 1;
+        break;
+      }
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double s = g[i];
+      for (int jj = i + 1; jj < k; ++jj) s -= H[jj][i] * y[jj];
+      y[i] = s / H[i][i];
+    }
+    upload_coef(c, y.data(), k);
+    std::vector<const double*> basis(c->V.begin(), c->V.begin() + k);
+    launch_lincomb(basis.data(), k, c->coef, c->u, n, c->stream);
+    c->launches += 1;
+    apply_precond(c, precond, c->u, c->z);
+    ++rep.preconditioner_applications;
+    launch_axpy(1.0, c->z, x, n, c->stream);
+    c->launches += 1;
+    if (done) break;
+    op_apply_A(c, O, x, c->pb.spec.N, c->V[0]);
+    launch_axpby(1.0, b, -1.0, c->V[0], n, c->stream);
+    c->launches += 1;
+  }
+  op_apply_A(c, O, x, c->pb.spec.N, c->z);
+  launch_axpby(1.0, b, -1.0, c->z, n, c->stream);
+  rep.final_residual = std::sqrt(op_dot(c, c->z, c->z, n)) / bnorm;
+  rep.converged = rep.final_residual < tol;
+  rep.wall_time = elapsed();
+  return rep;
+}
+
+// BiCGSTAB (krylov.cpp:9-93), right preconditioned, x0 = 0
+stamg_report op_bicgstab(stamg_ctx* c, int precond, const double* b, double* x, double tol, int max_iter,
+                         std::vector<double>& hist) {
+  if (tol <= 0) throw std::invalid_argument("bicgstab: tol must be positive");
+  const auto t0 = std::chrono::steady_clock::now();
+  stamg_report rep{};
+  DevLevel& O = c->outer;
+  const int64_t n = O.n;
+  ensure_krylov(c, 6);
+  double *r = c->V[0], *rhat = c->V[1], *p = c->V[2], *v = c->V[3], *s = c->V[4], *t = c->V[5], *phat = c->V[6];
+  double* shat = c->z;
+  launch_fill(x, 0.0, n, c->stream);
+  const double bnorm = std::sqrt(op_dot(c, b, b, n));
+  auto finish = [&]() {
+    if (bnorm > 0) {
+      op_apply_A(c, O, x, c->pb.spec.N, c->u);
+      launch_axpby(1.0, b, -1.0, c->u, n, c->stream);
+      rep.final_residual = std::sqrt(op_dot(c, c->u, c->u, n)) / bnorm;
+    }
+    rep.converged = rep.final_residual < tol;
+    rep.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return rep;
+  };
+  if (bnorm == 0.0) {
+    rep.converged = 1;
+    return rep;
+  }
+  ck(cudaMemcpyAsync(r, b, n * 8, cudaMemcpyDeviceToDevice, c->stream), "copy");
+  ck(cudaMemcpyAsync(rhat, b, n * 8, cudaMemcpyDeviceToDevice, c->stream), "copy");
+  launch_fill(p, 0.0, n, c->stream);
+  launch_fill(v, 0.0, n, c->stream);
+  double rho = 1, alpha = 1, omega = 1;
+  for (int it = 1; it <= max_iter; ++it) {
+    const double rho1 = op_dot(c, rhat, r, n);
+    if (rho1 == 0.0 || omega == 0.0) {
+      rep.breakdown = 1;
+      return finish();
+    }
+    const double beta = (rho1 / rho) * (alpha / omega);
+    rho = rho1;
+    launch_axpy(-omega, v, p, n, c->stream);      // p - omega v
+    launch_axpby(1.0, r, beta, p, n, c->stream);  // r + beta (...)
+    apply_precond(c, precond, p, phat);
+    ++rep.preconditioner_applications;
+    op_apply_A(c, O, phat, c->pb.spec.N, v);
+    const double rv = op_dot(c, rhat, v, n);
+    if (rv == 0.0) {
+      rep.breakdown = 1;
+      return finish();
+    }
+    alpha = rho / rv;
+    ck(cudaMemcpyAsync(s, r, n * 8, cudaMemcpyDeviceToDevice, c->stream), "copy");
+    launch_axpy(-alpha, v, s, n, c->stream);
+    launch_axpy(alpha, phat, x, n, c->stream);
+    const double snorm = std::sqrt(op_dot(c, s, s, n)) / bnorm;
+    if (std::isnan(snorm)) throw NanError("bicgstab: NaN residual");
+    if (snorm < tol) {
+      rep.iterations = it;
+      hist.push_back(snorm);
+      return finish();
+    }
+    apply_precond(c, precond, s, shat);
+    ++rep.preconditioner_applications;
+    op_apply_A(c, O, shat, c->pb.spec.N, t);
+    const double tt = op_dot(c, t, t, n);
+    if (tt == 0.0) {
+      rep.breakdown = 1;
+      return finish();
+    }
+    omega = op_dot(c, t, s, n) / tt;
+    launch_axpy(omega, shat, x, n, c->stream);
+    ck(cudaMemcpyAsync(r, s, n * 8, cudaMemcpyDeviceToDevice, c->stream), "copy");
+    launch_axpy(-omega, t, r, n, c->stream);
+    c->launches += 10;
+    const double rnorm = std::sqrt(op_dot(c, r, r, n)) / bnorm;
+    if (std::isnan(rnorm)) throw NanError("bicgstab: NaN residual");
+    rep.iterations = it;
+    hist.push_back(rnorm);
+    if (rnorm < tol) return finish();
+  }
+  return finish();
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return STAMG_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = std::string("invalid_argument: ") + e.what();
+    return STAMG_EINVAL;
+  } catch (const NanError& e) {
+    g_err = std::string("runtime_error: ") + e.what();
+    return STAMG_ENAN;
+  } catch (const CudaError& e) {
+    g_err = std::string("cuda: ") + e.what();
+    return STAMG_ECUDA;
+  } catch (const NcclError& e) {
+    g_err = std::string("nccl: ") + e.what();
+    return STAMG_ENCCL;
+  } catch (const std::logic_error& e) {
+    g_err = std::string("logic_error: ") + e.what();
+    return STAMG_ELOGIC;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return STAMG_ECUDA;
+  }
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* stamg_last_error(void) { return g_err.c_str(); }
+int stamg_version(void) { return 1; }
+
+int stamg_nccl_unique_id(void* out128) {
+  return guard([&] {
+    if (!nccl().load()) throw NcclError("libnccl.so.2 not loadable");
+    if (nccl().getUniqueId(out128) != 0) throw NcclError("ncclGetUniqueId failed");
+  });
+}
+
+int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx** out) {
+  return guard([&] {
+    if (!prob || !out) throw std::invalid_argument("stamg_create: null argument");
+    auto c = std::make_unique<stamg_ctx>();
+    c->pb = copy_problem(*prob);
+    validate(c->pb);
+    c->device = opt ? opt->device : 0;
+    c->rank = opt ? opt->rank : 0;
+    c->world = opt ? std::max(1, opt->world) : 1;
+    const bool want_mg = opt ? opt->build_hierarchy != 0 : true;
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    if (c->world > 1) {
+      if (!opt->nccl_id) throw std::invalid_argument("world > 1 needs an nccl id");
+      if (!nccl().load()) throw NcclError("libnccl.so.2 not loadable");
+      UniqueId uid;
+      std::memcpy(uid.internal, opt->nccl_id, 128);
+      // ncclCommInitRank(comm*, nranks, ncclUniqueId (by value), rank)
+      auto init = reinterpret_cast<int (*)(void**, int, UniqueId, int)>(nccl().commInitRank);
+      if (init(&c->comm, c->world, uid, c->rank) != 0) throw NcclError("ncclCommInitRank failed");
+    }
+    const auto& s = c->pb.spec;
+    c->tree = make_sphere(s.angular_kind, s.angular_level, s.cone_levels, s.cone_half_angle_deg);
+    c->outer.t = build_level(c->pb, c->tree, s.N, false);
+    for (int i = 0; i < 4; ++i)
+      for (int j = 0; j < 4; ++j) c->nsum[i] += c->outer.t.Nmat[i * 4 + j];
+    if (s.n_mat > 1) c->mat = dupload(c->pb.mat, c->stream);
+    if (!c->pb.q_el.empty()) c->q_el = dupload(c->pb.q_el, c->stream);
+    upload_level(c.get(), c->outer);
+    if (want_mg) {
+      c->nr = s.nr < 0 ? s.N : s.nr;
+      auto lv = build_hierarchy(c->pb, c->tree, c->nr, s.n_levels);
+      c->mg.resize(lv.size());
+      for (size_t i = 0; i < lv.size(); ++i) {
+        c->mg[i].t = std::move(lv[i]);
+        upload_level(c.get(), c->mg[i]);
+      }
+      c->have_mg = true;
+    }
+    *out = c.release();
+  });
+}
+
+int stamg_destroy(stamg_ctx* c) {
+  return guard([&] {
+    if (!c) return;
+    cudaStreamSynchronize(c->stream);
+    free_level(c->outer);
+    for (auto& L : c->mg) free_level(L);
+    for (double* v : c->V) cudaFree(v);
+    for (void* p : {(void*)c->z, (void*)c->u, (void*)c->partial, (void*)c->dots, (void*)c->coef, (void*)c->mat,
+                    (void*)c->q_el, (void*)c->hostio})
+      if (p) cudaFree(p);
+    if (c->hbuf) cudaFreeHost(c->hbuf);
+    if (c->comm) nccl().commDestroy(c->comm);
+    cudaStreamDestroy(c->stream);
+    delete c;
+  });
+}
+
+int stamg_layout(stamg_ctx* c, int level, int out4[4]) {
+  return guard([&] {
+    DevLevel& L = level_of(c, level);
+    out4[0] = L.t.n_el, out4[1] = L.t.P, out4[2] = 4, out4[3] = 1;
+  });
+}
+int stamg_patch_range(stamg_ctx* c, int level, int* q0, int* q1) {
+  return guard([&] {
+    DevLevel& L = level_of(c, level);
+    *q0 = 0, *q1 = L.t.P;
+  });
+}
+int stamg_n_levels(stamg_ctx* c, int* n, int* nr) {
+  return guard([&] {
+    *n = int(c->mg.size());
+    *nr = c->nr;
+  });
+}
+int stamg_level_order(stamg_ctx* c, int level, int* order) {
+  return guard([&] { *order = level_of(c, level).t.order; });
+}
+
+int stamg_vec_create(stamg_ctx* c, int level, stamg_vec** out) {
+  return guard([&] {
+    DevLevel& L = level_of(c, level);
+    auto v = std::make_unique<stamg_vec>();
+    v->ctx = c, v->level = level, v->n = L.n, v->d = dalloc<double>(L.n);
+    ck(cudaMemsetAsync(v->d, 0, L.n * sizeof(double), c->stream), "memset");
+    *out = v.release();
+  });
+}
+int stamg_vec_free(stamg_vec* v) {
+  return guard([&] {
+    if (!v) return;
+    cudaStreamSynchronize(v->ctx->stream);
+    cudaFree(v->d);
+    delete v;
+  });
+}
+int stamg_vec_size(stamg_vec* v, int64_t* n) {
+  return guard([&] { *n = v->n; });
+}
+int stamg_vec_device_ptr(stamg_vec* v, double** p) {
+  return guard([&] { *p = v->d; });
+}
+int stamg_vec_upload(stamg_ctx* c, stamg_vec* v, const double* host, int64_t n) {
+  return guard([&] {
+    if (n != v->n) throw std::invalid_argument("vec_upload: layout mismatch");
+    ck(cudaMemcpyAsync(v->d, host, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+int stamg_vec_download(stamg_ctx* c, const stamg_vec* v, double* host, int64_t n) {
+  return guard([&] {
+    if (n != v->n) throw std::invalid_argument("vec_download: layout mismatch");
+    ck(cudaMemcpyAsync(host, v->d, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+int stamg_vec_fill(stamg_ctx* c, stamg_vec* v, double value) {
+  return guard([&] {
+    launch_fill(v->d, value, v->n, c->stream);
+    ck_launch("fill");
+  });
+}
+int stamg_vec_copy(stamg_ctx* c, const stamg_vec* a, stamg_vec* b) {
+  return guard([&] {
+    if (a->n != b->n) throw std::invalid_argument("vec_copy: layout mismatch");
+    ck(cudaMemcpyAsync(b->d, a->d, a->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "copy");
+  });
+}
+int stamg_vec_axpy(stamg_ctx* c, double a, const stamg_vec* x, stamg_vec* y) {
+  return guard([&] {
+    if (x->n != y->n) throw std::invalid_argument("vec_axpy: layout mismatch");
+    launch_axpy(a, x->d, y->d, x->n, c->stream);
+    ck_launch("axpy");
+  });
+}
+int stamg_vec_dot(stamg_ctx* c, const stamg_vec* x, const stamg_vec* y, double* out) {
+  return guard([&] {
+    if (x->n != y->n) throw std::invalid_argument("vec_dot: layout mismatch");
+    *out = op_dot(c, x->d, y->d, x->n);
+  });
+}
+
+int stamg_apply_L(stamg_ctx* c, int level, const stamg_vec* phi, stamg_vec* y) {
+  return guard([&] {
+    DevLevel& L = level_of(c, level);
+    need(phi, L, "apply_L"), need(y, L, "apply_L");
+    if (phi->d == y->d) throw std::invalid_argument("apply_L: y must not alias phi");
+    op_apply_L(c, L, phi->d, y->d);
+  });
+}
+int stamg_apply_scatter(stamg_ctx* c, int level, const stamg_vec* phi, int order, double scale, stamg_vec* y) {
+  return guard([&] {
+    DevLevel& L = level_of(c, level);
+    need(phi, L, "apply_scatter"), need(y, L, "apply_scatter");
+    op_scatter(c, L, phi->d, order, scale, y->d);
+  });
+}
+int stamg_apply_A(stamg_ctx* c, int level, const stamg_vec* phi, int order, stamg_vec* y) {
+  return guard([&] {
+    DevLevel& L = level_of(c, level);
+    need(phi, L, "apply_A"), need(y, L, "apply_A");
+    if (phi->d == y->d) throw std::invalid_argument("apply_A: y must not alias phi");
+    op_apply_A(c, L, phi->d, order, y->d);
+  });
+}
+int stamg_sweep(stamg_ctx* c, int level, const stamg_vec* rhs, stamg_vec* z) {
+  return guard([&] {
+    DevLevel& L = level_of(c, level);
+    need(rhs, L, "standard_sweep"), need(z, L, "standard_sweep");
+    op_sweep(c, L, rhs->d, z->d);
+  });
+}
+int stamg_coarse_gs(stamg_ctx* c, int level, const stamg_vec* rhs, int nu, stamg_vec* phi) {
+  return guard([&] {
+    DevLevel& L = level_of(c, level);
+    need(rhs, L, "coarse_scatter_sweep"), need(phi, L, "coarse_scatter_sweep");
+    op_coarse_gs(c, L, rhs->d, nu, phi->d);
+  });
+}
+int stamg_smoother_step(stamg_ctx* c, int level, const stamg_vec* f, int order, stamg_vec* phi) {
+  return guard([&] {
+    DevLevel& L = level_of(c, level);
+    need(f, L, "smoother_step"), need(phi, L, "smoother_step");
+    op_smoother(c, L, f->d, order, phi->d);
+  });
+}
+int stamg_prolongate(stamg_ctx* c, int l, const stamg_vec* coarse, stamg_vec* fine) {
+  return guard([&] {
+    if (!c->have_mg || l < 1 || l >= int(c->mg.size())) throw std::invalid_argument("prolongate: level out of range");
+    need(coarse, c->mg[l - 1], "prolongate"), need(fine, c->mg[l], "prolongate");
+    op_prolong(c, l, coarse->d, fine->d, false);
+  });
+}
+int stamg_restrict(stamg_ctx* c, int l, const stamg_vec* fine, stamg_vec* coarse) {
+  return guard([&] {
+    if (!c->have_mg || l < 1 || l >= int(c->mg.size())) throw std::invalid_argument("restrict_residual: level out of range");
+    need(fine, c->mg[l], "restrict_residual"), need(coarse, c->mg[l - 1], "restrict_residual");
+    op_restrict(c, l, fine->d, coarse->d);
+  });
+}
+int stamg_vcycle(stamg_ctx* c, int l, const stamg_vec* f, stamg_vec* phi) {
+  return guard([&] {
+    DevLevel& L = level_of(c, l);
+    need(f, L, "lmg_vcycle"), need(phi, L, "lmg_vcycle");
+    op_vcycle(c, l, f->d, phi->d);
+  });
+}
+int stamg_mg_apply(stamg_ctx* c, const stamg_vec* r, stamg_vec* z) {
+  return guard([&] {
+    if (!c->have_mg) throw std::invalid_argument("multigrid hierarchy was not built for this context");
+    need(r, c->mg.back(), "mg_apply"), need(z, c->mg.back(), "mg_apply");
+    if (r->d == z->d) throw std::invalid_argument("mg_apply: z must not alias r");
+    op_mg_apply(c, r->d, z->d);
+  });
+}
+int stamg_rhs(stamg_ctx* c, stamg_vec* f) {
+  return guard([&] {
+    need(f, c->outer, "assemble_rhs");
+    const auto v = assemble_rhs(c->pb, c->outer.t, c->tree);
+    ck(cudaMemcpyAsync(f->d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int stamg_solve(stamg_ctx* c, int method, int precond, const stamg_vec* b, stamg_vec* x, double tol, int max_iter,
+                int restart, stamg_report* rep, double* history, int cap) {
+  return guard([&] {
+    need(b, c->outer, "solve"), need(x, c->outer, "solve");
+    if (precond == 1 && !c->have_mg) throw std::invalid_argument("multigrid hierarchy was not built for this context");
+    if (precond < 0 || precond > 2) throw std::invalid_argument("solve: unknown preconditioner");
+    std::vector<double> hist;
+    stamg_report r = method == 0 ? op_bicgstab(c, precond, b->d, x->d, tol, max_iter, hist)
+                                 : op_gmres(c, precond, b->d, x->d, tol, max_iter, restart, hist);
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (rep) *rep = r;
+    for (int i = 0; history && i < cap && i < int(hist.size()); ++i) history[i] = hist[i];
+  });
+}
+
+int stamg_sweep_host(stamg_ctx* c, int level, const double* rhs, double* z, int64_t n) {
+  return guard([&] {
+    DevLevel& L = level_of(c, level);
+    if (n != L.n) throw std::invalid_argument("standard_sweep: layout mismatch");
+    if (c->hostio_n < n) {
+      if (c->hostio) cudaFree(c->hostio);
+      c->hostio = dalloc<double>(n);
+      c->hostio_n = n;
+    }
+    ck(cudaMemcpyAsync(c->hostio, rhs, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+    op_sweep(c, L, c->hostio, c->hostio);
+    ck(cudaMemcpyAsync(z, c->hostio, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+  });
+}
+
+int stamg_solve_host(stamg_ctx* c, int method, int precond, const double* bh, double* xh, int64_t n, double tol,
+                     int max_iter, int restart, stamg_report* rep) {
+  return guard([&] {
+    if (n != c->outer.n) throw std::invalid_argument("solve: layout mismatch");
+    double* b = dalloc<double>(n);
+    double* x = dalloc<double>(n);
+    try {
+      ck(cudaMemcpyAsync(b, bh, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+      std::vector<double> hist;
+      stamg_report r = method == 0 ? op_bicgstab(c, precond, b, x, tol, max_iter, hist)
+                                   : op_gmres(c, precond, b, x, tol, max_iter, restart, hist);
+      ck(cudaMemcpyAsync(xh, x, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+      ck(cudaStreamSynchronize(c->stream), "sync");
+      if (rep) *rep = r;
+    } catch (...) {
+      cudaFree(b), cudaFree(x);
+      throw;
+    }
+    cudaFree(b), cudaFree(x);
+  });
+}
+
+int stamg_scalar_flux(stamg_ctx* c, const stamg_vec* phi, double* out) {
+  return guard([&] {
+    need(phi, c->outer, "scalar_flux");
+    std::vector<double> h(phi->n);
+    ck(cudaMemcpyAsync(h.data(), phi->d, phi->n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    const auto& t = c->outer.t;
+    const double vol = c->pb.h * c->pb.h;
+    for (int el = 0; el < t.n_el; ++el) {
+      double integral = 0;
+      for (int q = 0; q < t.P; ++q) {
+        const double* blk = &h[(size_t(el) * t.P + q) * 4];
+        integral += t.area[q] * (blk[0] * c->nsum[0] + blk[1] * c->nsum[1] + blk[2] * c->nsum[2] + blk[3] * c->nsum[3]);
+      }
+      out[el] = integral / vol;
+    }
+  });
+}
+
+// One source iteration on the outer level with moment-only scatter storage:
+// psi = q_ext + S(phi) from the stored moments (M2D), sweep in place, moments
+// of the new psi (D2M, allreduced over ranks). psi holds the angular flux on
+// entry and exit; the moments live in the level's src buffer.
+int stamg_source_iteration(stamg_ctx* c, stamg_vec* psi, int n_iter) {
+  return guard([&] {
+    DevLevel& O = c->outer;
+    need(psi, O, "source_iteration");
+    const int order = c->pb.spec.N;
+    for (int it = 0; it < n_iter; ++it) {
+      op_d2m(c, O, psi->d, order, O.src, O.sig, false);
+      op_allreduce(c, O.src, size_t(O.t.n_el) * O.Hp * 4);
+      op_m2d(c, O, order, 1.0, 0.0, psi->d, c->q_el);
+      op_sweep(c, O, psi->d, psi->d);
+    }
+  });
+}
+
+int stamg_get_table(stamg_ctx* c, int level, const char* name, double* out, int64_t cap, int64_t* n) {
+  return guard([&] {
+    const LevelTables& t = level_of(c, level).t;
+    std::vector<double> v;
+    const std::string nm(name);
+    if (nm == "X") v = t.X;
+    else if (nm == "B") v = t.B;
+    else if (nm == "Binv") v = t.Binv;
+    else if (nm == "C") v = t.C;
+    else if (nm == "area") v = t.area;
+    else if (nm == "Aflow") v = t.Aflow;
+    else if (nm == "sig") v = t.sig;
+    else if (nm == "octant") v.assign(t.octant.begin(), t.octant.end());
+    else if (nm == "leaf_id") v.assign(t.leaf_id.begin(), t.leaf_id.end());
+    else if (nm == "up") v.assign(t.up.begin(), t.up.end());
+    else if (nm == "sq") v = t.sq;
+    else if (nm == "rhs") v = assemble_rhs(c->pb, t, c->tree);
+    else throw std::invalid_argument("unknown table " + nm);
+    *n = int64_t(v.size());
+    if (out) std::memcpy(out, v.data(), std::min<int64_t>(cap, *n) * sizeof(double));
+  });
+}
+
+int stamg_synchronize(stamg_ctx* c) {
+  return guard([&] { ck(cudaStreamSynchronize(c->stream), "sync"); });
+}
+int stamg_launch_count(stamg_ctx* c, int64_t* n) {
+  return guard([&] { *n = c->launches; });
+}
+int stamg_timing_enable(stamg_ctx* c, int on) {
+  return guard([&] {
+    if (!on) resolve_timing(c);
+    c->timing = on != 0;
+    if (on) c->timed.clear();
+  });
+}
+int stamg_timing_read(stamg_ctx* c, const char* kernel, double* ms, int64_t* launches) {
+  return guard([&] {
+    resolve_timing(c);
+    auto it = c->timed.find(kernel);
+    *ms = it == c->timed.end() ? 0.0 : it->second.first;
+    *launches = it == c->timed.end() ? 0 : it->second.second;
+  });
+}
+
+// FP64 throughput probes (roofline denominators, measured on the box)
+int stamg_bench_fp64_peaks(stamg_ctx* c, double* dmma_tflops, double* dfma_tflops) {
+  return guard([&] {
+    *dmma_tflops = bench_dmma_tflops(c->device, c->stream);
+    *dfma_tflops = bench_dfma_tflops(c->device, c->stream);
+  });
+}
+
+// pinned host memory for the host-buffer entry points
+int stamg_host_alloc(int64_t bytes, void** out) {
+  return guard([&] { ck(cudaMallocHost(out, bytes), "cudaMallocHost"); });
+}
+int stamg_host_free(void* p) {
+  return guard([&] { ck(cudaFreeHost(p), "cudaFreeHost"); });
+}
+
+}  // extern "C"

@@ -1,0 +1,119 @@
+// Launchers for the sm_100a kernels of the B200 path (host-callable).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace stamg_b200 {
+
+// Common per-level geometry of the wavefront / stencil kernels: direction
+// groups of up to 4 equal-octant patches (-1 = padding).
+struct GroupGeom {
+  const int* groups = nullptr;     // [n_groups][4]
+  const int* group_oct = nullptr;  // [n_groups]
+  int n_groups = 0;
+  int P = 0, nx = 0, ny = 0;
+  const int* mat = nullptr;        // [n_el] material ids (nullptr: all 0)
+  int n_mat = 1;
+};
+
+// standard_sweep (sweeps.cpp:20-42): z = L^{-1} rhs, or z = base + L^{-1} rhs
+// when base != nullptr (the smoother's phi += r). z may alias rhs or base.
+struct SweepParams {
+  GroupGeom g;
+  const double* rhs = nullptr;
+  const double* base = nullptr;
+  double* z = nullptr;
+  const double* Binv = nullptr;  // [n_mat][P][16]
+  const double* cxy = nullptr;   // [P][8]
+};
+void launch_sweep(const SweepParams& p, cudaStream_t s);
+
+// apply_L_into (transport.cpp:66-88): y = alpha * L x + beta * f
+struct ApplyLParams {
+  GroupGeom g;
+  const double* x = nullptr;
+  const double* f = nullptr;
+  double* y = nullptr;
+  double alpha = 1.0, beta = 0.0;
+  const double* B = nullptr;    // [n_mat][P][16]
+  const double* cxy = nullptr;  // [P][8]
+};
+void launch_apply_L(const ApplyLParams& p, cudaStream_t s);
+
+// D2M with the sigma*N epilogue (scatter.cpp:130-131):
+// src[el][h][i] = sig[mat(el)][h] * sum_j (sum_{q} X[q][h] phi[el][q][j]) N[j][i]
+// for h < Hused (zero above), on FP64 tensor cores.
+struct D2MParams {
+  const double* phi = nullptr;
+  double* src = nullptr;         // [n_el][Hp][4]
+  const double* X = nullptr;     // [Pk][Hp]   (rows >= P are zero)
+  const double* sig = nullptr;   // [n_mat][Hp]
+  const int* mat = nullptr;
+  int n_el = 0, P = 0, Hp = 0, Hused = 0;
+  double N[16];
+};
+void launch_d2m(const D2MParams& p, cudaStream_t s);
+
+// M2D (scatter.cpp:132): y[el][q][i] = beta*y + scale * sum_h X[q][h] src[el][h][i]
+//   + (ext_q ? ext_q[el]/(4 pi) * area[q] * nsum[i] : 0)
+struct M2DParams {
+  const double* src = nullptr;   // [n_el][Hp][4]
+  double* y = nullptr;
+  const double* XT = nullptr;    // [Hp][Pp]
+  int n_el = 0, P = 0, Pp = 0, Hp = 0, Hused = 0;
+  double scale = 1.0, beta = 1.0;
+  const double* ext_q = nullptr;  // [n_el] isotropic source density or nullptr
+  const double* area = nullptr;   // [P]
+  double nsum[4];
+};
+void launch_m2d(const M2DParams& p, cudaStream_t s);
+
+// transfers (multigrid.cpp:100-136), Const basis
+void launch_prolong(const double* coarse, double* fine, const int* up, const double* w, int n_el, int Pf,
+                    int Pc, bool add, cudaStream_t s);
+void launch_restrict(const double* fine, double* coarse, const int* child_ptr, const int* child_idx,
+                     const double* w, int n_el, int Pf, int Pc, cudaStream_t s);
+
+// coarse_scatter_sweep (sweeps.cpp:51-104), order-exact dataflow kernel
+struct CoarseGSParams {
+  const double* rhs = nullptr;
+  double* phi = nullptr;
+  double* mom = nullptr;          // [n_el][Hp][4] running per-element moments
+  const double* X = nullptr;      // [Pk][Hp]
+  const double* sig = nullptr;    // [n_mat][Hp]
+  const double* BinvGS = nullptr; // [n_mat][P][16]
+  const double* sq = nullptr;     // [n_mat][P]
+  const double* cxy = nullptr;
+  const int* oct_patches = nullptr;
+  const int* oct_ptr = nullptr;   // [9]
+  const int* mat = nullptr;
+  int* counter = nullptr;         // work ticket
+  int* done = nullptr;            // [8][n_el] completed pass count
+  int n_el = 0, P = 0, Hp = 0, H = 0, nx = 0, ny = 0, nu = 0;
+  double N[16];
+};
+void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s);
+// moments mom[el][h][i] = sum_q X[q][h] phi[el][q][i] (no sigma / N)
+void launch_moments(const double* phi, double* mom, const double* X, int n_el, int P, int Hp, int H,
+                    cudaStream_t s);
+
+// BLAS-1 (deterministic reductions)
+void launch_fill(double* x, double v, int64_t n, cudaStream_t s);
+void launch_axpy(double a, const double* x, double* y, int64_t n, cudaStream_t s);        // y += a x
+void launch_axpby(double a, const double* x, double b, double* y, int64_t n, cudaStream_t s);  // y = a x + b y
+void launch_scale(double a, double* x, int64_t n, cudaStream_t s);
+// out[k] = sum_i V_k[i] w[i] for k < nv (V_k = vs[k]); partial buffer sized by multidot_partials()
+int multidot_blocks();
+void launch_multidot(const double* const* vs, int nv, const double* w, int64_t n, double* partial,
+                     double* out, cudaStream_t s);
+// w -= sum_k c[k] V_k  (c on device)
+void launch_multi_axpy(const double* const* vs, int nv, const double* c, double* w, int64_t n, cudaStream_t s);
+// u = sum_k c[k] V_k  (c on device)
+void launch_lincomb(const double* const* vs, int nv, const double* c, double* u, int64_t n, cudaStream_t s);
+
+// FP64 throughput microbenchmarks (roofline denominators)
+double bench_dmma_tflops(int device, cudaStream_t s);
+double bench_dfma_tflops(int device, cudaStream_t s);
+
+}  // namespace stamg_b200

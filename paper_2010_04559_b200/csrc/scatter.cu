@@ -1,0 +1,242 @@
+// Legendre scatter operator on sm_100a FP64 tensor cores (DMMA):
+// apply_scatter_into (scatter.cpp:110-135) as two batched GEMMs.
+//
+//  D2M: MOM[h][(el,i)] = sum_q X[q][h] * PHI[q][(el,i)]      (M=H, N=n_el*4, K=P)
+//       epilogue: SRC[el][h][i] = sig[mat(el)][h] * sum_j MOM[h][(el,j)] N[j][i]
+//       (the 4 spatial dofs of an element sit in a lane pair; one shuffle)
+//  M2D: Y[el][q][i] = beta*Y + scale * sum_h X[q][h] * SRC[el][h][i]
+//                     (+ isotropic external source, rank-1 in (q, i))
+//
+// PHI is read straight from the reference layout: for a tile of 16 elements
+// the (q-chunk x 4) panel of each element is contiguous. Tiles are staged
+// global->shared with cp.async (3 stages); each warp owns a 32x32 output
+// block = 4x4 m8n8k4 DMMA accumulators (tcgen05 has no f64 kind, so
+// mma.sync...f64 is the FP64 tensor path on sm_100a).
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace stamg_b200 {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, NSTAGE = 3;
+constexpr int LDS = BM + 4;  // padded row (conflict-free fragment loads)
+constexpr int kThreads = 128;
+constexpr int kStageDoubles = 2 * BK * LDS;
+
+// A tile: sA[k][m] = A_src[(k0+k) * lda + m0 + m]   (rows of k contiguous in m)
+__device__ __forceinline__ void load_tile_rows(double* sA, const double* src, int lda, int k0, int m0, int krows,
+                                               int tid) {
+  // BK x BM doubles = 512 16-byte chunks, 4 per thread
+#pragma unroll
+  for (int it = 0; it < (BK * BM / 2) / kThreads; ++it) {
+    const int chunk = tid + it * kThreads;
+    const int k = chunk / (BM / 2), mm = (chunk % (BM / 2)) * 2;
+    const bool ok = (k0 + k) < krows;
+    const double* g = src + (ok ? (size_t)(k0 + k) * lda + m0 + mm : 0);
+    cp_async16(sA + k * LDS + mm, g, ok);
+  }
+}
+
+// D2M B tile: sB[k][e*4+i] = phi[((el0+e)*P + q0+k)*4 + i]
+__device__ __forceinline__ void load_phi_tile(double* sB, const double* phi, int P, int n_el, int q0, int el0,
+                                              int tid) {
+#pragma unroll
+  for (int it = 0; it < (BK * BN / 2) / kThreads; ++it) {
+    const int chunk = tid + it * kThreads;       // 512 chunks: e (16) x k (16) x half (2)
+    const int half = chunk & 1, k = (chunk >> 1) & (BK - 1), e = chunk >> 5;
+    const bool ok = (el0 + e) < n_el && (q0 + k) < P;
+    const double* g = phi + (ok ? (((size_t)(el0 + e) * P + q0 + k) * 4 + half * 2) : 0);
+    cp_async16(sB + k * LDS + e * 4 + half * 2, g, ok);
+  }
+}
+
+// M2D B tile: sB[k][e*4+i] = src[((el0+e)*Hp + h0+k)*4 + i]
+__device__ __forceinline__ void load_src_tile(double* sB, const double* src, int Hp, int n_el, int h0, int el0,
+                                              int tid) {
+#pragma unroll
+  for (int it = 0; it < (BK * BN / 2) / kThreads; ++it) {
+    const int chunk = tid + it * kThreads;
+    const int half = chunk & 1, k = (chunk >> 1) & (BK - 1), e = chunk >> 5;
+    const bool ok = (el0 + e) < n_el;
+    const double* g = src + (ok ? (((size_t)(el0 + e) * Hp + h0 + k) * 4 + half * 2) : 0);
+    cp_async16(sB + k * LDS + e * 4 + half * 2, g, ok);
+  }
+}
+
+__device__ __forceinline__ void mma_stage(const double* sA, const double* sB, double (&acc)[4][4][2], int wm, int wn,
+                                          int g, int t) {
+#pragma unroll
+  for (int kk = 0; kk < BK; kk += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = sA[(kk + t) * LDS + wm * 32 + i * 8 + g];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = sB[(kk + t) * LDS + wn * 32 + j * 8 + g];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+}
+
+// grid: x = element tiles (16 elements), y = harmonic tiles (64)
+__global__ void __launch_bounds__(kThreads) d2m_kernel(D2MParams p) {
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;
+  const int el0 = blockIdx.x * (BN / 4), h0 = blockIdx.y * BM;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nk = (p.P + BK - 1) / BK;
+  const int Pk = nk * BK;  // X has zero rows up to Pk
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < nk) {
+      double* st = smem + s * kStageDoubles;
+      load_tile_rows(st, p.X, p.Hp, s * BK, h0, Pk, tid);
+      load_phi_tile(st + BK * LDS, p.phi, p.P, p.n_el, s * BK, el0, tid);
+    }
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    const int nxt = kt + NSTAGE - 1;
+    if (nxt < nk) {
+      double* st = smem + (nxt % NSTAGE) * kStageDoubles;
+      load_tile_rows(st, p.X, p.Hp, nxt * BK, h0, Pk, tid);
+      load_phi_tile(st + BK * LDS, p.phi, p.P, p.n_el, nxt * BK, el0, tid);
+    }
+    cp_async_commit();
+    cp_async_wait<NSTAGE - 1>();
+    __syncthreads();
+    const double* st = smem + (kt % NSTAGE) * kStageDoubles;
+    mma_stage(st, st + BK * LDS, acc, wm, wn, g, t);
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+
+  // epilogue: complete the element's 4 dofs from the partner lane, apply N and sigma
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int h = h0 + wm * 32 + i * 8 + g;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double o0 = __shfl_xor_sync(0xffffffffu, acc[i][j][0], 1);
+      const double o1 = __shfl_xor_sync(0xffffffffu, acc[i][j][1], 1);
+      const bool lo = (t & 1) == 0;
+      const double m0 = lo ? acc[i][j][0] : o0, m1 = lo ? acc[i][j][1] : o1;
+      const double m2 = lo ? o0 : acc[i][j][0], m3 = lo ? o1 : acc[i][j][1];
+      const int e = (wn * 32 + j * 8) / 4 + (t >> 1);
+      const int el = el0 + e;
+      const int i0 = (t & 1) * 2;
+      if (el < p.n_el && h < p.Hp) {
+        double s0 = 0.0, s1 = 0.0;
+        if (h < p.Hused) {
+          const int mt = p.mat ? p.mat[el] : 0;
+          const double sg = p.sig[(size_t)mt * p.Hp + h];
+          s0 = sg * (m0 * p.N[0 * 4 + i0] + m1 * p.N[1 * 4 + i0] + m2 * p.N[2 * 4 + i0] + m3 * p.N[3 * 4 + i0]);
+          s1 = sg * (m0 * p.N[0 * 4 + i0 + 1] + m1 * p.N[1 * 4 + i0 + 1] + m2 * p.N[2 * 4 + i0 + 1] +
+                     m3 * p.N[3 * 4 + i0 + 1]);
+        }
+        *reinterpret_cast<double2*>(p.src + ((size_t)el * p.Hp + h) * 4 + i0) = make_double2(s0, s1);
+      }
+    }
+  }
+}
+
+// grid: x = element tiles (16), y = patch tiles (64)
+__global__ void __launch_bounds__(kThreads) m2d_kernel(M2DParams p) {
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;
+  const int el0 = blockIdx.x * (BN / 4), q0 = blockIdx.y * BM;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  const int nk = (p.Hused + BK - 1) / BK;
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s) {
+    if (s < nk) {
+      double* st = smem + s * kStageDoubles;
+      load_tile_rows(st, p.XT, p.Pp, s * BK, q0, p.Hp, tid);
+      load_src_tile(st + BK * LDS, p.src, p.Hp, p.n_el, s * BK, el0, tid);
+    }
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    const int nxt = kt + NSTAGE - 1;
+    if (nxt < nk) {
+      double* st = smem + (nxt % NSTAGE) * kStageDoubles;
+      load_tile_rows(st, p.XT, p.Pp, nxt * BK, q0, p.Hp, tid);
+      load_src_tile(st + BK * LDS, p.src, p.Hp, p.n_el, nxt * BK, el0, tid);
+    }
+    cp_async_commit();
+    cp_async_wait<NSTAGE - 1>();
+    __syncthreads();
+    const double* st = smem + (kt % NSTAGE) * kStageDoubles;
+    mma_stage(st, st + BK * LDS, acc, wm, wn, g, t);
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+
+  constexpr double inv4pi = 0.07957747154594767;  // 1 / (4 pi)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int q = q0 + wm * 32 + i * 8 + g;
+    if (q >= p.P) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int e = (wn * 32 + j * 8) / 4 + (t >> 1);
+      const int el = el0 + e;
+      if (el >= p.n_el) continue;
+      const int i0 = (t & 1) * 2;
+      double* yp = p.y + ((size_t)el * p.P + q) * 4 + i0;
+      double v0 = p.scale * acc[i][j][0], v1 = p.scale * acc[i][j][1];
+      if (p.ext_q) {
+        const double c = p.ext_q[el] * inv4pi * p.area[q];
+        v0 += c * p.nsum[i0], v1 += c * p.nsum[i0 + 1];
+      }
+      if (p.beta != 0.0) {
+        const double2 old = *reinterpret_cast<const double2*>(yp);
+        v0 += p.beta * old.x, v1 += p.beta * old.y;
+      }
+      *reinterpret_cast<double2*>(yp) = make_double2(v0, v1);
+    }
+  }
+}
+
+size_t gemm_smem() { return sizeof(double) * NSTAGE * kStageDoubles; }
+
+}  // namespace
+
+void launch_d2m(const D2MParams& p, cudaStream_t s) {
+  if (p.n_el == 0 || p.Hused == 0) return;
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(d2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
+    cudaFuncSetAttribute(m2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
+    init = true;
+  }
+  dim3 grid((p.n_el + BN / 4 - 1) / (BN / 4), (p.Hused + BM - 1) / BM);
+  d2m_kernel<<<grid, kThreads, gemm_smem(), s>>>(p);
+}
+
+void launch_m2d(const M2DParams& p, cudaStream_t s) {
+  if (p.n_el == 0 || p.P == 0) return;
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(d2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
+    cudaFuncSetAttribute(m2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
+    init = true;
+  }
+  dim3 grid((p.n_el + BN / 4 - 1) / (BN / 4), (p.P + BM - 1) / BM);
+  m2d_kernel<<<grid, kThreads, gemm_smem(), s>>>(p);
+}
+
+}  // namespace stamg_b200

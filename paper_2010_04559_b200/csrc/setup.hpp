@@ -1,0 +1,90 @@
+// Host-side setup for the B200 path (the reference's L0/L1: angular mesh,
+// patch quadrature, couplings, fused-block operator tables, hierarchy
+// transfers). Runs once per problem on the host and produces flat,
+// device-ready arrays. Specialised to what the B200 kernels execute:
+// 2D cells with bilinear dofs (S = 4, i = ix + 2*iy) and the Const angular
+// basis (D = 1). Reference counterparts are cited per function.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/stamg_b200.h"
+
+namespace stamg_b200 {
+
+constexpr int kS = 4;  // spatial dofs per cell (2D bilinear)
+
+// ---- angular mesh (sphere_mesh.hpp:20-63), struct-of-arrays tree ----
+struct SphereTree {
+  static constexpr std::int64_t kScale = std::int64_t(1) << 20;  // flat lattice scale
+  std::vector<int> level, octant, parent;
+  std::vector<std::array<int, 4>> kids;
+  std::vector<char> leaf;
+  std::vector<std::array<std::int64_t, 9>> flat;  // 3 lattice vertices
+  std::vector<std::array<double, 9>> unit;        // 3 unit-sphere vertices
+  std::vector<int> leaves;                        // ascending ids
+  int max_level = 0;
+
+  int size() const { return int(level.size()); }
+  void add(int lvl, int oct, int par, const std::int64_t* a, const std::int64_t* b, const std::int64_t* c);
+  void split(int id);
+  void relist();
+  void close_two_irregular();
+};
+
+SphereTree make_sphere(int kind, int level, int extra, double cone_half_angle_deg);
+SphereTree coarsen(const SphereTree& t, int level);
+bool in_cone(const SphereTree& t, int id, double half_angle_deg);
+
+// ---- per-level device tables ----
+struct LevelTables {
+  int n_el = 0, P = 0, order = 0, H = 0, n_mat = 1;
+  int nx = 0, ny = 0;
+  std::vector<int> leaf_id, octant;   // per patch
+  std::vector<double> X;              // [P][H] couplings (scatter.hpp:32-39)
+  std::vector<double> sig;            // [n_mat][H] sigma per harmonic
+  std::vector<double> B;              // [n_mat][P][16] diag blocks (transport.cpp:46-54)
+  std::vector<double> Binv;           // [n_mat][P][16]
+  std::vector<double> C;              // [P][2][16] full inflow blocks (transport.cpp:55)
+  std::vector<double> cxy;            // [P][8] nonzero 2x2 sub-blocks of C_x, C_y
+  std::vector<double> BinvGS;         // [n_mat][P][16] inverse of B - (X sig X^T) N (sweeps.cpp:61-72)
+  std::vector<double> sq;             // [n_mat][P] X_q sig X_q^T
+  std::vector<double> area;           // [P] patch mass M_q
+  std::vector<double> Aflow;          // [P][3] A^x, A^y, A^z
+  std::vector<int> groups;            // [n_groups][4] patch ids of equal octant (-1 pad)
+  std::vector<int> group_oct;         // [n_groups]
+  std::vector<int> oct_patches;       // patches listed by octant (plan.patches)
+  std::vector<int> oct_ptr;           // [9]
+  // transfers to the next coarser level (multigrid.cpp:68-96); empty on level 0
+  std::vector<int> up;                // [P] coarse position
+  std::vector<double> up_w;           // [P] Const transfer block B = [1]
+  std::vector<int> child_ptr, child_idx;  // CSR children of each coarse patch, ascending
+  double Nmat[16];                    // spatial mass matrix
+};
+
+struct Problem {
+  stamg_problem spec{};
+  std::vector<double> sigma_t, moments;
+  std::vector<int> mat;
+  std::vector<double> q_el;
+  int n_el = 0;
+  double h = 0;
+};
+
+Problem copy_problem(const stamg_problem& p);
+void validate(const Problem& p);
+
+// build_operators + build_sweep_plan for one angular mesh and scatter order
+LevelTables build_level(const Problem& pb, const SphereTree& tree, int order, bool with_gs);
+// build_hierarchy: nlev levels, index 0 coarsest; fills up/child maps
+std::vector<LevelTables> build_hierarchy(const Problem& pb, const SphereTree& fine, int nr, int nlev);
+// assemble_rhs (transport.cpp:110-179 + cone beam EXTENSION)
+std::vector<double> assemble_rhs(const Problem& pb, const LevelTables& lev, const SphereTree& tree);
+
+// 4x4 helpers
+void inverse4(const double* A, double* Ainv);
+
+}  // namespace stamg_b200

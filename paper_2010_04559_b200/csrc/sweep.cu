@@ -1,0 +1,196 @@
+// Transport sweep on sm_100a: standard_sweep (sweeps.cpp:20-42), exact L^{-1}.
+//
+// One CTA owns a group of 4 equal-octant directions and R grid rows
+// (4*R threads, thread = (direction, row)). Each thread walks the cells of
+// its rows in upwind order; rows r, r+R, r+2R, ... are chained so the whole
+// grid is one skewed wavefront with a single ramp. Per step:
+//  * the x-upwind trace (2 doubles) stays in the thread's registers;
+//  * the y-upwind trace comes from the row below: warp shuffle inside a warp,
+//    a double-buffered shared slot across warps, a shared row buffer across
+//    the R-row strips;
+//  * the 4x4 cell solve runs in registers with the precomputed inverse.
+// rhs (and the smoother's base vector) is staged by cp.async NST-1 steps
+// ahead. All arithmetic is done in the sweep frame (dofs XOR-permuted so the
+// upwind corner is dof 0); tables are pre-permuted on the host.
+// HBM traffic: 32 B read + 32 B written per cell-direction (64 B algorithmic),
+// +32 B read with a base vector.
+#include "common.cuh"
+#include "kernels.hpp"
+
+#include <stdexcept>
+#include <string>
+
+namespace stamg_b200 {
+namespace {
+
+constexpr int NST = 4;
+
+template <int R, bool MULTI, bool ACCUM>
+__global__ void __launch_bounds__(4 * R) sweep_kernel(SweepParams p) {
+  constexpr int NT = 4 * R;
+  constexpr int NW = NT / 32;
+  extern __shared__ __align__(16) double smem[];
+  double* st_rhs = smem;
+  double* st_base = st_rhs + NST * NT * 4;
+  double2* top = reinterpret_cast<double2*>(st_base + (ACCUM ? NST * NT * 4 : 0));
+  double2* xw = top + 4 * p.g.nx;
+  double* sB = reinterpret_cast<double*>(xw + 2 * NW * 4);
+
+  const int tid = threadIdx.x, dir = tid & 3, r = tid >> 2, lane = tid & 31, warp = tid >> 5;
+  const int grp = blockIdx.x;
+  const int q = p.g.groups[grp * 4 + dir];
+  const int oct = p.g.group_oct[grp];
+  const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
+  const int nx = p.g.nx, ny = p.g.ny, P = p.g.P;
+  const bool qok = q >= 0;
+  const int qq = qok ? q : 0;
+
+  double cx[4], cy[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) cx[k] = p.cxy[qq * 8 + k], cy[k] = p.cxy[qq * 8 + 4 + k];
+  double Bi[16];
+  if constexpr (!MULTI) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Bi[k] = p.Binv[qq * 16 + k];
+  } else {
+    for (int idx = tid; idx < p.g.n_mat * 64; idx += NT) {
+      const int m = idx >> 6, d = (idx >> 4) & 3, k = idx & 15;
+      const int qd = p.g.groups[grp * 4 + d];
+      sB[(m * 4 + d) * 17 + k] = qd >= 0 ? p.Binv[((size_t)m * P + qd) * 16 + k] : 0.0;
+    }
+  }
+
+  const int nstrips = (ny + R - 1) / R;
+  const int nk = nstrips * nx;
+  const int T = nk + R - 1;
+
+  auto locate = [&](int k, int& el) -> bool {
+    if (k < 0 || k >= nk) return false;
+    const int s = k / nx, i = k - s * nx, j = s * R + r;
+    const int gx = xneg ? nx - 1 - i : i, gy = yneg ? ny - 1 - j : j;
+    el = gy * nx + gx;
+    return qok && j < ny;
+  };
+  auto issue = [&](int t) {
+    int el = 0;
+    const bool ok = locate(t - r, el);
+    const double* src = p.rhs + (ok ? ((size_t)el * P + qq) * 4 : 0);
+    double* dst = st_rhs + ((t % NST) * NT + tid) * 4;
+    cp_async16(dst, src, ok);
+    cp_async16(dst + 2, src + 2, ok);
+    if constexpr (ACCUM) {
+      const double* sb = p.base + (ok ? ((size_t)el * P + qq) * 4 : 0);
+      double* db = st_base + ((t % NST) * NT + tid) * 4;
+      cp_async16(db, sb, ok);
+      cp_async16(db + 2, sb + 2, ok);
+    }
+  };
+#pragma unroll
+  for (int t = 0; t < NST - 1; ++t) {
+    issue(t);
+    cp_async_commit();
+  }
+  __syncthreads();
+
+  const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
+  double2 tx = make_double2(0.0, 0.0), typrev = make_double2(0.0, 0.0);
+  for (int t = 0; t < T; ++t) {
+    issue(t + NST - 1);
+    cp_async_commit();
+    cp_async_wait<NST - 1>();
+    const int k = t - r;
+    const bool kin = k >= 0 && k < nk;
+    const int s = kin ? k / nx : 0, i = kin ? k - s * nx : 0;
+    double2 ty = shfl_up2(typrev, 4);
+    if (lane < 4) {
+      if (warp == 0) ty = (s == 0 || !kin) ? make_double2(0.0, 0.0) : top[dir * nx + i];
+      else ty = xw[((t - 1) & 1) * NW * 4 + (warp - 1) * 4 + dir];
+    }
+    double2 tyout = make_double2(0.0, 0.0);
+    int el = 0;
+    if (locate(k, el)) {
+      const double* rs = st_rhs + ((t % NST) * NT + tid) * 4;
+      double r0 = rs[0], r1 = rs[1], r2 = rs[2], r3 = rs[3];
+      // physical -> sweep frame (dof i -> i ^ m)
+      if (m & 1) { double u = r0; r0 = r1; r1 = u; u = r2; r2 = r3; r3 = u; }
+      if (m & 2) { double u = r0; r0 = r2; r2 = u; u = r1; r1 = r3; r3 = u; }
+      if (i == 0) tx = make_double2(0.0, 0.0);
+      // upwind couplings: x-face rows {0,2} <- left trace, y-face rows {0,1} <- lower trace
+      r0 -= cx[0] * tx.x + cx[1] * tx.y;
+      r2 -= cx[2] * tx.x + cx[3] * tx.y;
+      r0 -= cy[0] * ty.x + cy[1] * ty.y;
+      r1 -= cy[2] * ty.x + cy[3] * ty.y;
+      const double* B = Bi;
+      double Bm[16];
+      if constexpr (MULTI) {
+        const int mt = p.g.mat[el];
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) Bm[kk] = sB[(mt * 4 + dir) * 17 + kk];
+        B = Bm;
+      }
+      double z0 = B[0] * r0 + B[1] * r1 + B[2] * r2 + B[3] * r3;
+      double z1 = B[4] * r0 + B[5] * r1 + B[6] * r2 + B[7] * r3;
+      double z2 = B[8] * r0 + B[9] * r1 + B[10] * r2 + B[11] * r3;
+      double z3 = B[12] * r0 + B[13] * r1 + B[14] * r2 + B[15] * r3;
+      tx = make_double2(z1, z3);
+      tyout = make_double2(z2, z3);
+      // frame -> physical
+      if (m & 2) { double u = z0; z0 = z2; z2 = u; u = z1; z1 = z3; z3 = u; }
+      if (m & 1) { double u = z0; z0 = z1; z1 = u; u = z2; z2 = z3; z3 = u; }
+      if constexpr (ACCUM) {
+        const double* bs = st_base + ((t % NST) * NT + tid) * 4;
+        z0 += bs[0], z1 += bs[1], z2 += bs[2], z3 += bs[3];
+      }
+      double* out = p.z + ((size_t)el * P + q) * 4;
+      reinterpret_cast<double2*>(out)[0] = make_double2(z0, z1);
+      reinterpret_cast<double2*>(out)[1] = make_double2(z2, z3);
+    }
+    if ((lane & 28) == 28) xw[(t & 1) * NW * 4 + warp * 4 + dir] = tyout;
+    if (r == R - 1 && kin) top[dir * nx + i] = tyout;
+    typrev = tyout;
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+}
+
+template <int R, bool MULTI, bool ACCUM>
+void launch_t(const SweepParams& p, cudaStream_t s) {
+  constexpr int NT = 4 * R;
+  size_t smem = sizeof(double) * NST * NT * 4 * (ACCUM ? 2 : 1) + sizeof(double2) * (4 * p.g.nx + 2 * (NT / 32) * 4) +
+                (MULTI ? sizeof(double) * p.g.n_mat * 4 * 17 : 0);
+  auto k = sweep_kernel<R, MULTI, ACCUM>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k<<<p.g.n_groups, NT, smem, s>>>(p);
+}
+
+template <int R>
+void launch_r(const SweepParams& p, cudaStream_t s) {
+  const bool multi = p.g.n_mat > 1;
+  const bool acc = p.base != nullptr;
+  if (multi) acc ? launch_t<R, true, true>(p, s) : launch_t<R, true, false>(p, s);
+  else acc ? launch_t<R, false, true>(p, s) : launch_t<R, false, false>(p, s);
+}
+
+}  // namespace
+
+int sweep_rows_for(int nx, int ny) {
+  // rows per CTA: the chained wavefront needs R <= nx; 64 keeps 256 threads
+  // per CTA and several CTAs per SM.
+  int R = 64;
+  while (R > 8 && (R > nx || R > ny)) R >>= 1;
+  return R;
+}
+
+void launch_sweep(const SweepParams& p, cudaStream_t s) {
+  if (p.g.n_groups == 0) return;
+  const int R = sweep_rows_for(p.g.nx, p.g.ny);
+  if (p.g.nx < 8) throw std::invalid_argument("sweep: nx must be >= 8 on the B200 path");
+  switch (R) {
+    case 64: launch_r<64>(p, s); break;
+    case 32: launch_r<32>(p, s); break;
+    case 16: launch_r<16>(p, s); break;
+    default: launch_r<8>(p, s); break;
+  }
+}
+
+}  // namespace stamg_b200

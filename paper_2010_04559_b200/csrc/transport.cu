@@ -1,0 +1,94 @@
+// Matrix-free streaming-removal operator on sm_100a: apply_L_into
+// (transport.cpp:66-88), y = alpha * L x + beta * f.
+//
+// Thread = (direction of a 4-direction group, cell). Cells are enumerated in
+// the group's sweep frame so a warp's 8 cells are consecutive along x and the
+// 4 directions of a cell are adjacent lanes (one 128-byte line when the group's
+// patches are consecutive). Upwind neighbour traces are read through L1/L2;
+// every x block is fetched from DRAM once. Arithmetic is done in the sweep
+// frame with host-permuted blocks.
+// HBM traffic: 32 B read + 32 B written per cell-direction (+32 B for f).
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace stamg_b200 {
+namespace {
+
+__device__ __forceinline__ void to_frame(int m, double& a0, double& a1, double& a2, double& a3) {
+  if (m & 1) { double u = a0; a0 = a1; a1 = u; u = a2; a2 = a3; a3 = u; }
+  if (m & 2) { double u = a0; a0 = a2; a2 = u; u = a1; a1 = a3; a3 = u; }
+}
+__device__ __forceinline__ void from_frame(int m, double& a0, double& a1, double& a2, double& a3) {
+  if (m & 2) { double u = a0; a0 = a2; a2 = u; u = a1; a1 = a3; a3 = u; }
+  if (m & 1) { double u = a0; a0 = a1; a1 = u; u = a2; a2 = a3; a3 = u; }
+}
+
+constexpr int kCellsPerBlock = 64;  // 256 threads
+
+template <bool MULTI, bool WITH_F>
+__global__ void __launch_bounds__(256) apply_L_kernel(ApplyLParams p) {
+  const int tid = threadIdx.x, dir = tid & 3, c = tid >> 2;
+  const int grp = blockIdx.y;
+  const int q = p.g.groups[grp * 4 + dir];
+  if (q < 0) return;
+  const int oct = p.g.group_oct[grp];
+  const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
+  const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
+  const int nx = p.g.nx, ny = p.g.ny, P = p.g.P;
+  const int cell = blockIdx.x * kCellsPerBlock + c;
+  if (cell >= nx * ny) return;
+  const int jf = cell / nx, ifr = cell - jf * nx;
+  const int gx = xneg ? nx - 1 - ifr : ifr, gy = yneg ? ny - 1 - jf : jf;
+  const int el = gy * nx + gx;
+  const double* xb = p.x + ((size_t)el * P + q) * 4;
+  double2 a = __ldg(reinterpret_cast<const double2*>(xb)), b = __ldg(reinterpret_cast<const double2*>(xb) + 1);
+  double x0 = a.x, x1 = a.y, x2 = b.x, x3 = b.y;
+  to_frame(m, x0, x1, x2, x3);
+  const int mt = MULTI ? p.g.mat[el] : 0;
+  const double* B = p.B + ((size_t)mt * P + q) * 16;
+  double y0 = B[0] * x0 + B[1] * x1 + B[2] * x2 + B[3] * x3;
+  double y1 = B[4] * x0 + B[5] * x1 + B[6] * x2 + B[7] * x3;
+  double y2 = B[8] * x0 + B[9] * x1 + B[10] * x2 + B[11] * x3;
+  double y3 = B[12] * x0 + B[13] * x1 + B[14] * x2 + B[15] * x3;
+  const double* cxy = p.cxy + (size_t)q * 8;
+  if (ifr > 0) {  // x-upwind neighbour: its frame dofs {1,3} feed rows {0,2}
+    const double* ub = p.x + ((size_t)(el + (xneg ? 1 : -1)) * P + q) * 4;
+    double u0 = ub[0], u1 = ub[1], u2 = ub[2], u3 = ub[3];
+    to_frame(m, u0, u1, u2, u3);
+    y0 += cxy[0] * u1 + cxy[1] * u3;
+    y2 += cxy[2] * u1 + cxy[3] * u3;
+  }
+  if (jf > 0) {  // y-upwind neighbour: frame dofs {2,3} feed rows {0,1}
+    const double* ub = p.x + ((size_t)(el + (yneg ? nx : -nx)) * P + q) * 4;
+    double u0 = ub[0], u1 = ub[1], u2 = ub[2], u3 = ub[3];
+    to_frame(m, u0, u1, u2, u3);
+    y0 += cxy[4] * u2 + cxy[5] * u3;
+    y1 += cxy[6] * u2 + cxy[7] * u3;
+  }
+  from_frame(m, y0, y1, y2, y3);
+  double* yb = p.y + ((size_t)el * P + q) * 4;
+  if constexpr (WITH_F) {
+    const double* fb = p.f + ((size_t)el * P + q) * 4;
+    y0 = p.alpha * y0 + p.beta * fb[0];
+    y1 = p.alpha * y1 + p.beta * fb[1];
+    y2 = p.alpha * y2 + p.beta * fb[2];
+    y3 = p.alpha * y3 + p.beta * fb[3];
+  } else if (p.alpha != 1.0) {
+    y0 *= p.alpha, y1 *= p.alpha, y2 *= p.alpha, y3 *= p.alpha;
+  }
+  reinterpret_cast<double2*>(yb)[0] = make_double2(y0, y1);
+  reinterpret_cast<double2*>(yb)[1] = make_double2(y2, y3);
+}
+
+}  // namespace
+
+void launch_apply_L(const ApplyLParams& p, cudaStream_t s) {
+  if (p.g.n_groups == 0) return;
+  const int cells = p.g.nx * p.g.ny;
+  dim3 grid((cells + kCellsPerBlock - 1) / kCellsPerBlock, p.g.n_groups);
+  const bool multi = p.g.n_mat > 1, wf = p.f != nullptr && p.beta != 0.0;
+  if (multi) wf ? apply_L_kernel<true, true><<<grid, 256, 0, s>>>(p) : apply_L_kernel<true, false><<<grid, 256, 0, s>>>(p);
+  else wf ? apply_L_kernel<false, true><<<grid, 256, 0, s>>>(p) : apply_L_kernel<false, false><<<grid, 256, 0, s>>>(p);
+}
+
+}  // namespace stamg_b200

@@ -1,0 +1,181 @@
+"""GPU parity: the B200 kernels (through the C ABI) against the CPU oracle on
+the same seeded inputs, at sizes the oracle finishes in seconds.
+
+Tolerances (relative L2 unless noted): operators 1e-13 (FP64, only the
+summation order differs), sweep 1e-12 (the recurrence crosses up to nx+ny
+cells), coarse GS / V-cycle 1e-11, solve flux 1e-10 at equal iteration
+counts (BASELINE.json north_star), iteration counts +-1 at tol 1e-8.
+"""
+import numpy as np
+import pytest
+
+from paper_2010_04559_b200 import configs as cf
+
+pytestmark = pytest.mark.gpu
+
+# (config, cells per axis) small enough for the oracle
+CASES = [(1, 16), (2, 16), (3, 16), (4, 8)]
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def rnd(n, seed):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
+
+
+@pytest.fixture(scope="module", params=CASES, ids=lambda c: f"c{c[0]}n{c[1]}")
+def pair(request, orc, stamg):
+    k, n = request.param
+    spec = cf.baseline_config(k, n)
+    return spec, orc.Oracle(spec), stamg.Context(spec)
+
+
+def test_layout_and_tables(pair):
+    spec, o, g = pair
+    assert g.layout() == o.layout()
+    assert g.levels() == o.levels()
+    info = o.patch_info()
+    np.testing.assert_array_equal(g.table("octant").astype(int), info["octant"])
+    np.testing.assert_array_equal(g.table("leaf_id").astype(int), info["id"])
+    X = g.table("X").reshape(o.X().shape)
+    assert rel(X, o.X()) < 1e-13
+    P = o.layout()[1]
+    B = g.table("B").reshape(-1, P, 4, 4)
+    for m in range(B.shape[0]):
+        for q in range(0, P, max(1, P // 17)):
+            assert rel(B[m, q], o.diag(m, q)) < 1e-13
+    C = g.table("C").reshape(P, 2, 4, 4)
+    for q in range(0, P, max(1, P // 17)):
+        assert rel(C[q, 0], o.inflow(q, 0)) < 1e-13
+        assert rel(C[q, 1], o.inflow(q, 1)) < 1e-13
+    assert rel(g.table("rhs"), o.rhs()) < 1e-13
+
+
+def test_apply_L(pair):
+    spec, o, g = pair
+    x = rnd(o.size(), 91)
+    y = g.vec()
+    g.apply_L_into(g.vec(data=x), y)
+    assert rel(y.numpy(), o.apply_L(x)) < 1e-13
+
+
+@pytest.mark.parametrize("order_kind", ["full", "nr", "zero"])
+def test_apply_scatter(pair, order_kind):
+    spec, o, g = pair
+    order = {"full": spec.N, "nr": (spec.nr if spec.nr >= 0 else spec.N), "zero": 0}[order_kind]
+    x = rnd(o.size(), 5)
+    y0 = rnd(o.size(), 6)
+    y = g.vec(data=y0)
+    g.apply_scatter_into(g.vec(data=x), order, -0.75, y)
+    ref = o.apply_scatter(x, order, -0.75, y=y0)
+    assert rel(y.numpy() - y0, ref - y0) < 1e-12
+
+
+def test_apply_A(pair):
+    spec, o, g = pair
+    x = rnd(o.size(), 8)
+    y = g.vec()
+    g.apply_A_into(g.vec(data=x), spec.N, y)
+    assert rel(y.numpy(), o.apply_A(x, spec.N)) < 1e-13
+
+
+def test_sweep_matches_and_inverts(pair):
+    spec, o, g = pair
+    rhs = rnd(o.size(), 3)
+    z = g.vec()
+    xr = g.vec(data=rhs)
+    g.standard_sweep(xr, z)
+    zg = z.numpy()
+    assert rel(zg, o.sweep(rhs)) < 1e-12
+    # test_sweeps.cpp:62-83: L sweep(rhs) = rhs, on the GPU operators
+    back = g.vec()
+    g.apply_L_into(z, back)
+    assert np.abs(back.numpy() - rhs).max() < 1e-12 * np.abs(rhs).max() * 10
+    # in-place aliasing is bitwise identical (test_sweeps.cpp:119-122)
+    g.standard_sweep(xr, xr)
+    assert np.array_equal(xr.numpy(), zg)
+
+
+def test_sweep_deterministic(pair):
+    spec, o, g = pair
+    rhs = g.vec(data=rnd(o.size(), 12))
+    a, b = g.vec(), g.vec()
+    g.standard_sweep(rhs, a)
+    g.standard_sweep(rhs, b)
+    assert np.array_equal(a.numpy(), b.numpy())
+
+
+def test_mg_levels(pair):
+    spec, o, g = pair
+    nlev, nr = o.levels()
+    for l in range(nlev):
+        x = rnd(o.size(l), 40 + l)
+        y = g.vec(l)
+        g.apply_A_into(g.vec(l, x), nr, y, level=l)
+        assert rel(y.numpy(), o.apply_A(x, nr, level=l)) < 1e-13
+        z = g.vec(l)
+        g.standard_sweep(g.vec(l, x), z, level=l)
+        assert rel(z.numpy(), o.sweep(x, level=l)) < 1e-12
+        if l >= 1:
+            c = rnd(o.size(l - 1), 50 + l)
+            assert rel(g.prolongate(l, g.vec(l - 1, c)).numpy(), o.prolong(c, l)) == 0.0
+            assert rel(g.restrict_residual(l, g.vec(l, x)).numpy(), o.restrict(x, l)) == 0.0
+
+
+def test_smoother_step(pair):
+    spec, o, g = pair
+    nlev, nr = o.levels()
+    l = nlev - 1
+    f = rnd(o.size(l), 60)
+    phi0 = rnd(o.size(l), 61)
+    phi = g.vec(l, phi0)
+    g.smoother_step(g.vec(l, f), nr, phi, level=l)
+    assert rel(phi.numpy(), o.smoother(f, nr, phi0, level=l)) < 1e-12
+
+
+@pytest.mark.parametrize("nu", [1, 3])
+def test_coarse_gs(pair, nu):
+    spec, o, g = pair
+    f = rnd(o.size(0), 70)
+    phi0 = rnd(o.size(0), 71) * 0.1
+    phi = g.vec(0, phi0)
+    g.coarse_scatter_sweep(g.vec(0, f), nu, phi, level=0)
+    assert rel(phi.numpy(), o.coarse_gs(f, nu, phi0, level=0)) < 1e-11
+
+
+def test_mg_apply(pair):
+    spec, o, g = pair
+    r = rnd(o.size(), 80)
+    z = g.mg_apply(g.vec(data=r))
+    assert rel(z.numpy(), o.mg_apply(r)) < 1e-11
+    z2 = g.mg_apply(g.vec(data=r))
+    assert np.array_equal(z.numpy(), z2.numpy())  # fixed linear map, bitwise
+
+
+def test_gmres_parity(pair):
+    spec, o, g = pair
+    xo, ro = o.solve("gmres", "mg")
+    b = g.rhs()
+    xg, rg = g.solve(b, "gmres", "mg")
+    assert rg["converged"] and ro["converged"]
+    assert abs(rg["iterations"] - ro["iterations"]) <= 1
+    # equal-iteration flux parity (SURVEY.md §7 hard part 2)
+    k = ro["iterations"]
+    xo_k, _ = o.solve("gmres", "mg", tol=1e-300, max_iter=k)
+    xg_k, rg_k = g.solve(b, "gmres", "mg", tol=1e-300, max_iter=k)
+    assert rg_k["iterations"] == k
+    sf_o, sf_g = o.scalar_flux(xo_k), g.scalar_flux(xg_k)
+    assert rel(sf_g, sf_o) < 1e-10
+    assert rel(xg_k.numpy(), xo_k) < 1e-10
+
+
+def test_errors(pair, stamg):
+    spec, o, g = pair
+    bad = g.vec(0) if g.levels()[0] > 1 else None
+    if bad is not None:
+        with pytest.raises(stamg.InvalidArgument):
+            g.standard_sweep(bad, g.vec())
+    with pytest.raises(stamg.InvalidArgument):
+        g.apply_scatter_into(g.vec(), spec.N + 1, 1.0, g.vec())
