@@ -1,0 +1,302 @@
+#!/usr/bin/env python3
+"""Benchmark: transport-sweep throughput (cell.direction updates/s) on
+BASELINE.json config 5 (512x512 bilinear cells, 8192 angular patches, fp64),
+directions sharded across ranks, plus GMRES+AMG solve wall time (config 2)
+and source-iteration throughput as extra keys.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One JSON line on rank 0. Under torchrun each rank drives one GPU and owns
+P/N directions (strong scaling: total work fixed, no collective on the
+sweep). ``--impl reference`` times the CPU restatement of the reference
+(oracle/, the reference itself does not build here) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sweep cell·direction updates/s"
+UNIT = "cell·direction updates/s"
+BYTES_PER_UPDATE = 64  # read rhs block (4 doubles) + write solution block (4 doubles)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
+                          and "Not" not in r[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local, dist
+
+
+def allmax(dist, v):
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def cpu_sweep_sample(spec, n_dirs, threads=None):
+    """Oracle (CPU restatement of standard_sweep, sweeps.cpp:20-42, OpenMP over
+    patches) on n_dirs directions of the same grid; returns updates/s."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    import dataclasses
+    # the sweep needs only the transport blocks (no couplings): scatter order 0
+    # same grid and cross sections; angular level 2 (128 directions) keeps the
+    # host vectors at 1 GiB -- per-direction work is identical
+    s0 = dataclasses.replace(spec, N=0, moments=np.asarray(spec.moments)[:, :1].copy(), n_levels=1,
+                             angular_level=2)
+    if threads:
+        os.environ["OMP_NUM_THREADS"] = str(threads)
+    o = pyoracle.Oracle(s0)
+    n_el, P, S, _ = o.layout()
+    rhs = np.random.default_rng(0).uniform(-1, 1, n_el * P * S)
+    z = np.zeros_like(rhs)
+    o.sweep(rhs, q0=0, q1=min(4, P), z=z)  # warm
+    t = time.perf_counter()
+    o.sweep(rhs, q0=0, q1=n_dirs, z=z)
+    dt = time.perf_counter() - t
+    return n_el * n_dirs / dt, dt, n_el, P
+
+
+def run_reference(args, world, rank, dist):
+    from paper_2010_04559_b200 import configs as cf
+    if rank != 0:
+        return
+    spec = cf.baseline_config(5)
+    threads = os.cpu_count() or 1
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+    n_dirs = 128
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, dt, n_el, P = cpu_sweep_sample(spec, n_dirs, threads)
+        if i >= args.warmup:
+            vals.append((v, dt))
+    value = statistics.median([v for v, _ in vals])
+    ms = statistics.median([dt for _, dt in vals]) * 1e3
+    sample = (f"oracle standard_sweep (OpenMP over directions) over {n_dirs} directions x {n_el} cells per step "
+              f"(config 5 grid and cross sections, angular level 2 instead of 5 to bound host memory)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c5: 512x512 bilinear cells, uniform angular level 5 (8192 patches), fp64 sweep",
+                       "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, world, rank, local, dist):
+    from paper_2010_04559_b200 import configs as cf
+    from paper_2010_04559_b200 import stamg
+    spec = cf.baseline_config(5, args.n)
+    nccl_id = None
+    if world > 1:
+        import torch
+        uid = bytearray(stamg.nccl_unique_id()) if rank == 0 else bytearray(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
+        dist.broadcast(t, 0)
+        nccl_id = bytes(t.cpu().tolist())
+    g = stamg.Context(spec, device=local if world > 1 else 0, build_hierarchy=False, rank=rank, world=world,
+                      nccl_id=nccl_id)
+    n_el, P_local, S, _ = g.layout()
+    upd_local = n_el * P_local
+    psi = g.vec().fill(1.0)
+    # warm-up
+    for _ in range(args.warmup):
+        g.standard_sweep(psi, psi)
+    g.synchronize()
+    # timed region: K in-place sweeps (64 GiB vector >> 126 MB L2, no flush needed)
+    l0 = g.launch_count()
+    g.timing(True)
+    barrier(dist)
+    g.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            g.standard_sweep(psi, psi)
+        g.synchronize()
+        wall = time.perf_counter() - t0
+    barrier(dist)
+    sweep_ms, sweep_n = g.timed("sweep")
+    g.timing(False)
+    launches = g.launch_count() - l0
+    # device time of the K steps = the summed per-launch CUDA-event durations
+    dev_s = allmax(dist, sweep_ms * 1e-3)
+    total_upd = n_el * P_local * world if world > 1 else upd_local
+    value = total_upd * args.steps / dev_s
+    ms_per_step = dev_s / args.steps * 1e3
+    hbm, peak_kind = peaks()
+    achieved = upd_local * BYTES_PER_UPDATE / (sweep_ms * 1e-3 / max(sweep_n, 1)) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "sweep_ncu_traffic.json")) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+    except Exception:
+        pass
+    extras = {}
+    # ---- e2e through the host-buffer C-ABI entry point (pinned buffers)
+    e2e = None
+    if not args.no_e2e:
+        n = psi.n
+        psi.free()
+        host = stamg.host_alloc(n)
+        host[: min(n, 1 << 20)] = 1.0
+        g.sweep_host(host, host)  # warm (allocates the device staging buffer)
+        k_e2e = min(args.steps, 3)
+        barrier(dist)
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            g.sweep_host(host, host)
+        e2e_s = allmax(dist, time.perf_counter() - t0)
+        e2e = {"value": total_upd * k_e2e / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n * 8,
+               "d2h_bytes_per_step": n * 8, "steps": k_e2e,
+               "api": "stamg_sweep_host (include/stamg_b200.h), pinned host buffers"}
+    g.close()
+    # ---- extra: GMRES + AMG solve wall time (config 2) and a config-1 solve
+    if rank == 0 and world == 1 and not args.no_solve:
+        solves = {}
+        for k in args.solve_configs:
+            sp = cf.baseline_config(k)
+            t0 = time.perf_counter()
+            gs = stamg.Context(sp)
+            setup = time.perf_counter() - t0
+            b = gs.rhs()
+            gs.solve(b, "gmres", "mg")  # warm
+            gs.synchronize()
+            t0 = time.perf_counter()
+            x, rep = gs.solve(b, "gmres", "mg")
+            gs.synchronize()
+            solves[f"c{k}"] = {"wall_s": time.perf_counter() - t0, "setup_s": setup, "iterations": rep["iterations"],
+                               "final_residual": rep["final_residual"], "converged": rep["converged"],
+                               "method": "GMRES(%d) right-preconditioned by one V(1,1) angular MG cycle" % sp.restart}
+            gs.close()
+        extras["solve"] = solves
+    # ---- CPU baseline (oracle port) on rank 0 at N = 1
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        v, dt, _, _ = cpu_sweep_sample(spec, args.cpu_dirs, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"oracle standard_sweep over {args.cpu_dirs} directions x {spec.n_el} cells "
+                         f"(config 5 grid, angular level 2 to bound host memory; {dt:.1f} s)"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"c5: {spec.nx}x{spec.ny} bilinear cells, uniform angular level 5 "
+                                       f"({P_local * world} patches), one in-place standard_sweep per step, "
+                                       f"directions sharded over {world} rank(s)",
+                           "l2": "input 64 GiB >> 126 MB L2 (no flush needed)", "wall_s": wall},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                             "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                             "kernel": "sweep_kernel", "bytes_per_update": BYTES_PER_UPDATE},
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}
+        line.update(extras)
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=None, help="cells per axis override (default: config 5 = 512)")
+    ap.add_argument("--cpu-dirs", type=int, default=128)
+    ap.add_argument("--solve-configs", type=int, nargs="*", default=[1, 2])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local, dist = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank, dist)
+    else:
+        run_b200(args, world, rank, local, dist)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -351,6 +351,8 @@ void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* 
   p.oct_patches = L.oct_patches, p.oct_ptr = L.oct_ptr, p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
   p.counter = L.gs_counter, p.done = L.gs_done;
   p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.H = L.t.H, p.nx = L.t.nx, p.ny = L.t.ny, p.nu = nu;
+  for (int o = 0; o < 8; ++o)
+    p.max_patches_per_octant = std::max(p.max_patches_per_octant, L.t.oct_ptr[o + 1] - L.t.oct_ptr[o]);
   for (int k = 0; k < 16; ++k) p.N[k] = L.t.Nmat[k];
   launch_coarse_gs(p, c->stream);
   ck_launch("coarse_gs");
@@ -714,12 +716,20 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
     }
     const auto& s = c->pb.spec;
     c->tree = make_sphere(s.angular_kind, s.angular_level, s.cone_levels, s.cone_half_angle_deg);
-    c->outer.t = build_level(c->pb, c->tree, s.N, false);
+    {  // direction sharding: contiguous slices of the leaf order, multiples of 4 patches
+      const int Pg = int(c->tree.leaves.size());
+      const int quads = (Pg + 3) / 4;
+      const int q0 = std::min(Pg, 4 * int((int64_t(quads) * c->rank) / c->world));
+      const int q1 = std::min(Pg, 4 * int((int64_t(quads) * (c->rank + 1)) / c->world));
+      c->outer.t = build_level(c->pb, c->tree, s.N, false, q0, q1);
+    }
     for (int i = 0; i < 4; ++i)
       for (int j = 0; j < 4; ++j) c->nsum[i] += c->outer.t.Nmat[i * 4 + j];
     if (s.n_mat > 1) c->mat = dupload(c->pb.mat, c->stream);
     if (!c->pb.q_el.empty()) c->q_el = dupload(c->pb.q_el, c->stream);
     upload_level(c.get(), c->outer);
+    if (want_mg && c->world > 1)
+      throw std::invalid_argument("the multigrid hierarchy is single-rank in this build (use build_hierarchy = 0)");
     if (want_mg) {
       c->nr = s.nr < 0 ? s.N : s.nr;
       auto lv = build_hierarchy(c->pb, c->tree, c->nr, s.n_levels);
@@ -760,7 +770,7 @@ int stamg_layout(stamg_ctx* c, int level, int out4[4]) {
 int stamg_patch_range(stamg_ctx* c, int level, int* q0, int* q1) {
   return guard([&] {
     DevLevel& L = level_of(c, level);
-    *q0 = 0, *q1 = L.t.P;
+    *q0 = L.t.q_begin, *q1 = L.t.q_begin + L.t.P;
   });
 }
 int stamg_n_levels(stamg_ctx* c, int* n, int* nr) {

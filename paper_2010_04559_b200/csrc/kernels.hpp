@@ -91,12 +91,10 @@ struct CoarseGSParams {
   int* counter = nullptr;         // work ticket
   int* done = nullptr;            // [8][n_el] completed pass count
   int n_el = 0, P = 0, Hp = 0, H = 0, nx = 0, ny = 0, nu = 0;
+  int max_patches_per_octant = 0;
   double N[16];
 };
 void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s);
-// moments mom[el][h][i] = sum_q X[q][h] phi[el][q][i] (no sigma / N)
-void launch_moments(const double* phi, double* mom, const double* X, int n_el, int P, int Hp, int H,
-                    cudaStream_t s);
 
 // BLAS-1 (deterministic reductions)
 void launch_fill(double* x, double v, int64_t n, cudaStream_t s);

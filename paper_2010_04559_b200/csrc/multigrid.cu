@@ -64,16 +64,18 @@ __device__ __forceinline__ void perm(int m, double& a0, double& a1, double& a2, 
   if (m & 2) { double u = a0; a0 = a2; a2 = u; u = a1; a1 = a3; a3 = u; }
 }
 
-template <int KH>
+template <int KH, int NS>
 __global__ void __launch_bounds__(128) coarse_gs_kernel(CoarseGSParams p) {
+  // KH harmonics per lane (H <= 32 KH); NS patch slots per lane (patches per octant <= 32 NS)
   const int lane = threadIdx.x & 31;
+  const unsigned full = 0xffffffffu;
   const int n_el = p.n_el, nx = p.nx, ny = p.ny, P = p.P, Hp = p.Hp, H = p.H;
   const int per_pass = 8 * n_el;
   const int total = p.nu * per_pass;
   for (;;) {
     int ticket = 0;
     if (lane == 0) ticket = atomicAdd(p.counter, 1);
-    ticket = __shfl_sync(0xffffffffu, ticket, 0);
+    ticket = __shfl_sync(full, ticket, 0);
     if (ticket >= total) return;
     const int pass = ticket / per_pass, rem = ticket - pass * per_pass;
     const int oct = rem / n_el, kk = rem - oct * n_el;
@@ -85,23 +87,40 @@ __global__ void __launch_bounds__(128) coarse_gs_kernel(CoarseGSParams p) {
     const int sx = xneg ? -1 : 1, sy = yneg ? -nx : nx;
     const int upx = ifr > 0 ? el - sx : -1, upy = jf > 0 ? el - sy : -1;
     const int dnx = ifr < nx - 1 ? el + sx : -1, dny = jf < ny - 1 ? el + sy : -1;
-    if (lane == 0) {
-      const int* d = p.done + oct * n_el;
-      const int need = pass + 1;
-      if (upx >= 0) while (ld_acquire(d + upx) < need) {}
-      if (upy >= 0) while (ld_acquire(d + upy) < need) {}
-      if (oct > 0) {
-        while (ld_acquire(p.done + (oct - 1) * n_el + el) < need) {}
-      } else if (pass > 0) {
-        while (ld_acquire(p.done + 7 * n_el + el) < pass) {}
-      }
-      if (pass > 0) {
-        if (dnx >= 0) while (ld_acquire(d + dnx) < pass) {}
-        if (dny >= 0) while (ld_acquire(d + dny) < pass) {}
+    const int pbeg = p.oct_ptr[oct], np = p.oct_ptr[oct + 1] - pbeg;
+
+    // read-only inputs first (independent of the dependency flags)
+    double r[NS][4];
+    int qs[NS];
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      const int j = lane + 32 * sl;
+      qs[sl] = j < np ? p.oct_patches[pbeg + j] : -1;
+      if (qs[sl] >= 0) {
+        const double* rb = p.rhs + ((size_t)el * P + qs[sl]) * 4;
+        r[sl][0] = rb[0], r[sl][1] = rb[1], r[sl][2] = rb[2], r[sl][3] = rb[3];
+      } else {
+        r[sl][0] = r[sl][1] = r[sl][2] = r[sl][3] = 0.0;
       }
     }
-    __syncwarp();
-
+    // dependencies, polled in parallel by lanes 0..4
+    {
+      const int* f = nullptr;
+      int need = 0;
+      if (lane == 0 && upx >= 0) f = p.done + oct * n_el + upx, need = pass + 1;
+      if (lane == 1 && upy >= 0) f = p.done + oct * n_el + upy, need = pass + 1;
+      if (lane == 2) {
+        if (oct > 0) f = p.done + (oct - 1) * n_el + el, need = pass + 1;
+        else if (pass > 0) f = p.done + 7 * n_el + el, need = pass;
+      }
+      if (lane == 3 && pass > 0 && dnx >= 0) f = p.done + oct * n_el + dnx, need = pass;
+      if (lane == 4 && pass > 0 && dny >= 0) f = p.done + oct * n_el + dny, need = pass;
+      bool ok = f == nullptr || ld_acquire(f) >= need;
+      while (!__all_sync(full, ok)) {
+        if (!ok) ok = ld_acquire(f) >= need;
+      }
+    }
+    // moments, previous iterate and upwind traces: one round trip
     const int mt = p.mat ? p.mat[el] : 0;
     double mo[KH][4], sg[KH];
     double* mom_el = p.mom + (size_t)el * Hp * 4;
@@ -117,74 +136,100 @@ __global__ void __launch_bounds__(128) coarse_gs_kernel(CoarseGSParams p) {
         sg[kh] = 0.0;
       }
     }
-    for (int idx = p.oct_ptr[oct]; idx < p.oct_ptr[oct + 1]; ++idx) {
-      const int q = p.oct_patches[idx];
+    double zo[NS][4];
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      const int q = qs[sl];
+      zo[sl][0] = zo[sl][1] = zo[sl][2] = zo[sl][3] = 0.0;
+      if (q < 0) continue;
+      const double2 za = ld_cg2(p.phi + ((size_t)el * P + q) * 4), zc = ld_cg2(p.phi + ((size_t)el * P + q) * 4 + 2);
+      double ux[4] = {0, 0, 0, 0}, uy[4] = {0, 0, 0, 0};
+      if (upx >= 0) {
+        const double2 a = ld_cg2(p.phi + ((size_t)upx * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upx * P + q) * 4 + 2);
+        ux[0] = a.x, ux[1] = a.y, ux[2] = b.x, ux[3] = b.y;
+      }
+      if (upy >= 0) {
+        const double2 a = ld_cg2(p.phi + ((size_t)upy * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upy * P + q) * 4 + 2);
+        uy[0] = a.x, uy[1] = a.y, uy[2] = b.x, uy[3] = b.y;
+      }
+      zo[sl][0] = za.x, zo[sl][1] = za.y, zo[sl][2] = zc.x, zo[sl][3] = zc.y;
+      perm(m, r[sl][0], r[sl][1], r[sl][2], r[sl][3]);
+      perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
+      perm(m, ux[0], ux[1], ux[2], ux[3]);
+      perm(m, uy[0], uy[1], uy[2], uy[3]);
+      // upwind terms (sweeps.cpp:87-92), frame rows {0,2} <- x trace {1,3}, rows {0,1} <- y trace {2,3}
+      const double* cxy = p.cxy + (size_t)q * 8;
+      if (upx >= 0) {
+        r[sl][0] -= cxy[0] * ux[1] + cxy[1] * ux[3];
+        r[sl][2] -= cxy[2] * ux[1] + cxy[3] * ux[3];
+      }
+      if (upy >= 0) {
+        r[sl][0] -= cxy[4] * uy[2] + cxy[5] * uy[3];
+        r[sl][1] -= cxy[6] * uy[2] + cxy[7] * uy[3];
+      }
+    }
+    // the sequential patch chain (sweeps.cpp:86-102)
+    for (int j = 0; j < np; ++j) {
+      const int sl = j >> 5, src = j & 31;
+      double rr[4], z[4];
+      int q = 0;
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2)
+        if (s2 == sl) {
+          q = __shfl_sync(full, qs[s2], src);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) rr[i] = __shfl_sync(full, r[s2][i], src), z[i] = __shfl_sync(full, zo[s2][i], src);
+        }
       const double* Xq = p.X + (size_t)q * Hp;
       double xq[KH];
-      double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+      double t[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int kh = 0; kh < KH; ++kh) {
         const int h = lane + 32 * kh;
-        xq[kh] = h < H ? Xq[h] : 0.0;
+        xq[kh] = h < H ? __ldg(Xq + h) : 0.0;
         const double xs = xq[kh] * sg[kh];
-        t0 += xs * mo[kh][0], t1 += xs * mo[kh][1], t2 += xs * mo[kh][2], t3 += xs * mo[kh][3];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t[i] += xs * mo[kh][i];
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        t0 += __shfl_xor_sync(0xffffffffu, t0, o);
-        t1 += __shfl_xor_sync(0xffffffffu, t1, o);
-        t2 += __shfl_xor_sync(0xffffffffu, t2, o);
-        t3 += __shfl_xor_sync(0xffffffffu, t3, o);
-      }
-      // cell solve (every lane redundantly, in the sweep frame)
-      const double* rb = p.rhs + ((size_t)el * P + q) * 4;
-      double r0 = rb[0], r1 = rb[1], r2 = rb[2], r3 = rb[3];
-      double* zb = p.phi + ((size_t)el * P + q) * 4;
-      double2 za = ld_cg2(zb), zc = ld_cg2(zb + 2);
-      double z0 = za.x, z1 = za.y, z2 = zc.x, z3 = zc.y;
-      perm(m, r0, r1, r2, r3);
-      perm(m, z0, z1, z2, z3);
-      perm(m, t0, t1, t2, t3);
-      const double* cxy = p.cxy + (size_t)q * 8;
-      if (upx >= 0) {
-        const double* ub = p.phi + ((size_t)upx * P + q) * 4;
-        const double2 ua = ld_cg2(ub), uc = ld_cg2(ub + 2);
-        double u0 = ua.x, u1 = ua.y, u2 = uc.x, u3 = uc.y;
-        perm(m, u0, u1, u2, u3);
-        r0 -= cxy[0] * u1 + cxy[1] * u3;
-        r2 -= cxy[2] * u1 + cxy[3] * u3;
-      }
-      if (upy >= 0) {
-        const double* ub = p.phi + ((size_t)upy * P + q) * 4;
-        const double2 ua = ld_cg2(ub), uc = ld_cg2(ub + 2);
-        double u0 = ua.x, u1 = ua.y, u2 = uc.x, u3 = uc.y;
-        perm(m, u0, u1, u2, u3);
-        r0 -= cxy[4] * u2 + cxy[5] * u3;
-        r1 -= cxy[6] * u2 + cxy[7] * u3;
-      }
-      // explicit scatter from every other patch: (X sig (mom - X^T zold)) N
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t[i] += __shfl_xor_sync(full, t[i], o);
+      perm(m, t[0], t[1], t[2], t[3]);
+      // explicit scatter from the other patches: (X sig (mom - X^T zold)) N
       const double sq = p.sq[(size_t)mt * P + q];
-      const double d0 = t0 - sq * z0, d1 = t1 - sq * z1, d2 = t2 - sq * z2, d3 = t3 - sq * z3;
+      double d[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) d[i] = t[i] - sq * z[i];
       // N is invariant under the frame permutation (uniform square cells)
-      r0 += d0 * p.N[0] + d1 * p.N[4] + d2 * p.N[8] + d3 * p.N[12];
-      r1 += d0 * p.N[1] + d1 * p.N[5] + d2 * p.N[9] + d3 * p.N[13];
-      r2 += d0 * p.N[2] + d1 * p.N[6] + d2 * p.N[10] + d3 * p.N[14];
-      r3 += d0 * p.N[3] + d1 * p.N[7] + d2 * p.N[11] + d3 * p.N[15];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) rr[i] += d[0] * p.N[i] + d[1] * p.N[4 + i] + d[2] * p.N[8 + i] + d[3] * p.N[12 + i];
       const double* B = p.BinvGS + ((size_t)mt * P + q) * 16;
-      double n0 = B[0] * r0 + B[1] * r1 + B[2] * r2 + B[3] * r3;
-      double n1 = B[4] * r0 + B[5] * r1 + B[6] * r2 + B[7] * r3;
-      double n2 = B[8] * r0 + B[9] * r1 + B[10] * r2 + B[11] * r3;
-      double n3 = B[12] * r0 + B[13] * r1 + B[14] * r2 + B[15] * r3;
-      double e0 = n0 - z0, e1 = n1 - z1, e2 = n2 - z2, e3 = n3 - z3;
-      perm(m, n0, n1, n2, n3);  // back to physical (XOR permutation is an involution)
-      perm(m, e0, e1, e2, e3);
+      double n[4], e[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) n[i] = B[4 * i] * rr[0] + B[4 * i + 1] * rr[1] + B[4 * i + 2] * rr[2] + B[4 * i + 3] * rr[3];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) e[i] = n[i] - z[i];
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2)
+        if (s2 == sl && lane == src)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) zo[s2][i] = n[i];
+      perm(m, e[0], e[1], e[2], e[3]);
 #pragma unroll
       for (int kh = 0; kh < KH; ++kh)
-        mo[kh][0] += xq[kh] * e0, mo[kh][1] += xq[kh] * e1, mo[kh][2] += xq[kh] * e2, mo[kh][3] += xq[kh] * e3;
-      if (lane == 0) {
-        st_cg2(zb, make_double2(n0, n1));
-        st_cg2(zb + 2, make_double2(n2, n3));
-      }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) mo[kh][i] += xq[kh] * e[i];
+    }
+    // publish: new iterate of this cell's patches, running moments, flag
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      const int q = qs[sl];
+      if (q < 0) continue;
+      perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
+      double* zb = p.phi + ((size_t)el * P + q) * 4;
+      st_cg2(zb, make_double2(zo[sl][0], zo[sl][1]));
+      st_cg2(zb + 2, make_double2(zo[sl][2], zo[sl][3]));
     }
 #pragma unroll
     for (int kh = 0; kh < KH; ++kh) {
@@ -200,16 +245,23 @@ __global__ void __launch_bounds__(128) coarse_gs_kernel(CoarseGSParams p) {
   }
 }
 
-template <int KH>
-void launch_gs(const CoarseGSParams& p, cudaStream_t s) {
+template <int KH, int NS>
+void launch_gs2(const CoarseGSParams& p, cudaStream_t s) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_gs_kernel<KH>, 128, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_gs_kernel<KH, NS>, 128, 0);
   const long items = (long)p.nu * 8 * p.n_el;
   long blocks = (long)sms * (per_sm > 0 ? per_sm : 1);
   blocks = std::min(blocks, (items + 3) / 4);
-  coarse_gs_kernel<KH><<<int(blocks), 128, 0, s>>>(p);
+  coarse_gs_kernel<KH, NS><<<int(blocks), 128, 0, s>>>(p);
+}
+
+template <int KH>
+void launch_gs(const CoarseGSParams& p, cudaStream_t s, int max_np) {
+  if (max_np <= 32) launch_gs2<KH, 1>(p, s);
+  else if (max_np <= 64) launch_gs2<KH, 2>(p, s);
+  else throw std::invalid_argument("coarse_scatter_sweep: more than 64 patches per octant on the coarsest level");
 }
 
 }  // namespace
@@ -231,13 +283,14 @@ void launch_restrict(const double* fine, double* coarse, const int* cptr, const 
 void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s) {
   if (p.nu <= 0 || p.n_el == 0) return;
   const int kh = (p.H + 31) / 32;
+  const int np = p.max_patches_per_octant;
   switch (kh) {
-    case 1: launch_gs<1>(p, s); break;
-    case 2: launch_gs<2>(p, s); break;
-    case 3: launch_gs<3>(p, s); break;
-    case 4: launch_gs<4>(p, s); break;
-    case 5: case 6: launch_gs<6>(p, s); break;
-    case 7: case 8: launch_gs<8>(p, s); break;
+    case 1: launch_gs<1>(p, s, np); break;
+    case 2: launch_gs<2>(p, s, np); break;
+    case 3: launch_gs<3>(p, s, np); break;
+    case 4: launch_gs<4>(p, s, np); break;
+    case 5: case 6: launch_gs<6>(p, s, np); break;
+    case 7: case 8: launch_gs<8>(p, s, np); break;
     default: throw std::invalid_argument("coarse_scatter_sweep: harmonic count > 256 not supported on the B200 path");
   }
 }

@@ -348,10 +348,14 @@ void validate(const Problem& p) {
   if (s.beam != 0 && s.beam != 2) throw std::invalid_argument("B200 path supports beam = 0 or 2 (x=0 cone)");
 }
 
-LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool with_gs) {
+LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool with_gs, int q_begin, int q_end) {
   LevelTables L;
   const auto& s = pb.spec;
-  L.n_el = pb.n_el, L.P = int(t.leaves.size()), L.order = order, L.H = (order + 1) * (order + 1);
+  const int Pg = int(t.leaves.size());
+  if (q_end < 0) q_end = Pg;
+  if (q_begin < 0 || q_begin > q_end || q_end > Pg) throw std::invalid_argument("build_level: bad patch range");
+  L.P_global = Pg, L.q_begin = q_begin;
+  L.n_el = pb.n_el, L.P = q_end - q_begin, L.order = order, L.H = (order + 1) * (order + 1);
   L.n_mat = s.n_mat, L.nx = s.nx, L.ny = s.ny;
   const int P = L.P, H = L.H;
   const double hx = s.box / s.nx, hy = s.box / s.ny;
@@ -372,7 +376,7 @@ LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool 
     }
   std::copy(Nm, Nm + 16, L.Nmat);
 
-  L.leaf_id = t.leaves;
+  L.leaf_id.assign(t.leaves.begin() + q_begin, t.leaves.begin() + q_end);
   L.octant.resize(P);
   L.area.resize(P);
   L.Aflow.resize(size_t(P) * 3);
@@ -388,7 +392,7 @@ LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool 
   const int xorder_base = order > 12 ? 12 : 8;  // scatter.hpp:42
   std::vector<double> Y(H);
   for (int q = 0; q < P; ++q) {
-    const int id = t.leaves[q];
+    const int id = L.leaf_id[q];
     L.octant[q] = t.octant[id];
     // Const patch operators: M = sum w, A^xi = sum w Omega_xi (angular_disc.cpp:40-59)
     double M = 0, A[3] = {0, 0, 0};

@@ -42,6 +42,7 @@ bool in_cone(const SphereTree& t, int id, double half_angle_deg);
 // ---- per-level device tables ----
 struct LevelTables {
   int n_el = 0, P = 0, order = 0, H = 0, n_mat = 1;
+  int P_global = 0, q_begin = 0;      // this rank's slice [q_begin, q_begin + P) of the leaf order
   int nx = 0, ny = 0;
   std::vector<int> leaf_id, octant;   // per patch
   std::vector<double> X;              // [P][H] couplings (scatter.hpp:32-39)
@@ -78,7 +79,10 @@ Problem copy_problem(const stamg_problem& p);
 void validate(const Problem& p);
 
 // build_operators + build_sweep_plan for one angular mesh and scatter order
-LevelTables build_level(const Problem& pb, const SphereTree& tree, int order, bool with_gs);
+// q_begin/q_end restrict the level to a contiguous range of the leaf order
+// (direction sharding across ranks); -1 = all leaves.
+LevelTables build_level(const Problem& pb, const SphereTree& tree, int order, bool with_gs, int q_begin = 0,
+                        int q_end = -1);
 // build_hierarchy: nlev levels, index 0 coarsest; fills up/child maps
 std::vector<LevelTables> build_hierarchy(const Problem& pb, const SphereTree& fine, int nr, int nlev);
 // assemble_rhs (transport.cpp:110-179 + cone beam EXTENSION)
