@@ -16,6 +16,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 
 import numpy as np
 
@@ -106,17 +107,20 @@ class Vec:
     def __init__(self, ctx: "Context", level: int = OUTER):
         self.ctx = ctx
         self.level = level
+        self.h = None
         h = C.c_void_p()
         _check(lib().stamg_vec_create(ctx.h, level, C.byref(h)))
         self.h = h
+        ctx._vecs.add(self)
         n = C.c_int64()
         _check(lib().stamg_vec_size(self.h, C.byref(n)))
         self.n = n.value
 
     def free(self):
-        if getattr(self, "h", None):
+        # a vector must not outlive its context: Context.close() frees the live ones first
+        if getattr(self, "h", None) and getattr(self.ctx, "h", None):
             lib().stamg_vec_free(self.h)
-            self.h = None
+        self.h = None
 
     def __del__(self):
         try:
@@ -153,6 +157,8 @@ class Context:
     def __init__(self, spec: ProblemSpec, device: int = 0, build_hierarchy: bool = True, rank: int = 0,
                  world: int = 1, nccl_id: bytes | None = None):
         self.spec = spec
+        self.h = None
+        self._vecs = weakref.WeakSet()
         st, mo = spec.kernel_arrays()
         mat = None if spec.mat_of_el is None else np.ascontiguousarray(spec.mat_of_el, dtype=np.int32)
         q = None if spec.q_el is None else _f64(spec.q_el)
@@ -173,6 +179,8 @@ class Context:
 
     def close(self):
         if getattr(self, "h", None):
+            for v in list(self._vecs):
+                v.free()
             lib().stamg_destroy(self.h)
             self.h = None
 
