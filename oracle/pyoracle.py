@@ -69,6 +69,12 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
+def _need(o, x, level, what):
+    # the reference throws std::invalid_argument on layout mismatch (e.g. sweeps.cpp:23-24)
+    if np.asarray(x).size != o.size(level):
+        raise OracleError(1, f"invalid_argument: {what}: layout mismatch")
+
+
 class Oracle:
     """One problem (fine operators + lazily built MG hierarchy)."""
 
@@ -115,48 +121,58 @@ class Oracle:
         return f
 
     def apply_L(self, x, level=-1):
+        _need(self, x, level, "apply_L")
         x = _f64(x)
         y = np.empty_like(x)
         _check(lib().orc_apply_L(self.h, level, _p(x), _p(y)))
         return y
 
     def apply_A(self, x, order, level=-1):
+        _need(self, x, level, "apply_A")
         x = _f64(x)
         y = np.empty_like(x)
         _check(lib().orc_apply_A(self.h, level, _p(x), order, _p(y)))
         return y
 
     def apply_scatter(self, x, order, scale=1.0, y=None, level=-1):
+        _need(self, x, level, "apply_scatter")
         x = _f64(x)
         y = np.zeros_like(x) if y is None else _f64(y).copy()
         _check(lib().orc_apply_scatter(self.h, level, _p(x), order, C.c_double(scale), _p(y)))
         return y
 
     def sweep(self, rhs, level=-1, q0=0, q1=-1, z=None):
+        _need(self, rhs, level, "standard_sweep")
         rhs = _f64(rhs)
         z = np.zeros_like(rhs) if z is None else z
         _check(lib().orc_sweep(self.h, level, _p(rhs), _p(z), q0, q1))
         return z
 
     def coarse_gs(self, rhs, nu, phi, level=0):
+        _need(self, rhs, level, "coarse_scatter_sweep")
+        _need(self, phi, level, "coarse_scatter_sweep")
         rhs = _f64(rhs)
         phi = _f64(phi).copy()
         _check(lib().orc_coarse_gs(self.h, level, _p(rhs), nu, _p(phi)))
         return phi
 
     def smoother(self, f, order, phi, level=-1):
+        _need(self, f, level, "smoother_step")
+        _need(self, phi, level, "smoother_step")
         f = _f64(f)
         phi = _f64(phi).copy()
         _check(lib().orc_smoother(self.h, level, _p(f), order, _p(phi)))
         return phi
 
     def prolong(self, coarse, l):
+        _need(self, coarse, l - 1, "prolongate")
         coarse = _f64(coarse)
         fine = np.empty(self.size(l))
         _check(lib().orc_prolong(self.h, l, _p(coarse), _p(fine)))
         return fine
 
     def restrict(self, fine, l):
+        _need(self, fine, l, "restrict_residual")
         fine = _f64(fine)
         coarse = np.empty(self.size(l - 1))
         _check(lib().orc_restrict(self.h, l, _p(fine), _p(coarse)))
@@ -169,6 +185,7 @@ class Oracle:
         return phi
 
     def mg_apply(self, r):
+        _need(self, r, -1, "mg_apply")
         r = _f64(r)
         z = np.empty_like(r)
         _check(lib().orc_mg_apply(self.h, _p(r), _p(z)))
