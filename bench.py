@@ -208,8 +208,10 @@ def run_b200(args, world, rank, local, dist):
     achieved = upd_local * BYTES_PER_UPDATE / (sweep_ms * 1e-3 / max(sweep_n, 1)) / 1e9
     traffic = None
     try:
+        # ncu --set full capture (profiles/sweep_ncu_traffic.json): dram read+write per launch
+        # at 128^2 cells x 8192 directions, scaled by its ratio to the algorithmic bytes
         with open(os.path.join(ROOT, "profiles", "sweep_ncu_traffic.json")) as f:
-            traffic = json.load(f).get("bytes_per_launch")
+            traffic = json.load(f)["traffic_over_algorithmic"] * upd_local * BYTES_PER_UPDATE
     except Exception:
         pass
     extras = {}
