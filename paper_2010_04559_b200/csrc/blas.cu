@@ -145,7 +145,44 @@ double time_kernel(K kern, int blocks, int threads, int iters, cudaStream_t s) {
   return ms * 1e-3;
 }
 
+// in-place read+write of 128-byte chunks (8 lanes x 16 B); chunk c maps to
+// address c (mode 0, streaming) or to cell-major / group-minor order (mode 1,
+// the sweep's pattern: consecutive chunks 'stride' chunks apart)
+__global__ void chunk_rw_kernel(double* x, int64_t n_chunks, int64_t stride, int mode) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t c = tid >> 3;
+  if (c >= n_chunks) return;
+  int64_t dst = c;
+  if (mode == 1) {
+    const int64_t per = n_chunks / stride;
+    dst = (c % per) * stride + c / per;
+  }
+  double2* p = reinterpret_cast<double2*>(x + dst * 16) + (tid & 7);
+  double2 v = *p;
+  v.x += 1.0, v.y += 1.0;
+  *p = v;
+}
+
 }  // namespace
+
+double bench_chunk_rw_gbs(double* buf, int64_t n_doubles, int64_t stride_chunks, int mode, cudaStream_t s) {
+  const int64_t n_chunks = n_doubles / 16;
+  const int64_t threads = n_chunks * 8;
+  const int blocks = int((threads + 255) / 256);
+  chunk_rw_kernel<<<blocks, 256, 0, s>>>(buf, n_chunks, stride_chunks, mode);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, s);
+  for (int r = 0; r < 5; ++r) chunk_rw_kernel<<<blocks, 256, 0, s>>>(buf, n_chunks, stride_chunks, mode);
+  cudaEventRecord(e1, s);
+  cudaEventSynchronize(e1);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return 5.0 * 2.0 * n_doubles * 8 / (ms * 1e-3) / 1e9;
+}
 
 void launch_fill(double* x, double v, int64_t n, cudaStream_t s) {
   if (n > 0) fill_kernel<<<grid_for(n), kBlk, 0, s>>>(x, v, n);

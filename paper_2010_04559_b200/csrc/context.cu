@@ -101,7 +101,9 @@ struct DevLevel {
   int *up = nullptr, *child_ptr = nullptr, *child_idx = nullptr;
   double* src = nullptr;  // scatter moments workspace [n_el][Hp][4]
   double* mom = nullptr;  // coarse GS moments
-  int *gs_counter = nullptr, *gs_done = nullptr;
+  int *gs_done = nullptr, *gs_order = nullptr;
+  double* gs_K = nullptr;
+  int gs_blocks = 0, gs_cpw = 0, gs_kpad = 0, gs_max_np = 0;
   double *tmp = nullptr, *cf = nullptr, *ce = nullptr;  // V-cycle workspace
   std::vector<void*> owned;
 };
@@ -228,8 +230,40 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     L.BinvGS = dupload(frame_blocks(t.BinvGS, t), s);
     L.sq = dupload(t.sq, s);
     L.mom = dalloc<double>(size_t(t.n_el) * L.Hp * 4);
-    L.gs_counter = dalloc<int>(1);
     L.gs_done = dalloc<int>(size_t(8) * t.n_el);
+    // K[m][q][b] = X_q sig_m X_b^T for b in q's octant (coarse GS chain)
+    for (int o = 0; o < 8; ++o) L.gs_max_np = std::max(L.gs_max_np, t.oct_ptr[o + 1] - t.oct_ptr[o]);
+    L.gs_kpad = std::max(1, L.gs_max_np);
+    std::vector<double> K(size_t(t.n_mat) * t.P * L.gs_kpad, 0.0);
+    for (int m = 0; m < t.n_mat; ++m)
+      for (int o = 0; o < 8; ++o)
+        for (int a = t.oct_ptr[o]; a < t.oct_ptr[o + 1]; ++a)
+          for (int b = t.oct_ptr[o]; b < t.oct_ptr[o + 1]; ++b) {
+            const int qa = t.oct_patches[a], qb = t.oct_patches[b];
+            double k = 0;
+            for (int h = 0; h < t.H; ++h)
+              k += t.X[size_t(qa) * t.H + h] * t.sig[size_t(m) * t.H + h] * t.X[size_t(qb) * t.H + h];
+            K[(size_t(m) * t.P + qa) * L.gs_kpad + (b - t.oct_ptr[o])] = k;
+          }
+    L.gs_K = dupload(K, s);
+    // static ownership: cell el -> warp el % W; per octant, each warp's cells in sweep order
+    const int max_blocks = coarse_gs_max_blocks(t.H, L.gs_max_np);
+    const int W = std::min(max_blocks * 8, t.n_el);
+    L.gs_blocks = (W + 7) / 8;
+    const int Wr = L.gs_blocks * 8;
+    L.gs_cpw = (t.n_el + Wr - 1) / Wr;
+    std::vector<int> order(size_t(8) * Wr * L.gs_cpw, -1);
+    for (int o = 0; o < 8; ++o) {
+      std::vector<int> fill(Wr, 0);
+      const bool xn = o & 1, yn = (o >> 1) & 1;
+      for (int k = 0; k < t.n_el; ++k) {
+        const int jf = k / t.nx, ifr = k % t.nx;
+        const int el = (yn ? t.ny - 1 - jf : jf) * t.nx + (xn ? t.nx - 1 - ifr : ifr);
+        const int w = el % Wr;
+        order[size_t(o) * Wr * L.gs_cpw + size_t(w) * L.gs_cpw + fill[w]++] = el;
+      }
+    }
+    L.gs_order = dupload(order, s);
   }
   if (!t.up.empty()) {
     L.up = dupload(t.up, s), L.up_w = dupload(t.up_w, s);
@@ -243,7 +277,7 @@ void free_level(DevLevel& L) {
   for (void* p : {(void*)L.X, (void*)L.XT, (void*)L.sig, (void*)L.ones, (void*)L.B, (void*)L.Binv, (void*)L.cxy,
                   (void*)L.BinvGS, (void*)L.sq, (void*)L.area, (void*)L.up_w, (void*)L.groups, (void*)L.group_oct,
                   (void*)L.oct_patches, (void*)L.oct_ptr, (void*)L.up, (void*)L.child_ptr, (void*)L.child_idx,
-                  (void*)L.src, (void*)L.mom, (void*)L.gs_counter, (void*)L.gs_done, (void*)L.tmp, (void*)L.cf,
+                  (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_order, (void*)L.gs_K, (void*)L.tmp, (void*)L.cf,
                   (void*)L.ce})
     if (p) cudaFree(p);
 }
@@ -343,13 +377,14 @@ void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* 
   if (!L.BinvGS) throw std::invalid_argument("coarse_scatter_sweep: not the coarsest level");
   // per-element moments of the current iterate (sweeps.cpp:74-79)
   op_d2m(c, L, phi, L.t.order, L.mom, L.ones, true);
-  ck(cudaMemsetAsync(L.gs_counter, 0, sizeof(int), c->stream), "memset");
   ck(cudaMemsetAsync(L.gs_done, 0, sizeof(int) * 8 * size_t(L.t.n_el), c->stream), "memset");
   Timed tm(c, "coarse_gs");
   CoarseGSParams p;
   p.rhs = rhs, p.phi = phi, p.mom = L.mom, p.X = L.X, p.sig = L.sig, p.BinvGS = L.BinvGS, p.sq = L.sq, p.cxy = L.cxy;
   p.oct_patches = L.oct_patches, p.oct_ptr = L.oct_ptr, p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
-  p.counter = L.gs_counter, p.done = L.gs_done;
+  p.done = L.gs_done, p.order = L.gs_order, p.K = L.gs_K;
+  p.order_stride = L.gs_blocks * 8 * L.gs_cpw, p.cells_per_warp = L.gs_cpw, p.kpad = L.gs_kpad;
+  p.grid_blocks = L.gs_blocks;
   p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.H = L.t.H, p.nx = L.t.nx, p.ny = L.t.ny, p.nu = nu;
   for (int o = 0; o < 8; ++o)
     p.max_patches_per_octant = std::max(p.max_patches_per_octant, L.t.oct_ptr[o + 1] - L.t.oct_ptr[o]);
@@ -1069,6 +1104,11 @@ int stamg_bench_fp64_peaks(stamg_ctx* c, double* dmma_tflops, double* dfma_tflop
     *dmma_tflops = bench_dmma_tflops(c->device, c->stream);
     *dfma_tflops = bench_dfma_tflops(c->device, c->stream);
   });
+}
+
+// access-pattern probe: GB/s of an in-place 128-byte-chunk read+write over a vector
+int stamg_bench_chunk_rw(stamg_ctx* c, stamg_vec* v, int64_t stride_chunks, int mode, double* gbs) {
+  return guard([&] { *gbs = bench_chunk_rw_gbs(v->d, v->n, stride_chunks, mode, c->stream); });
 }
 
 // pinned host memory for the host-buffer entry points

@@ -88,13 +88,17 @@ struct CoarseGSParams {
   const int* oct_patches = nullptr;
   const int* oct_ptr = nullptr;   // [9]
   const int* mat = nullptr;
-  int* counter = nullptr;         // work ticket
   int* done = nullptr;            // [8][n_el] completed pass count
+  const int* order = nullptr;     // [8][order_stride] cells per octant, grouped by owner warp
+  const double* K = nullptr;      // [n_mat][P][kpad] X_q sig X_b^T, b = index within q's octant
+  int order_stride = 0, cells_per_warp = 0, kpad = 0, grid_blocks = 0;
   int n_el = 0, P = 0, Hp = 0, H = 0, nx = 0, ny = 0, nu = 0;
   int max_patches_per_octant = 0;
   double N[16];
 };
 void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s);
+// co-resident CTAs (256 threads) of the coarse GS kernel for this harmonic count
+int coarse_gs_max_blocks(int H, int max_np);
 
 // BLAS-1 (deterministic reductions)
 void launch_fill(double* x, double v, int64_t n, cudaStream_t s);
@@ -113,5 +117,6 @@ void launch_lincomb(const double* const* vs, int nv, const double* c, double* u,
 // FP64 throughput microbenchmarks (roofline denominators)
 double bench_dmma_tflops(int device, cudaStream_t s);
 double bench_dfma_tflops(int device, cudaStream_t s);
+double bench_chunk_rw_gbs(double* buf, int64_t n_doubles, int64_t stride_chunks, int mode, cudaStream_t s);
 
 }  // namespace stamg_b200

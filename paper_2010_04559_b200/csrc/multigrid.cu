@@ -16,6 +16,7 @@
 // reproducible run to run.
 #include <algorithm>
 #include <stdexcept>
+#include <string>
 
 #include "common.cuh"
 #include "kernels.hpp"
@@ -64,197 +65,219 @@ __device__ __forceinline__ void perm(int m, double& a0, double& a1, double& a2, 
   if (m & 2) { double u = a0; a0 = a2; a2 = u; u = a1; a1 = a3; a3 = u; }
 }
 
+// Static-ownership variant: warp w owns a fixed set of cells for the whole
+// call and processes its items in the global (pass, octant, sweep-order)
+// order, so the previous-octant dependency is program order and the cell's
+// own data (moments, rhs, previous iterate) is loaded before any wait. The
+// patch chain uses K = X_q sig X_b^T (per material): t_a = t0_a + sum_{b<a}
+// K[a][b] dz_b, algebraically the reference's running-moment update
+// (sweeps.cpp:93-101). Requires co-residency (cooperative launch).
 template <int KH, int NS>
-__global__ void __launch_bounds__(128) coarse_gs_kernel(CoarseGSParams p) {
-  // KH harmonics per lane (H <= 32 KH); NS patch slots per lane (patches per octant <= 32 NS)
+__global__ void __launch_bounds__(256) coarse_gs_static_kernel(CoarseGSParams p) {
   const int lane = threadIdx.x & 31;
   const unsigned full = 0xffffffffu;
-  const int n_el = p.n_el, nx = p.nx, ny = p.ny, P = p.P, Hp = p.Hp, H = p.H;
-  const int per_pass = 8 * n_el;
-  const int total = p.nu * per_pass;
-  for (;;) {
-    int ticket = 0;
-    if (lane == 0) ticket = atomicAdd(p.counter, 1);
-    ticket = __shfl_sync(full, ticket, 0);
-    if (ticket >= total) return;
-    const int pass = ticket / per_pass, rem = ticket - pass * per_pass;
-    const int oct = rem / n_el, kk = rem - oct * n_el;
-    const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
-    const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
-    const int jf = kk / nx, ifr = kk - jf * nx;
-    const int gx = xneg ? nx - 1 - ifr : ifr, gy = yneg ? ny - 1 - jf : jf;
-    const int el = gy * nx + gx;
-    const int sx = xneg ? -1 : 1, sy = yneg ? -nx : nx;
-    const int upx = ifr > 0 ? el - sx : -1, upy = jf > 0 ? el - sy : -1;
-    const int dnx = ifr < nx - 1 ? el + sx : -1, dny = jf < ny - 1 ? el + sy : -1;
-    const int pbeg = p.oct_ptr[oct], np = p.oct_ptr[oct + 1] - pbeg;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int n_el = p.n_el, nx = p.nx, ny = p.ny, P = p.P, Hp = p.Hp, H = p.H, cpw = p.cells_per_warp;
+  for (int pass = 0; pass < p.nu; ++pass)
+    for (int oct = 0; oct < 8; ++oct) {
+      const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
+      const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
+      const int pbeg = p.oct_ptr[oct], np = p.oct_ptr[oct + 1] - pbeg;
+      for (int j = 0; j < cpw; ++j) {
+        const int el = p.order[(size_t)oct * p.order_stride + (size_t)gw * cpw + j];
+        if (el < 0) continue;
+        const int gx = el % nx, gy = el / nx;
+        const int ifr = xneg ? nx - 1 - gx : gx, jf = yneg ? ny - 1 - gy : gy;
+        const int sx = xneg ? -1 : 1, sy = yneg ? -nx : nx;
+        const int upx = ifr > 0 ? el - sx : -1, upy = jf > 0 ? el - sy : -1;
+        const int dnx = ifr < nx - 1 ? el + sx : -1, dny = jf < ny - 1 ? el + sy : -1;
+        const int mt = p.mat ? p.mat[el] : 0;
 
-    // read-only inputs first (independent of the dependency flags)
-    double r[NS][4];
-    int qs[NS];
+        // ---- own data: moments, rhs, previous iterate (no dependency wait)
+        double mo[KH][4], sg[KH];
+        double* mom_el = p.mom + (size_t)el * Hp * 4;
 #pragma unroll
-    for (int sl = 0; sl < NS; ++sl) {
-      const int j = lane + 32 * sl;
-      qs[sl] = j < np ? p.oct_patches[pbeg + j] : -1;
-      if (qs[sl] >= 0) {
-        const double* rb = p.rhs + ((size_t)el * P + qs[sl]) * 4;
-        r[sl][0] = rb[0], r[sl][1] = rb[1], r[sl][2] = rb[2], r[sl][3] = rb[3];
-      } else {
-        r[sl][0] = r[sl][1] = r[sl][2] = r[sl][3] = 0.0;
-      }
-    }
-    // dependencies, polled in parallel by lanes 0..4
-    {
-      const int* f = nullptr;
-      int need = 0;
-      if (lane == 0 && upx >= 0) f = p.done + oct * n_el + upx, need = pass + 1;
-      if (lane == 1 && upy >= 0) f = p.done + oct * n_el + upy, need = pass + 1;
-      if (lane == 2) {
-        if (oct > 0) f = p.done + (oct - 1) * n_el + el, need = pass + 1;
-        else if (pass > 0) f = p.done + 7 * n_el + el, need = pass;
-      }
-      if (lane == 3 && pass > 0 && dnx >= 0) f = p.done + oct * n_el + dnx, need = pass;
-      if (lane == 4 && pass > 0 && dny >= 0) f = p.done + oct * n_el + dny, need = pass;
-      bool ok = f == nullptr || ld_acquire(f) >= need;
-      while (!__all_sync(full, ok)) {
-        if (!ok) ok = ld_acquire(f) >= need;
-      }
-    }
-    // moments, previous iterate and upwind traces: one round trip
-    const int mt = p.mat ? p.mat[el] : 0;
-    double mo[KH][4], sg[KH];
-    double* mom_el = p.mom + (size_t)el * Hp * 4;
-#pragma unroll
-    for (int kh = 0; kh < KH; ++kh) {
-      const int h = lane + 32 * kh;
-      if (h < H) {
-        const double2 a = ld_cg2(mom_el + h * 4), b = ld_cg2(mom_el + h * 4 + 2);
-        mo[kh][0] = a.x, mo[kh][1] = a.y, mo[kh][2] = b.x, mo[kh][3] = b.y;
-        sg[kh] = p.sig[(size_t)mt * Hp + h];
-      } else {
-        mo[kh][0] = mo[kh][1] = mo[kh][2] = mo[kh][3] = 0.0;
-        sg[kh] = 0.0;
-      }
-    }
-    double zo[NS][4];
-#pragma unroll
-    for (int sl = 0; sl < NS; ++sl) {
-      const int q = qs[sl];
-      zo[sl][0] = zo[sl][1] = zo[sl][2] = zo[sl][3] = 0.0;
-      if (q < 0) continue;
-      const double2 za = ld_cg2(p.phi + ((size_t)el * P + q) * 4), zc = ld_cg2(p.phi + ((size_t)el * P + q) * 4 + 2);
-      double ux[4] = {0, 0, 0, 0}, uy[4] = {0, 0, 0, 0};
-      if (upx >= 0) {
-        const double2 a = ld_cg2(p.phi + ((size_t)upx * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upx * P + q) * 4 + 2);
-        ux[0] = a.x, ux[1] = a.y, ux[2] = b.x, ux[3] = b.y;
-      }
-      if (upy >= 0) {
-        const double2 a = ld_cg2(p.phi + ((size_t)upy * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upy * P + q) * 4 + 2);
-        uy[0] = a.x, uy[1] = a.y, uy[2] = b.x, uy[3] = b.y;
-      }
-      zo[sl][0] = za.x, zo[sl][1] = za.y, zo[sl][2] = zc.x, zo[sl][3] = zc.y;
-      perm(m, r[sl][0], r[sl][1], r[sl][2], r[sl][3]);
-      perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
-      perm(m, ux[0], ux[1], ux[2], ux[3]);
-      perm(m, uy[0], uy[1], uy[2], uy[3]);
-      // upwind terms (sweeps.cpp:87-92), frame rows {0,2} <- x trace {1,3}, rows {0,1} <- y trace {2,3}
-      const double* cxy = p.cxy + (size_t)q * 8;
-      if (upx >= 0) {
-        r[sl][0] -= cxy[0] * ux[1] + cxy[1] * ux[3];
-        r[sl][2] -= cxy[2] * ux[1] + cxy[3] * ux[3];
-      }
-      if (upy >= 0) {
-        r[sl][0] -= cxy[4] * uy[2] + cxy[5] * uy[3];
-        r[sl][1] -= cxy[6] * uy[2] + cxy[7] * uy[3];
-      }
-    }
-    // the sequential patch chain (sweeps.cpp:86-102)
-    for (int j = 0; j < np; ++j) {
-      const int sl = j >> 5, src = j & 31;
-      double rr[4], z[4];
-      int q = 0;
-#pragma unroll
-      for (int s2 = 0; s2 < NS; ++s2)
-        if (s2 == sl) {
-          q = __shfl_sync(full, qs[s2], src);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) rr[i] = __shfl_sync(full, r[s2][i], src), z[i] = __shfl_sync(full, zo[s2][i], src);
+        for (int kh = 0; kh < KH; ++kh) {
+          const int h = lane + 32 * kh;
+          if (h < H) {
+            const double2 a = ld_cg2(mom_el + h * 4), b = ld_cg2(mom_el + h * 4 + 2);
+            mo[kh][0] = a.x, mo[kh][1] = a.y, mo[kh][2] = b.x, mo[kh][3] = b.y;
+            sg[kh] = p.sig[(size_t)mt * Hp + h];
+          } else {
+            mo[kh][0] = mo[kh][1] = mo[kh][2] = mo[kh][3] = 0.0;
+            sg[kh] = 0.0;
+          }
         }
-      const double* Xq = p.X + (size_t)q * Hp;
-      double xq[KH];
-      double t[4] = {0.0, 0.0, 0.0, 0.0};
+        double r[NS][4], zo[NS][4], t[NS][4];
+        int qs[NS];
 #pragma unroll
-      for (int kh = 0; kh < KH; ++kh) {
-        const int h = lane + 32 * kh;
-        xq[kh] = h < H ? __ldg(Xq + h) : 0.0;
-        const double xs = xq[kh] * sg[kh];
+        for (int sl = 0; sl < NS; ++sl) {
+          const int a = lane + 32 * sl;
+          qs[sl] = a < np ? p.oct_patches[pbeg + a] : -1;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) t[i] += xs * mo[kh][i];
+          for (int i = 0; i < 4; ++i) r[sl][i] = zo[sl][i] = t[sl][i] = 0.0;
+          if (qs[sl] >= 0) {
+            const double* rb = p.rhs + ((size_t)el * P + qs[sl]) * 4;
+            const double2 ra = __ldg(reinterpret_cast<const double2*>(rb)), rc = __ldg(reinterpret_cast<const double2*>(rb) + 1);
+            const double2 za = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4), zc = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4 + 2);
+            r[sl][0] = ra.x, r[sl][1] = ra.y, r[sl][2] = rc.x, r[sl][3] = rc.y;
+            zo[sl][0] = za.x, zo[sl][1] = za.y, zo[sl][2] = zc.x, zo[sl][3] = zc.y;
+          }
+        }
+        // ---- t0_a = X_qa sig mom (all patches of the octant), off the critical path
+        for (int a = 0; a < np; ++a) {
+          const double* Xq = p.X + (size_t)p.oct_patches[pbeg + a] * Hp;
+          double u[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int kh = 0; kh < KH; ++kh) {
+            const int h = lane + 32 * kh;
+            const double xs = (h < H ? __ldg(Xq + h) : 0.0) * sg[kh];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) u[i] += xs * mo[kh][i];
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) u[i] += __shfl_xor_sync(full, u[i], o);
+#pragma unroll
+          for (int sl = 0; sl < NS; ++sl)
+            if (a == lane + 32 * sl)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) t[sl][i] = u[i];
+        }
+        // ---- wait for the upwind cells (this pass) and the downwind readers (last pass)
+        {
+          const int* f = nullptr;
+          int need = 0;
+          const int* d = p.done + (size_t)oct * n_el;
+          if (lane == 0 && upx >= 0) f = d + upx, need = pass + 1;
+          if (lane == 1 && upy >= 0) f = d + upy, need = pass + 1;
+          if (lane == 2 && pass > 0 && dnx >= 0) f = d + dnx, need = pass;
+          if (lane == 3 && pass > 0 && dny >= 0) f = d + dny, need = pass;
+          bool ok = f == nullptr || ld_acquire(f) >= need;
+          while (!__all_sync(full, ok))
+            if (!ok) ok = ld_acquire(f) >= need;
+        }
+        // ---- upwind traces, folded into r (sweeps.cpp:87-92); everything in the sweep frame
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) {
+          const int q = qs[sl];
+          if (q < 0) continue;
+          double ux[4] = {0, 0, 0, 0}, uy[4] = {0, 0, 0, 0};
+          if (upx >= 0) {
+            const double2 a = ld_cg2(p.phi + ((size_t)upx * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upx * P + q) * 4 + 2);
+            ux[0] = a.x, ux[1] = a.y, ux[2] = b.x, ux[3] = b.y;
+          }
+          if (upy >= 0) {
+            const double2 a = ld_cg2(p.phi + ((size_t)upy * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upy * P + q) * 4 + 2);
+            uy[0] = a.x, uy[1] = a.y, uy[2] = b.x, uy[3] = b.y;
+          }
+          perm(m, r[sl][0], r[sl][1], r[sl][2], r[sl][3]);
+          perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
+          perm(m, t[sl][0], t[sl][1], t[sl][2], t[sl][3]);
+          perm(m, ux[0], ux[1], ux[2], ux[3]);
+          perm(m, uy[0], uy[1], uy[2], uy[3]);
+          const double* cxy = p.cxy + (size_t)q * 8;
+          if (upx >= 0) {
+            r[sl][0] -= cxy[0] * ux[1] + cxy[1] * ux[3];
+            r[sl][2] -= cxy[2] * ux[1] + cxy[3] * ux[3];
+          }
+          if (upy >= 0) {
+            r[sl][0] -= cxy[4] * uy[2] + cxy[5] * uy[3];
+            r[sl][1] -= cxy[6] * uy[2] + cxy[7] * uy[3];
+          }
+        }
+        // ---- the sequential patch chain
+        const double* Kb = p.K + (size_t)mt * P * p.kpad;
+        double dzs[NS][4];
+        for (int a = 0; a < np; ++a) {
+          const int sl = a >> 5, src = a & 31;
+          double dz[4] = {0.0, 0.0, 0.0, 0.0};
+          if (lane == src) {
+#pragma unroll
+            for (int s2 = 0; s2 < NS; ++s2)
+              if (s2 == sl) {
+                const int q = qs[s2];
+                const double sq = Kb[(size_t)q * p.kpad + a];
+                double d[4], rr[4], n[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) d[i] = t[s2][i] - sq * zo[s2][i];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                  rr[i] = r[s2][i] + (d[0] * p.N[i] + d[1] * p.N[4 + i] + d[2] * p.N[8 + i] + d[3] * p.N[12 + i]);
+                const double* B = p.BinvGS + ((size_t)mt * P + q) * 16;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                  n[i] = B[4 * i] * rr[0] + B[4 * i + 1] * rr[1] + B[4 * i + 2] * rr[2] + B[4 * i + 3] * rr[3];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dz[i] = n[i] - zo[s2][i], zo[s2][i] = n[i];
+              }
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dz[i] = __shfl_sync(full, dz[i], src);
+#pragma unroll
+          for (int s2 = 0; s2 < NS; ++s2) {
+            if (lane + 32 * s2 == a)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) dzs[s2][i] = dz[i];
+            const int q = qs[s2];
+            if (q >= 0 && lane + 32 * s2 > a) {
+              const double k = Kb[(size_t)q * p.kpad + a];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) t[s2][i] += k * dz[i];
+            }
+          }
+        }
+        // ---- publish the new iterate of this cell's patches, then the flag
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) {
+          const int q = qs[sl];
+          if (q < 0) continue;
+          perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
+          perm(m, dzs[sl][0], dzs[sl][1], dzs[sl][2], dzs[sl][3]);
+          double* zb = p.phi + ((size_t)el * P + q) * 4;
+          st_cg2(zb, make_double2(zo[sl][0], zo[sl][1]));
+          st_cg2(zb + 2, make_double2(zo[sl][2], zo[sl][3]));
+        }
+        __syncwarp();
+        if (lane == 0) st_release(p.done + (size_t)oct * n_el + el, pass + 1);
+        // ---- running moments: mom += sum_a X_qa^T dz_a (private to this warp)
+        for (int a = 0; a < np; ++a) {
+          const int sl = a >> 5, src = a & 31;
+          double dz[4];
+#pragma unroll
+          for (int s2 = 0; s2 < NS; ++s2)
+            if (s2 == sl)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) dz[i] = __shfl_sync(full, dzs[s2][i], src);
+          const double* Xq = p.X + (size_t)p.oct_patches[pbeg + a] * Hp;
+#pragma unroll
+          for (int kh = 0; kh < KH; ++kh) {
+            const int h = lane + 32 * kh;
+            const double x = h < H ? __ldg(Xq + h) : 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) mo[kh][i] += x * dz[i];
+          }
+        }
+#pragma unroll
+        for (int kh = 0; kh < KH; ++kh) {
+          const int h = lane + 32 * kh;
+          if (h < H) {
+            st_cg2(mom_el + h * 4, make_double2(mo[kh][0], mo[kh][1]));
+            st_cg2(mom_el + h * 4 + 2, make_double2(mo[kh][2], mo[kh][3]));
+          }
+        }
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) t[i] += __shfl_xor_sync(full, t[i], o);
-      perm(m, t[0], t[1], t[2], t[3]);
-      // explicit scatter from the other patches: (X sig (mom - X^T zold)) N
-      const double sq = p.sq[(size_t)mt * P + q];
-      double d[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) d[i] = t[i] - sq * z[i];
-      // N is invariant under the frame permutation (uniform square cells)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) rr[i] += d[0] * p.N[i] + d[1] * p.N[4 + i] + d[2] * p.N[8 + i] + d[3] * p.N[12 + i];
-      const double* B = p.BinvGS + ((size_t)mt * P + q) * 16;
-      double n[4], e[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) n[i] = B[4 * i] * rr[0] + B[4 * i + 1] * rr[1] + B[4 * i + 2] * rr[2] + B[4 * i + 3] * rr[3];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) e[i] = n[i] - z[i];
-#pragma unroll
-      for (int s2 = 0; s2 < NS; ++s2)
-        if (s2 == sl && lane == src)
-#pragma unroll
-          for (int i = 0; i < 4; ++i) zo[s2][i] = n[i];
-      perm(m, e[0], e[1], e[2], e[3]);
-#pragma unroll
-      for (int kh = 0; kh < KH; ++kh)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) mo[kh][i] += xq[kh] * e[i];
     }
-    // publish: new iterate of this cell's patches, running moments, flag
-#pragma unroll
-    for (int sl = 0; sl < NS; ++sl) {
-      const int q = qs[sl];
-      if (q < 0) continue;
-      perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
-      double* zb = p.phi + ((size_t)el * P + q) * 4;
-      st_cg2(zb, make_double2(zo[sl][0], zo[sl][1]));
-      st_cg2(zb + 2, make_double2(zo[sl][2], zo[sl][3]));
-    }
-#pragma unroll
-    for (int kh = 0; kh < KH; ++kh) {
-      const int h = lane + 32 * kh;
-      if (h < H) {
-        st_cg2(mom_el + h * 4, make_double2(mo[kh][0], mo[kh][1]));
-        st_cg2(mom_el + h * 4 + 2, make_double2(mo[kh][2], mo[kh][3]));
-      }
-    }
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_release(p.done + oct * n_el + el, pass + 1);
-  }
 }
 
 template <int KH, int NS>
 void launch_gs2(const CoarseGSParams& p, cudaStream_t s) {
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_gs_kernel<KH, NS>, 128, 0);
-  const long items = (long)p.nu * 8 * p.n_el;
-  long blocks = (long)sms * (per_sm > 0 ? per_sm : 1);
-  blocks = std::min(blocks, (items + 3) / 4);
-  coarse_gs_kernel<KH, NS><<<int(blocks), 128, 0, s>>>(p);
+  auto k = coarse_gs_static_kernel<KH, NS>;
+  CoarseGSParams q = p;
+  void* args[] = {&q};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(p.grid_blocks), dim3(256), args, 0, s);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("coarse_gs cooperative launch: ") + cudaGetErrorString(e));
 }
 
 template <int KH>
@@ -262,6 +285,15 @@ void launch_gs(const CoarseGSParams& p, cudaStream_t s, int max_np) {
   if (max_np <= 32) launch_gs2<KH, 1>(p, s);
   else if (max_np <= 64) launch_gs2<KH, 2>(p, s);
   else throw std::invalid_argument("coarse_scatter_sweep: more than 64 patches per octant on the coarsest level");
+}
+
+template <int KH, int NS>
+int occ_blocks() {
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_gs_static_kernel<KH, NS>, 256, 0);
+  return sms * std::max(per_sm, 1);
 }
 
 }  // namespace
@@ -278,6 +310,19 @@ void launch_restrict(const double* fine, double* coarse, const int* cptr, const 
   const int64_t n = (int64_t)n_el * Pc;
   if (n == 0) return;
   restrict_kernel<<<int((n + 255) / 256), 256, 0, s>>>(fine, coarse, cptr, cidx, w, n_el, Pf, Pc);
+}
+
+int coarse_gs_max_blocks(int H, int max_np) {
+  const int kh = (H + 31) / 32;
+  const bool two = max_np > 32;
+  switch (kh) {
+    case 1: return two ? occ_blocks<1, 2>() : occ_blocks<1, 1>();
+    case 2: return two ? occ_blocks<2, 2>() : occ_blocks<2, 1>();
+    case 3: return two ? occ_blocks<3, 2>() : occ_blocks<3, 1>();
+    case 4: return two ? occ_blocks<4, 2>() : occ_blocks<4, 1>();
+    case 5: case 6: return two ? occ_blocks<6, 2>() : occ_blocks<6, 1>();
+    default: return two ? occ_blocks<8, 2>() : occ_blocks<8, 1>();
+  }
 }
 
 void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s) {

@@ -71,6 +71,29 @@ def main():
         out[f"c{k}_solve"] = {"setup_s": setup, "wall_s": wall, "iters": rep["iterations"],
                               "final_residual": rep["final_residual"], "kernels_ms": kt}
         g.close()
+    if "c4v" in which:  # one V-cycle and one outer apply_A at full config-4 size
+        spec = cf.baseline_config(4)
+        t0 = time.perf_counter()
+        g = stamg.Context(spec)
+        setup = time.perf_counter() - t0
+        b = g.rhs()
+        z = g.mg_apply(b)
+        y = g.vec()
+        g.synchronize()
+        g.timing(True)
+        t0 = time.perf_counter()
+        g.mg_apply(b, z)
+        g.synchronize()
+        tv = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        g.apply_A_into(b, spec.N, y)
+        g.synchronize()
+        ta = time.perf_counter() - t0
+        kt = {kk: g.timed(kk) for kk in ("sweep", "apply_L", "d2m", "m2d", "coarse_gs", "prolong", "restrict")}
+        g.timing(False)
+        out["c4_vcycle"] = {"setup_s": setup, "mg_apply_s": tv, "apply_A_outer_s": ta, "kernels_ms": kt,
+                            "levels": g.levels(), "layout": g.layout()}
+        g.close()
     print(json.dumps(out, indent=1))
 
 
