@@ -246,24 +246,17 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
             K[(size_t(m) * t.P + qa) * L.gs_kpad + (b - t.oct_ptr[o])] = k;
           }
     L.gs_K = dupload(K, s);
-    // static ownership: cell el -> warp el % W; per octant, each warp's cells in sweep order
-    const int max_blocks = coarse_gs_max_blocks(t.H, L.gs_max_np);
-    const int W = std::min(max_blocks * 8, t.n_el);
-    L.gs_blocks = (W + 7) / 8;
-    const int Wr = L.gs_blocks * 8;
-    L.gs_cpw = (t.n_el + Wr - 1) / Wr;
-    std::vector<int> order(size_t(8) * Wr * L.gs_cpw, -1);
-    for (int o = 0; o < 8; ++o) {
-      std::vector<int> fill(Wr, 0);
-      const bool xn = o & 1, yn = (o >> 1) & 1;
-      for (int k = 0; k < t.n_el; ++k) {
-        const int jf = k / t.nx, ifr = k % t.nx;
-        const int el = (yn ? t.ny - 1 - jf : jf) * t.nx + (xn ? t.nx - 1 - ifr : ifr);
-        const int w = el % Wr;
-        order[size_t(o) * Wr * L.gs_cpw + size_t(w) * L.gs_cpw + fill[w]++] = el;
-      }
+    // static ownership: each warp owns a segment of gs_cpw consecutive cells of one row
+    const int max_warps = coarse_gs_max_warps(L.Hp, L.gs_kpad, L.gs_max_np);
+    int seg = 1;
+    while (int64_t(t.n_el) / seg > max_warps || t.nx % seg != 0) {
+      if (seg >= t.nx) throw std::invalid_argument("coarse_scatter_sweep: grid too large for co-resident warps");
+      seg *= 2;
     }
-    L.gs_order = dupload(order, s);
+    L.gs_cpw = seg;
+    const int W = t.n_el / seg;
+    L.gs_blocks = (W + coarse_gs_warps_per_block() - 1) / coarse_gs_warps_per_block();
+
   }
   if (!t.up.empty()) {
     L.up = dupload(t.up, s), L.up_w = dupload(t.up_w, s);
@@ -382,9 +375,8 @@ void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* 
   CoarseGSParams p;
   p.rhs = rhs, p.phi = phi, p.mom = L.mom, p.X = L.X, p.sig = L.sig, p.BinvGS = L.BinvGS, p.sq = L.sq, p.cxy = L.cxy;
   p.oct_patches = L.oct_patches, p.oct_ptr = L.oct_ptr, p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
-  p.done = L.gs_done, p.order = L.gs_order, p.K = L.gs_K;
-  p.order_stride = L.gs_blocks * 8 * L.gs_cpw, p.cells_per_warp = L.gs_cpw, p.kpad = L.gs_kpad;
-  p.grid_blocks = L.gs_blocks;
+  p.done = L.gs_done, p.K = L.gs_K, p.XT = L.XT, p.Pp = L.Pp;
+  p.cells_per_warp = L.gs_cpw, p.kpad = L.gs_kpad, p.grid_blocks = L.gs_blocks;
   p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.H = L.t.H, p.nx = L.t.nx, p.ny = L.t.ny, p.nu = nu;
   for (int o = 0; o < 8; ++o)
     p.max_patches_per_octant = std::max(p.max_patches_per_octant, L.t.oct_ptr[o + 1] - L.t.oct_ptr[o]);

@@ -89,16 +89,18 @@ struct CoarseGSParams {
   const int* oct_ptr = nullptr;   // [9]
   const int* mat = nullptr;
   int* done = nullptr;            // [8][n_el] completed pass count
-  const int* order = nullptr;     // [8][order_stride] cells per octant, grouped by owner warp
+  const double* XT = nullptr;     // [Hp][Pp]
+  int Pp = 0;
   const double* K = nullptr;      // [n_mat][P][kpad] X_q sig X_b^T, b = index within q's octant
-  int order_stride = 0, cells_per_warp = 0, kpad = 0, grid_blocks = 0;
+  int cells_per_warp = 0, kpad = 0, grid_blocks = 0;  // warp owns a row segment of cells_per_warp cells
   int n_el = 0, P = 0, Hp = 0, H = 0, nx = 0, ny = 0, nu = 0;
   int max_patches_per_octant = 0;
   double N[16];
 };
 void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s);
-// co-resident CTAs (256 threads) of the coarse GS kernel for this harmonic count
-int coarse_gs_max_blocks(int H, int max_np);
+// co-resident warps of the coarse GS kernel, and warps per CTA
+int coarse_gs_max_warps(int Hp, int kpad, int max_np);
+int coarse_gs_warps_per_block();
 
 // BLAS-1 (deterministic reductions)
 void launch_fill(double* x, double v, int64_t n, cudaStream_t s);

@@ -65,49 +65,48 @@ __device__ __forceinline__ void perm(int m, double& a0, double& a1, double& a2, 
   if (m & 2) { double u = a0; a0 = a2; a2 = u; u = a1; a1 = a3; a3 = u; }
 }
 
-// Static-ownership variant: warp w owns a fixed set of cells for the whole
-// call and processes its items in the global (pass, octant, sweep-order)
-// order, so the previous-octant dependency is program order and the cell's
-// own data (moments, rhs, previous iterate) is loaded before any wait. The
-// patch chain uses K = X_q sig X_b^T (per material): t_a = t0_a + sum_{b<a}
-// K[a][b] dz_b, algebraically the reference's running-moment update
-// (sweeps.cpp:93-101). Requires co-residency (cooperative launch).
-template <int KH, int NS>
-__global__ void __launch_bounds__(256) coarse_gs_static_kernel(CoarseGSParams p) {
-  const int lane = threadIdx.x & 31;
+// Static-ownership variant: warp w owns a contiguous segment of `seg` cells
+// of one grid row for the whole call and processes its items in the global
+// (pass, octant, sweep-order) order. Cells of a segment are x-neighbours, so
+// walking them in order adds nothing to the critical path, and consecutive
+// octants alternate the x direction so the hand-over cell is the same. The
+// previous-octant dependency is program order; the cell's own data is loaded
+// before any wait. The patch chain uses K = X_q sig X_b^T (per material):
+// t_a = t0_a + sum_{b<a} K[a][b] dz_b, algebraically the reference's
+// running-moment update (sweeps.cpp:93-101). Needs co-residency
+// (cooperative launch).
+constexpr int GS_WARPS = 8;
+
+template <int NS>
+__global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseGSParams p) {
+  extern __shared__ __align__(16) double gsm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const unsigned full = 0xffffffffu;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int n_el = p.n_el, nx = p.nx, ny = p.ny, P = p.P, Hp = p.Hp, H = p.H, cpw = p.cells_per_warp;
+  const int gw = blockIdx.x * GS_WARPS + wib;
+  const int n_el = p.n_el, nx = p.nx, ny = p.ny, P = p.P, Hp = p.Hp, H = p.H, seg = p.cells_per_warp;
+  double* smom = gsm + (size_t)wib * (Hp * 4 + p.kpad * 4);  // [Hp][4]
+  double* sdz = smom + Hp * 4;                               // [kpad][4]
+  const int segs_per_row = nx / seg;
+  if (gw >= segs_per_row * ny) return;
+  const int gy = gw / segs_per_row, gx0 = (gw - gy * segs_per_row) * seg;
   for (int pass = 0; pass < p.nu; ++pass)
     for (int oct = 0; oct < 8; ++oct) {
       const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
       const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
       const int pbeg = p.oct_ptr[oct], np = p.oct_ptr[oct + 1] - pbeg;
-      for (int j = 0; j < cpw; ++j) {
-        const int el = p.order[(size_t)oct * p.order_stride + (size_t)gw * cpw + j];
-        if (el < 0) continue;
-        const int gx = el % nx, gy = el / nx;
+      for (int j = 0; j < seg; ++j) {
+        const int gx = gx0 + (xneg ? seg - 1 - j : j);
+        const int el = gy * nx + gx;
         const int ifr = xneg ? nx - 1 - gx : gx, jf = yneg ? ny - 1 - gy : gy;
         const int sx = xneg ? -1 : 1, sy = yneg ? -nx : nx;
         const int upx = ifr > 0 ? el - sx : -1, upy = jf > 0 ? el - sy : -1;
         const int dnx = ifr < nx - 1 ? el + sx : -1, dny = jf < ny - 1 ? el + sy : -1;
         const int mt = p.mat ? p.mat[el] : 0;
-
-        // ---- own data: moments, rhs, previous iterate (no dependency wait)
-        double mo[KH][4], sg[KH];
+        const double* sig = p.sig + (size_t)mt * Hp;
+        // ---- own data: moments -> shared, rhs / previous iterate -> registers
         double* mom_el = p.mom + (size_t)el * Hp * 4;
-#pragma unroll
-        for (int kh = 0; kh < KH; ++kh) {
-          const int h = lane + 32 * kh;
-          if (h < H) {
-            const double2 a = ld_cg2(mom_el + h * 4), b = ld_cg2(mom_el + h * 4 + 2);
-            mo[kh][0] = a.x, mo[kh][1] = a.y, mo[kh][2] = b.x, mo[kh][3] = b.y;
-            sg[kh] = p.sig[(size_t)mt * Hp + h];
-          } else {
-            mo[kh][0] = mo[kh][1] = mo[kh][2] = mo[kh][3] = 0.0;
-            sg[kh] = 0.0;
-          }
-        }
+        for (int c = lane; c < H * 2; c += 32)
+          reinterpret_cast<double2*>(smom)[c] = ld_cg2(mom_el + c * 2);
         double r[NS][4], zo[NS][4], t[NS][4];
         int qs[NS];
 #pragma unroll
@@ -124,26 +123,29 @@ __global__ void __launch_bounds__(256) coarse_gs_static_kernel(CoarseGSParams p)
             zo[sl][0] = za.x, zo[sl][1] = za.y, zo[sl][2] = zc.x, zo[sl][3] = zc.y;
           }
         }
-        // ---- t0_a = X_qa sig mom (all patches of the octant), off the critical path
-        for (int a = 0; a < np; ++a) {
-          const double* Xq = p.X + (size_t)p.oct_patches[pbeg + a] * Hp;
-          double u[4] = {0.0, 0.0, 0.0, 0.0};
+        __syncwarp();
+        // ---- t0_a = X_qa sig mom for the lane's patches (off the critical path)
 #pragma unroll
-          for (int kh = 0; kh < KH; ++kh) {
-            const int h = lane + 32 * kh;
-            const double xs = (h < H ? __ldg(Xq + h) : 0.0) * sg[kh];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) u[i] += xs * mo[kh][i];
+        for (int sl = 0; sl < NS; ++sl) {
+          if (qs[sl] < 0) continue;
+          const double* xt = p.XT + qs[sl];
+          double u0[4] = {0, 0, 0, 0}, u1[4] = {0, 0, 0, 0};
+          int h = 0;
+          for (; h + 1 < H; h += 2) {
+            const double xa = __ldg(xt + (size_t)h * p.Pp) * sig[h];
+            const double xb = __ldg(xt + (size_t)(h + 1) * p.Pp) * sig[h + 1];
+            const double2 ma = reinterpret_cast<const double2*>(smom)[2 * h], mb = reinterpret_cast<const double2*>(smom)[2 * h + 1];
+            const double2 na = reinterpret_cast<const double2*>(smom)[2 * h + 2], nb = reinterpret_cast<const double2*>(smom)[2 * h + 3];
+            u0[0] += xa * ma.x, u0[1] += xa * ma.y, u0[2] += xa * mb.x, u0[3] += xa * mb.y;
+            u1[0] += xb * na.x, u1[1] += xb * na.y, u1[2] += xb * nb.x, u1[3] += xb * nb.y;
+          }
+          if (h < H) {
+            const double xa = __ldg(xt + (size_t)h * p.Pp) * sig[h];
+            const double2 ma = reinterpret_cast<const double2*>(smom)[2 * h], mb = reinterpret_cast<const double2*>(smom)[2 * h + 1];
+            u0[0] += xa * ma.x, u0[1] += xa * ma.y, u0[2] += xa * mb.x, u0[3] += xa * mb.y;
           }
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) u[i] += __shfl_xor_sync(full, u[i], o);
-#pragma unroll
-          for (int sl = 0; sl < NS; ++sl)
-            if (a == lane + 32 * sl)
-#pragma unroll
-              for (int i = 0; i < 4; ++i) t[sl][i] = u[i];
+          for (int i = 0; i < 4; ++i) t[sl][i] = u0[i] + u1[i];
         }
         // ---- wait for the upwind cells (this pass) and the downwind readers (last pass)
         {
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(256) coarse_gs_static_kernel(CoarseGSParams p)
           while (!__all_sync(full, ok))
             if (!ok) ok = ld_acquire(f) >= need;
         }
-        // ---- upwind traces, folded into r (sweeps.cpp:87-92); everything in the sweep frame
+        // ---- upwind traces folded into r (sweeps.cpp:87-92), everything in the sweep frame
 #pragma unroll
         for (int sl = 0; sl < NS; ++sl) {
           const int q = qs[sl];
@@ -189,7 +191,6 @@ __global__ void __launch_bounds__(256) coarse_gs_static_kernel(CoarseGSParams p)
         }
         // ---- the sequential patch chain
         const double* Kb = p.K + (size_t)mt * P * p.kpad;
-        double dzs[NS][4];
         for (int a = 0; a < np; ++a) {
           const int sl = a >> 5, src = a & 31;
           double dz[4] = {0.0, 0.0, 0.0, 0.0};
@@ -217,15 +218,18 @@ __global__ void __launch_bounds__(256) coarse_gs_static_kernel(CoarseGSParams p)
           for (int i = 0; i < 4; ++i) dz[i] = __shfl_sync(full, dz[i], src);
 #pragma unroll
           for (int s2 = 0; s2 < NS; ++s2) {
-            if (lane + 32 * s2 == a)
-#pragma unroll
-              for (int i = 0; i < 4; ++i) dzs[s2][i] = dz[i];
             const int q = qs[s2];
             if (q >= 0 && lane + 32 * s2 > a) {
               const double k = Kb[(size_t)q * p.kpad + a];
 #pragma unroll
               for (int i = 0; i < 4; ++i) t[s2][i] += k * dz[i];
             }
+          }
+          if (lane == 0) {  // physical-frame dz for the moment update
+            double e0 = dz[0], e1 = dz[1], e2 = dz[2], e3 = dz[3];
+            perm(m, e0, e1, e2, e3);
+            reinterpret_cast<double2*>(sdz)[2 * a] = make_double2(e0, e1);
+            reinterpret_cast<double2*>(sdz)[2 * a + 1] = make_double2(e2, e3);
           }
         }
         // ---- publish the new iterate of this cell's patches, then the flag
@@ -234,7 +238,6 @@ __global__ void __launch_bounds__(256) coarse_gs_static_kernel(CoarseGSParams p)
           const int q = qs[sl];
           if (q < 0) continue;
           perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
-          perm(m, dzs[sl][0], dzs[sl][1], dzs[sl][2], dzs[sl][3]);
           double* zb = p.phi + ((size_t)el * P + q) * 4;
           st_cg2(zb, make_double2(zo[sl][0], zo[sl][1]));
           st_cg2(zb + 2, make_double2(zo[sl][2], zo[sl][3]));
@@ -242,57 +245,42 @@ __global__ void __launch_bounds__(256) coarse_gs_static_kernel(CoarseGSParams p)
         __syncwarp();
         if (lane == 0) st_release(p.done + (size_t)oct * n_el + el, pass + 1);
         // ---- running moments: mom += sum_a X_qa^T dz_a (private to this warp)
-        for (int a = 0; a < np; ++a) {
-          const int sl = a >> 5, src = a & 31;
-          double dz[4];
-#pragma unroll
-          for (int s2 = 0; s2 < NS; ++s2)
-            if (s2 == sl)
-#pragma unroll
-              for (int i = 0; i < 4; ++i) dz[i] = __shfl_sync(full, dzs[s2][i], src);
-          const double* Xq = p.X + (size_t)p.oct_patches[pbeg + a] * Hp;
-#pragma unroll
-          for (int kh = 0; kh < KH; ++kh) {
-            const int h = lane + 32 * kh;
-            const double x = h < H ? __ldg(Xq + h) : 0.0;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) mo[kh][i] += x * dz[i];
+        for (int h = lane; h < H; h += 32) {
+          double2 a0 = reinterpret_cast<const double2*>(smom)[2 * h], a1 = reinterpret_cast<const double2*>(smom)[2 * h + 1];
+          for (int a = 0; a < np; ++a) {
+            const double x = __ldg(p.X + (size_t)p.oct_patches[pbeg + a] * Hp + h);
+            const double2 d0 = reinterpret_cast<const double2*>(sdz)[2 * a], d1 = reinterpret_cast<const double2*>(sdz)[2 * a + 1];
+            a0.x += x * d0.x, a0.y += x * d0.y, a1.x += x * d1.x, a1.y += x * d1.y;
           }
+          st_cg2(mom_el + h * 4, a0);
+          st_cg2(mom_el + h * 4 + 2, a1);
         }
-#pragma unroll
-        for (int kh = 0; kh < KH; ++kh) {
-          const int h = lane + 32 * kh;
-          if (h < H) {
-            st_cg2(mom_el + h * 4, make_double2(mo[kh][0], mo[kh][1]));
-            st_cg2(mom_el + h * 4 + 2, make_double2(mo[kh][2], mo[kh][3]));
-          }
-        }
+        __syncwarp();
       }
     }
 }
 
-template <int KH, int NS>
+size_t gs_smem(int Hp, int kpad) { return sizeof(double) * GS_WARPS * (size_t(Hp) * 4 + size_t(kpad) * 4); }
+
+template <int NS>
 void launch_gs2(const CoarseGSParams& p, cudaStream_t s) {
-  auto k = coarse_gs_static_kernel<KH, NS>;
+  auto k = coarse_gs_static_kernel<NS>;
+  const size_t smem = gs_smem(p.Hp, p.kpad);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   CoarseGSParams q = p;
   void* args[] = {&q};
-  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(p.grid_blocks), dim3(256), args, 0, s);
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(p.grid_blocks), dim3(GS_WARPS * 32), args, smem, s);
   if (e != cudaSuccess) throw std::runtime_error(std::string("coarse_gs cooperative launch: ") + cudaGetErrorString(e));
 }
 
-template <int KH>
-void launch_gs(const CoarseGSParams& p, cudaStream_t s, int max_np) {
-  if (max_np <= 32) launch_gs2<KH, 1>(p, s);
-  else if (max_np <= 64) launch_gs2<KH, 2>(p, s);
-  else throw std::invalid_argument("coarse_scatter_sweep: more than 64 patches per octant on the coarsest level");
-}
-
-template <int KH, int NS>
-int occ_blocks() {
+template <int NS>
+int occ_blocks(size_t smem) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_gs_static_kernel<KH, NS>, 256, 0);
+  auto k = coarse_gs_static_kernel<NS>;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, GS_WARPS * 32, smem);
   return sms * std::max(per_sm, 1);
 }
 
@@ -312,32 +300,17 @@ void launch_restrict(const double* fine, double* coarse, const int* cptr, const 
   restrict_kernel<<<int((n + 255) / 256), 256, 0, s>>>(fine, coarse, cptr, cidx, w, n_el, Pf, Pc);
 }
 
-int coarse_gs_max_blocks(int H, int max_np) {
-  const int kh = (H + 31) / 32;
-  const bool two = max_np > 32;
-  switch (kh) {
-    case 1: return two ? occ_blocks<1, 2>() : occ_blocks<1, 1>();
-    case 2: return two ? occ_blocks<2, 2>() : occ_blocks<2, 1>();
-    case 3: return two ? occ_blocks<3, 2>() : occ_blocks<3, 1>();
-    case 4: return two ? occ_blocks<4, 2>() : occ_blocks<4, 1>();
-    case 5: case 6: return two ? occ_blocks<6, 2>() : occ_blocks<6, 1>();
-    default: return two ? occ_blocks<8, 2>() : occ_blocks<8, 1>();
-  }
+int coarse_gs_max_warps(int Hp, int kpad, int max_np) {
+  const size_t smem = gs_smem(Hp, kpad);
+  if (max_np > 64) throw std::invalid_argument("coarse_scatter_sweep: more than 64 patches per octant on the coarsest level");
+  return (max_np > 32 ? occ_blocks<2>(smem) : occ_blocks<1>(smem)) * GS_WARPS;
 }
+int coarse_gs_warps_per_block() { return GS_WARPS; }
 
 void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s) {
   if (p.nu <= 0 || p.n_el == 0) return;
-  const int kh = (p.H + 31) / 32;
-  const int np = p.max_patches_per_octant;
-  switch (kh) {
-    case 1: launch_gs<1>(p, s, np); break;
-    case 2: launch_gs<2>(p, s, np); break;
-    case 3: launch_gs<3>(p, s, np); break;
-    case 4: launch_gs<4>(p, s, np); break;
-    case 5: case 6: launch_gs<6>(p, s, np); break;
-    case 7: case 8: launch_gs<8>(p, s, np); break;
-    default: throw std::invalid_argument("coarse_scatter_sweep: harmonic count > 256 not supported on the B200 path");
-  }
+  if (p.max_patches_per_octant <= 32) launch_gs2<1>(p, s);
+  else launch_gs2<2>(p, s);
 }
 
 }  // namespace stamg_b200
