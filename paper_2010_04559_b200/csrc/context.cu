@@ -101,8 +101,8 @@ struct DevLevel {
   int *up = nullptr, *child_ptr = nullptr, *child_idx = nullptr;
   double* src = nullptr;  // scatter moments workspace [n_el][Hp][4]
   double* mom = nullptr;  // coarse GS moments
-  int *gs_done = nullptr, *gs_order = nullptr;
-  double* gs_K = nullptr;
+  int* gs_done = nullptr;
+  double *gs_K = nullptr, *gs_Xo = nullptr, *gs_XoT = nullptr;
   int gs_blocks = 0, gs_cpw = 0, gs_kpad = 0, gs_max_np = 0;
   double *tmp = nullptr, *cf = nullptr, *ce = nullptr;  // V-cycle workspace
   std::vector<void*> owned;
@@ -243,9 +243,15 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
             double k = 0;
             for (int h = 0; h < t.H; ++h)
               k += t.X[size_t(qa) * t.H + h] * t.sig[size_t(m) * t.H + h] * t.X[size_t(qb) * t.H + h];
-            K[(size_t(m) * t.P + qa) * L.gs_kpad + (b - t.oct_ptr[o])] = k;
+            K[(size_t(m) * t.P + a) * L.gs_kpad + (b - t.oct_ptr[o])] = k;
           }
     L.gs_K = dupload(K, s);
+    std::vector<double> Xo(size_t(t.P) * L.Hp, 0.0), XoT(size_t(L.Hp) * t.P, 0.0);
+    for (int a = 0; a < t.P; ++a)
+      for (int h = 0; h < t.H; ++h)
+        Xo[size_t(a) * L.Hp + h] = XoT[size_t(h) * t.P + a] = t.X[size_t(t.oct_patches[a]) * t.H + h];
+    L.gs_Xo = dupload(Xo, s);
+    L.gs_XoT = dupload(XoT, s);
     // static ownership: each warp owns a segment of gs_cpw consecutive cells of one row
     const int max_warps = coarse_gs_max_warps(L.Hp, L.gs_kpad, L.gs_max_np);
     int seg = 1;
@@ -270,7 +276,7 @@ void free_level(DevLevel& L) {
   for (void* p : {(void*)L.X, (void*)L.XT, (void*)L.sig, (void*)L.ones, (void*)L.B, (void*)L.Binv, (void*)L.cxy,
                   (void*)L.BinvGS, (void*)L.sq, (void*)L.area, (void*)L.up_w, (void*)L.groups, (void*)L.group_oct,
                   (void*)L.oct_patches, (void*)L.oct_ptr, (void*)L.up, (void*)L.child_ptr, (void*)L.child_idx,
-                  (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_order, (void*)L.gs_K, (void*)L.tmp, (void*)L.cf,
+                  (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_K, (void*)L.gs_Xo, (void*)L.gs_XoT, (void*)L.tmp, (void*)L.cf,
                   (void*)L.ce})
     if (p) cudaFree(p);
 }
@@ -375,7 +381,7 @@ void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* 
   CoarseGSParams p;
   p.rhs = rhs, p.phi = phi, p.mom = L.mom, p.X = L.X, p.sig = L.sig, p.BinvGS = L.BinvGS, p.sq = L.sq, p.cxy = L.cxy;
   p.oct_patches = L.oct_patches, p.oct_ptr = L.oct_ptr, p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
-  p.done = L.gs_done, p.K = L.gs_K, p.XT = L.XT, p.Pp = L.Pp;
+  p.done = L.gs_done, p.K = L.gs_K, p.Xo = L.gs_Xo, p.XoT = L.gs_XoT;
   p.cells_per_warp = L.gs_cpw, p.kpad = L.gs_kpad, p.grid_blocks = L.gs_blocks;
   p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.H = L.t.H, p.nx = L.t.nx, p.ny = L.t.ny, p.nu = nu;
   for (int o = 0; o < 8; ++o)

@@ -89,9 +89,9 @@ struct CoarseGSParams {
   const int* oct_ptr = nullptr;   // [9]
   const int* mat = nullptr;
   int* done = nullptr;            // [8][n_el] completed pass count
-  const double* XT = nullptr;     // [Hp][Pp]
-  int Pp = 0;
-  const double* K = nullptr;      // [n_mat][P][kpad] X_q sig X_b^T, b = index within q's octant
+  const double* Xo = nullptr;     // [P][Hp] X rows in octant order (oct_patches)
+  const double* XoT = nullptr;    // [Hp][P] its transpose
+  const double* K = nullptr;      // [n_mat][P][kpad] X_a sig X_b^T, a = octant-ordered row, b = index in octant
   int cells_per_warp = 0, kpad = 0, grid_blocks = 0;  // warp owns a row segment of cells_per_warp cells
   int n_el = 0, P = 0, Hp = 0, H = 0, nx = 0, ny = 0, nu = 0;
   int max_patches_per_octant = 0;

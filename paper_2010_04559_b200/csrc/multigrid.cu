@@ -84,183 +84,219 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
   const unsigned full = 0xffffffffu;
   const int gw = blockIdx.x * GS_WARPS + wib;
   const int n_el = p.n_el, nx = p.nx, ny = p.ny, P = p.P, Hp = p.Hp, H = p.H, seg = p.cells_per_warp;
-  double* smom = gsm + (size_t)wib * (Hp * 4 + p.kpad * 4);  // [Hp][4]
-  double* sdz = smom + Hp * 4;                               // [kpad][4]
+  double* sbase = gsm + (size_t)wib * (Hp * 8 + p.kpad * 4);
+  // double-buffered moments [2][Hp][4] at sbase
+  double* sdz = sbase + Hp * 8;               // [kpad][4]
   const int segs_per_row = nx / seg;
   if (gw >= segs_per_row * ny) return;
   const int gy = gw / segs_per_row, gx0 = (gw - gy * segs_per_row) * seg;
-  for (int pass = 0; pass < p.nu; ++pass)
-    for (int oct = 0; oct < 8; ++oct) {
-      const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
-      const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
-      const int pbeg = p.oct_ptr[oct], np = p.oct_ptr[oct + 1] - pbeg;
-      for (int j = 0; j < seg; ++j) {
-        const int gx = gx0 + (xneg ? seg - 1 - j : j);
-        const int el = gy * nx + gx;
-        const int ifr = xneg ? nx - 1 - gx : gx, jf = yneg ? ny - 1 - gy : gy;
-        const int sx = xneg ? -1 : 1, sy = yneg ? -nx : nx;
-        const int upx = ifr > 0 ? el - sx : -1, upy = jf > 0 ? el - sy : -1;
-        const int dnx = ifr < nx - 1 ? el + sx : -1, dny = jf < ny - 1 ? el + sy : -1;
-        const int mt = p.mat ? p.mat[el] : 0;
-        const double* sig = p.sig + (size_t)mt * Hp;
-        // ---- own data: moments -> shared, rhs / previous iterate -> registers
-        double* mom_el = p.mom + (size_t)el * Hp * 4;
-        for (int c = lane; c < H * 2; c += 32)
-          reinterpret_cast<double2*>(smom)[c] = ld_cg2(mom_el + c * 2);
-        double r[NS][4], zo[NS][4], t[NS][4];
-        int qs[NS];
+  const int n_items = p.nu * 8 * seg;
+  auto cell_of = [&](int it) {
+    const int oct = (it / seg) & 7, j = it % seg;
+    return gy * nx + gx0 + ((oct & 1) ? seg - 1 - j : j);
+  };
+  auto prefetch_mom = [&](int el, double* dst) {
+    const double* src = p.mom + (size_t)el * Hp * 4;
+    for (int c = lane; c < H * 2; c += 32) cp_async16(dst + c * 2, src + c * 2, true);
+    cp_async_commit();
+  };
+  int cur = 0;
+  prefetch_mom(cell_of(0), sbase);
+  cp_async_wait<0>();
+  __syncwarp();
+  for (int it = 0; it < n_items; ++it) {
+    const int pass = it / (8 * seg), oct = (it / seg) & 7;
+    const int el = cell_of(it);
+    const int el_next = it + 1 < n_items ? cell_of(it + 1) : -1;
+    const bool reuse = el_next == el;  // next item is this cell again (next octant)
+    if (el_next >= 0 && !reuse) prefetch_mom(el_next, sbase + (cur ^ 1) * Hp * 4);
+    const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
+    const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
+    const int pbeg = p.oct_ptr[oct], np = p.oct_ptr[oct + 1] - pbeg;
+    const int gx = el - gy * nx;
+    const int ifr = xneg ? nx - 1 - gx : gx, jf = yneg ? ny - 1 - gy : gy;
+    const int sx = xneg ? -1 : 1, sy = yneg ? -nx : nx;
+    const int upx = ifr > 0 ? el - sx : -1, upy = jf > 0 ? el - sy : -1;
+    const int dnx = ifr < nx - 1 ? el + sx : -1, dny = jf < ny - 1 ? el + sy : -1;
+    const int mt = p.mat ? p.mat[el] : 0;
+    const double* sig = p.sig + (size_t)mt * Hp;
+    const double* mom = sbase + cur * Hp * 4;
+    // ---- own data: rhs / previous iterate -> registers (patch a = lane + 32 sl, octant order)
+    double r[NS][4], zo[NS][4], t[NS][4];
+    int qs[NS];
 #pragma unroll
-        for (int sl = 0; sl < NS; ++sl) {
-          const int a = lane + 32 * sl;
-          qs[sl] = a < np ? p.oct_patches[pbeg + a] : -1;
+    for (int sl = 0; sl < NS; ++sl) {
+      const int a = lane + 32 * sl;
+      qs[sl] = a < np ? p.oct_patches[pbeg + a] : -1;
 #pragma unroll
-          for (int i = 0; i < 4; ++i) r[sl][i] = zo[sl][i] = t[sl][i] = 0.0;
-          if (qs[sl] >= 0) {
-            const double* rb = p.rhs + ((size_t)el * P + qs[sl]) * 4;
-            const double2 ra = __ldg(reinterpret_cast<const double2*>(rb)), rc = __ldg(reinterpret_cast<const double2*>(rb) + 1);
-            const double2 za = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4), zc = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4 + 2);
-            r[sl][0] = ra.x, r[sl][1] = ra.y, r[sl][2] = rc.x, r[sl][3] = rc.y;
-            zo[sl][0] = za.x, zo[sl][1] = za.y, zo[sl][2] = zc.x, zo[sl][3] = zc.y;
-          }
-        }
-        __syncwarp();
-        // ---- t0_a = X_qa sig mom for the lane's patches (off the critical path)
-#pragma unroll
-        for (int sl = 0; sl < NS; ++sl) {
-          if (qs[sl] < 0) continue;
-          const double* xt = p.XT + qs[sl];
-          double u0[4] = {0, 0, 0, 0}, u1[4] = {0, 0, 0, 0};
-          int h = 0;
-          for (; h + 1 < H; h += 2) {
-            const double xa = __ldg(xt + (size_t)h * p.Pp) * sig[h];
-            const double xb = __ldg(xt + (size_t)(h + 1) * p.Pp) * sig[h + 1];
-            const double2 ma = reinterpret_cast<const double2*>(smom)[2 * h], mb = reinterpret_cast<const double2*>(smom)[2 * h + 1];
-            const double2 na = reinterpret_cast<const double2*>(smom)[2 * h + 2], nb = reinterpret_cast<const double2*>(smom)[2 * h + 3];
-            u0[0] += xa * ma.x, u0[1] += xa * ma.y, u0[2] += xa * mb.x, u0[3] += xa * mb.y;
-            u1[0] += xb * na.x, u1[1] += xb * na.y, u1[2] += xb * nb.x, u1[3] += xb * nb.y;
-          }
-          if (h < H) {
-            const double xa = __ldg(xt + (size_t)h * p.Pp) * sig[h];
-            const double2 ma = reinterpret_cast<const double2*>(smom)[2 * h], mb = reinterpret_cast<const double2*>(smom)[2 * h + 1];
-            u0[0] += xa * ma.x, u0[1] += xa * ma.y, u0[2] += xa * mb.x, u0[3] += xa * mb.y;
-          }
-#pragma unroll
-          for (int i = 0; i < 4; ++i) t[sl][i] = u0[i] + u1[i];
-        }
-        // ---- wait for the upwind cells (this pass) and the downwind readers (last pass)
-        {
-          const int* f = nullptr;
-          int need = 0;
-          const int* d = p.done + (size_t)oct * n_el;
-          if (lane == 0 && upx >= 0) f = d + upx, need = pass + 1;
-          if (lane == 1 && upy >= 0) f = d + upy, need = pass + 1;
-          if (lane == 2 && pass > 0 && dnx >= 0) f = d + dnx, need = pass;
-          if (lane == 3 && pass > 0 && dny >= 0) f = d + dny, need = pass;
-          bool ok = f == nullptr || ld_acquire(f) >= need;
-          while (!__all_sync(full, ok))
-            if (!ok) ok = ld_acquire(f) >= need;
-        }
-        // ---- upwind traces folded into r (sweeps.cpp:87-92), everything in the sweep frame
-#pragma unroll
-        for (int sl = 0; sl < NS; ++sl) {
-          const int q = qs[sl];
-          if (q < 0) continue;
-          double ux[4] = {0, 0, 0, 0}, uy[4] = {0, 0, 0, 0};
-          if (upx >= 0) {
-            const double2 a = ld_cg2(p.phi + ((size_t)upx * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upx * P + q) * 4 + 2);
-            ux[0] = a.x, ux[1] = a.y, ux[2] = b.x, ux[3] = b.y;
-          }
-          if (upy >= 0) {
-            const double2 a = ld_cg2(p.phi + ((size_t)upy * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upy * P + q) * 4 + 2);
-            uy[0] = a.x, uy[1] = a.y, uy[2] = b.x, uy[3] = b.y;
-          }
-          perm(m, r[sl][0], r[sl][1], r[sl][2], r[sl][3]);
-          perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
-          perm(m, t[sl][0], t[sl][1], t[sl][2], t[sl][3]);
-          perm(m, ux[0], ux[1], ux[2], ux[3]);
-          perm(m, uy[0], uy[1], uy[2], uy[3]);
-          const double* cxy = p.cxy + (size_t)q * 8;
-          if (upx >= 0) {
-            r[sl][0] -= cxy[0] * ux[1] + cxy[1] * ux[3];
-            r[sl][2] -= cxy[2] * ux[1] + cxy[3] * ux[3];
-          }
-          if (upy >= 0) {
-            r[sl][0] -= cxy[4] * uy[2] + cxy[5] * uy[3];
-            r[sl][1] -= cxy[6] * uy[2] + cxy[7] * uy[3];
-          }
-        }
-        // ---- the sequential patch chain
-        const double* Kb = p.K + (size_t)mt * P * p.kpad;
-        for (int a = 0; a < np; ++a) {
-          const int sl = a >> 5, src = a & 31;
-          double dz[4] = {0.0, 0.0, 0.0, 0.0};
-          if (lane == src) {
-#pragma unroll
-            for (int s2 = 0; s2 < NS; ++s2)
-              if (s2 == sl) {
-                const int q = qs[s2];
-                const double sq = Kb[(size_t)q * p.kpad + a];
-                double d[4], rr[4], n[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) d[i] = t[s2][i] - sq * zo[s2][i];
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                  rr[i] = r[s2][i] + (d[0] * p.N[i] + d[1] * p.N[4 + i] + d[2] * p.N[8 + i] + d[3] * p.N[12 + i]);
-                const double* B = p.BinvGS + ((size_t)mt * P + q) * 16;
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                  n[i] = B[4 * i] * rr[0] + B[4 * i + 1] * rr[1] + B[4 * i + 2] * rr[2] + B[4 * i + 3] * rr[3];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) dz[i] = n[i] - zo[s2][i], zo[s2][i] = n[i];
-              }
-          }
-#pragma unroll
-          for (int i = 0; i < 4; ++i) dz[i] = __shfl_sync(full, dz[i], src);
-#pragma unroll
-          for (int s2 = 0; s2 < NS; ++s2) {
-            const int q = qs[s2];
-            if (q >= 0 && lane + 32 * s2 > a) {
-              const double k = Kb[(size_t)q * p.kpad + a];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) t[s2][i] += k * dz[i];
-            }
-          }
-          if (lane == 0) {  // physical-frame dz for the moment update
-            double e0 = dz[0], e1 = dz[1], e2 = dz[2], e3 = dz[3];
-            perm(m, e0, e1, e2, e3);
-            reinterpret_cast<double2*>(sdz)[2 * a] = make_double2(e0, e1);
-            reinterpret_cast<double2*>(sdz)[2 * a + 1] = make_double2(e2, e3);
-          }
-        }
-        // ---- publish the new iterate of this cell's patches, then the flag
-#pragma unroll
-        for (int sl = 0; sl < NS; ++sl) {
-          const int q = qs[sl];
-          if (q < 0) continue;
-          perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
-          double* zb = p.phi + ((size_t)el * P + q) * 4;
-          st_cg2(zb, make_double2(zo[sl][0], zo[sl][1]));
-          st_cg2(zb + 2, make_double2(zo[sl][2], zo[sl][3]));
-        }
-        __syncwarp();
-        if (lane == 0) st_release(p.done + (size_t)oct * n_el + el, pass + 1);
-        // ---- running moments: mom += sum_a X_qa^T dz_a (private to this warp)
-        for (int h = lane; h < H; h += 32) {
-          double2 a0 = reinterpret_cast<const double2*>(smom)[2 * h], a1 = reinterpret_cast<const double2*>(smom)[2 * h + 1];
-          for (int a = 0; a < np; ++a) {
-            const double x = __ldg(p.X + (size_t)p.oct_patches[pbeg + a] * Hp + h);
-            const double2 d0 = reinterpret_cast<const double2*>(sdz)[2 * a], d1 = reinterpret_cast<const double2*>(sdz)[2 * a + 1];
-            a0.x += x * d0.x, a0.y += x * d0.y, a1.x += x * d1.x, a1.y += x * d1.y;
-          }
-          st_cg2(mom_el + h * 4, a0);
-          st_cg2(mom_el + h * 4 + 2, a1);
-        }
-        __syncwarp();
+      for (int i = 0; i < 4; ++i) r[sl][i] = zo[sl][i] = t[sl][i] = 0.0;
+      if (qs[sl] >= 0) {
+        const double* rb = p.rhs + ((size_t)el * P + qs[sl]) * 4;
+        const double2 ra = __ldg(reinterpret_cast<const double2*>(rb)), rc = __ldg(reinterpret_cast<const double2*>(rb) + 1);
+        const double2 za = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4), zc = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4 + 2);
+        r[sl][0] = ra.x, r[sl][1] = ra.y, r[sl][2] = rc.x, r[sl][3] = rc.y;
+        zo[sl][0] = za.x, zo[sl][1] = za.y, zo[sl][2] = zc.x, zo[sl][3] = zc.y;
       }
     }
+    // ---- t0_a = X_qa sig mom (off the critical path); XoT is [Hp][P] in octant order
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      if (qs[sl] < 0) continue;
+      const double* xt = p.XoT + pbeg + lane + 32 * sl;
+      double u[4][4] = {};
+      int h = 0;
+      for (; h + 3 < H; h += 4) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double xs = __ldg(xt + (size_t)(h + k) * P) * sig[h + k];
+          const double2 ma = reinterpret_cast<const double2*>(mom)[2 * (h + k)];
+          const double2 mb = reinterpret_cast<const double2*>(mom)[2 * (h + k) + 1];
+          u[k][0] += xs * ma.x, u[k][1] += xs * ma.y, u[k][2] += xs * mb.x, u[k][3] += xs * mb.y;
+        }
+      }
+      for (; h < H; ++h) {
+        const double xs = __ldg(xt + (size_t)h * P) * sig[h];
+        const double2 ma = reinterpret_cast<const double2*>(mom)[2 * h], mb = reinterpret_cast<const double2*>(mom)[2 * h + 1];
+        u[0][0] += xs * ma.x, u[0][1] += xs * ma.y, u[0][2] += xs * mb.x, u[0][3] += xs * mb.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) t[sl][i] = (u[0][i] + u[1][i]) + (u[2][i] + u[3][i]);
+    }
+    // ---- wait for the upwind cells (this pass) and the downwind readers (last pass)
+    {
+      const int* f = nullptr;
+      int need = 0;
+      const int* d = p.done + (size_t)oct * n_el;
+      if (lane == 0 && upx >= 0) f = d + upx, need = pass + 1;
+      if (lane == 1 && upy >= 0) f = d + upy, need = pass + 1;
+      if (lane == 2 && pass > 0 && dnx >= 0) f = d + dnx, need = pass;
+      if (lane == 3 && pass > 0 && dny >= 0) f = d + dny, need = pass;
+      bool ok = f == nullptr || ld_acquire(f) >= need;
+      while (!__all_sync(full, ok))
+        if (!ok) ok = ld_acquire(f) >= need;
+    }
+    // ---- upwind traces folded into r (sweeps.cpp:87-92), everything in the sweep frame
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      const int q = qs[sl];
+      if (q < 0) continue;
+      double ux[4] = {0, 0, 0, 0}, uy[4] = {0, 0, 0, 0};
+      if (upx >= 0) {
+        const double2 a = ld_cg2(p.phi + ((size_t)upx * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upx * P + q) * 4 + 2);
+        ux[0] = a.x, ux[1] = a.y, ux[2] = b.x, ux[3] = b.y;
+      }
+      if (upy >= 0) {
+        const double2 a = ld_cg2(p.phi + ((size_t)upy * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upy * P + q) * 4 + 2);
+        uy[0] = a.x, uy[1] = a.y, uy[2] = b.x, uy[3] = b.y;
+      }
+      perm(m, r[sl][0], r[sl][1], r[sl][2], r[sl][3]);
+      perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
+      perm(m, t[sl][0], t[sl][1], t[sl][2], t[sl][3]);
+      perm(m, ux[0], ux[1], ux[2], ux[3]);
+      perm(m, uy[0], uy[1], uy[2], uy[3]);
+      const double* cxy = p.cxy + (size_t)q * 8;
+      if (upx >= 0) {
+        r[sl][0] -= cxy[0] * ux[1] + cxy[1] * ux[3];
+        r[sl][2] -= cxy[2] * ux[1] + cxy[3] * ux[3];
+      }
+      if (upy >= 0) {
+        r[sl][0] -= cxy[4] * uy[2] + cxy[5] * uy[3];
+        r[sl][1] -= cxy[6] * uy[2] + cxy[7] * uy[3];
+      }
+    }
+    // ---- the sequential patch chain; K rows in octant order: Ko[m][pbeg + a][b]
+    const double* Kb = p.K + ((size_t)mt * P + pbeg) * p.kpad;
+    double kr[NS];
+    for (int a = 0; a < np; ++a) {
+      const int sl = a >> 5, src = a & 31;
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2) kr[s2] = qs[s2] >= 0 ? Kb[(size_t)(lane + 32 * s2) * p.kpad + a] : 0.0;
+      double dz[4] = {0.0, 0.0, 0.0, 0.0};
+      if (lane == src) {
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2)
+          if (s2 == sl) {
+            const int q = qs[s2];
+            const double sq = kr[s2];
+            double d[4], rr[4], n[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) d[i] = t[s2][i] - sq * zo[s2][i];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              rr[i] = r[s2][i] + (d[0] * p.N[i] + d[1] * p.N[4 + i] + d[2] * p.N[8 + i] + d[3] * p.N[12 + i]);
+            const double* B = p.BinvGS + ((size_t)mt * P + q) * 16;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              n[i] = B[4 * i] * rr[0] + B[4 * i + 1] * rr[1] + B[4 * i + 2] * rr[2] + B[4 * i + 3] * rr[3];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dz[i] = n[i] - zo[s2][i], zo[s2][i] = n[i];
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dz[i] = __shfl_sync(full, dz[i], src);
+#pragma unroll
+      for (int s2 = 0; s2 < NS; ++s2)
+        if (qs[s2] >= 0 && lane + 32 * s2 > a)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) t[s2][i] += kr[s2] * dz[i];
+      if (lane == 0) {  // physical-frame dz for the moment update
+        double e0 = dz[0], e1 = dz[1], e2 = dz[2], e3 = dz[3];
+        perm(m, e0, e1, e2, e3);
+        reinterpret_cast<double2*>(sdz)[2 * a] = make_double2(e0, e1);
+        reinterpret_cast<double2*>(sdz)[2 * a + 1] = make_double2(e2, e3);
+      }
+    }
+    // ---- publish the new iterate of this cell's patches, then the flag
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      const int q = qs[sl];
+      if (q < 0) continue;
+      perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
+      double* zb = p.phi + ((size_t)el * P + q) * 4;
+      st_cg2(zb, make_double2(zo[sl][0], zo[sl][1]));
+      st_cg2(zb + 2, make_double2(zo[sl][2], zo[sl][3]));
+    }
+    __syncwarp();
+    if (lane == 0) st_release(p.done + (size_t)oct * n_el + el, pass + 1);
+    // ---- running moments: mom += sum_a X_qa^T dz_a; Xo is [P][Hp] in octant order
+    double* mom_el = p.mom + (size_t)el * Hp * 4;
+    double* mw = const_cast<double*>(mom);
+    for (int h = lane; h < H; h += 32) {
+      double2 a0 = reinterpret_cast<const double2*>(mom)[2 * h], a1 = reinterpret_cast<const double2*>(mom)[2 * h + 1];
+      const double* xo = p.Xo + (size_t)pbeg * Hp + h;
+      int a = 0;
+      for (; a + 3 < np; a += 4) {
+        double x[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = __ldg(xo + (size_t)(a + k) * Hp);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double2 d0 = reinterpret_cast<const double2*>(sdz)[2 * (a + k)];
+          const double2 d1 = reinterpret_cast<const double2*>(sdz)[2 * (a + k) + 1];
+          a0.x += x[k] * d0.x, a0.y += x[k] * d0.y, a1.x += x[k] * d1.x, a1.y += x[k] * d1.y;
+        }
+      }
+      for (; a < np; ++a) {
+        const double x = __ldg(xo + (size_t)a * Hp);
+        const double2 d0 = reinterpret_cast<const double2*>(sdz)[2 * a], d1 = reinterpret_cast<const double2*>(sdz)[2 * a + 1];
+        a0.x += x * d0.x, a0.y += x * d0.y, a1.x += x * d1.x, a1.y += x * d1.y;
+      }
+      st_cg2(mom_el + h * 4, a0);
+      st_cg2(mom_el + h * 4 + 2, a1);
+      if (reuse) {
+        reinterpret_cast<double2*>(mw)[2 * h] = a0;
+        reinterpret_cast<double2*>(mw)[2 * h + 1] = a1;
+      }
+    }
+    if (!reuse) {
+      cur ^= 1;
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+  }
 }
 
-size_t gs_smem(int Hp, int kpad) { return sizeof(double) * GS_WARPS * (size_t(Hp) * 4 + size_t(kpad) * 4); }
+size_t gs_smem(int Hp, int kpad) { return sizeof(double) * GS_WARPS * (size_t(Hp) * 8 + size_t(kpad) * 4); }
 
 template <int NS>
 void launch_gs2(const CoarseGSParams& p, cudaStream_t s) {
