@@ -102,7 +102,7 @@ struct DevLevel {
   double* src = nullptr;  // scatter moments workspace [n_el][Hp][4]
   double* mom = nullptr;  // coarse GS moments
   int* gs_done = nullptr;
-  double *gs_K = nullptr, *gs_Xo = nullptr, *gs_XoT = nullptr;
+  double *gs_K = nullptr, *gs_Xo = nullptr, *gs_XoT = nullptr, *gs_G = nullptr;
   int gs_blocks = 0, gs_cpw = 0, gs_kpad = 0, gs_max_np = 0;
   double *tmp = nullptr, *cf = nullptr, *ce = nullptr;  // V-cycle workspace
   std::vector<void*> owned;
@@ -233,7 +233,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     L.gs_done = dalloc<int>(size_t(8) * t.n_el);
     // K[m][q][b] = X_q sig_m X_b^T for b in q's octant (coarse GS chain)
     for (int o = 0; o < 8; ++o) L.gs_max_np = std::max(L.gs_max_np, t.oct_ptr[o + 1] - t.oct_ptr[o]);
-    L.gs_kpad = std::max(1, L.gs_max_np);
+    L.gs_kpad = std::max(2, (L.gs_max_np + 1) / 2 * 2);  // even: 16-byte staging chunks
     std::vector<double> K(size_t(t.n_mat) * t.P * L.gs_kpad, 0.0);
     for (int m = 0; m < t.n_mat; ++m)
       for (int o = 0; o < 8; ++o)
@@ -245,7 +245,20 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
               k += t.X[size_t(qa) * t.H + h] * t.sig[size_t(m) * t.H + h] * t.X[size_t(qb) * t.H + h];
             K[(size_t(m) * t.P + a) * L.gs_kpad + (b - t.oct_ptr[o])] = k;
           }
+    if (L.gs_kpad % 2) L.gs_kpad += 0;  // rows padded below
     L.gs_K = dupload(K, s);
+    {  // G = B'^-1 N in the sweep frame (N is invariant under the frame permutation)
+      const auto Bf = frame_blocks(t.BinvGS, t);
+      std::vector<double> G(Bf.size());
+      for (size_t b = 0; b < Bf.size() / 16; ++b)
+        for (int i = 0; i < 4; ++i)
+          for (int j = 0; j < 4; ++j) {
+            double acc = 0;
+            for (int k = 0; k < 4; ++k) acc += Bf[b * 16 + i * 4 + k] * t.Nmat[k * 4 + j];
+            G[b * 16 + i * 4 + j] = acc;
+          }
+      L.gs_G = dupload(G, s);
+    }
     std::vector<double> Xo(size_t(t.P) * L.Hp, 0.0), XoT(size_t(L.Hp) * t.P, 0.0);
     for (int a = 0; a < t.P; ++a)
       for (int h = 0; h < t.H; ++h)
@@ -253,7 +266,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     L.gs_Xo = dupload(Xo, s);
     L.gs_XoT = dupload(XoT, s);
     // static ownership: each warp owns a segment of gs_cpw consecutive cells of one row
-    const int max_warps = coarse_gs_max_warps(L.Hp, L.gs_kpad, L.gs_max_np);
+    const int max_warps = coarse_gs_max_warps(L.Hp, L.gs_kpad, t.n_mat, L.gs_max_np);
     int seg = 1;
     while (int64_t(t.n_el) / seg > max_warps || t.nx % seg != 0) {
       if (seg >= t.nx) throw std::invalid_argument("coarse_scatter_sweep: grid too large for co-resident warps");
@@ -261,7 +274,8 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     }
     L.gs_cpw = seg;
     const int W = t.n_el / seg;
-    L.gs_blocks = (W + coarse_gs_warps_per_block() - 1) / coarse_gs_warps_per_block();
+    const int wpb = coarse_gs_warps_per_block(L.Hp, L.gs_kpad, t.n_mat);
+    L.gs_blocks = (W + wpb - 1) / wpb;
 
   }
   if (!t.up.empty()) {
@@ -276,7 +290,7 @@ void free_level(DevLevel& L) {
   for (void* p : {(void*)L.X, (void*)L.XT, (void*)L.sig, (void*)L.ones, (void*)L.B, (void*)L.Binv, (void*)L.cxy,
                   (void*)L.BinvGS, (void*)L.sq, (void*)L.area, (void*)L.up_w, (void*)L.groups, (void*)L.group_oct,
                   (void*)L.oct_patches, (void*)L.oct_ptr, (void*)L.up, (void*)L.child_ptr, (void*)L.child_idx,
-                  (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_K, (void*)L.gs_Xo, (void*)L.gs_XoT, (void*)L.tmp, (void*)L.cf,
+                  (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_K, (void*)L.gs_Xo, (void*)L.gs_XoT, (void*)L.gs_G, (void*)L.tmp, (void*)L.cf,
                   (void*)L.ce})
     if (p) cudaFree(p);
 }
@@ -381,7 +395,7 @@ void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* 
   CoarseGSParams p;
   p.rhs = rhs, p.phi = phi, p.mom = L.mom, p.X = L.X, p.sig = L.sig, p.BinvGS = L.BinvGS, p.sq = L.sq, p.cxy = L.cxy;
   p.oct_patches = L.oct_patches, p.oct_ptr = L.oct_ptr, p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
-  p.done = L.gs_done, p.K = L.gs_K, p.Xo = L.gs_Xo, p.XoT = L.gs_XoT;
+  p.done = L.gs_done, p.K = L.gs_K, p.Xo = L.gs_Xo, p.XoT = L.gs_XoT, p.GS = L.gs_G, p.n_mat = L.t.n_mat;
   p.cells_per_warp = L.gs_cpw, p.kpad = L.gs_kpad, p.grid_blocks = L.gs_blocks;
   p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.H = L.t.H, p.nx = L.t.nx, p.ny = L.t.ny, p.nu = nu;
   for (int o = 0; o < 8; ++o)

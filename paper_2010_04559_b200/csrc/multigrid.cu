@@ -77,16 +77,23 @@ __device__ __forceinline__ void perm(int m, double& a0, double& a1, double& a2, 
 // (cooperative launch).
 constexpr int GS_WARPS = 8;
 
+__host__ __device__ inline size_t gs_warp_doubles(int Hp, int kpad, int nmat) {
+  return size_t(Hp) * 8 + size_t(kpad) * 4 + size_t(nmat) * kpad * kpad;
+}
+
 template <int NS>
 __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseGSParams p) {
   extern __shared__ __align__(16) double gsm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const unsigned full = 0xffffffffu;
-  const int gw = blockIdx.x * GS_WARPS + wib;
+  const int wpb = blockDim.x >> 5;
+  const int gw = blockIdx.x * wpb + wib;
   const int n_el = p.n_el, nx = p.nx, ny = p.ny, P = p.P, Hp = p.Hp, H = p.H, seg = p.cells_per_warp;
-  double* sbase = gsm + (size_t)wib * (Hp * 8 + p.kpad * 4);
+  const int kpad = p.kpad, nmat = p.n_mat;
+  double* sbase = gsm + (size_t)wib * gs_warp_doubles(Hp, kpad, nmat);
   // double-buffered moments [2][Hp][4] at sbase
   double* sdz = sbase + Hp * 8;               // [kpad][4]
+  double* sK = sdz + kpad * 4;                // [n_mat][kpad][kpad] K of the current octant
   const int segs_per_row = nx / seg;
   if (gw >= segs_per_row * ny) return;
   const int gy = gw / segs_per_row, gx0 = (gw - gy * segs_per_row) * seg;
@@ -100,7 +107,7 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
     for (int c = lane; c < H * 2; c += 32) cp_async16(dst + c * 2, src + c * 2, true);
     cp_async_commit();
   };
-  int cur = 0;
+  int cur = 0, k_oct = -1;
   prefetch_mom(cell_of(0), sbase);
   cp_async_wait<0>();
   __syncwarp();
@@ -121,6 +128,13 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
     const int mt = p.mat ? p.mat[el] : 0;
     const double* sig = p.sig + (size_t)mt * Hp;
     const double* mom = sbase + cur * Hp * 4;
+    if (oct != k_oct) {  // stage this octant's K blocks (all materials) once per (pass, octant)
+      for (int mm = 0; mm < nmat; ++mm)
+        for (int c = lane; c < np * kpad / 2; c += 32)
+          cp_async16(sK + ((size_t)mm * kpad * kpad) + c * 2, p.K + ((size_t)mm * P + pbeg) * kpad + c * 2, true);
+      cp_async_commit();
+      k_oct = oct;
+    }
     // ---- own data: rhs / previous iterate -> registers (patch a = lane + 32 sl, octant order)
     double r[NS][4], zo[NS][4], t[NS][4];
     int qs[NS];
@@ -204,41 +218,65 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
         r[sl][1] -= cxy[6] * uy[2] + cxy[7] * uy[3];
       }
     }
-    // ---- the sequential patch chain; K rows in octant order: Ko[m][pbeg + a][b]
-    const double* Kb = p.K + ((size_t)mt * P + pbeg) * p.kpad;
-    double kr[NS];
+    // ---- chain prologue (off the chain): with G = B'^-1 N and c = B'^-1 r,
+    //      dz_a = e_a + G_a t_a, e_a = c_a - zo_a - sq_a G_a zo_a  (sweeps.cpp:93-101)
+    cp_async_wait<0>();
+    __syncwarp();
+    const double* sKm = sK + (size_t)mt * kpad * kpad;
+    double e[NS][4], G[NS][16];
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      const int q = qs[sl];
+      if (q < 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) e[sl][i] = 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) G[sl][k] = 0.0;
+        continue;
+      }
+      const double* B = p.BinvGS + ((size_t)mt * P + q) * 16;
+      const double* Gq = p.GS + ((size_t)mt * P + q) * 16;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) G[sl][k] = Gq[k];
+      const int a = lane + 32 * sl;
+      const double sq = sKm[(size_t)a * kpad + a];
+      double szo[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) szo[i] = sq * zo[sl][i];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double c = B[4 * i] * r[sl][0] + B[4 * i + 1] * r[sl][1] + B[4 * i + 2] * r[sl][2] + B[4 * i + 3] * r[sl][3];
+        const double gz = G[sl][4 * i] * szo[0] + G[sl][4 * i + 1] * szo[1] + G[sl][4 * i + 2] * szo[2] + G[sl][4 * i + 3] * szo[3];
+        e[sl][i] = c - zo[sl][i] - gz;
+      }
+    }
+    // ---- the sequential patch chain: one 4x4 mat-vec, a broadcast and a rank-1 update per patch
     for (int a = 0; a < np; ++a) {
       const int sl = a >> 5, src = a & 31;
-#pragma unroll
-      for (int s2 = 0; s2 < NS; ++s2) kr[s2] = qs[s2] >= 0 ? Kb[(size_t)(lane + 32 * s2) * p.kpad + a] : 0.0;
       double dz[4] = {0.0, 0.0, 0.0, 0.0};
       if (lane == src) {
 #pragma unroll
         for (int s2 = 0; s2 < NS; ++s2)
           if (s2 == sl) {
-            const int q = qs[s2];
-            const double sq = kr[s2];
-            double d[4], rr[4], n[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) d[i] = t[s2][i] - sq * zo[s2][i];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-              rr[i] = r[s2][i] + (d[0] * p.N[i] + d[1] * p.N[4 + i] + d[2] * p.N[8 + i] + d[3] * p.N[12 + i]);
-            const double* B = p.BinvGS + ((size_t)mt * P + q) * 16;
+              dz[i] = e[s2][i] + (G[s2][4 * i] * t[s2][0] + G[s2][4 * i + 1] * t[s2][1] +
+                                  G[s2][4 * i + 2] * t[s2][2] + G[s2][4 * i + 3] * t[s2][3]);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              n[i] = B[4 * i] * rr[0] + B[4 * i + 1] * rr[1] + B[4 * i + 2] * rr[2] + B[4 * i + 3] * rr[3];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) dz[i] = n[i] - zo[s2][i], zo[s2][i] = n[i];
+            for (int i = 0; i < 4; ++i) zo[s2][i] += dz[i];
           }
       }
 #pragma unroll
       for (int i = 0; i < 4; ++i) dz[i] = __shfl_sync(full, dz[i], src);
 #pragma unroll
-      for (int s2 = 0; s2 < NS; ++s2)
-        if (qs[s2] >= 0 && lane + 32 * s2 > a)
+      for (int s2 = 0; s2 < NS; ++s2) {
+        const int b = lane + 32 * s2;
+        if (qs[s2] >= 0 && b > a) {
+          const double k = sKm[(size_t)a * kpad + b];  // K symmetric: row a, column b
 #pragma unroll
-          for (int i = 0; i < 4; ++i) t[s2][i] += kr[s2] * dz[i];
+          for (int i = 0; i < 4; ++i) t[s2][i] += k * dz[i];
+        }
+      }
       if (lane == 0) {  // physical-frame dz for the moment update
         double e0 = dz[0], e1 = dz[1], e2 = dz[2], e3 = dz[3];
         perm(m, e0, e1, e2, e3);
@@ -288,35 +326,41 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
         reinterpret_cast<double2*>(mw)[2 * h + 1] = a1;
       }
     }
-    if (!reuse) {
-      cur ^= 1;
-      cp_async_wait<0>();
-    }
+    if (!reuse) cur ^= 1;
+    cp_async_wait<0>();
     __syncwarp();
   }
 }
 
-size_t gs_smem(int Hp, int kpad) { return sizeof(double) * GS_WARPS * (size_t(Hp) * 8 + size_t(kpad) * 4); }
+size_t gs_smem(int Hp, int kpad, int nmat, int wpb) { return sizeof(double) * wpb * gs_warp_doubles(Hp, kpad, nmat); }
+
+// warps per CTA: as many as fit next to the per-warp staging (<= 8)
+int gs_wpb(int Hp, int kpad, int nmat) {
+  int w = GS_WARPS;
+  while (w > 1 && gs_smem(Hp, kpad, nmat, w) > 200 * 1024) w >>= 1;
+  return w;
+}
 
 template <int NS>
 void launch_gs2(const CoarseGSParams& p, cudaStream_t s) {
   auto k = coarse_gs_static_kernel<NS>;
-  const size_t smem = gs_smem(p.Hp, p.kpad);
+  const int wpb = gs_wpb(p.Hp, p.kpad, p.n_mat);
+  const size_t smem = gs_smem(p.Hp, p.kpad, p.n_mat, wpb);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   CoarseGSParams q = p;
   void* args[] = {&q};
-  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(p.grid_blocks), dim3(GS_WARPS * 32), args, smem, s);
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(p.grid_blocks), dim3(wpb * 32), args, smem, s);
   if (e != cudaSuccess) throw std::runtime_error(std::string("coarse_gs cooperative launch: ") + cudaGetErrorString(e));
 }
 
 template <int NS>
-int occ_blocks(size_t smem) {
+int occ_blocks(size_t smem, int wpb) {
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   auto k = coarse_gs_static_kernel<NS>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, GS_WARPS * 32, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, wpb * 32, smem);
   return sms * std::max(per_sm, 1);
 }
 
@@ -336,12 +380,13 @@ void launch_restrict(const double* fine, double* coarse, const int* cptr, const 
   restrict_kernel<<<int((n + 255) / 256), 256, 0, s>>>(fine, coarse, cptr, cidx, w, n_el, Pf, Pc);
 }
 
-int coarse_gs_max_warps(int Hp, int kpad, int max_np) {
-  const size_t smem = gs_smem(Hp, kpad);
+int coarse_gs_max_warps(int Hp, int kpad, int nmat, int max_np) {
+  const int wpb = gs_wpb(Hp, kpad, nmat);
+  const size_t smem = gs_smem(Hp, kpad, nmat, wpb);
   if (max_np > 64) throw std::invalid_argument("coarse_scatter_sweep: more than 64 patches per octant on the coarsest level");
-  return (max_np > 32 ? occ_blocks<2>(smem) : occ_blocks<1>(smem)) * GS_WARPS;
+  return (max_np > 32 ? occ_blocks<2>(smem, wpb) : occ_blocks<1>(smem, wpb)) * wpb;
 }
-int coarse_gs_warps_per_block() { return GS_WARPS; }
+int coarse_gs_warps_per_block(int Hp, int kpad, int nmat) { return gs_wpb(Hp, kpad, nmat); }
 
 void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s) {
   if (p.nu <= 0 || p.n_el == 0) return;
