@@ -77,8 +77,10 @@ __device__ __forceinline__ void perm(int m, double& a0, double& a1, double& a2, 
 // (cooperative launch).
 constexpr int GS_WARPS = 8;
 
+// per-warp shared staging: moments [2][Hp][4], dz [kpad][4], K [nmat][kpad][kpad],
+// X of the octant [kpad][Hp+1] (odd row stride: conflict-free both ways), sigma [nmat][Hp]
 __host__ __device__ inline size_t gs_warp_doubles(int Hp, int kpad, int nmat) {
-  return size_t(Hp) * 8 + size_t(kpad) * 4 + size_t(nmat) * kpad * kpad;
+  return size_t(Hp) * 8 + size_t(kpad) * 4 + size_t(nmat) * kpad * kpad + size_t(kpad) * (Hp + 1) + size_t(nmat) * Hp;
 }
 
 template <int NS>
@@ -94,6 +96,10 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
   // double-buffered moments [2][Hp][4] at sbase
   double* sdz = sbase + Hp * 8;               // [kpad][4]
   double* sK = sdz + kpad * 4;                // [n_mat][kpad][kpad] K of the current octant
+  double* sX = sK + (size_t)nmat * kpad * kpad;  // [kpad][Hp+1] X rows of the current octant
+  double* sS = sX + (size_t)kpad * (Hp + 1);     // [n_mat][Hp] sigma
+  const int XS = Hp + 1;
+  for (int c = lane; c < nmat * Hp; c += 32) sS[c] = p.sig[c];
   const int segs_per_row = nx / seg;
   if (gw >= segs_per_row * ny) return;
   const int gy = gw / segs_per_row, gx0 = (gw - gy * segs_per_row) * seg;
@@ -126,15 +132,21 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
     const int upx = ifr > 0 ? el - sx : -1, upy = jf > 0 ? el - sy : -1;
     const int dnx = ifr < nx - 1 ? el + sx : -1, dny = jf < ny - 1 ? el + sy : -1;
     const int mt = p.mat ? p.mat[el] : 0;
-    const double* sig = p.sig + (size_t)mt * Hp;
     const double* mom = sbase + cur * Hp * 4;
-    if (oct != k_oct) {  // stage this octant's K blocks (all materials) once per (pass, octant)
+    if (oct != k_oct) {  // stage this octant's K blocks and X rows once per (pass, octant)
       for (int mm = 0; mm < nmat; ++mm)
         for (int c = lane; c < np * kpad / 2; c += 32)
           cp_async16(sK + ((size_t)mm * kpad * kpad) + c * 2, p.K + ((size_t)mm * P + pbeg) * kpad + c * 2, true);
+      for (int c = lane; c < np * H; c += 32) {
+        const int a = c / H, h = c - a * H;
+        cp_async8(sX + (size_t)a * XS + h, p.Xo + (size_t)(pbeg + a) * Hp + h, true);
+      }
       cp_async_commit();
+      cp_async_wait<0>();
+      __syncwarp();
       k_oct = oct;
     }
+    const double* sg = sS + (size_t)mt * Hp;
     // ---- own data: rhs / previous iterate -> registers (patch a = lane + 32 sl, octant order)
     double r[NS][4], zo[NS][4], t[NS][4];
     int qs[NS];
@@ -152,24 +164,24 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
         zo[sl][0] = za.x, zo[sl][1] = za.y, zo[sl][2] = zc.x, zo[sl][3] = zc.y;
       }
     }
-    // ---- t0_a = X_qa sig mom (off the critical path); XoT is [Hp][P] in octant order
+    // ---- t0_a = X_qa sig mom (off the critical path), all operands in shared memory
 #pragma unroll
     for (int sl = 0; sl < NS; ++sl) {
       if (qs[sl] < 0) continue;
-      const double* xt = p.XoT + pbeg + lane + 32 * sl;
+      const double* xr = sX + (size_t)(lane + 32 * sl) * XS;
       double u[4][4] = {};
       int h = 0;
       for (; h + 3 < H; h += 4) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          const double xs = __ldg(xt + (size_t)(h + k) * P) * sig[h + k];
+          const double xs = xr[h + k] * sg[h + k];
           const double2 ma = reinterpret_cast<const double2*>(mom)[2 * (h + k)];
           const double2 mb = reinterpret_cast<const double2*>(mom)[2 * (h + k) + 1];
           u[k][0] += xs * ma.x, u[k][1] += xs * ma.y, u[k][2] += xs * mb.x, u[k][3] += xs * mb.y;
         }
       }
       for (; h < H; ++h) {
-        const double xs = __ldg(xt + (size_t)h * P) * sig[h];
+        const double xs = xr[h] * sg[h];
         const double2 ma = reinterpret_cast<const double2*>(mom)[2 * h], mb = reinterpret_cast<const double2*>(mom)[2 * h + 1];
         u[0][0] += xs * ma.x, u[0][1] += xs * ma.y, u[0][2] += xs * mb.x, u[0][3] += xs * mb.y;
       }
@@ -301,12 +313,12 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
     double* mw = const_cast<double*>(mom);
     for (int h = lane; h < H; h += 32) {
       double2 a0 = reinterpret_cast<const double2*>(mom)[2 * h], a1 = reinterpret_cast<const double2*>(mom)[2 * h + 1];
-      const double* xo = p.Xo + (size_t)pbeg * Hp + h;
+      const double* xo = sX + h;
       int a = 0;
       for (; a + 3 < np; a += 4) {
         double x[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) x[k] = __ldg(xo + (size_t)(a + k) * Hp);
+        for (int k = 0; k < 4; ++k) x[k] = xo[(size_t)(a + k) * XS];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const double2 d0 = reinterpret_cast<const double2*>(sdz)[2 * (a + k)];
@@ -315,7 +327,7 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
         }
       }
       for (; a < np; ++a) {
-        const double x = __ldg(xo + (size_t)a * Hp);
+        const double x = xo[(size_t)a * XS];
         const double2 d0 = reinterpret_cast<const double2*>(sdz)[2 * a], d1 = reinterpret_cast<const double2*>(sdz)[2 * a + 1];
         a0.x += x * d0.x, a0.y += x * d0.y, a1.x += x * d1.x, a1.y += x * d1.y;
       }
