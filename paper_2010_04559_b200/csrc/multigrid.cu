@@ -197,9 +197,12 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
       if (lane == 1 && upy >= 0) f = d + upy, need = pass + 1;
       if (lane == 2 && pass > 0 && dnx >= 0) f = d + dnx, need = pass;
       if (lane == 3 && pass > 0 && dny >= 0) f = d + dny, need = pass;
-      bool ok = f == nullptr || ld_acquire(f) >= need;
+      // spin with relaxed loads (an acquire load invalidates L1 on every poll), then
+      // one acquire fence: the fence-based acquire pattern of the PTX memory model
+      bool ok = f == nullptr || ld_relaxed(f) >= need;
       while (!__all_sync(full, ok))
-        if (!ok) ok = ld_acquire(f) >= need;
+        if (!ok) ok = ld_relaxed(f) >= need;
+      fence_acq_rel();
     }
     // ---- upwind traces folded into r (sweeps.cpp:87-92), everything in the sweep frame
 #pragma unroll
@@ -262,31 +265,30 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
         e[sl][i] = c - zo[sl][i] - gz;
       }
     }
-    // ---- the sequential patch chain: one 4x4 mat-vec, a broadcast and a rank-1 update per patch
+    // ---- the sequential patch chain: one 4x4 mat-vec, a broadcast and a rank-1 update per
+    //      patch. Branch-free: every lane forms the candidate from its own slot, the owner's
+    //      value is broadcast.
     for (int a = 0; a < np; ++a) {
       const int sl = a >> 5, src = a & 31;
-      double dz[4] = {0.0, 0.0, 0.0, 0.0};
-      if (lane == src) {
+      double dz[4];
 #pragma unroll
-        for (int s2 = 0; s2 < NS; ++s2)
-          if (s2 == sl) {
+      for (int s2 = 0; s2 < NS; ++s2)
+        if (s2 == sl)  // warp-uniform
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-              dz[i] = e[s2][i] + (G[s2][4 * i] * t[s2][0] + G[s2][4 * i + 1] * t[s2][1] +
-                                  G[s2][4 * i + 2] * t[s2][2] + G[s2][4 * i + 3] * t[s2][3]);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) zo[s2][i] += dz[i];
-          }
-      }
+          for (int i = 0; i < 4; ++i)
+            dz[i] = e[s2][i] + (G[s2][4 * i] * t[s2][0] + G[s2][4 * i + 1] * t[s2][1] +
+                                G[s2][4 * i + 2] * t[s2][2] + G[s2][4 * i + 3] * t[s2][3]);
 #pragma unroll
       for (int i = 0; i < 4; ++i) dz[i] = __shfl_sync(full, dz[i], src);
 #pragma unroll
       for (int s2 = 0; s2 < NS; ++s2) {
         const int b = lane + 32 * s2;
-        if (qs[s2] >= 0 && b > a) {
-          const double k = sKm[(size_t)a * kpad + b];  // K symmetric: row a, column b
+        const bool mine = b == a, later = b > a && b < np;
+        const double k = sKm[(size_t)a * kpad + b];  // K symmetric: row a, column b
 #pragma unroll
-          for (int i = 0; i < 4; ++i) t[s2][i] += k * dz[i];
+        for (int i = 0; i < 4; ++i) {
+          zo[s2][i] = mine ? zo[s2][i] + dz[i] : zo[s2][i];
+          t[s2][i] = later ? t[s2][i] + k * dz[i] : t[s2][i];
         }
       }
       if (lane == 0) {  // physical-frame dz for the moment update

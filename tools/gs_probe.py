@@ -1,0 +1,16 @@
+"""Run the config-4 coarse Gauss-Seidel (one call, nu passes) for profiling."""
+import os, sys, time
+import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2010_04559_b200 import configs as cf, stamg
+k = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+nu = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+spec = cf.baseline_config(k)
+g = stamg.Context(spec)
+f = g.vec(0).fill(1e-3)
+phi = g.vec(0)
+for rep in range(2):
+    g.synchronize(); t = time.perf_counter()
+    g.coarse_scatter_sweep(f, nu, phi, level=0)
+    g.synchronize(); print(f"c{k} coarse_gs nu={nu}: {time.perf_counter()-t:.4f} s", flush=True)
+g.close()
