@@ -215,6 +215,37 @@ def run_b200(args, world, rank, local, dist):
     except Exception:
         pass
     extras = {}
+    # ---- extra: source-iteration throughput on the same workload (M2D source from the
+    # moments + in-place sweep + D2M moments [+ allreduce]), FP64-tensor roofline of the GEMMs
+    if not args.no_si:
+        g.source_iteration(psi, 1)  # warm
+        g.synchronize()
+        g.timing(True)
+        barrier(dist)
+        t0 = time.perf_counter()
+        g.source_iteration(psi, args.si_iters)
+        g.synchronize()
+        si_wall = allmax(dist, time.perf_counter() - t0)
+        d2m_ms, _ = g.timed("d2m")
+        m2d_ms, _ = g.timed("m2d")
+        sw_ms, _ = g.timed("sweep")
+        g.timing(False)
+        H = (spec.N + 1) ** 2
+        gemm_flop = 2.0 * H * P_local * 4 * n_el * args.si_iters  # per contraction, all iterations
+        dmma_peak, dfma_peak = g.fp64_peaks()
+        extras["source_iteration"] = {
+            "value": total_upd * args.si_iters / si_wall, "unit": UNIT, "iterations": args.si_iters,
+            "ms_per_iter": si_wall / args.si_iters * 1e3,
+            "kernel_ms_per_iter": {"d2m": d2m_ms / args.si_iters, "m2d": m2d_ms / args.si_iters,
+                                   "sweep": sw_ms / args.si_iters},
+            "gemm_roofline": {"bound": "fp64_tensor", "unit": "TFLOP/s",
+                              "d2m_achieved": gemm_flop / (d2m_ms * 1e-3) * 1e-12,
+                              "m2d_achieved": gemm_flop / (m2d_ms * 1e-3) * 1e-12,
+                              "peak": dmma_peak, "peak_kind": "measured DMMA m8n8k4 probe on this GPU",
+                              "dfma_peak": dfma_peak,
+                              "frac": (2 * gemm_flop / ((d2m_ms + m2d_ms) * 1e-3) * 1e-12) / dmma_peak,
+                              "flop_per_contraction": 2.0 * H * P_local * 4 * n_el},
+            "step": "D2M(psi) -> [allreduce] -> M2D (q + S psi) -> in-place sweep, full order N=%d" % spec.N}
     # ---- e2e through the host-buffer C-ABI entry point (pinned buffers)
     e2e = None
     if not args.no_e2e:
@@ -284,7 +315,9 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--n", type=int, default=None, help="cells per axis override (default: config 5 = 512)")
     ap.add_argument("--cpu-dirs", type=int, default=128)
-    ap.add_argument("--solve-configs", type=int, nargs="*", default=[1, 2])
+    ap.add_argument("--solve-configs", type=int, nargs="*", default=[1, 2, 3])
+    ap.add_argument("--si-iters", type=int, default=2)
+    ap.add_argument("--no-si", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
