@@ -105,6 +105,12 @@ struct DevLevel {
   double *gs_K = nullptr, *gs_Xo = nullptr, *gs_XoT = nullptr, *gs_G = nullptr;
   int gs_blocks = 0, gs_cpw = 0, gs_kpad = 0, gs_max_np = 0;
   double *tmp = nullptr, *cf = nullptr, *ce = nullptr;  // V-cycle workspace
+  // reflection-symmetry folded scatter (setup.hpp find_symmetry)
+  int fold_G = 0, fold_R = 0, fold_Rp = 0, fold_Hf = 0;
+  std::vector<int> fold_hoff;                 // [G+1] class column offsets
+  std::vector<std::vector<int>> fold_hs;      // per class: ascending original harmonics
+  double *Xf = nullptr, *XfT = nullptr, *sigf = nullptr, *foldbuf = nullptr;
+  int* orbit = nullptr;
   std::vector<void*> owned;
 };
 
@@ -282,7 +288,30 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     L.up = dupload(t.up, s), L.up_w = dupload(t.up_w, s);
     L.child_ptr = dupload(t.child_ptr, s), L.child_idx = dupload(t.child_idx, s);
   }
-  L.src = dalloc<double>(size_t(t.n_el) * L.Hp * 4);
+  size_t src_rows = L.Hp;
+  if (t.n_sym_axes > 0 && t.H >= 128 && c->world == 1) {  // fold only where the GEMMs are big
+    const int G = 1 << t.n_sym_axes, R = t.P / G;
+    L.fold_G = G, L.fold_R = R, L.fold_Rp = round_up(R, 64);
+    const int Rk = round_up(R, 16);
+    L.fold_hs.assign(G, {});
+    for (int h = 0; h < t.H; ++h) L.fold_hs[t.hclass[h]].push_back(h);
+    L.fold_hoff.assign(G + 1, 0);
+    for (int cl = 0; cl < G; ++cl) L.fold_hoff[cl + 1] = L.fold_hoff[cl] + round_up(std::max<int>(1, L.fold_hs[cl].size()), 64);
+    L.fold_Hf = L.fold_hoff[G];
+    std::vector<double> Xf(size_t(Rk) * L.fold_Hf, 0.0), XfT(size_t(L.fold_Hf) * L.fold_Rp, 0.0);
+    std::vector<double> sigf(size_t(t.n_mat) * L.fold_Hf, 0.0);
+    for (int cl = 0; cl < G; ++cl)
+      for (size_t j = 0; j < L.fold_hs[cl].size(); ++j) {
+        const int h = L.fold_hs[cl][j], col = L.fold_hoff[cl] + int(j);
+        for (int r = 0; r < R; ++r)
+          Xf[size_t(r) * L.fold_Hf + col] = XfT[size_t(col) * L.fold_Rp + r] = t.X[size_t(t.orbit[r * G]) * t.H + h];
+        for (int m = 0; m < t.n_mat; ++m) sigf[size_t(m) * L.fold_Hf + col] = t.sig[size_t(m) * t.H + h];
+      }
+    L.Xf = dupload(Xf, s), L.XfT = dupload(XfT, s), L.sigf = dupload(sigf, s);
+    L.orbit = dupload(t.orbit, s);
+    src_rows = std::max<size_t>(src_rows, L.fold_Hf);
+  }
+  L.src = dalloc<double>(size_t(t.n_el) * src_rows * 4);
   ck(cudaStreamSynchronize(s), "upload sync");
 }
 
@@ -290,7 +319,8 @@ void free_level(DevLevel& L) {
   for (void* p : {(void*)L.X, (void*)L.XT, (void*)L.sig, (void*)L.ones, (void*)L.B, (void*)L.Binv, (void*)L.cxy,
                   (void*)L.BinvGS, (void*)L.sq, (void*)L.area, (void*)L.up_w, (void*)L.groups, (void*)L.group_oct,
                   (void*)L.oct_patches, (void*)L.oct_ptr, (void*)L.up, (void*)L.child_ptr, (void*)L.child_idx,
-                  (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_K, (void*)L.gs_Xo, (void*)L.gs_XoT, (void*)L.gs_G, (void*)L.tmp, (void*)L.cf,
+                  (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_K, (void*)L.gs_Xo, (void*)L.gs_XoT, (void*)L.gs_G, (void*)L.Xf, (void*)L.XfT,
+                  (void*)L.sigf, (void*)L.foldbuf, (void*)L.orbit, (void*)L.tmp, (void*)L.cf,
                   (void*)L.ce})
     if (p) cudaFree(p);
 }
@@ -347,13 +377,73 @@ void op_m2d(stamg_ctx* c, DevLevel& L, int order, double scale, double beta, dou
   c->launches += 1;
 }
 
-// apply_scatter_into (scatter.cpp:110-135): y += scale * S_order phi
+// y = beta*y + scale * S_order phi (+ isotropic source): apply_scatter_into
+// (scatter.cpp:110-135) as D2M -> [allreduce] -> M2D. With a reflection
+// symmetry group G the patches are folded over their orbits (Walsh-Hadamard),
+// each harmonic parity class is one GEMM with K = P/|G|, and the result is
+// unfolded: the same algebra with |G| times fewer flops.
+void scatter_into(stamg_ctx* c, DevLevel& L, const double* phi, int order, double scale, double beta, double* y,
+                  const double* ext) {
+  if (order > L.t.order) throw std::invalid_argument("sigma_by_harmonic: max_order exceeds kernel order");
+  const int Hu = (order + 1) * (order + 1);
+  if (L.fold_G == 0) {
+    op_d2m(c, L, phi, order, L.src, L.sig, false);
+    op_allreduce(c, L.src, size_t(L.t.n_el) * L.Hp * 4);
+    op_m2d(c, L, order, scale, beta, y, ext);
+    return;
+  }
+  const int G = L.fold_G, R = L.fold_R, n_el = L.t.n_el;
+  if (!L.foldbuf) L.foldbuf = dalloc<double>(size_t(n_el) * L.t.P * 4);
+  const size_t cls = size_t(n_el) * R * 4;
+  {
+    Timed tm(c, "fold");
+    launch_fold(phi, L.foldbuf, L.orbit, n_el, L.t.P, R, G, c->stream);
+    ck_launch("fold");
+    c->launches += 1;
+  }
+  std::vector<int> hu(G, 0);
+  for (int cl = 0; cl < G; ++cl)
+    for (int h : L.fold_hs[cl]) hu[cl] += h < Hu ? 1 : 0;
+  for (int cl = 0; cl < G; ++cl) {
+    if (hu[cl] == 0) continue;
+    Timed tm(c, "d2m");
+    D2MParams p;
+    p.phi = L.foldbuf + cl * cls, p.src = L.src + size_t(L.fold_hoff[cl]) * 4, p.X = L.Xf + L.fold_hoff[cl];
+    p.sig = L.sigf + L.fold_hoff[cl], p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
+    p.n_el = n_el, p.P = R, p.Hp = L.fold_Hf, p.Hused = hu[cl];
+    for (int k = 0; k < 16; ++k) p.N[k] = L.t.Nmat[k];
+    launch_d2m(p, c->stream);
+    ck_launch("d2m");
+    c->launches += 1;
+  }
+  op_allreduce(c, L.src, size_t(n_el) * L.fold_Hf * 4);
+  for (int cl = 0; cl < G; ++cl) {
+    double* Yc = L.foldbuf + cl * cls;
+    if (hu[cl] == 0) {
+      launch_fill(Yc, 0.0, int64_t(cls), c->stream);
+      c->launches += 1;
+      continue;
+    }
+    Timed tm(c, "m2d");
+    M2DParams p;
+    p.src = L.src + size_t(L.fold_hoff[cl]) * 4, p.y = Yc, p.XT = L.XfT + size_t(L.fold_hoff[cl]) * L.fold_Rp;
+    p.n_el = n_el, p.P = R, p.Pp = L.fold_Rp, p.Hp = L.fold_Hf, p.Hused = hu[cl];
+    p.scale = 1.0, p.beta = 0.0, p.ext_q = nullptr, p.area = L.area;
+    for (int i = 0; i < 4; ++i) p.nsum[i] = c->nsum[i];
+    launch_m2d(p, c->stream);
+    ck_launch("m2d");
+    c->launches += 1;
+  }
+  Timed tm(c, "unfold");
+  launch_unfold(L.foldbuf, y, L.orbit, n_el, L.t.P, R, G, scale, beta, ext, L.area, c->nsum, c->stream);
+  ck_launch("unfold");
+  c->launches += 1;
+}
+
 void op_scatter(stamg_ctx* c, DevLevel& L, const double* phi, int order, double scale, double* y) {
   if (order > L.t.order) throw std::invalid_argument("sigma_by_harmonic: max_order exceeds kernel order");
   if (order < 0) return;
-  op_d2m(c, L, phi, order, L.src, L.sig, false);
-  op_allreduce(c, L.src, size_t(L.t.n_el) * L.Hp * 4);
-  op_m2d(c, L, order, scale, 1.0, y, nullptr);
+  scatter_into(c, L, phi, order, scale, 1.0, y, nullptr);
 }
 
 // apply_A_into (transport.cpp:96-101)
@@ -1057,9 +1147,7 @@ int stamg_source_iteration(stamg_ctx* c, stamg_vec* psi, int n_iter) {
     need(psi, O, "source_iteration");
     const int order = c->pb.spec.N;
     for (int it = 0; it < n_iter; ++it) {
-      op_d2m(c, O, psi->d, order, O.src, O.sig, false);
-      op_allreduce(c, O.src, size_t(O.t.n_el) * O.Hp * 4);
-      op_m2d(c, O, order, 1.0, 0.0, psi->d, c->q_el);
+      scatter_into(c, O, psi->d, order, 1.0, 0.0, psi->d, c->q_el);  // psi = q + S psi
       op_sweep(c, O, psi->d, psi->d);
     }
   });

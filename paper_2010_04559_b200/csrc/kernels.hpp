@@ -69,6 +69,13 @@ struct M2DParams {
 };
 void launch_m2d(const M2DParams& p, cudaStream_t s);
 
+// reflection-symmetry fold / unfold around the per-class moment GEMMs:
+// Phi[c][el][r][i] = sum_g chi_c(g) phi[el][orbit[r][g]][i];
+// y[el][orbit[r][g]][i] = beta*y + scale*sum_c chi_c(g) Y[c][el][r][i] (+ isotropic source)
+void launch_fold(const double* phi, double* Phi, const int* orbit, int n_el, int P, int R, int G, cudaStream_t s);
+void launch_unfold(const double* Y, double* y, const int* orbit, int n_el, int P, int R, int G, double scale,
+                   double beta, const double* ext_q, const double* area, const double* nsum, cudaStream_t s);
+
 // transfers (multigrid.cpp:100-136), Const basis
 void launch_prolong(const double* coarse, double* fine, const int* up, const double* w, int n_el, int Pf,
                     int Pc, bool add, cudaStream_t s);

@@ -213,7 +213,105 @@ __global__ void __launch_bounds__(kThreads) m2d_kernel(M2DParams p) {
 
 size_t gemm_smem() { return sizeof(double) * NSTAGE * kStageDoubles; }
 
+// Walsh-Hadamard transform over the G = 2^na members of an orbit (unnormalised):
+// out[c] = sum_g (-1)^popcount(c & g) in[g]
+template <int G>
+__device__ __forceinline__ void wht(double (&v)[G][4]) {
+#pragma unroll
+  for (int bit = 1; bit < G; bit <<= 1)
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (!(g & bit))
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double a = v[g][i], b = v[g | bit][i];
+          v[g][i] = a + b, v[g | bit][i] = a - b;
+        }
+}
+
+// Phi[c][el][r][i] = sum_g chi_c(g) phi[el][orbit[r][g]][i]
+template <int G>
+__global__ void fold_kernel(const double* __restrict__ phi, double* __restrict__ Phi, const int* __restrict__ orbit,
+                            int n_el, int P, int R) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n_el * R) return;
+  const int el = int(idx / R), r = int(idx - (int64_t)el * R);
+  double v[G][4];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const double2* b = reinterpret_cast<const double2*>(phi + ((size_t)el * P + orbit[r * G + g]) * 4);
+    const double2 a0 = b[0], a1 = b[1];
+    v[g][0] = a0.x, v[g][1] = a0.y, v[g][2] = a1.x, v[g][3] = a1.y;
+  }
+  wht<G>(v);
+#pragma unroll
+  for (int c = 0; c < G; ++c) {
+    double2* o = reinterpret_cast<double2*>(Phi + (((size_t)c * n_el + el) * R + r) * 4);
+    o[0] = make_double2(v[c][0], v[c][1]);
+    o[1] = make_double2(v[c][2], v[c][3]);
+  }
+}
+
+// y[el][orbit[r][g]][i] = beta*y + scale * sum_c chi_c(g) Y[c][el][r][i] (+ isotropic source)
+template <int G>
+__global__ void unfold_kernel(const double* __restrict__ Y, double* __restrict__ y, const int* __restrict__ orbit,
+                              int n_el, int P, int R, double scale, double beta, const double* __restrict__ ext_q,
+                              const double* __restrict__ area, double4 nsum) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n_el * R) return;
+  const int el = int(idx / R), r = int(idx - (int64_t)el * R);
+  double v[G][4];
+#pragma unroll
+  for (int c = 0; c < G; ++c) {
+    const double2* b = reinterpret_cast<const double2*>(Y + (((size_t)c * n_el + el) * R + r) * 4);
+    const double2 a0 = b[0], a1 = b[1];
+    v[c][0] = a0.x, v[c][1] = a0.y, v[c][2] = a1.x, v[c][3] = a1.y;
+  }
+  wht<G>(v);
+  constexpr double inv4pi = 0.07957747154594767;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int q = orbit[r * G + g];
+    double2* o = reinterpret_cast<double2*>(y + ((size_t)el * P + q) * 4);
+    double w0 = scale * v[g][0], w1 = scale * v[g][1], w2 = scale * v[g][2], w3 = scale * v[g][3];
+    if (ext_q) {
+      const double c = ext_q[el] * inv4pi * area[q];
+      w0 += c * nsum.x, w1 += c * nsum.y, w2 += c * nsum.z, w3 += c * nsum.w;
+    }
+    if (beta != 0.0) {
+      const double2 a0 = o[0], a1 = o[1];
+      w0 += beta * a0.x, w1 += beta * a0.y, w2 += beta * a1.x, w3 += beta * a1.y;
+    }
+    o[0] = make_double2(w0, w1);
+    o[1] = make_double2(w2, w3);
+  }
+}
+
 }  // namespace
+
+void launch_fold(const double* phi, double* Phi, const int* orbit, int n_el, int P, int R, int G, cudaStream_t s) {
+  const int64_t n = (int64_t)n_el * R;
+  const int blocks = int((n + 255) / 256);
+  switch (G) {
+    case 2: fold_kernel<2><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, P, R); break;
+    case 4: fold_kernel<4><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, P, R); break;
+    case 8: fold_kernel<8><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, P, R); break;
+    default: break;
+  }
+}
+
+void launch_unfold(const double* Y, double* y, const int* orbit, int n_el, int P, int R, int G, double scale,
+                   double beta, const double* ext_q, const double* area, const double* nsum, cudaStream_t s) {
+  const int64_t n = (int64_t)n_el * R;
+  const int blocks = int((n + 255) / 256);
+  const double4 ns = make_double4(nsum[0], nsum[1], nsum[2], nsum[3]);
+  switch (G) {
+    case 2: unfold_kernel<2><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns); break;
+    case 4: unfold_kernel<4><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns); break;
+    case 8: unfold_kernel<8><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns); break;
+    default: break;
+  }
+}
 
 void launch_d2m(const D2MParams& p, cudaStream_t s) {
   if (p.n_el == 0 || p.Hused == 0) return;

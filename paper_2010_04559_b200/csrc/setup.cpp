@@ -468,7 +468,74 @@ LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool 
         inverse4(Bp, &L.BinvGS[(size_t(m) * P + q) * 16]);
       }
   }
+  find_symmetry(L, t);
   return L;
+}
+
+void find_symmetry(LevelTables& L, const SphereTree& t) {
+  // key of a patch: its three lattice vertices, sorted
+  using Key = std::array<std::int64_t, 9>;
+  auto key_of = [](std::array<std::int64_t, 9> f) {
+    std::array<std::array<std::int64_t, 3>, 3> v{{{f[0], f[1], f[2]}, {f[3], f[4], f[5]}, {f[6], f[7], f[8]}}};
+    std::sort(v.begin(), v.end());
+    Key k;
+    for (int i = 0; i < 3; ++i)
+      for (int r = 0; r < 3; ++r) k[3 * i + r] = v[i][r];
+    return k;
+  };
+  std::map<Key, int> pos;
+  for (int q = 0; q < L.P; ++q) pos[key_of(t.flat[L.leaf_id[q]])] = q;
+  std::vector<std::vector<int>> mirror;  // per symmetric axis: q -> mirror q
+  L.n_sym_axes = 0;
+  for (int axis = 0; axis < 3; ++axis) {
+    std::vector<int> mq(L.P, -1);
+    bool ok = L.P_global == L.P;  // a rank's slice is not closed under reflections
+    for (int q = 0; ok && q < L.P; ++q) {
+      auto f = t.flat[L.leaf_id[q]];
+      for (int v = 0; v < 3; ++v) f[3 * v + axis] = -f[3 * v + axis];
+      auto it = pos.find(key_of(f));
+      if (it == pos.end()) ok = false;
+      else mq[q] = it->second;
+    }
+    if (!ok) continue;
+    L.sym_axes[L.n_sym_axes++] = axis;
+    mirror.push_back(mq);
+  }
+  const int G = 1 << L.n_sym_axes;
+  L.orbit.clear();
+  if (L.n_sym_axes == 0) return;
+  // representatives: patches whose octant bits on the symmetric axes are all 0
+  for (int q = 0; q < L.P; ++q) {
+    bool rep = true;
+    for (int k = 0; k < L.n_sym_axes; ++k)
+      if ((L.octant[q] >> L.sym_axes[k]) & 1) rep = false;
+    if (!rep) continue;
+    for (int g = 0; g < G; ++g) {
+      int m = q;
+      for (int k = 0; k < L.n_sym_axes; ++k)
+        if ((g >> k) & 1) m = mirror[k][m];
+      L.orbit.push_back(m);
+    }
+  }
+  if (int(L.orbit.size()) != L.P) {  // every patch must lie in exactly one orbit
+    L.orbit.clear();
+    L.n_sym_axes = 0;
+    return;
+  }
+  // harmonic parity classes: Y_{n,o} under x: (-1)^m (cos) / -(-1)^m (sin); y: +1 (cos) / -1 (sin);
+  // z: (-1)^(n+m); class bit k set when odd under sym_axes[k]
+  L.hclass.assign(L.H, 0);
+  for (int n = 0; n <= L.order; ++n)
+    for (int o = -n; o <= n; ++o) {
+      const int m = o < 0 ? -o : o;
+      const int px = o >= 0 ? (m & 1) : ((m + 1) & 1);
+      const int py = o >= 0 ? 0 : 1;
+      const int pz = (n + m) & 1;
+      const int par[3] = {px, py, pz};
+      int c = 0;
+      for (int k = 0; k < L.n_sym_axes; ++k) c |= par[L.sym_axes[k]] << k;
+      L.hclass[n * n + n + o] = c;
+    }
 }
 
 std::vector<LevelTables> build_hierarchy(const Problem& pb, const SphereTree& fine, int nr, int nlev) {

@@ -64,7 +64,16 @@ struct LevelTables {
   std::vector<double> up_w;           // [P] Const transfer block B = [1]
   std::vector<int> child_ptr, child_idx;  // CSR children of each coarse patch, ascending
   double Nmat[16];                    // spatial mass matrix
+  // ---- reflection symmetry of the scatter operator (exact algebra: X[g(q)][h] = chi_h(g) X[q][h])
+  int n_sym_axes = 0;                 // |G| = 2^n_sym_axes
+  int sym_axes[3] = {0, 0, 0};
+  std::vector<int> orbit;             // [R][|G|] patch index of member g of orbit r (r = representative)
+  std::vector<int> hclass;            // [H] parity class of each harmonic under the symmetric axes
 };
+
+// Reflections (x, y, z) that map the leaf set onto itself; fills n_sym_axes,
+// sym_axes, orbit and hclass (an empty orbit table means no folding).
+void find_symmetry(LevelTables& L, const SphereTree& tree);
 
 struct Problem {
   stamg_problem spec{};
