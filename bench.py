@@ -231,7 +231,9 @@ def run_b200(args, world, rank, local, dist):
         sw_ms, _ = g.timed("sweep")
         g.timing(False)
         H = (spec.N + 1) ** 2
-        gemm_flop = 2.0 * H * P_local * 4 * n_el * args.si_iters  # per contraction, all iterations
+        gemm_flop = 2.0 * H * P_local * 4 * n_el * args.si_iters  # per contraction, all iterations (algorithmic)
+        fold_g = max(1, int(g.table("fold")[0]))  # reflection-symmetry fold: executed = algorithmic / |G|
+        exe_flop = gemm_flop / fold_g
         dmma_peak, dfma_peak = g.fp64_peaks()
         extras["source_iteration"] = {
             "value": total_upd * args.si_iters / si_wall, "unit": UNIT, "iterations": args.si_iters,
@@ -239,13 +241,18 @@ def run_b200(args, world, rank, local, dist):
             "kernel_ms_per_iter": {"d2m": d2m_ms / args.si_iters, "m2d": m2d_ms / args.si_iters,
                                    "sweep": sw_ms / args.si_iters},
             "gemm_roofline": {"bound": "fp64_tensor", "unit": "TFLOP/s",
-                              "d2m_achieved": gemm_flop / (d2m_ms * 1e-3) * 1e-12,
-                              "m2d_achieved": gemm_flop / (m2d_ms * 1e-3) * 1e-12,
+                              "d2m_achieved": exe_flop / (d2m_ms * 1e-3) * 1e-12,
+                              "m2d_achieved": exe_flop / (m2d_ms * 1e-3) * 1e-12,
                               "peak": dmma_peak, "peak_kind": "measured DMMA m8n8k4 probe on this GPU",
                               "dfma_peak": dfma_peak,
-                              "frac": (2 * gemm_flop / ((d2m_ms + m2d_ms) * 1e-3) * 1e-12) / dmma_peak,
-                              "flop_per_contraction": 2.0 * H * P_local * 4 * n_el},
-            "step": "D2M(psi) -> [allreduce] -> M2D (q + S psi) -> in-place sweep, full order N=%d" % spec.N}
+                              "frac": (2 * exe_flop / ((d2m_ms + m2d_ms) * 1e-3) * 1e-12) / dmma_peak,
+                              "achieved_basis": "executed flops (algorithmic / fold group size)",
+                              "fold_group_size": fold_g,
+                              "algorithmic_flop_per_contraction": 2.0 * H * P_local * 4 * n_el,
+                              "algorithmic_equivalent_tflops": 2 * gemm_flop / ((d2m_ms + m2d_ms) * 1e-3) * 1e-12},
+            "kernel_ms_per_iter_fold": {k: g.timed(k)[0] / args.si_iters for k in ("fold", "unfold")},
+            "step": "fold -> D2M(psi) -> [allreduce] -> M2D -> unfold (q + S psi) -> in-place sweep, full "
+                    "order N=%d" % spec.N}
     # ---- e2e through the host-buffer C-ABI entry point (pinned buffers)
     e2e = None
     if not args.no_e2e:

@@ -149,15 +149,17 @@ double time_kernel(K kern, int blocks, int threads, int iters, cudaStream_t s) {
 // address c (mode 0, streaming) or to cell-major / group-minor order (mode 1,
 // the sweep's pattern: consecutive chunks 'stride' chunks apart)
 __global__ void chunk_rw_kernel(double* x, int64_t n_chunks, int64_t stride, int mode) {
+  // mode 1: 128-byte chunks; mode k>1: chunks of k*128 bytes (k*8 lanes)
+  const int lanes = 8 * (mode > 1 ? mode : 1);
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t c = tid >> 3;
+  const int64_t c = tid / lanes;
   if (c >= n_chunks) return;
   int64_t dst = c;
-  if (mode == 1) {
+  if (mode >= 1) {
     const int64_t per = n_chunks / stride;
     dst = (c % per) * stride + c / per;
   }
-  double2* p = reinterpret_cast<double2*>(x + dst * 16) + (tid & 7);
+  double2* p = reinterpret_cast<double2*>(x + dst * 2 * lanes) + (tid % lanes);
   double2 v = *p;
   v.x += 1.0, v.y += 1.0;
   *p = v;
@@ -166,8 +168,9 @@ __global__ void chunk_rw_kernel(double* x, int64_t n_chunks, int64_t stride, int
 }  // namespace
 
 double bench_chunk_rw_gbs(double* buf, int64_t n_doubles, int64_t stride_chunks, int mode, cudaStream_t s) {
-  const int64_t n_chunks = n_doubles / 16;
-  const int64_t threads = n_chunks * 8;
+  const int lanes = 8 * (mode > 1 ? mode : 1);
+  const int64_t n_chunks = n_doubles / (2 * lanes);
+  const int64_t threads = n_chunks * lanes;
   const int blocks = int((threads + 255) / 256);
   chunk_rw_kernel<<<blocks, 256, 0, s>>>(buf, n_chunks, stride_chunks, mode);
   cudaEvent_t e0, e1;

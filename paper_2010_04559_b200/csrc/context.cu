@@ -1155,10 +1155,12 @@ int stamg_source_iteration(stamg_ctx* c, stamg_vec* psi, int n_iter) {
 
 int stamg_get_table(stamg_ctx* c, int level, const char* name, double* out, int64_t cap, int64_t* n) {
   return guard([&] {
-    const LevelTables& t = level_of(c, level).t;
+    const DevLevel& L = level_of(c, level);
+    const LevelTables& t = L.t;
     std::vector<double> v;
     const std::string nm(name);
-    if (nm == "X") v = t.X;
+    if (nm == "fold") v = {double(L.fold_G), double(L.fold_R), double(L.fold_Hf)};
+    else if (nm == "X") v = t.X;
     else if (nm == "B") v = t.B;
     else if (nm == "Binv") v = t.Binv;
     else if (nm == "C") v = t.C;

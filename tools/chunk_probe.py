@@ -5,7 +5,7 @@ from paper_2010_04559_b200 import configs as cf, stamg
 spec = cf.baseline_config(5, 128)
 g = stamg.Context(spec, build_hierarchy=False)
 v = g.vec().fill(0.0)
-for mode, stride in [(0, 1), (1, 2048), (1, 256), (1, 32), (1, 8)]:
+for mode, stride in [(0, 1), (1, 2048), (2, 1024), (4, 512), (8, 256), (16, 128)]:
     out = C.c_double()
     stamg._check(stamg.lib().stamg_bench_chunk_rw(g.h, v.h, C.c_int64(stride), mode, C.byref(out)))
-    print(f"mode={mode} stride_chunks={stride} GB/s={out.value:.1f}", flush=True)
+    print(f"chunk={128 * max(mode, 1)}B {'stream' if mode == 0 else 'cell-major'} stride={stride} GB/s={out.value:.1f}", flush=True)
