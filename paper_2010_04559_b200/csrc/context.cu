@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -98,6 +99,8 @@ struct DevLevel {
   double *X = nullptr, *XT = nullptr, *sig = nullptr, *ones = nullptr, *B = nullptr, *Binv = nullptr;
   double *cxy = nullptr, *BinvGS = nullptr, *sq = nullptr, *area = nullptr, *up_w = nullptr;
   int *groups = nullptr, *group_oct = nullptr, *oct_patches = nullptr, *oct_ptr = nullptr;
+  int *groups8 = nullptr, *group8_oct = nullptr;
+  double2* sweep_top = nullptr;  // 8-direction sweep: strip-boundary trace scratch
   int *up = nullptr, *child_ptr = nullptr, *child_idx = nullptr;
   double* src = nullptr;  // scatter moments workspace [n_el][Hp][4]
   double* mom = nullptr;  // coarse GS moments
@@ -231,6 +234,10 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
   L.cxy = dupload(cxyf, s);
   L.area = dupload(t.area, s);
   L.groups = dupload(t.groups, s), L.group_oct = dupload(t.group_oct, s);
+  if (!t.groups8.empty() && t.nx >= 36 && t.ny >= 32 && std::getenv("STAMG_SWEEP_DIRS4") == nullptr) {
+    L.groups8 = dupload(t.groups8, s), L.group8_oct = dupload(t.group8_oct, s);
+    L.sweep_top = dalloc<double2>(t.group8_oct.size() * 8 * size_t(t.nx));
+  }
   L.oct_patches = dupload(t.oct_patches, s), L.oct_ptr = dupload(t.oct_ptr, s);
   if (!t.BinvGS.empty()) {
     L.BinvGS = dupload(frame_blocks(t.BinvGS, t), s);
@@ -319,7 +326,7 @@ void free_level(DevLevel& L) {
   for (void* p : {(void*)L.X, (void*)L.XT, (void*)L.sig, (void*)L.ones, (void*)L.B, (void*)L.Binv, (void*)L.cxy,
                   (void*)L.BinvGS, (void*)L.sq, (void*)L.area, (void*)L.up_w, (void*)L.groups, (void*)L.group_oct,
                   (void*)L.oct_patches, (void*)L.oct_ptr, (void*)L.up, (void*)L.child_ptr, (void*)L.child_idx,
-                  (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_K, (void*)L.gs_Xo, (void*)L.gs_XoT, (void*)L.gs_G, (void*)L.Xf, (void*)L.XfT,
+                  (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_K, (void*)L.gs_Xo, (void*)L.gs_XoT, (void*)L.gs_G, (void*)L.Xf, (void*)L.XfT, (void*)L.groups8, (void*)L.group8_oct, (void*)L.sweep_top,
                   (void*)L.sigf, (void*)L.foldbuf, (void*)L.orbit, (void*)L.tmp, (void*)L.cf,
                   (void*)L.ce})
     if (p) cudaFree(p);
@@ -462,6 +469,10 @@ void op_sweep(stamg_ctx* c, DevLevel& L, const double* rhs, double* z, const dou
   Timed tm(c, "sweep");
   SweepParams p;
   p.g = geom(c, L);
+  if (L.sweep_top) {
+    p.dirs = 8, p.top = L.sweep_top;
+    p.g.groups = L.groups8, p.g.group_oct = L.group8_oct, p.g.n_groups = int(L.t.group8_oct.size());
+  }
   p.rhs = rhs, p.z = z, p.base = base, p.Binv = L.Binv, p.cxy = L.cxy;
   launch_sweep(p, c->stream);
   ck_launch("sweep");

@@ -20,7 +20,9 @@ struct GroupGeom {
 // standard_sweep (sweeps.cpp:20-42): z = L^{-1} rhs, or z = base + L^{-1} rhs
 // when base != nullptr (the smoother's phi += r). z may alias rhs or base.
 struct SweepParams {
-  GroupGeom g;
+  GroupGeom g;                   // groups of g-width directions (4, or 8 when dirs == 8)
+  int dirs = 4;
+  double2* top = nullptr;        // dirs == 8: [n_groups][8][nx] strip-boundary trace scratch
   const double* rhs = nullptr;
   const double* base = nullptr;
   double* z = nullptr;

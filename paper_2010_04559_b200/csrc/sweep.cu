@@ -25,25 +25,34 @@ namespace {
 
 constexpr int NST = 4;
 
-template <int R, bool MULTI, bool ACCUM>
-__global__ void __launch_bounds__(4 * R) sweep_kernel(SweepParams p) {
-  constexpr int NT = 4 * R;
+// DIRS directions x R rows per CTA (DIRS*R = 256 threads). thread = (dir, row):
+// dir = tid % DIRS, row = tid / DIRS. With DIRS = 8 a cell's 8 directions are
+// one 256-byte run (better DRAM efficiency than 128 B), and the strip-boundary
+// traces go through an L2-resident global scratch (TOPG) instead of shared
+// memory so the CTA still fits 3 per SM.
+template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG>
+__global__ void __launch_bounds__(DIRS * R) sweep_kernel(SweepParams p) {
+  constexpr int NT = DIRS * R;
   constexpr int NW = NT / 32;
+  constexpr int RPW = 32 / DIRS;  // rows per warp
   extern __shared__ __align__(16) double smem[];
   double* st_rhs = smem;
   double* st_base = st_rhs + NST * NT * 4;
-  double2* top = reinterpret_cast<double2*>(st_base + (ACCUM ? NST * NT * 4 : 0));
-  double2* xw = top + 4 * p.g.nx;
-  double* sB = reinterpret_cast<double*>(xw + 2 * NW * 4);
+  double* after_base = st_base + (ACCUM ? NST * NT * 4 : 0);
+  double2* st_top = reinterpret_cast<double2*>(after_base);                       // TOPG: [NST][DIRS]
+  double2* top = reinterpret_cast<double2*>(after_base) + (TOPG ? NST * DIRS : 0);  // !TOPG: [DIRS][nx]
+  double2* xw = top + (TOPG ? 0 : DIRS * p.g.nx);
+  double* sB = reinterpret_cast<double*>(xw + 2 * NW * DIRS);
 
-  const int tid = threadIdx.x, dir = tid & 3, r = tid >> 2, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, dir = tid % DIRS, r = tid / DIRS, lane = tid & 31, warp = tid >> 5;
   const int grp = blockIdx.x;
-  const int q = p.g.groups[grp * 4 + dir];
+  const int q = p.g.groups[grp * DIRS + dir];
   const int oct = p.g.group_oct[grp];
   const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
   const int nx = p.g.nx, ny = p.g.ny, P = p.g.P;
   const bool qok = q >= 0;
   const int qq = qok ? q : 0;
+  double2* gtop = p.top + (size_t)grp * DIRS * nx;  // TOPG scratch of this group
 
   double cx[4], cy[4];
 #pragma unroll
@@ -53,10 +62,10 @@ __global__ void __launch_bounds__(4 * R) sweep_kernel(SweepParams p) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) Bi[k] = p.Binv[qq * 16 + k];
   } else {
-    for (int idx = tid; idx < p.g.n_mat * 64; idx += NT) {
-      const int m = idx >> 6, d = (idx >> 4) & 3, k = idx & 15;
-      const int qd = p.g.groups[grp * 4 + d];
-      sB[(m * 4 + d) * 17 + k] = qd >= 0 ? p.Binv[((size_t)m * P + qd) * 16 + k] : 0.0;
+    for (int idx = tid; idx < p.g.n_mat * DIRS * 16; idx += NT) {
+      const int m = idx / (DIRS * 16), d = (idx / 16) % DIRS, k = idx & 15;
+      const int qd = p.g.groups[grp * DIRS + d];
+      sB[(m * DIRS + d) * 17 + k] = qd >= 0 ? p.Binv[((size_t)m * P + qd) * 16 + k] : 0.0;
     }
   }
 
@@ -73,7 +82,8 @@ __global__ void __launch_bounds__(4 * R) sweep_kernel(SweepParams p) {
   };
   auto issue = [&](int t) {
     int el = 0;
-    const bool ok = locate(t - r, el);
+    const int k = t - r;
+    const bool ok = locate(k, el);
     const double* src = p.rhs + (ok ? ((size_t)el * P + qq) * 4 : 0);
     double* dst = st_rhs + ((t % NST) * NT + tid) * 4;
     cp_async16(dst, src, ok);
@@ -83,6 +93,13 @@ __global__ void __launch_bounds__(4 * R) sweep_kernel(SweepParams p) {
       double* db = st_base + ((t % NST) * NT + tid) * 4;
       cp_async16(db, sb, ok);
       cp_async16(db + 2, sb + 2, ok);
+    }
+    if constexpr (TOPG) {  // row 0 of strip s >= 1 needs the trace row R-1 left in the scratch
+      if (r == 0) {
+        const bool tk = k >= nx && k < nk;
+        const int i = tk ? k % nx : 0;
+        cp_async16(st_top + (t % NST) * DIRS + dir, gtop + (size_t)dir * nx + i, tk);
+      }
     }
   };
 #pragma unroll
@@ -101,10 +118,17 @@ __global__ void __launch_bounds__(4 * R) sweep_kernel(SweepParams p) {
     const int k = t - r;
     const bool kin = k >= 0 && k < nk;
     const int s = kin ? k / nx : 0, i = kin ? k - s * nx : 0;
-    double2 ty = shfl_up2(typrev, 4);
-    if (lane < 4) {
-      if (warp == 0) ty = (s == 0 || !kin) ? make_double2(0.0, 0.0) : top[dir * nx + i];
-      else ty = xw[((t - 1) & 1) * NW * 4 + (warp - 1) * 4 + dir];
+    double2 ty;
+    ty.x = __shfl_up_sync(0xffffffffu, typrev.x, DIRS);
+    ty.y = __shfl_up_sync(0xffffffffu, typrev.y, DIRS);
+    if (lane < DIRS) {
+      if (warp == 0) {
+        if (s == 0 || !kin) ty = make_double2(0.0, 0.0);
+        else if constexpr (TOPG) ty = st_top[(t % NST) * DIRS + dir];
+        else ty = top[dir * nx + i];
+      } else {
+        ty = xw[((t - 1) & 1) * NW * DIRS + (warp - 1) * DIRS + dir];
+      }
     }
     double2 tyout = make_double2(0.0, 0.0);
     int el = 0;
@@ -125,7 +149,7 @@ __global__ void __launch_bounds__(4 * R) sweep_kernel(SweepParams p) {
       if constexpr (MULTI) {
         const int mt = p.g.mat[el];
 #pragma unroll
-        for (int kk = 0; kk < 16; ++kk) Bm[kk] = sB[(mt * 4 + dir) * 17 + kk];
+        for (int kk = 0; kk < 16; ++kk) Bm[kk] = sB[(mt * DIRS + dir) * 17 + kk];
         B = Bm;
       }
       double z0 = B[0] * r0 + B[1] * r1 + B[2] * r2 + B[3] * r3;
@@ -145,37 +169,41 @@ __global__ void __launch_bounds__(4 * R) sweep_kernel(SweepParams p) {
       reinterpret_cast<double2*>(out)[0] = make_double2(z0, z1);
       reinterpret_cast<double2*>(out)[1] = make_double2(z2, z3);
     }
-    if ((lane & 28) == 28) xw[(t & 1) * NW * 4 + warp * 4 + dir] = tyout;
-    if (r == R - 1 && kin) top[dir * nx + i] = tyout;
+    if (lane >= 32 - DIRS) xw[(t & 1) * NW * DIRS + warp * DIRS + dir] = tyout;
+    if (r == R - 1 && kin) {
+      if constexpr (TOPG) reinterpret_cast<double2*>(gtop)[(size_t)dir * nx + i] = tyout;
+      else top[dir * nx + i] = tyout;
+    }
     typrev = tyout;
     __syncthreads();
   }
   cp_async_wait<0>();
+  (void)RPW;
 }
 
-template <int R, bool MULTI, bool ACCUM>
+template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG>
 void launch_t(const SweepParams& p, cudaStream_t s) {
-  constexpr int NT = 4 * R;
-  size_t smem = sizeof(double) * NST * NT * 4 * (ACCUM ? 2 : 1) + sizeof(double2) * (4 * p.g.nx + 2 * (NT / 32) * 4) +
-                (MULTI ? sizeof(double) * p.g.n_mat * 4 * 17 : 0);
-  auto k = sweep_kernel<R, MULTI, ACCUM>;
+  constexpr int NT = DIRS * R;
+  size_t smem = sizeof(double) * NST * NT * 4 * (ACCUM ? 2 : 1) +
+                sizeof(double2) * ((TOPG ? NST * DIRS : DIRS * p.g.nx) + 2 * (NT / 32) * DIRS) +
+                (MULTI ? sizeof(double) * p.g.n_mat * DIRS * 17 : 0);
+  auto k = sweep_kernel<DIRS, R, MULTI, ACCUM, TOPG>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<p.g.n_groups, NT, smem, s>>>(p);
 }
 
-template <int R>
+template <int DIRS, int R, bool TOPG>
 void launch_r(const SweepParams& p, cudaStream_t s) {
   const bool multi = p.g.n_mat > 1;
   const bool acc = p.base != nullptr;
-  if (multi) acc ? launch_t<R, true, true>(p, s) : launch_t<R, true, false>(p, s);
-  else acc ? launch_t<R, false, true>(p, s) : launch_t<R, false, false>(p, s);
+  if (multi) acc ? launch_t<DIRS, R, true, true, TOPG>(p, s) : launch_t<DIRS, R, true, false, TOPG>(p, s);
+  else acc ? launch_t<DIRS, R, false, true, TOPG>(p, s) : launch_t<DIRS, R, false, false, TOPG>(p, s);
 }
 
 }  // namespace
 
 int sweep_rows_for(int nx, int ny) {
-  // rows per CTA: the chained wavefront needs R <= nx; 64 keeps 256 threads
-  // per CTA and several CTAs per SM.
+  // rows per CTA for 4-direction groups: the chained wavefront needs R <= nx
   int R = 64;
   while (R > 8 && (R > nx || R > ny)) R >>= 1;
   return R;
@@ -183,13 +211,18 @@ int sweep_rows_for(int nx, int ny) {
 
 void launch_sweep(const SweepParams& p, cudaStream_t s) {
   if (p.g.n_groups == 0) return;
-  const int R = sweep_rows_for(p.g.nx, p.g.ny);
   if (p.g.nx < 8) throw std::invalid_argument("sweep: nx must be >= 8 on the B200 path");
+  if (p.dirs == 8) {  // 8-direction groups, R = 32, traces across strips through the L2 scratch
+    if (p.g.nx < 32 + NST || p.g.ny < 32 || !p.top) throw std::invalid_argument("sweep: 8-direction groups need nx, ny >= 36");
+    launch_r<8, 32, true>(p, s);
+    return;
+  }
+  const int R = sweep_rows_for(p.g.nx, p.g.ny);
   switch (R) {
-    case 64: launch_r<64>(p, s); break;
-    case 32: launch_r<32>(p, s); break;
-    case 16: launch_r<16>(p, s); break;
-    default: launch_r<8>(p, s); break;
+    case 64: launch_r<4, 64, false>(p, s); break;
+    case 32: launch_r<4, 32, false>(p, s); break;
+    case 16: launch_r<4, 16, false>(p, s); break;
+    default: launch_r<4, 8, false>(p, s); break;
   }
 }
 

@@ -179,3 +179,22 @@ def test_errors(pair, stamg):
             g.standard_sweep(bad, g.vec())
     with pytest.raises(stamg.InvalidArgument):
         g.apply_scatter_into(g.vec(), spec.N + 1, 1.0, g.vec())
+
+
+@pytest.mark.parametrize("k", [2, 3])
+def test_sweep_8dir_groups(orc, stamg, k):
+    """nx >= 36 with octant counts divisible by 8 selects the 8-direction sweep
+    (L2 strip-boundary scratch); check it against the oracle, in-place, with a
+    base vector (smoother) and with two materials (config 3)."""
+    spec = cf.baseline_config(k, 40)
+    o, g = orc.Oracle(spec), stamg.Context(spec)
+    rhs = rnd(o.size(), 21)
+    z = g.vec()
+    g.standard_sweep(g.vec(data=rhs), z)
+    assert rel(z.numpy(), o.sweep(rhs)) < 1e-12
+    nlev, nr = o.levels()
+    l = nlev - 1
+    f, phi0 = rnd(o.size(l), 22), rnd(o.size(l), 23)
+    phi = g.vec(l, phi0)
+    g.smoother_step(g.vec(l, f), nr, phi, level=l)
+    assert rel(phi.numpy(), o.smoother(f, nr, phi0, level=l)) < 1e-12
