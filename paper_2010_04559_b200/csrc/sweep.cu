@@ -31,7 +31,8 @@ constexpr int NST = 4;
 // traces go through an L2-resident global scratch (TOPG) instead of shared
 // memory so the CTA still fits 3 per SM.
 template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG>
-__global__ void __launch_bounds__(DIRS * R) sweep_kernel(SweepParams p) {
+__global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepParams p) {
+  // TOPG (8-direction) variant: 4 CTAs/SM (<= 64 registers), B^-1 read from shared memory
   constexpr int NT = DIRS * R;
   constexpr int NW = NT / 32;
   constexpr int RPW = 32 / DIRS;  // rows per warp
@@ -57,8 +58,9 @@ __global__ void __launch_bounds__(DIRS * R) sweep_kernel(SweepParams p) {
   double cx[4], cy[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) cx[k] = p.cxy[qq * 8 + k], cy[k] = p.cxy[qq * 8 + 4 + k];
+  constexpr bool BSMEM = MULTI || TOPG;
   double Bi[16];
-  if constexpr (!MULTI) {
+  if constexpr (!BSMEM) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) Bi[k] = p.Binv[qq * 16 + k];
   } else {
@@ -146,8 +148,8 @@ __global__ void __launch_bounds__(DIRS * R) sweep_kernel(SweepParams p) {
       r1 -= cy[2] * ty.x + cy[3] * ty.y;
       const double* B = Bi;
       double Bm[16];
-      if constexpr (MULTI) {
-        const int mt = p.g.mat[el];
+      if constexpr (BSMEM) {
+        const int mt = MULTI ? p.g.mat[el] : 0;
 #pragma unroll
         for (int kk = 0; kk < 16; ++kk) Bm[kk] = sB[(mt * DIRS + dir) * 17 + kk];
         B = Bm;
@@ -186,7 +188,7 @@ void launch_t(const SweepParams& p, cudaStream_t s) {
   constexpr int NT = DIRS * R;
   size_t smem = sizeof(double) * NST * NT * 4 * (ACCUM ? 2 : 1) +
                 sizeof(double2) * ((TOPG ? NST * DIRS : DIRS * p.g.nx) + 2 * (NT / 32) * DIRS) +
-                (MULTI ? sizeof(double) * p.g.n_mat * DIRS * 17 : 0);
+                ((MULTI || TOPG) ? sizeof(double) * p.g.n_mat * DIRS * 17 : 0);
   auto k = sweep_kernel<DIRS, R, MULTI, ACCUM, TOPG>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<p.g.n_groups, NT, smem, s>>>(p);
