@@ -130,7 +130,7 @@ def baseline_config(k: int, n: Optional[int] = None) -> ProblemSpec:
         return ProblemSpec(name="c4", nx=nn, ny=nn, angular_kind=ANGULAR_CONE, angular_level=4,
                            cone_levels=2, cone_half_angle_deg=15.0, N=N,
                            sigma_t=np.array([200.0]), moments=hg_moments(N, 200.0, 0.9999, 0.99)[None],
-                           beam=BEAM_CONE_X0, nr=8, n_levels=4, restart=20)
+                           beam=BEAM_CONE_X0, nr=8, n_levels=4, restart=12)
     if k == 5:
         nn = n or 512
         N = 32
