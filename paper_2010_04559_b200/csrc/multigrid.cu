@@ -267,7 +267,8 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
     }
     // ---- the sequential patch chain: one 4x4 mat-vec, a broadcast and a rank-1 update per
     //      patch. Branch-free: every lane forms the candidate from its own slot, the owner's
-    //      value is broadcast.
+    //      value is broadcast; dz stays in the sweep frame (shared memory, for zo and the
+    //      moment update after the chain).
     for (int a = 0; a < np; ++a) {
       const int sl = a >> 5, src = a & 31;
       double dz[4];
@@ -283,20 +284,22 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
 #pragma unroll
       for (int s2 = 0; s2 < NS; ++s2) {
         const int b = lane + 32 * s2;
-        const bool mine = b == a, later = b > a && b < np;
-        const double k = sKm[(size_t)a * kpad + b];  // K symmetric: row a, column b
+        const double k = b > a ? sKm[(size_t)a * kpad + b] : 0.0;  // K symmetric: row a, column b
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          zo[s2][i] = mine ? zo[s2][i] + dz[i] : zo[s2][i];
-          t[s2][i] = later ? t[s2][i] + k * dz[i] : t[s2][i];
-        }
+        for (int i = 0; i < 4; ++i) t[s2][i] += k * dz[i];
       }
-      if (lane == 0) {  // physical-frame dz for the moment update
-        double e0 = dz[0], e1 = dz[1], e2 = dz[2], e3 = dz[3];
-        perm(m, e0, e1, e2, e3);
-        reinterpret_cast<double2*>(sdz)[2 * a] = make_double2(e0, e1);
-        reinterpret_cast<double2*>(sdz)[2 * a + 1] = make_double2(e2, e3);
+      if (lane == 0) {
+        reinterpret_cast<double2*>(sdz)[2 * a] = make_double2(dz[0], dz[1]);
+        reinterpret_cast<double2*>(sdz)[2 * a + 1] = make_double2(dz[2], dz[3]);
       }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int sl = 0; sl < NS; ++sl) {
+      const int a = lane + 32 * sl;
+      if (qs[sl] < 0) continue;
+      const double2 d0 = reinterpret_cast<const double2*>(sdz)[2 * a], d1 = reinterpret_cast<const double2*>(sdz)[2 * a + 1];
+      zo[sl][0] += d0.x, zo[sl][1] += d0.y, zo[sl][2] += d1.x, zo[sl][3] += d1.y;
     }
     // ---- publish the new iterate of this cell's patches, then the flag
 #pragma unroll
@@ -314,7 +317,10 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
     double* mom_el = p.mom + (size_t)el * Hp * 4;
     double* mw = const_cast<double*>(mom);
     for (int h = lane; h < H; h += 32) {
+      // view the physical moments [i] in the sweep frame (index i ^ m) so frame dz applies directly
       double2 a0 = reinterpret_cast<const double2*>(mom)[2 * h], a1 = reinterpret_cast<const double2*>(mom)[2 * h + 1];
+      if (m & 2) { const double2 u = a0; a0 = a1; a1 = u; }
+      if (m & 1) { double u = a0.x; a0.x = a0.y; a0.y = u; u = a1.x; a1.x = a1.y; a1.y = u; }
       const double* xo = sX + h;
       int a = 0;
       for (; a + 3 < np; a += 4) {
@@ -333,6 +339,8 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
         const double2 d0 = reinterpret_cast<const double2*>(sdz)[2 * a], d1 = reinterpret_cast<const double2*>(sdz)[2 * a + 1];
         a0.x += x * d0.x, a0.y += x * d0.y, a1.x += x * d1.x, a1.y += x * d1.y;
       }
+      if (m & 1) { double u = a0.x; a0.x = a0.y; a0.y = u; u = a1.x; a1.x = a1.y; a1.y = u; }
+      if (m & 2) { const double2 u = a0; a0 = a1; a1 = u; }
       st_cg2(mom_el + h * 4, a0);
       st_cg2(mom_el + h * 4 + 2, a1);
       if (reuse) {
