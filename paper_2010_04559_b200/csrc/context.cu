@@ -356,6 +356,10 @@ void op_apply_L(stamg_ctx* c, DevLevel& L, const double* x, double* y, double al
   Timed tm(c, "apply_L");
   ApplyLParams p;
   p.g = geom(c, L);
+  if (L.groups8) {
+    p.dirs = 8;
+    p.g.groups = L.groups8, p.g.group_oct = L.group8_oct, p.g.n_groups = int(L.t.group8_oct.size());
+  }
   p.x = x, p.y = y, p.f = f, p.alpha = alpha, p.beta = beta, p.B = L.B, p.cxy = L.cxy;
   launch_apply_L(p, c->stream);
   ck_launch("apply_L");

@@ -33,7 +33,8 @@ void launch_sweep(const SweepParams& p, cudaStream_t s);
 
 // apply_L_into (transport.cpp:66-88): y = alpha * L x + beta * f
 struct ApplyLParams {
-  GroupGeom g;
+  GroupGeom g;                  // 4-direction groups, or 8 when dirs == 8 (row-walk kernel)
+  int dirs = 4;
   const double* x = nullptr;
   const double* f = nullptr;
   double* y = nullptr;

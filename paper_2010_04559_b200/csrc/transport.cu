@@ -80,10 +80,115 @@ __global__ void __launch_bounds__(256) apply_L_kernel(ApplyLParams p) {
   reinterpret_cast<double2*>(yb)[1] = make_double2(y2, y3);
 }
 
+// Row-walk variant for 8-direction groups: CTA = 8 directions x 32 rows of one
+// 32-row strip; thread (dir, row) walks its row in upwind order. The x-upwind
+// block is the thread's previous one (registers), the y-upwind block comes from
+// the row below by a shuffle (lanes of the warp's first row load it), so each x
+// block is read from DRAM once, in 256-byte runs per (cell, 8 directions).
+template <bool MULTI, bool WITH_F>
+__global__ void __launch_bounds__(256) apply_L_rows_kernel(ApplyLParams p) {
+  constexpr int DIRS = 8, R = 32;
+  const int tid = threadIdx.x, dir = tid % DIRS, r = tid / DIRS, lane = tid & 31;
+  const int grp = blockIdx.y, strip = blockIdx.x;
+  const int q = p.g.groups[grp * DIRS + dir];
+  const int oct = p.g.group_oct[grp];
+  const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
+  const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
+  const int nx = p.g.nx, ny = p.g.ny, P = p.g.P;
+  const int jf = strip * R + r;
+  const bool rowok = jf < ny && q >= 0;
+  const int qq = q >= 0 ? q : 0;
+  const int gy = yneg ? ny - 1 - (jf < ny ? jf : 0) : (jf < ny ? jf : 0);
+  const int gyd = jf > 0 ? (yneg ? gy + 1 : gy - 1) : gy;  // y-upwind row (lanes of the warp's first row)
+  const double* cxy = p.cxy + (size_t)qq * 8;
+  const double c0 = cxy[0], c1 = cxy[1], c2 = cxy[2], c3 = cxy[3], c4 = cxy[4], c5 = cxy[5], c6 = cxy[6], c7 = cxy[7];
+  const double* Bq = p.B + (size_t)qq * 16;
+  double Bl[16];
+  if constexpr (!MULTI) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Bl[k] = Bq[k];
+  }
+  const bool first_row_of_warp = lane < DIRS;
+  double px1 = 0.0, px3 = 0.0;  // x-upwind trace (frame dofs 1, 3)
+  auto load = [&](int el) {
+    const double2* b = reinterpret_cast<const double2*>(p.x + ((size_t)el * P + qq) * 4);
+    const double2 a = __ldg(b), c = __ldg(b + 1);
+    double v0 = a.x, v1 = a.y, v2 = c.x, v3 = c.y;
+    return make_double4(v0, v1, v2, v3);
+  };
+  int gx = xneg ? nx - 1 : 0;
+  double4 cur = rowok ? load(gy * nx + gx) : make_double4(0, 0, 0, 0);
+  double4 low = (rowok && first_row_of_warp && jf > 0) ? load(gyd * nx + gx) : make_double4(0, 0, 0, 0);
+  for (int i = 0; i < nx; ++i) {
+    const int el = gy * nx + gx;
+    const int gxn = xneg ? gx - 1 : gx + 1;
+    double4 nxt = make_double4(0, 0, 0, 0), nlow = make_double4(0, 0, 0, 0);
+    if (i + 1 < nx && rowok) {  // prefetch the next cell
+      nxt = load(gy * nx + gxn);
+      if (first_row_of_warp && jf > 0) nlow = load(gyd * nx + gxn);
+    }
+    double x0 = cur.x, x1 = cur.y, x2 = cur.z, x3 = cur.w;
+    to_frame(m, x0, x1, x2, x3);
+    // y-upwind block: the row below's current block (shuffle), its frame dofs {2,3}
+    double u2 = __shfl_up_sync(0xffffffffu, x2, DIRS), u3 = __shfl_up_sync(0xffffffffu, x3, DIRS);
+    if (first_row_of_warp) {
+      double l0 = low.x, l1 = low.y, l2 = low.z, l3 = low.w;
+      to_frame(m, l0, l1, l2, l3);
+      u2 = l2, u3 = l3;
+    }
+    if (rowok) {
+      const double* B = Bl;
+      double Bm[16];
+      if constexpr (MULTI) {
+        const double* Bs = p.B + ((size_t)p.g.mat[el] * P + qq) * 16;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) Bm[k] = Bs[k];
+        B = Bm;
+      }
+      double y0 = B[0] * x0 + B[1] * x1 + B[2] * x2 + B[3] * x3;
+      double y1 = B[4] * x0 + B[5] * x1 + B[6] * x2 + B[7] * x3;
+      double y2 = B[8] * x0 + B[9] * x1 + B[10] * x2 + B[11] * x3;
+      double y3 = B[12] * x0 + B[13] * x1 + B[14] * x2 + B[15] * x3;
+      if (i > 0) {
+        y0 += c0 * px1 + c1 * px3;
+        y2 += c2 * px1 + c3 * px3;
+      }
+      if (jf > 0) {
+        y0 += c4 * u2 + c5 * u3;
+        y1 += c6 * u2 + c7 * u3;
+      }
+      from_frame(m, y0, y1, y2, y3);
+      double* yb = p.y + ((size_t)el * P + q) * 4;
+      if constexpr (WITH_F) {
+        const double2* fb = reinterpret_cast<const double2*>(p.f + ((size_t)el * P + q) * 4);
+        const double2 fa = fb[0], fc = fb[1];
+        y0 = p.alpha * y0 + p.beta * fa.x;
+        y1 = p.alpha * y1 + p.beta * fa.y;
+        y2 = p.alpha * y2 + p.beta * fc.x;
+        y3 = p.alpha * y3 + p.beta * fc.y;
+      } else if (p.alpha != 1.0) {
+        y0 *= p.alpha, y1 *= p.alpha, y2 *= p.alpha, y3 *= p.alpha;
+      }
+      reinterpret_cast<double2*>(yb)[0] = make_double2(y0, y1);
+      reinterpret_cast<double2*>(yb)[1] = make_double2(y2, y3);
+    }
+    px1 = x1, px3 = x3;
+    cur = nxt, low = nlow;
+    gx = gxn;
+  }
+}
+
 }  // namespace
 
 void launch_apply_L(const ApplyLParams& p, cudaStream_t s) {
   if (p.g.n_groups == 0) return;
+  if (p.dirs == 8) {
+    dim3 grid((p.g.ny + 31) / 32, p.g.n_groups);
+    const bool multi = p.g.n_mat > 1, wf = p.f != nullptr && p.beta != 0.0;
+    if (multi) wf ? apply_L_rows_kernel<true, true><<<grid, 256, 0, s>>>(p) : apply_L_rows_kernel<true, false><<<grid, 256, 0, s>>>(p);
+    else wf ? apply_L_rows_kernel<false, true><<<grid, 256, 0, s>>>(p) : apply_L_rows_kernel<false, false><<<grid, 256, 0, s>>>(p);
+    return;
+  }
   const int cells = p.g.nx * p.g.ny;
   dim3 grid((cells + kCellsPerBlock - 1) / kCellsPerBlock, p.g.n_groups);
   const bool multi = p.g.n_mat > 1, wf = p.f != nullptr && p.beta != 0.0;

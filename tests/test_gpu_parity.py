@@ -192,6 +192,9 @@ def test_sweep_8dir_groups(orc, stamg, k):
     z = g.vec()
     g.standard_sweep(g.vec(data=rhs), z)
     assert rel(z.numpy(), o.sweep(rhs)) < 1e-12
+    y = g.vec()
+    g.apply_L_into(g.vec(data=rhs), y)  # row-walk apply_L of the 8-direction groups
+    assert rel(y.numpy(), o.apply_L(rhs)) < 1e-13
     nlev, nr = o.levels()
     l = nlev - 1
     f, phi0 = rnd(o.size(l), 22), rnd(o.size(l), 23)
