@@ -234,7 +234,12 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
   L.cxy = dupload(cxyf, s);
   L.area = dupload(t.area, s);
   L.groups = dupload(t.groups, s), L.group_oct = dupload(t.group_oct, s);
-  if (!t.groups8.empty() && t.nx >= 36 && t.ny >= 32 && std::getenv("STAMG_SWEEP_DIRS4") == nullptr) {
+  // 8-direction groups (256-byte runs) only where they still give >= 2 CTAs per SM;
+  // small levels keep the 4-direction kernels (twice the CTAs, latency-bound anyway)
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  if (!t.groups8.empty() && t.nx >= 36 && t.ny >= 32 && int(t.group8_oct.size()) >= 2 * sms &&
+      std::getenv("STAMG_SWEEP_DIRS4") == nullptr) {
     L.groups8 = dupload(t.groups8, s), L.group8_oct = dupload(t.group8_oct, s);
     L.sweep_top = dalloc<double2>(t.group8_oct.size() * 8 * size_t(t.nx));
   }

@@ -183,10 +183,12 @@ def test_errors(pair, stamg):
 
 @pytest.mark.parametrize("k", [2, 3])
 def test_sweep_8dir_groups(orc, stamg, k):
-    """nx >= 36 with octant counts divisible by 8 selects the 8-direction sweep
-    (L2 strip-boundary scratch); check it against the oracle, in-place, with a
-    base vector (smoother) and with two materials (config 3)."""
+    """nx >= 36, octant counts divisible by 8 and >= 2 groups of 8 per SM select
+    the 8-direction sweep / row-walk apply_L (L2 strip-boundary scratch); check
+    them against the oracle, in-place, with a base vector (smoother) and with two
+    materials (config 3). Angular level 5 (8192 directions) on a 40^2 grid."""
     spec = cf.baseline_config(k, 40)
+    spec.angular_level, spec.nr, spec.n_levels = 5, min(spec.nr if spec.nr >= 0 else 4, 4), 2
     o, g = orc.Oracle(spec), stamg.Context(spec)
     rhs = rnd(o.size(), 21)
     z = g.vec()
