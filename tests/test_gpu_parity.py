@@ -188,7 +188,7 @@ def test_sweep_8dir_groups(orc, stamg, k):
     them against the oracle, in-place, with a base vector (smoother) and with two
     materials (config 3). Angular level 5 (8192 directions) on a 40^2 grid."""
     spec = cf.baseline_config(k, 40)
-    spec.angular_level, spec.nr, spec.n_levels = 5, min(spec.nr if spec.nr >= 0 else 4, 4), 2
+    spec.angular_level, spec.nr, spec.n_levels = 5, min(spec.nr if spec.nr >= 0 else 4, 4), 3
     o, g = orc.Oracle(spec), stamg.Context(spec)
     rhs = rnd(o.size(), 21)
     z = g.vec()
