@@ -164,10 +164,9 @@ def run_reference(args, world, rank, dist):
     print(json.dumps(line), flush=True)
 
 
-def run_b200(args, world, rank, local, dist):
-    from paper_2010_04559_b200 import configs as cf
-    from paper_2010_04559_b200 import stamg
-    spec = cf.baseline_config(5, args.n)
+def make_context(stamg, spec, world, rank, local, dist, build_hierarchy):
+    """One context per rank; ranks > 1 share a fresh NCCL communicator (unique id
+    from rank 0, broadcast over torch.distributed)."""
     nccl_id = None
     if world > 1:
         import torch
@@ -175,8 +174,15 @@ def run_b200(args, world, rank, local, dist):
         t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
         dist.broadcast(t, 0)
         nccl_id = bytes(t.cpu().tolist())
-    g = stamg.Context(spec, device=local if world > 1 else 0, build_hierarchy=False, rank=rank, world=world,
-                      nccl_id=nccl_id)
+    return stamg.Context(spec, device=local if world > 1 else 0, build_hierarchy=build_hierarchy, rank=rank,
+                         world=world, nccl_id=nccl_id)
+
+
+def run_b200(args, world, rank, local, dist):
+    from paper_2010_04559_b200 import configs as cf
+    from paper_2010_04559_b200 import stamg
+    spec = cf.baseline_config(5, args.n)
+    g = make_context(stamg, spec, world, rank, local, dist, False)
     n_el, P_local, S, _ = g.layout()
     upd_local = n_el * P_local
     psi = g.vec().fill(1.0)
@@ -271,21 +277,24 @@ def run_b200(args, world, rank, local, dist):
                "d2h_bytes_per_step": n * 8, "steps": k_e2e,
                "api": "stamg_sweep_host (include/stamg_b200.h), pinned host buffers"}
     g.close()
-    # ---- extra: GMRES + AMG solve wall time (config 2) and a config-1 solve
-    if rank == 0 and world == 1 and not args.no_solve:
+    # ---- extra: GMRES + AMG solve wall time to 1e-8 from a device-resident b
+    # (directions sharded over the ranks, coarsest MG level replicated)
+    if not args.no_solve:
         solves = {}
         for k in args.solve_configs:
             sp = cf.baseline_config(k)
             t0 = time.perf_counter()
-            gs = stamg.Context(sp)
+            gs = make_context(stamg, sp, world, rank, local, dist, True)
             setup = time.perf_counter() - t0
             b = gs.rhs()
             gs.solve(b, "gmres", "mg")  # warm
             gs.synchronize()
+            barrier(dist)
             t0 = time.perf_counter()
             x, rep = gs.solve(b, "gmres", "mg")
             gs.synchronize()
-            solves[f"c{k}"] = {"wall_s": time.perf_counter() - t0, "setup_s": setup, "iterations": rep["iterations"],
+            wall = allmax(dist, time.perf_counter() - t0)
+            solves[f"c{k}"] = {"wall_s": wall, "setup_s": setup, "iterations": rep["iterations"],
                                "final_residual": rep["final_residual"], "converged": rep["converged"],
                                "method": "GMRES(%d) right-preconditioned by one V(1,1) angular MG cycle" % sp.restart}
             gs.close()

@@ -95,8 +95,14 @@ int stamg_nccl_unique_id(void* out128);
 
 /* Layout of a level (layout.hpp:16-32): out4 = {n_el, n_patch, S, D}. */
 int stamg_layout(stamg_ctx* ctx, int level, int out4[4]);
-/* patch range [q_begin, q_end) owned by this rank at `level` */
+/* patch range [q_begin, q_end) owned by this rank at `level` (first/last+1 of the list) */
 int stamg_patch_range(stamg_ctx* ctx, int level, int* q_begin, int* q_end);
+/* leaf-order positions of this rank's patches at `level` (vectors hold them in this order) */
+int stamg_patch_list(stamg_ctx* ctx, int level, int* out, int cap, int* n);
+/* host only, no device: the partition rank `rank` of `world` gets (level 0 = coarsest MG
+ * level, replicated) and, for level >= 1, each patch's parent position in the coarser
+ * level's list held by the same rank */
+int stamg_partition(const stamg_problem* prob, int rank, int world, int level, int* qpos, int* up, int cap, int* n);
 int stamg_n_levels(stamg_ctx* ctx, int* n_levels, int* nr);
 /* scatter order of a level's coupling table (ops.kernel.N) */
 int stamg_level_order(stamg_ctx* ctx, int level, int* order);

@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <unordered_map>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -95,6 +96,7 @@ struct UniqueId {
 struct DevLevel {
   LevelTables t;
   int64_t n = 0;  // vector length n_el * P * 4
+  bool sharded = false;  // holds only this rank's directions (scatter moments need an allreduce)
   int Hp = 0, Pk = 0, Pp = 0;
   double *X = nullptr, *XT = nullptr, *sig = nullptr, *ones = nullptr, *B = nullptr, *Binv = nullptr;
   double *cxy = nullptr, *BinvGS = nullptr, *sq = nullptr, *area = nullptr, *up_w = nullptr;
@@ -404,7 +406,7 @@ void scatter_into(stamg_ctx* c, DevLevel& L, const double* phi, int order, doubl
   const int Hu = (order + 1) * (order + 1);
   if (L.fold_G == 0) {
     op_d2m(c, L, phi, order, L.src, L.sig, false);
-    op_allreduce(c, L.src, size_t(L.t.n_el) * L.Hp * 4);
+    if (L.sharded) op_allreduce(c, L.src, size_t(L.t.n_el) * L.Hp * 4);
     op_m2d(c, L, order, scale, beta, y, ext);
     return;
   }
@@ -432,7 +434,7 @@ void scatter_into(stamg_ctx* c, DevLevel& L, const double* phi, int order, doubl
     ck_launch("d2m");
     c->launches += 1;
   }
-  op_allreduce(c, L.src, size_t(n_el) * L.fold_Hf * 4);
+  if (L.sharded) op_allreduce(c, L.src, size_t(n_el) * L.fold_Hf * 4);
   for (int cl = 0; cl < G; ++cl) {
     double* Yc = L.foldbuf + cl * cls;
     if (hu[cl] == 0) {
@@ -532,9 +534,12 @@ void op_restrict(stamg_ctx* c, int l, const double* fine, double* coarse) {
   launch_restrict(fine, coarse, F.child_ptr, F.child_idx, F.up_w, F.t.n_el, F.t.P, Cl.t.P, c->stream);
   ck_launch("restrict");
   c->launches += 1;
+  // into the replicated coarsest level: each rank filled only its own parents
+  // (zeros elsewhere); the sum over ranks is exact
+  if (F.sharded && !Cl.sharded) op_allreduce(c, coarse, size_t(Cl.n));
 }
 
-double op_dot(stamg_ctx* c, const double* x, const double* y, int64_t n);
+double op_dot(stamg_ctx* c, const double* x, const double* y, int64_t n, bool sharded);
 
 // lmg_vcycle (multigrid.cpp:138-170)
 void op_vcycle(stamg_ctx* c, int l, const double* f, double* phi) {
@@ -543,11 +548,11 @@ void op_vcycle(stamg_ctx* c, int l, const double* f, double* phi) {
   if (l == 0) {
     if (spec.coarse_tol > 0) {
       if (!L.tmp) L.tmp = dalloc<double>(L.n);
-      const double fnorm = std::sqrt(op_dot(c, f, f, L.n));
+      const double fnorm = std::sqrt(op_dot(c, f, f, L.n, L.sharded));
       for (int s = 0; s < 200; ++s) {
         op_coarse_gs(c, L, f, 1, phi);
         op_residual(c, L, f, phi, L.t.order, L.tmp);
-        if (std::sqrt(op_dot(c, L.tmp, L.tmp, L.n)) <= spec.coarse_tol * fnorm) break;
+        if (std::sqrt(op_dot(c, L.tmp, L.tmp, L.n, L.sharded)) <= spec.coarse_tol * fnorm) break;
       }
     } else {
       op_coarse_gs(c, L, f, spec.coarse_sweeps, phi);
@@ -596,20 +601,21 @@ void ensure_scalars(stamg_ctx* c) {
   ck(cudaMallocHost(&c->hbuf, 82 * sizeof(double)), "cudaMallocHost");
 }
 
-void op_multidot(stamg_ctx* c, const std::vector<const double*>& vs, const double* w, int64_t n, double* out_host) {
+void op_multidot(stamg_ctx* c, const std::vector<const double*>& vs, const double* w, int64_t n, double* out_host,
+                 bool sharded) {
   ensure_scalars(c);
   launch_multidot(vs.data(), int(vs.size()), w, n, c->partial, c->dots, c->stream);
   ck_launch("multidot");
   c->launches += 2;
+  if (sharded && c->world > 1) op_allreduce(c, c->dots, vs.size());  // partial dots of sharded vectors
   ck(cudaMemcpyAsync(c->hbuf, c->dots, vs.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
   ck(cudaStreamSynchronize(c->stream), "sync");
   std::memcpy(out_host, c->hbuf, vs.size() * sizeof(double));
-  if (c->world > 1) throw std::logic_error("multi-rank Krylov reductions are not enabled in this build");
 }
 
-double op_dot(stamg_ctx* c, const double* x, const double* y, int64_t n) {
+double op_dot(stamg_ctx* c, const double* x, const double* y, int64_t n, bool sharded) {
   double d = 0;
-  op_multidot(c, {x}, y, n, &d);
+  op_multidot(c, {x}, y, n, &d, sharded);
   (void)y;
   return d;
 }
@@ -640,7 +646,7 @@ stamg_report op_gmres(stamg_ctx* c, int precond, const double* b, double* x, dou
   const int64_t n = O.n;
   ensure_krylov(c, m);
   launch_fill(x, 0.0, n, c->stream);
-  const double bnorm = std::sqrt(op_dot(c, b, b, n));
+  const double bnorm = std::sqrt(op_dot(c, b, b, n, O.sharded));
   auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
   if (bnorm == 0.0) {
     rep.converged = 1;
@@ -653,7 +659,7 @@ stamg_report op_gmres(stamg_ctx* c, int precond, const double* b, double* x, dou
   std::vector<double> cs(m), sn(m), g(m + 1), y(m), dots(m + 1);
   std::vector<std::vector<double>> H(m, std::vector<double>(m + 1));
   while (!done) {
-    const double beta = std::sqrt(op_dot(c, c->V[0], c->V[0], n));
+    const double beta = std::sqrt(op_dot(c, c->V[0], c->V[0], n, O.sharded));
     launch_scale(1.0 / beta, c->V[0], n, c->stream);
     std::fill(g.begin(), g.end(), 0.0);
     for (auto& col : H) std::fill(col.begin(), col.end(), 0.0);
@@ -668,13 +674,13 @@ stamg_report op_gmres(stamg_ctx* c, int precond, const double* b, double* x, dou
       auto& h = H[j];
       std::vector<const double*> basis(c->V.begin(), c->V.begin() + j + 1);
       for (int pass = 0; pass < 2; ++pass) {  // CGS2
-        op_multidot(c, basis, w, n, dots.data());
+        op_multidot(c, basis, w, n, dots.data(), O.sharded);
         upload_coef(c, dots.data(), j + 1);
         launch_multi_axpy(basis.data(), j + 1, c->coef, w, n, c->stream);
         c->launches += 1;
         for (int i = 0; i <= j; ++i) h[i] += dots[i];
       }
-      h[j + 1] = std::sqrt(op_dot(c, w, w, n));
+      h[j + 1] = std::sqrt(op_dot(c, w, w, n, O.sharded));
       if (h[j + 1] != 0.0) launch_scale(1.0 / h[j + 1], w, n, c->stream), c->launches += 1;
       for (int i = 0; i < j; ++i) {
         const double tmp = cs[i] * h[i] + sn[i] * h[i + 1];
@@ -720,7 +726,7 @@ stamg_report op_gmres(stamg_ctx* c, int precond, const double* b, double* x, dou
   }
   op_apply_A(c, O, x, c->pb.spec.N, c->z);
   launch_axpby(1.0, b, -1.0, c->z, n, c->stream);
-  rep.final_residual = std::sqrt(op_dot(c, c->z, c->z, n)) / bnorm;
+  rep.final_residual = std::sqrt(op_dot(c, c->z, c->z, n, O.sharded)) / bnorm;
   rep.converged = rep.final_residual < tol;
   rep.wall_time = elapsed();
   return rep;
@@ -738,12 +744,12 @@ stamg_report op_bicgstab(stamg_ctx* c, int precond, const double* b, double* x, 
   double *r = c->V[0], *rhat = c->V[1], *p = c->V[2], *v = c->V[3], *s = c->V[4], *t = c->V[5], *phat = c->V[6];
   double* shat = c->z;
   launch_fill(x, 0.0, n, c->stream);
-  const double bnorm = std::sqrt(op_dot(c, b, b, n));
+  const double bnorm = std::sqrt(op_dot(c, b, b, n, O.sharded));
   auto finish = [&]() {
     if (bnorm > 0) {
       op_apply_A(c, O, x, c->pb.spec.N, c->u);
       launch_axpby(1.0, b, -1.0, c->u, n, c->stream);
-      rep.final_residual = std::sqrt(op_dot(c, c->u, c->u, n)) / bnorm;
+      rep.final_residual = std::sqrt(op_dot(c, c->u, c->u, n, O.sharded)) / bnorm;
     }
     rep.converged = rep.final_residual < tol;
     rep.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -759,7 +765,7 @@ stamg_report op_bicgstab(stamg_ctx* c, int precond, const double* b, double* x, 
   launch_fill(v, 0.0, n, c->stream);
   double rho = 1, alpha = 1, omega = 1;
   for (int it = 1; it <= max_iter; ++it) {
-    const double rho1 = op_dot(c, rhat, r, n);
+    const double rho1 = op_dot(c, rhat, r, n, O.sharded);
     if (rho1 == 0.0 || omega == 0.0) {
       rep.breakdown = 1;
       return finish();
@@ -771,7 +777,7 @@ stamg_report op_bicgstab(stamg_ctx* c, int precond, const double* b, double* x, 
     apply_precond(c, precond, p, phat);
     ++rep.preconditioner_applications;
     op_apply_A(c, O, phat, c->pb.spec.N, v);
-    const double rv = op_dot(c, rhat, v, n);
+    const double rv = op_dot(c, rhat, v, n, O.sharded);
     if (rv == 0.0) {
       rep.breakdown = 1;
       return finish();
@@ -780,7 +786,7 @@ stamg_report op_bicgstab(stamg_ctx* c, int precond, const double* b, double* x, 
     ck(cudaMemcpyAsync(s, r, n * 8, cudaMemcpyDeviceToDevice, c->stream), "copy");
     launch_axpy(-alpha, v, s, n, c->stream);
     launch_axpy(alpha, phat, x, n, c->stream);
-    const double snorm = std::sqrt(op_dot(c, s, s, n)) / bnorm;
+    const double snorm = std::sqrt(op_dot(c, s, s, n, O.sharded)) / bnorm;
     if (std::isnan(snorm)) throw NanError("bicgstab: NaN residual");
     if (snorm < tol) {
       rep.iterations = it;
@@ -790,17 +796,17 @@ stamg_report op_bicgstab(stamg_ctx* c, int precond, const double* b, double* x, 
     apply_precond(c, precond, s, shat);
     ++rep.preconditioner_applications;
     op_apply_A(c, O, shat, c->pb.spec.N, t);
-    const double tt = op_dot(c, t, t, n);
+    const double tt = op_dot(c, t, t, n, O.sharded);
     if (tt == 0.0) {
       rep.breakdown = 1;
       return finish();
     }
-    omega = op_dot(c, t, s, n) / tt;
+    omega = op_dot(c, t, s, n, O.sharded) / tt;
     launch_axpy(omega, shat, x, n, c->stream);
     ck(cudaMemcpyAsync(r, s, n * 8, cudaMemcpyDeviceToDevice, c->stream), "copy");
     launch_axpy(-omega, t, r, n, c->stream);
     c->launches += 10;
-    const double rnorm = std::sqrt(op_dot(c, r, r, n)) / bnorm;
+    const double rnorm = std::sqrt(op_dot(c, r, r, n, O.sharded)) / bnorm;
     if (std::isnan(rnorm)) throw NanError("bicgstab: NaN residual");
     rep.iterations = it;
     hist.push_back(rnorm);
@@ -873,28 +879,36 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
     }
     const auto& s = c->pb.spec;
     c->tree = make_sphere(s.angular_kind, s.angular_level, s.cone_levels, s.cone_half_angle_deg);
-    {  // direction sharding: contiguous slices of the leaf order, multiples of 4 patches
+    std::vector<std::vector<int>> parts;
+    if (c->world > 1 && want_mg) {
+      // sharded hierarchy: subtrees of the coarsest level per rank, coarsest replicated
+      parts = partition_levels(c->tree, s.n_levels, c->rank, c->world);
+      c->outer.t = build_level(c->pb, c->tree, s.N, false, &parts.back());
+    } else {  // direction sharding: contiguous slices of the leaf order, multiples of 4 patches
       const int Pg = int(c->tree.leaves.size());
       const int quads = (Pg + 3) / 4;
       const int q0 = std::min(Pg, 4 * int((int64_t(quads) * c->rank) / c->world));
       const int q1 = std::min(Pg, 4 * int((int64_t(quads) * (c->rank + 1)) / c->world));
-      c->outer.t = build_level(c->pb, c->tree, s.N, false, q0, q1);
+      const auto sub = range_subset(q0, q1);
+      c->outer.t = build_level(c->pb, c->tree, s.N, false, &sub);
     }
+    c->outer.sharded = c->world > 1;
     for (int i = 0; i < 4; ++i)
       for (int j = 0; j < 4; ++j) c->nsum[i] += c->outer.t.Nmat[i * 4 + j];
     if (s.n_mat > 1) c->mat = dupload(c->pb.mat, c->stream);
     if (!c->pb.q_el.empty()) c->q_el = dupload(c->pb.q_el, c->stream);
     upload_level(c.get(), c->outer);
-    if (want_mg && c->world > 1)
-      throw std::invalid_argument("the multigrid hierarchy is single-rank in this build (use build_hierarchy = 0)");
     if (want_mg) {
       c->nr = s.nr < 0 ? s.N : s.nr;
-      auto lv = build_hierarchy(c->pb, c->tree, c->nr, s.n_levels);
+      auto lv = build_hierarchy(c->pb, c->tree, c->nr, s.n_levels, c->world > 1 ? &parts : nullptr);
       c->mg.resize(lv.size());
       for (size_t i = 0; i < lv.size(); ++i) {
         c->mg[i].t = std::move(lv[i]);
+        c->mg[i].sharded = c->world > 1 && (i > 0 || lv.size() == 1);
         upload_level(c.get(), c->mg[i]);
       }
+      if (c->world > 1 && c->mg.size() == 1)
+        throw std::invalid_argument("a sharded hierarchy needs at least two levels (the coarsest is replicated)");
       c->have_mg = true;
     }
     *out = c.release();
@@ -927,7 +941,45 @@ int stamg_layout(stamg_ctx* c, int level, int out4[4]) {
 int stamg_patch_range(stamg_ctx* c, int level, int* q0, int* q1) {
   return guard([&] {
     DevLevel& L = level_of(c, level);
-    *q0 = L.t.q_begin, *q1 = L.t.q_begin + L.t.P;
+    *q0 = L.t.P ? L.t.qpos.front() : 0, *q1 = L.t.P ? L.t.qpos.back() + 1 : 0;
+  });
+}
+// Host-only (no device): the direction partition a rank would get, for tests.
+// level 0 = coarsest MG level (replicated); up[] = parent position in the
+// coarser level's list held by the same rank (level 0: the full list).
+int stamg_partition(const stamg_problem* prob, int rank, int world, int level, int* qpos, int* up, int cap,
+                    int* n) {
+  return guard([&] {
+    Problem pb = copy_problem(*prob);
+    validate(pb);
+    const auto& s = pb.spec;
+    SphereTree tree = make_sphere(s.angular_kind, s.angular_level, s.cone_levels, s.cone_half_angle_deg);
+    auto parts = partition_levels(tree, s.n_levels, rank, world);
+    if (level < 0 || level >= int(parts.size())) throw std::invalid_argument("partition: level out of range");
+    const int Lmax = tree.max_level, nlev = int(parts.size()), lmin = Lmax + 1 - nlev;
+    auto tree_at = [&](int i) { return lmin + i == Lmax ? tree : coarsen(tree, lmin + i); };
+    const SphereTree ft = tree_at(level);
+    *n = int(parts[level].size());
+    for (int k = 0; k < *n && k < cap; ++k) qpos[k] = parts[level][k];
+    if (level >= 1 && up) {
+      const SphereTree ct = tree_at(level - 1);
+      std::unordered_map<int, int> pos;
+      for (size_t c = 0; c < parts[level - 1].size(); ++c) pos[ct.leaves[parts[level - 1][c]]] = int(c);
+      for (int k = 0; k < *n && k < cap; ++k) {
+        const int id = ft.leaves[parts[level][k]];
+        auto it = pos.find(id);
+        if (it == pos.end()) it = pos.find(ft.parent[id]);
+        up[k] = it == pos.end() ? -1 : it->second;
+      }
+    }
+  });
+}
+
+int stamg_patch_list(stamg_ctx* c, int level, int* out, int cap, int* n) {
+  return guard([&] {
+    DevLevel& L = level_of(c, level);
+    *n = L.t.P;
+    for (int q = 0; out && q < L.t.P && q < cap; ++q) out[q] = L.t.qpos[q];
   });
 }
 int stamg_n_levels(stamg_ctx* c, int* n, int* nr) {
@@ -999,7 +1051,8 @@ int stamg_vec_axpy(stamg_ctx* c, double a, const stamg_vec* x, stamg_vec* y) {
 int stamg_vec_dot(stamg_ctx* c, const stamg_vec* x, const stamg_vec* y, double* out) {
   return guard([&] {
     if (x->n != y->n) throw std::invalid_argument("vec_dot: layout mismatch");
-    *out = op_dot(c, x->d, y->d, x->n);
+    const DevLevel& L = level_of(c, x->level);
+    *out = op_dot(c, x->d, y->d, x->n, L.sharded);
   });
 }
 
@@ -1153,6 +1206,14 @@ int stamg_scalar_flux(stamg_ctx* c, const stamg_vec* phi, double* out) {
         integral += t.area[q] * (blk[0] * c->nsum[0] + blk[1] * c->nsum[1] + blk[2] * c->nsum[2] + blk[3] * c->nsum[3]);
       }
       out[el] = integral / vol;
+    }
+    if (c->world > 1 && c->outer.sharded) {  // partial sums over this rank's directions
+      double* d = dalloc<double>(t.n_el);
+      ck(cudaMemcpyAsync(d, out, t.n_el * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+      op_allreduce(c, d, t.n_el);
+      ck(cudaMemcpyAsync(out, d, t.n_el * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+      ck(cudaStreamSynchronize(c->stream), "sync");
+      cudaFree(d);
     }
   });
 }

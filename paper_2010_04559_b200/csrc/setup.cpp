@@ -348,14 +348,26 @@ void validate(const Problem& p) {
   if (s.beam != 0 && s.beam != 2) throw std::invalid_argument("B200 path supports beam = 0 or 2 (x=0 cone)");
 }
 
-LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool with_gs, int q_begin, int q_end) {
+std::vector<int> range_subset(int q_begin, int q_end) {
+  std::vector<int> v;
+  for (int q = q_begin; q < q_end; ++q) v.push_back(q);
+  return v;
+}
+
+LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool with_gs, const std::vector<int>* subset) {
   LevelTables L;
   const auto& s = pb.spec;
   const int Pg = int(t.leaves.size());
-  if (q_end < 0) q_end = Pg;
-  if (q_begin < 0 || q_begin > q_end || q_end > Pg) throw std::invalid_argument("build_level: bad patch range");
-  L.P_global = Pg, L.q_begin = q_begin;
-  L.n_el = pb.n_el, L.P = q_end - q_begin, L.order = order, L.H = (order + 1) * (order + 1);
+  if (subset) {
+    for (size_t k = 0; k < subset->size(); ++k)
+      if ((*subset)[k] < 0 || (*subset)[k] >= Pg || (k && (*subset)[k] <= (*subset)[k - 1]))
+        throw std::invalid_argument("build_level: bad patch subset");
+    L.qpos = *subset;
+  } else {
+    L.qpos = range_subset(0, Pg);
+  }
+  L.P_global = Pg, L.q_begin = L.qpos.empty() ? 0 : L.qpos[0];
+  L.n_el = pb.n_el, L.P = int(L.qpos.size()), L.order = order, L.H = (order + 1) * (order + 1);
   L.n_mat = s.n_mat, L.nx = s.nx, L.ny = s.ny;
   const int P = L.P, H = L.H;
   const double hx = s.box / s.nx, hy = s.box / s.ny;
@@ -376,7 +388,8 @@ LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool 
     }
   std::copy(Nm, Nm + 16, L.Nmat);
 
-  L.leaf_id.assign(t.leaves.begin() + q_begin, t.leaves.begin() + q_end);
+  L.leaf_id.resize(L.P);
+  for (int q = 0; q < L.P; ++q) L.leaf_id[q] = t.leaves[L.qpos[q]];
   L.octant.resize(P);
   L.area.resize(P);
   L.Aflow.resize(size_t(P) * 3);
@@ -546,7 +559,40 @@ void find_symmetry(LevelTables& L, const SphereTree& t) {
     }
 }
 
-std::vector<LevelTables> build_hierarchy(const Problem& pb, const SphereTree& fine, int nr, int nlev) {
+std::vector<std::vector<int>> partition_levels(const SphereTree& fine, int nlev, int rank, int world) {
+  const int Lmax = fine.max_level;
+  nlev = nlev <= 0 ? Lmax + 1 : std::min(nlev, Lmax + 1);
+  const int lmin = Lmax + 1 - nlev;
+  std::vector<SphereTree> trees;
+  for (int i = 0; i < nlev; ++i) trees.push_back(lmin + i == Lmax ? fine : coarsen(fine, lmin + i));
+  // root (coarsest-level position) of every leaf of every level
+  std::unordered_map<int, int> root_pos;
+  for (int c = 0; c < int(trees[0].leaves.size()); ++c) root_pos[trees[0].leaves[c]] = c;
+  auto root_of = [&](int id) {
+    while (!root_pos.count(id)) id = fine.parent[id];
+    return root_pos[id];
+  };
+  const int R = int(trees[0].leaves.size());
+  std::vector<long> weight(R, 0);
+  for (int id : trees.back().leaves) weight[root_of(id)]++;
+  long total = 0;
+  for (long w : weight) total += w;
+  // contiguous roots, cut where the cumulative weight crosses rank boundaries
+  std::vector<int> owner(R, 0);
+  long acc = 0;
+  for (int c = 0; c < R; ++c) {
+    owner[c] = std::min(world - 1, int((acc + weight[c] / 2) * world / std::max(1L, total)));
+    acc += weight[c];
+  }
+  std::vector<std::vector<int>> parts(nlev);
+  for (int i = 0; i < nlev; ++i)
+    for (int q = 0; q < int(trees[i].leaves.size()); ++q)
+      if (i == 0 || owner[root_of(trees[i].leaves[q])] == rank) parts[i].push_back(q);
+  return parts;
+}
+
+std::vector<LevelTables> build_hierarchy(const Problem& pb, const SphereTree& fine, int nr, int nlev,
+                                         const std::vector<std::vector<int>>* parts) {
   const int Lmax = fine.max_level;
   nlev = nlev <= 0 ? Lmax + 1 : std::min(nlev, Lmax + 1);
   const int lmin = Lmax + 1 - nlev;
@@ -555,24 +601,26 @@ std::vector<LevelTables> build_hierarchy(const Problem& pb, const SphereTree& fi
   for (int i = 0; i < nlev; ++i) {
     const int l = lmin + i;
     trees.push_back(l == Lmax ? fine : coarsen(fine, l));
-    lv.push_back(build_level(pb, trees.back(), nr, i == 0));
+    lv.push_back(build_level(pb, trees.back(), nr, i == 0, parts && i > 0 ? &(*parts)[i] : nullptr));
   }
   for (int i = 1; i < nlev; ++i) {  // transfer maps (multigrid.cpp:68-96), Const: B = [1]
     const auto& ct = trees[i - 1];
     const auto& ft = trees[i];
-    std::unordered_map<int, int> pos;
-    for (int c = 0; c < int(ct.leaves.size()); ++c) pos[ct.leaves[c]] = c;
+    const LevelTables& C = lv[i - 1];
+    std::unordered_map<int, int> pos;  // coarse leaf id -> position in the coarse level's (local) list
+    for (int c = 0; c < C.P; ++c) pos[C.leaf_id[c]] = c;
     auto& L = lv[i];
     L.up.resize(L.P);
     L.up_w.assign(L.P, 1.0);
     for (int q = 0; q < L.P; ++q) {
-      const int id = ft.leaves[q];
+      const int id = L.leaf_id[q];
       auto it = pos.find(id);
       if (it == pos.end()) it = pos.find(ft.parent[id]);
       if (it == pos.end()) throw std::logic_error("build_hierarchy: meshes are not nested");
       L.up[q] = it->second;
     }
-    const int Pc = int(ct.leaves.size());
+    (void)ct;
+    const int Pc = C.P;
     L.child_ptr.assign(Pc + 1, 0);
     for (int q = 0; q < L.P; ++q) L.child_ptr[L.up[q] + 1]++;
     for (int c = 0; c < Pc; ++c) L.child_ptr[c + 1] += L.child_ptr[c];

@@ -42,7 +42,8 @@ bool in_cone(const SphereTree& t, int id, double half_angle_deg);
 // ---- per-level device tables ----
 struct LevelTables {
   int n_el = 0, P = 0, order = 0, H = 0, n_mat = 1;
-  int P_global = 0, q_begin = 0;      // this rank's slice [q_begin, q_begin + P) of the leaf order
+  int P_global = 0, q_begin = 0;      // direction sharding: leaf-order positions of the local patches
+  std::vector<int> qpos;              // [P] position of each local patch in the level's full leaf order
   int nx = 0, ny = 0;
   std::vector<int> leaf_id, octant;   // per patch
   std::vector<double> X;              // [P][H] couplings (scatter.hpp:32-39)
@@ -90,12 +91,24 @@ Problem copy_problem(const stamg_problem& p);
 void validate(const Problem& p);
 
 // build_operators + build_sweep_plan for one angular mesh and scatter order
-// q_begin/q_end restrict the level to a contiguous range of the leaf order
-// (direction sharding across ranks); -1 = all leaves.
-LevelTables build_level(const Problem& pb, const SphereTree& tree, int order, bool with_gs, int q_begin = 0,
-                        int q_end = -1);
-// build_hierarchy: nlev levels, index 0 coarsest; fills up/child maps
-std::vector<LevelTables> build_hierarchy(const Problem& pb, const SphereTree& fine, int nr, int nlev);
+// `subset` (ascending leaf-order positions) restricts the level to a rank's
+// directions; nullptr = all leaves.
+LevelTables build_level(const Problem& pb, const SphereTree& tree, int order, bool with_gs,
+                        const std::vector<int>* subset = nullptr);
+// contiguous leaf-order range [q_begin, q_end) as a subset
+std::vector<int> range_subset(int q_begin, int q_end);
+
+// Direction sharding of a hierarchy: rank r owns whole subtrees rooted at the
+// coarsest used level's patches (contiguous roots, balanced by the number of
+// finest-level descendants). Returns per level (0 = coarsest) the ascending
+// leaf positions held by `rank`; level 0 is replicated (all positions).
+std::vector<std::vector<int>> partition_levels(const SphereTree& fine, int nlev, int rank, int world);
+
+// build_hierarchy: nlev levels, index 0 coarsest; fills up/child maps. With
+// `parts` (from partition_levels) levels >= 1 hold only the rank's patches and
+// up[] indexes the coarser level's local list (level 0: the full list).
+std::vector<LevelTables> build_hierarchy(const Problem& pb, const SphereTree& fine, int nr, int nlev,
+                                         const std::vector<std::vector<int>>* parts = nullptr);
 // assemble_rhs (transport.cpp:110-179 + cone beam EXTENSION)
 std::vector<double> assemble_rhs(const Problem& pb, const LevelTables& lev, const SphereTree& tree);
 

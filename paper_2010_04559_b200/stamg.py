@@ -196,6 +196,13 @@ class Context:
         _check(lib().stamg_layout(self.h, level, out))
         return tuple(out)
 
+    def patch_list(self, level=OUTER):
+        n = C.c_int()
+        _check(lib().stamg_patch_list(self.h, level, None, 0, C.byref(n)))
+        out = np.empty(n.value, dtype=np.int32)
+        _check(lib().stamg_patch_list(self.h, level, out.ctypes.data_as(ip), n.value, C.byref(n)))
+        return out
+
     def levels(self):
         n, nr = C.c_int(), C.c_int()
         _check(lib().stamg_n_levels(self.h, C.byref(n), C.byref(nr)))
@@ -324,6 +331,33 @@ class Context:
                                       self.spec.max_iter if max_iter is None else max_iter,
                                       self.spec.restart if restart is None else restart, C.byref(rep)))
         return rep.as_dict()
+
+
+def _problem_struct(spec: ProblemSpec):
+    st, mo = spec.kernel_arrays()
+    mat = None if spec.mat_of_el is None else np.ascontiguousarray(spec.mat_of_el, dtype=np.int32)
+    q = None if spec.q_el is None else _f64(spec.q_el)
+    keep = [st, mo, mat, q]
+    pr = _Problem(spec.dim, spec.nx, spec.ny, spec.nz, spec.box, spec.basis, spec.p, spec.angular_kind,
+                  spec.angular_level, spec.cone_levels, spec.cone_half_angle_deg, spec.N, len(st),
+                  st.ctypes.data_as(dp), mo.ctypes.data_as(dp), mat.ctypes.data_as(ip) if mat is not None else None,
+                  q.ctypes.data_as(dp) if q is not None else None, spec.beam, spec.strength, spec.x0, spec.x1,
+                  spec.y0, spec.y1, spec.nr, spec.n_levels, spec.nu_pre, spec.nu_post, spec.coarse_sweeps,
+                  spec.coarse_tol)
+    return pr, keep
+
+
+def partition(spec: ProblemSpec, rank: int, world: int, level: int):
+    """Host-only: (leaf positions, parent positions in the coarser local list) of
+    `rank`'s directions at MG level `level` (0 = coarsest, replicated)."""
+    pr, keep = _problem_struct(spec)
+    n = C.c_int()
+    _check(lib().stamg_partition(C.byref(pr), rank, world, level, None, None, 0, C.byref(n)))
+    qpos = np.empty(n.value, dtype=np.int32)
+    up = np.full(n.value, -1, dtype=np.int32)
+    _check(lib().stamg_partition(C.byref(pr), rank, world, level, qpos.ctypes.data_as(ip), up.ctypes.data_as(ip),
+                                 n.value, C.byref(n)))
+    return qpos, up
 
 
 def nccl_unique_id() -> bytes:
