@@ -93,6 +93,14 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
   const int n_el = p.n_el, nx = p.nx, ny = p.ny, P = p.P, Hp = p.Hp, H = p.H, seg = p.cells_per_warp;
   const int kpad = p.kpad, nmat = p.n_mat;
   double* sbase = gsm + (size_t)wib * gs_warp_doubles(Hp, kpad, nmat);
+  // row mode (a warp owns a whole grid row, the CTA owns wpb consecutive rows): y-traces
+  // between rows of the CTA go through a shared mailbox [wpb][2 parities][nx][kpad] of
+  // (dof2, dof3) in the sweep frame, published by per-warp item counters
+  const bool rows = p.rows_mode != 0;
+  double2* mbox = reinterpret_cast<double2*>(gsm + (size_t)wpb * gs_warp_doubles(Hp, kpad, nmat));
+  volatile int* cnt = reinterpret_cast<volatile int*>(mbox + (rows ? (size_t)wpb * 2 * nx * kpad : 0));
+  if (rows && lane == 0) cnt[wib] = 0;
+  __syncthreads();
   // double-buffered moments [2][Hp][4] at sbase
   double* sdz = sbase + Hp * 8;               // [kpad][4]
   double* sK = sdz + kpad * 4;                // [n_mat][kpad][kpad] K of the current octant
@@ -117,8 +125,9 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
   prefetch_mom(cell_of(0), sbase);
   cp_async_wait<0>();
   __syncwarp();
+  double xtr[NS][2];  // x-upwind traces (frame dofs 1, 3) from the previous cell of the segment
   for (int it = 0; it < n_items; ++it) {
-    const int pass = it / (8 * seg), oct = (it / seg) & 7;
+    const int pass = it / (8 * seg), oct = (it / seg) & 7, jseg = it % seg;
     const int el = cell_of(it);
     const int el_next = it + 1 < n_items ? cell_of(it + 1) : -1;
     const bool reuse = el_next == el;  // next item is this cell again (next octant)
@@ -188,21 +197,31 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
 #pragma unroll
       for (int i = 0; i < 4; ++i) t[sl][i] = (u[0][i] + u[1][i]) + (u[2][i] + u[3][i]);
     }
-    // ---- wait for the upwind cells (this pass) and the downwind readers (last pass)
+    // ---- dependencies. x-upwind inside the segment: previous item of this warp (registers).
+    //      y-upwind in row mode inside the CTA: shared mailbox. Everything else: global
+    //      per-(octant, cell) counters (relaxed polling + one acquire fence).
+    const bool x_in_seg = upx >= 0 && jseg > 0;
+    const int pw = wib + (yneg ? 1 : -1), cw = wib + (yneg ? -1 : 1);
+    const bool y_in_cta = rows && upy >= 0 && pw >= 0 && pw < wpb;
+    const bool ydn_in_cta = rows && dny >= 0 && cw >= 0 && cw < wpb;
+    const int item_id = (pass * 8 + oct) * seg + jseg;  // == global order within the row
     {
       const int* f = nullptr;
       int need = 0;
       const int* d = p.done + (size_t)oct * n_el;
-      if (lane == 0 && upx >= 0) f = d + upx, need = pass + 1;
-      if (lane == 1 && upy >= 0) f = d + upy, need = pass + 1;
-      if (lane == 2 && pass > 0 && dnx >= 0) f = d + dnx, need = pass;
-      if (lane == 3 && pass > 0 && dny >= 0) f = d + dny, need = pass;
-      // spin with relaxed loads (an acquire load invalidates L1 on every poll), then
-      // one acquire fence: the fence-based acquire pattern of the PTX memory model
+      if (lane == 0 && upx >= 0 && !x_in_seg) f = d + upx, need = pass + 1;
+      if (lane == 1 && upy >= 0 && !y_in_cta) f = d + upy, need = pass + 1;
+      if (lane == 2 && pass > 0 && dnx >= 0 && jseg == seg - 1) f = d + dnx, need = pass;
+      if (lane == 3 && pass > 0 && dny >= 0 && !ydn_in_cta) f = d + dny, need = pass;
       bool ok = f == nullptr || ld_relaxed(f) >= need;
+      bool any = __any_sync(full, f != nullptr);
       while (!__all_sync(full, ok))
         if (!ok) ok = ld_relaxed(f) >= need;
-      fence_acq_rel();
+      if (any) fence_acq_rel();
+      if (y_in_cta) {  // producer row of this CTA finished the same (pass, octant, column)
+        while (cnt[pw] < item_id + 1) {}
+        __threadfence_block();
+      }
     }
     // ---- upwind traces folded into r (sweeps.cpp:87-92), everything in the sweep frame
 #pragma unroll
@@ -210,19 +229,24 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
       const int q = qs[sl];
       if (q < 0) continue;
       double ux[4] = {0, 0, 0, 0}, uy[4] = {0, 0, 0, 0};
-      if (upx >= 0) {
+      if (upx >= 0 && !x_in_seg) {
         const double2 a = ld_cg2(p.phi + ((size_t)upx * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upx * P + q) * 4 + 2);
         ux[0] = a.x, ux[1] = a.y, ux[2] = b.x, ux[3] = b.y;
+        perm(m, ux[0], ux[1], ux[2], ux[3]);
+      } else if (x_in_seg) {
+        ux[1] = xtr[sl][0], ux[3] = xtr[sl][1];
       }
-      if (upy >= 0) {
+      if (upy >= 0 && !y_in_cta) {
         const double2 a = ld_cg2(p.phi + ((size_t)upy * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upy * P + q) * 4 + 2);
         uy[0] = a.x, uy[1] = a.y, uy[2] = b.x, uy[3] = b.y;
+        perm(m, uy[0], uy[1], uy[2], uy[3]);
+      } else if (y_in_cta) {
+        const double2 v = mbox[(((size_t)pw * 2 + (oct & 1)) * nx + jseg) * kpad + lane + 32 * sl];
+        uy[2] = v.x, uy[3] = v.y;
       }
       perm(m, r[sl][0], r[sl][1], r[sl][2], r[sl][3]);
       perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
       perm(m, t[sl][0], t[sl][1], t[sl][2], t[sl][3]);
-      perm(m, ux[0], ux[1], ux[2], ux[3]);
-      perm(m, uy[0], uy[1], uy[2], uy[3]);
       const double* cxy = p.cxy + (size_t)q * 8;
       if (upx >= 0) {
         r[sl][0] -= cxy[0] * ux[1] + cxy[1] * ux[3];
@@ -301,18 +325,31 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
       const double2 d0 = reinterpret_cast<const double2*>(sdz)[2 * a], d1 = reinterpret_cast<const double2*>(sdz)[2 * a + 1];
       zo[sl][0] += d0.x, zo[sl][1] += d0.y, zo[sl][2] += d1.x, zo[sl][3] += d1.y;
     }
-    // ---- publish the new iterate of this cell's patches, then the flag
+    // ---- publish the new iterate of this cell's patches, then the flags
+    if (ydn_in_cta && pass * 8 + oct >= 2) {  // mailbox slot reuse: the consumer row is past it
+      const int need2 = (pass * 8 + oct - 2) * seg + jseg + 1;
+      while (cnt[cw] < need2) {}
+    }
 #pragma unroll
     for (int sl = 0; sl < NS; ++sl) {
       const int q = qs[sl];
+      xtr[sl][0] = zo[sl][1], xtr[sl][1] = zo[sl][3];  // frame x-outflow traces for the next cell
       if (q < 0) continue;
+      if (rows) mbox[(((size_t)wib * 2 + (oct & 1)) * nx + jseg) * kpad + lane + 32 * sl] = make_double2(zo[sl][2], zo[sl][3]);
       perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
       double* zb = p.phi + ((size_t)el * P + q) * 4;
       st_cg2(zb, make_double2(zo[sl][0], zo[sl][1]));
       st_cg2(zb + 2, make_double2(zo[sl][2], zo[sl][3]));
     }
     __syncwarp();
-    if (lane == 0) st_release(p.done + (size_t)oct * n_el + el, pass + 1);
+    if (rows && lane == 0) {
+      __threadfence_block();
+      cnt[wib] = item_id + 1;
+    }
+    // global counter only where another warp reads or waits on this cell
+    const bool need_flag = (dnx >= 0 && jseg == seg - 1) || (upx >= 0 && jseg == 0) || (dny >= 0 && !ydn_in_cta) ||
+                           (upy >= 0 && !y_in_cta);
+    if (need_flag && lane == 0) st_release(p.done + (size_t)oct * n_el + el, pass + 1);
     // ---- running moments: mom += sum_a X_qa^T dz_a; Xo is [P][Hp] in octant order
     double* mom_el = p.mom + (size_t)el * Hp * 4;
     double* mw = const_cast<double*>(mom);
@@ -354,7 +391,10 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
   }
 }
 
-size_t gs_smem(int Hp, int kpad, int nmat, int wpb) { return sizeof(double) * wpb * gs_warp_doubles(Hp, kpad, nmat); }
+size_t gs_smem(int Hp, int kpad, int nmat, int wpb, int rows_nx = 0) {
+  return sizeof(double) * wpb * gs_warp_doubles(Hp, kpad, nmat) +
+         (rows_nx ? sizeof(double2) * size_t(wpb) * 2 * rows_nx * kpad + sizeof(int) * 8 : 0);
+}
 
 // warps per CTA: as many as fit next to the per-warp staging (<= 8)
 int gs_wpb(int Hp, int kpad, int nmat) {
@@ -366,8 +406,8 @@ int gs_wpb(int Hp, int kpad, int nmat) {
 template <int NS>
 void launch_gs2(const CoarseGSParams& p, cudaStream_t s) {
   auto k = coarse_gs_static_kernel<NS>;
-  const int wpb = gs_wpb(p.Hp, p.kpad, p.n_mat);
-  const size_t smem = gs_smem(p.Hp, p.kpad, p.n_mat, wpb);
+  const int wpb = p.rows_mode ? p.rows_mode : gs_wpb(p.Hp, p.kpad, p.n_mat);
+  const size_t smem = gs_smem(p.Hp, p.kpad, p.n_mat, wpb, p.rows_mode ? p.nx : 0);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   CoarseGSParams q = p;
   void* args[] = {&q};
@@ -400,6 +440,17 @@ void launch_restrict(const double* fine, double* coarse, const int* cptr, const 
   const int64_t n = (int64_t)n_el * Pc;
   if (n == 0) return;
   restrict_kernel<<<int((n + 255) / 256), 256, 0, s>>>(fine, coarse, cptr, cidx, w, n_el, Pf, Pc);
+}
+
+// row mode: warps per CTA (consecutive grid rows) that fit with the mailbox, 0 if none
+int coarse_gs_rows_wpb(int Hp, int kpad, int nmat, int nx, int ny, int max_np) {
+  if (max_np > 32) return 0;
+  for (int w = 4; w >= 2; w >>= 1)
+    if (ny % w == 0 && gs_smem(Hp, kpad, nmat, w, nx) <= 200 * 1024) {
+      const size_t smem = gs_smem(Hp, kpad, nmat, w, nx);
+      if (occ_blocks<1>(smem, w) * w >= ny) return w;
+    }
+  return 0;
 }
 
 int coarse_gs_max_warps(int Hp, int kpad, int nmat, int max_np) {
