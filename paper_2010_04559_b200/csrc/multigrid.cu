@@ -173,29 +173,49 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
         zo[sl][0] = za.x, zo[sl][1] = za.y, zo[sl][2] = zc.x, zo[sl][3] = zc.y;
       }
     }
-    // ---- t0_a = X_qa sig mom (off the critical path), all operands in shared memory
-#pragma unroll
-    for (int sl = 0; sl < NS; ++sl) {
-      if (qs[sl] < 0) continue;
-      const double* xr = sX + (size_t)(lane + 32 * sl) * XS;
-      double u[4][4] = {};
-      int h = 0;
-      for (; h + 3 < H; h += 4) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const double xs = xr[h + k] * sg[h + k];
-          const double2 ma = reinterpret_cast<const double2*>(mom)[2 * (h + k)];
-          const double2 mb = reinterpret_cast<const double2*>(mom)[2 * (h + k) + 1];
-          u[k][0] += xs * ma.x, u[k][1] += xs * ma.y, u[k][2] += xs * mb.x, u[k][3] += xs * mb.y;
+    // ---- t0_a = X_qa sig mom (off the critical path), all operands in shared memory.
+    //      np <= 16: Lp = 32/np lanes per patch split the harmonics, then reduce.
+    if (NS == 1 && np <= 16) {
+      const int Lp = np <= 1 ? 32 : np <= 2 ? 16 : np <= 4 ? 8 : np <= 8 ? 4 : 2;
+      const int a = lane / Lp, part = lane % Lp;
+      double u[4] = {0.0, 0.0, 0.0, 0.0};
+      if (a < np) {
+        const double* xr = sX + (size_t)a * XS;
+        for (int h = part; h < H; h += Lp) {
+          const double xs = xr[h] * sg[h];
+          const double2 ma = reinterpret_cast<const double2*>(mom)[2 * h], mb = reinterpret_cast<const double2*>(mom)[2 * h + 1];
+          u[0] += xs * ma.x, u[1] += xs * ma.y, u[2] += xs * mb.x, u[3] += xs * mb.y;
         }
       }
-      for (; h < H; ++h) {
-        const double xs = xr[h] * sg[h];
-        const double2 ma = reinterpret_cast<const double2*>(mom)[2 * h], mb = reinterpret_cast<const double2*>(mom)[2 * h + 1];
-        u[0][0] += xs * ma.x, u[0][1] += xs * ma.y, u[0][2] += xs * mb.x, u[0][3] += xs * mb.y;
-      }
+      for (int o = Lp >> 1; o > 0; o >>= 1)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) t[sl][i] = (u[0][i] + u[1][i]) + (u[2][i] + u[3][i]);
+        for (int i = 0; i < 4; ++i) u[i] += __shfl_xor_sync(full, u[i], o);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) t[0][i] = __shfl_sync(full, u[i], (lane < np ? lane : 0) * Lp);
+    } else {
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) {
+        if (qs[sl] < 0) continue;
+        const double* xr = sX + (size_t)(lane + 32 * sl) * XS;
+        double u[4][4] = {};
+        int h = 0;
+        for (; h + 3 < H; h += 4) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double xs = xr[h + k] * sg[h + k];
+            const double2 ma = reinterpret_cast<const double2*>(mom)[2 * (h + k)];
+            const double2 mb = reinterpret_cast<const double2*>(mom)[2 * (h + k) + 1];
+            u[k][0] += xs * ma.x, u[k][1] += xs * ma.y, u[k][2] += xs * mb.x, u[k][3] += xs * mb.y;
+          }
+        }
+        for (; h < H; ++h) {
+          const double xs = xr[h] * sg[h];
+          const double2 ma = reinterpret_cast<const double2*>(mom)[2 * h], mb = reinterpret_cast<const double2*>(mom)[2 * h + 1];
+          u[0][0] += xs * ma.x, u[0][1] += xs * ma.y, u[0][2] += xs * mb.x, u[0][3] += xs * mb.y;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t[sl][i] = (u[0][i] + u[1][i]) + (u[2][i] + u[3][i]);
+      }
     }
     // ---- dependencies. x-upwind inside the segment: previous item of this warp (registers).
     //      y-upwind in row mode inside the CTA: shared mailbox. Everything else: global
