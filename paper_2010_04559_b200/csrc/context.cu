@@ -286,8 +286,10 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     L.gs_Xo = dupload(Xo, s);
     L.gs_XoT = dupload(XoT, s);
     // static ownership: each warp owns a segment of gs_cpw consecutive cells of one row
-    L.gs_rows = std::getenv("STAMG_GS_SEGMENTS") ? 0
-                : coarse_gs_rows_wpb(L.Hp, L.gs_kpad, t.n_mat, t.nx, t.ny, L.gs_max_np);
+    // row mode pays off once rows are long (measured: c2, c3 faster; c1 at 32^2 slower)
+    L.gs_rows = (std::getenv("STAMG_GS_SEGMENTS") || t.nx < 64)
+                    ? 0
+                    : coarse_gs_rows_wpb(L.Hp, L.gs_kpad, t.n_mat, t.nx, t.ny, L.gs_max_np);
     const int max_warps = coarse_gs_max_warps(L.Hp, L.gs_kpad, t.n_mat, L.gs_max_np);
     int seg = 1;
     while (int64_t(t.n_el) / seg > max_warps || t.nx % seg != 0) {
@@ -515,6 +517,7 @@ void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* 
   p.oct_patches = L.oct_patches, p.oct_ptr = L.oct_ptr, p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
   p.done = L.gs_done, p.K = L.gs_K, p.Xo = L.gs_Xo, p.XoT = L.gs_XoT, p.GS = L.gs_G, p.n_mat = L.t.n_mat;
   p.cells_per_warp = L.gs_cpw, p.kpad = L.gs_kpad, p.grid_blocks = L.gs_blocks, p.rows_mode = L.gs_rows;
+  p.xreg = std::getenv("STAMG_GS_XGLOBAL") ? 0 : 1;
   p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.H = L.t.H, p.nx = L.t.nx, p.ny = L.t.ny, p.nu = nu;
   for (int o = 0; o < 8; ++o)
     p.max_patches_per_octant = std::max(p.max_patches_per_octant, L.t.oct_ptr[o + 1] - L.t.oct_ptr[o]);

@@ -104,6 +104,7 @@ struct CoarseGSParams {
   const double* XoT = nullptr;    // [Hp][P] its transpose
   const double* K = nullptr;      // [n_mat][P][kpad] X_a sig X_b^T, a = octant-ordered row, b = index in octant
   int cells_per_warp = 0, kpad = 0, grid_blocks = 0;  // warp owns a row segment of cells_per_warp cells
+  int xreg = 1;       // x-upwind traces inside a segment from registers (0: through global memory)
   int rows_mode = 0;  // > 0: warp owns a whole row, CTA = rows_mode consecutive rows (shared mailbox)
   int n_el = 0, P = 0, Hp = 0, H = 0, nx = 0, ny = 0, nu = 0, n_mat = 1;
   int max_patches_per_octant = 0;

@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
     // ---- dependencies. x-upwind inside the segment: previous item of this warp (registers).
     //      y-upwind in row mode inside the CTA: shared mailbox. Everything else: global
     //      per-(octant, cell) counters (relaxed polling + one acquire fence).
-    const bool x_in_seg = upx >= 0 && jseg > 0;
+    const bool x_in_seg = p.xreg && upx >= 0 && jseg > 0;
     const int pw = wib + (yneg ? 1 : -1), cw = wib + (yneg ? -1 : 1);
     const bool y_in_cta = rows && upy >= 0 && pw >= 0 && pw < wpb;
     const bool ydn_in_cta = rows && dny >= 0 && cw >= 0 && cw < wpb;
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
       const int* d = p.done + (size_t)oct * n_el;
       if (lane == 0 && upx >= 0 && !x_in_seg) f = d + upx, need = pass + 1;
       if (lane == 1 && upy >= 0 && !y_in_cta) f = d + upy, need = pass + 1;
-      if (lane == 2 && pass > 0 && dnx >= 0 && jseg == seg - 1) f = d + dnx, need = pass;
+      if (lane == 2 && pass > 0 && dnx >= 0 && (jseg == seg - 1 || !p.xreg)) f = d + dnx, need = pass;
       if (lane == 3 && pass > 0 && dny >= 0 && !ydn_in_cta) f = d + dny, need = pass;
       bool ok = f == nullptr || ld_relaxed(f) >= need;
       bool any = __any_sync(full, f != nullptr);
@@ -367,8 +367,8 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
       cnt[wib] = item_id + 1;
     }
     // global counter only where another warp reads or waits on this cell
-    const bool need_flag = (dnx >= 0 && jseg == seg - 1) || (upx >= 0 && jseg == 0) || (dny >= 0 && !ydn_in_cta) ||
-                           (upy >= 0 && !y_in_cta);
+    const bool need_flag = !p.xreg || (dnx >= 0 && jseg == seg - 1) || (upx >= 0 && jseg == 0) ||
+                           (dny >= 0 && !ydn_in_cta) || (upy >= 0 && !y_in_cta);
     if (need_flag && lane == 0) st_release(p.done + (size_t)oct * n_el + el, pass + 1);
     // ---- running moments: mom += sum_a X_qa^T dz_a; Xo is [P][Hp] in octant order
     double* mom_el = p.mom + (size_t)el * Hp * 4;
