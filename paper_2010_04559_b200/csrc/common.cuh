@@ -63,6 +63,27 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// ---- wavefront layout (throughput contexts): per 8-direction group, cells are stored
+// strip by strip (R rows), along the sweep's anti-diagonals d = i + r of the group's
+// frame, row within the diagonal fastest. A sweep step then touches R consecutive
+// slots (R x 256 bytes). Slot count per group: nstrips * (nx + R - 1) * R (padding = 0).
+struct WLGeom {
+  int nx = 0, ny = 0, R = 32, nd = 0;
+  long long slots = 0;        // slots per group
+  const int* goct = nullptr;  // octant of each group
+};
+__host__ __device__ __forceinline__ long long wl_slot_frame(const WLGeom& w, int i, int j) {
+  const int s = j / w.R, r = j - s * w.R;
+  return ((long long)s * w.nd + i + r) * w.R + r;
+}
+// index of the 32-byte block of (element el, internal direction k)
+__device__ __forceinline__ long long wl_block(const WLGeom& w, int el, int k) {
+  const int g = k >> 3, oct = w.goct[g];
+  const int gx = el % w.nx, gy = el / w.nx;
+  const int i = (oct & 1) ? w.nx - 1 - gx : gx, j = (oct & 2) ? w.ny - 1 - gy : gy;
+  return ((long long)g * w.slots + wl_slot_frame(w, i, j)) * 8 + (k & 7);
+}
+
 __device__ __forceinline__ double2 shfl_up2(double2 v, int d) {
   v.x = __shfl_up_sync(0xffffffffu, v.x, d);
   v.y = __shfl_up_sync(0xffffffffu, v.y, d);

@@ -103,6 +103,13 @@ struct DevLevel {
   int *groups = nullptr, *group_oct = nullptr, *oct_patches = nullptr, *oct_ptr = nullptr;
   int *groups8 = nullptr, *group8_oct = nullptr;
   double2* sweep_top = nullptr;  // 8-direction sweep: strip-boundary trace scratch
+  // wavefront layout (contexts without a hierarchy): tables in internal (group-major)
+  // patch order; vectors padded to n_groups8 * slots * 8 blocks
+  WLGeom wl;                      // wl.nd == 0: reference layout
+  std::vector<int> ipos;          // local reference patch index -> internal index
+  int *d_ipos = nullptr, *d_iid = nullptr;
+  double* stage = nullptr;        // chunked host <-> device conversion
+  int64_t stage_n = 0;
   int *up = nullptr, *child_ptr = nullptr, *child_idx = nullptr;
   double* src = nullptr;  // scatter moments workspace [n_el][Hp][4]
   double* mom = nullptr;  // coarse GS moments
@@ -128,6 +135,7 @@ struct stamg_ctx {
   std::vector<DevLevel> mg;
   int nr = 0;
   bool have_mg = false;
+  bool wl_allowed = false;
   int* mat = nullptr;
   double* q_el = nullptr;
   double nsum[4] = {0, 0, 0, 0};
@@ -208,10 +216,77 @@ std::vector<double> frame_blocks(const std::vector<double>& blk, const LevelTabl
   return out;
 }
 
+// Reorder every per-patch table of a level into the internal (group-major) order
+// iperm[k] = q; returns ipos (q -> k). Reference patch order stays in t.qpos.
+std::vector<int> apply_internal_order(LevelTables& t) {
+  const std::vector<int> iperm = t.groups8;  // flattened 8-direction groups (full, no padding)
+  const int P = t.P;
+  std::vector<int> ipos(P);
+  for (int k = 0; k < P; ++k) ipos[iperm[k]] = k;
+  auto perm_rows = [&](std::vector<double>& v, int row) {
+    if (v.empty()) return;
+    std::vector<double> o(v.size());
+    const size_t blocks = v.size() / (size_t(P) * row);
+    for (size_t b = 0; b < blocks; ++b)
+      for (int k = 0; k < P; ++k)
+        for (int j = 0; j < row; ++j) o[(b * P + k) * row + j] = v[(b * P + iperm[k]) * row + j];
+    v.swap(o);
+  };
+  auto perm_int = [&](std::vector<int>& v) {
+    std::vector<int> o(P);
+    for (int k = 0; k < P; ++k) o[k] = v[iperm[k]];
+    v.swap(o);
+  };
+  perm_int(t.leaf_id);
+  perm_int(t.octant);
+  perm_rows(t.X, t.H);
+  perm_rows(t.B, 16);
+  perm_rows(t.Binv, 16);
+  perm_rows(t.C, 32);
+  perm_rows(t.cxy, 8);
+  perm_rows(t.area, 1);
+  perm_rows(t.Aflow, 3);
+  for (int& q : t.orbit) q = ipos[q];
+  for (size_t k = 0; k < t.groups8.size(); ++k) t.groups8[k] = int(k);
+  // 4-direction groups and octant lists in the new order
+  t.groups.clear(), t.group_oct.clear(), t.oct_patches.clear();
+  t.oct_ptr.assign(9, 0);
+  for (int oct = 0; oct < 8; ++oct) {
+    t.oct_ptr[oct] = int(t.oct_patches.size());
+    std::vector<int> mine;
+    for (int q = 0; q < P; ++q)
+      if (t.octant[q] == oct) mine.push_back(q);
+    t.oct_patches.insert(t.oct_patches.end(), mine.begin(), mine.end());
+    for (size_t k = 0; k < mine.size(); k += 4) {
+      for (int j = 0; j < 4; ++j) t.groups.push_back(k + j < mine.size() ? mine[k + j] : -1);
+      t.group_oct.push_back(oct);
+    }
+  }
+  t.oct_ptr[8] = int(t.oct_patches.size());
+  return ipos;
+}
+
 void upload_level(stamg_ctx* c, DevLevel& L) {
-  const auto& t = L.t;
   cudaStream_t s = c->stream;
-  L.n = int64_t(t.n_el) * t.P * 4;
+  {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const auto& t0 = L.t;
+    if (c->wl_allowed && !t0.groups8.empty() && t0.nx >= 36 && t0.ny >= 32 &&
+        int(t0.group8_oct.size()) >= 2 * sms && std::getenv("STAMG_SWEEP_DIRS4") == nullptr &&
+        std::getenv("STAMG_NO_WAVEFRONT_LAYOUT") == nullptr) {
+      L.ipos = apply_internal_order(L.t);
+      L.wl.nx = t0.nx, L.wl.ny = t0.ny, L.wl.R = 32, L.wl.nd = t0.nx + 32 - 1;
+      L.wl.slots = (long long)((t0.ny + 31) / 32) * L.wl.nd * 32;
+    }
+  }
+  const auto& t = L.t;
+  L.n = L.wl.nd ? int64_t(t.group8_oct.size()) * L.wl.slots * 32 : int64_t(t.n_el) * t.P * 4;
+  if (L.wl.nd) {
+    std::vector<int> iid(t.P);
+    for (int k = 0; k < t.P; ++k) iid[k] = k;
+    L.d_ipos = dupload(L.ipos, s), L.d_iid = dupload(iid, s);
+  }
   L.Hp = round_up(t.H, 64);
   L.Pk = round_up(t.P, 16);
   L.Pp = round_up(t.P, 64);
@@ -244,6 +319,10 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
       std::getenv("STAMG_SWEEP_DIRS4") == nullptr) {
     L.groups8 = dupload(t.groups8, s), L.group8_oct = dupload(t.group8_oct, s);
     L.sweep_top = dalloc<double2>(t.group8_oct.size() * 8 * size_t(t.nx));
+  }
+  if (L.wl.nd) {
+    if (!L.groups8) throw std::logic_error("wavefront layout needs the 8-direction groups");
+    L.wl.goct = L.group8_oct;
   }
   L.oct_patches = dupload(t.oct_patches, s), L.oct_ptr = dupload(t.oct_ptr, s);
   if (!t.BinvGS.empty()) {
@@ -342,6 +421,7 @@ void free_level(DevLevel& L) {
                   (void*)L.BinvGS, (void*)L.sq, (void*)L.area, (void*)L.up_w, (void*)L.groups, (void*)L.group_oct,
                   (void*)L.oct_patches, (void*)L.oct_ptr, (void*)L.up, (void*)L.child_ptr, (void*)L.child_idx,
                   (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_K, (void*)L.gs_Xo, (void*)L.gs_XoT, (void*)L.gs_G, (void*)L.Xf, (void*)L.XfT, (void*)L.groups8, (void*)L.group8_oct, (void*)L.sweep_top,
+                  (void*)L.d_ipos, (void*)L.d_iid, (void*)L.stage,
                   (void*)L.sigf, (void*)L.foldbuf, (void*)L.orbit, (void*)L.tmp, (void*)L.cf,
                   (void*)L.ce})
     if (p) cudaFree(p);
@@ -369,6 +449,18 @@ void op_allreduce(stamg_ctx* c, double* buf, size_t n) {
 void op_apply_L(stamg_ctx* c, DevLevel& L, const double* x, double* y, double alpha = 1.0, double beta = 0.0,
                 const double* f = nullptr) {
   Timed tm(c, "apply_L");
+  if (L.wl.nd) {  // wavefront layout: the sweep's skewed schedule, apply_L arithmetic
+    SweepParams p;
+    p.g = geom(c, L);
+    p.dirs = 8, p.top = L.sweep_top, p.wl = L.wl, p.mode = 1;
+    p.g.groups = L.groups8, p.g.group_oct = L.group8_oct, p.g.n_groups = int(L.t.group8_oct.size());
+    p.rhs = x, p.z = y, p.base = (f && beta != 0.0) ? f : nullptr, p.alpha = alpha, p.beta = beta;
+    p.Bfwd = L.B, p.Binv = L.Binv, p.cxy = L.cxy;
+    launch_sweep(p, c->stream);
+    ck_launch("apply_L");
+    c->launches += 1;
+    return;
+  }
   ApplyLParams p;
   p.g = geom(c, L);
   if (L.groups8) {
@@ -384,6 +476,7 @@ void op_apply_L(stamg_ctx* c, DevLevel& L, const double* x, double* y, double al
 void op_d2m(stamg_ctx* c, DevLevel& L, const double* phi, int order, double* out, const double* sig, bool identity_N) {
   Timed tm(c, "d2m");
   D2MParams p;
+  p.wl = L.wl;
   p.phi = phi, p.src = out, p.X = L.X, p.sig = sig, p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
   p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.Hused = (order + 1) * (order + 1);
   for (int k = 0; k < 16; ++k) p.N[k] = identity_N ? ((k % 5) == 0 ? 1.0 : 0.0) : L.t.Nmat[k];
@@ -395,6 +488,7 @@ void op_d2m(stamg_ctx* c, DevLevel& L, const double* phi, int order, double* out
 void op_m2d(stamg_ctx* c, DevLevel& L, int order, double scale, double beta, double* y, const double* ext) {
   Timed tm(c, "m2d");
   M2DParams p;
+  p.wl = L.wl;
   p.src = L.src, p.y = y, p.XT = L.XT, p.n_el = L.t.n_el, p.P = L.t.P, p.Pp = L.Pp, p.Hp = L.Hp;
   p.Hused = (order + 1) * (order + 1), p.scale = scale, p.beta = beta, p.ext_q = ext, p.area = L.area;
   for (int i = 0; i < 4; ++i) p.nsum[i] = c->nsum[i];
@@ -423,7 +517,7 @@ void scatter_into(stamg_ctx* c, DevLevel& L, const double* phi, int order, doubl
   const size_t cls = size_t(n_el) * R * 4;
   {
     Timed tm(c, "fold");
-    launch_fold(phi, L.foldbuf, L.orbit, n_el, L.t.P, R, G, c->stream);
+    launch_fold(phi, L.foldbuf, L.orbit, n_el, L.t.P, R, G, L.wl, c->stream);
     ck_launch("fold");
     c->launches += 1;
   }
@@ -461,7 +555,7 @@ void scatter_into(stamg_ctx* c, DevLevel& L, const double* phi, int order, doubl
     c->launches += 1;
   }
   Timed tm(c, "unfold");
-  launch_unfold(L.foldbuf, y, L.orbit, n_el, L.t.P, R, G, scale, beta, ext, L.area, c->nsum, c->stream);
+  launch_unfold(L.foldbuf, y, L.orbit, n_el, L.t.P, R, G, scale, beta, ext, L.area, c->nsum, L.wl, c->stream);
   ck_launch("unfold");
   c->launches += 1;
 }
@@ -489,7 +583,7 @@ void op_sweep(stamg_ctx* c, DevLevel& L, const double* rhs, double* z, const dou
   SweepParams p;
   p.g = geom(c, L);
   if (L.sweep_top) {
-    p.dirs = 8, p.top = L.sweep_top;
+    p.dirs = 8, p.top = L.sweep_top, p.wl = L.wl;
     p.g.groups = L.groups8, p.g.group_oct = L.group8_oct, p.g.n_groups = int(L.t.group8_oct.size());
   }
   p.rhs = rhs, p.z = z, p.base = base, p.Binv = L.Binv, p.cxy = L.cxy;
@@ -824,6 +918,51 @@ stamg_report op_bicgstab(stamg_ctx* c, int precond, const double* b, double* x, 
   return finish();
 }
 
+// host (reference layout, or internal patch order with `internal`) <-> device vector of a level
+void host_to_vec(stamg_ctx* c, DevLevel& L, const double* host, double* dev, bool internal) {
+  const int64_t nref = int64_t(L.t.n_el) * L.t.P * 4;
+  if (!L.wl.nd) {
+    ck(cudaMemcpyAsync(dev, host, nref * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+    return;
+  }
+  const int64_t per_el = int64_t(L.t.P) * 4;
+  const int chunk = int(std::max<int64_t>(1, std::min<int64_t>(L.t.n_el, (int64_t(64) << 20) / per_el)));
+  if (L.stage_n < chunk * per_el) {
+    if (L.stage) cudaFree(L.stage);
+    L.stage = dalloc<double>(size_t(chunk) * per_el);
+    L.stage_n = chunk * per_el;
+  }
+  for (int el0 = 0; el0 < L.t.n_el; el0 += chunk) {
+    const int n = std::min(chunk, L.t.n_el - el0);
+    ck(cudaMemcpyAsync(L.stage, host + el0 * per_el, n * per_el * sizeof(double), cudaMemcpyHostToDevice, c->stream),
+       "h2d");
+    launch_to_wl(L.stage, dev, internal ? L.d_iid : L.d_ipos, el0, n, L.t.P, L.wl, c->stream);
+    ck_launch("to_wl");
+  }
+}
+void vec_to_host(stamg_ctx* c, DevLevel& L, const double* dev, double* host, bool internal) {
+  const int64_t nref = int64_t(L.t.n_el) * L.t.P * 4;
+  if (!L.wl.nd) {
+    ck(cudaMemcpyAsync(host, dev, nref * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    return;
+  }
+  const int64_t per_el = int64_t(L.t.P) * 4;
+  const int chunk = int(std::max<int64_t>(1, std::min<int64_t>(L.t.n_el, (int64_t(64) << 20) / per_el)));
+  if (L.stage_n < chunk * per_el) {
+    if (L.stage) cudaFree(L.stage);
+    L.stage = dalloc<double>(size_t(chunk) * per_el);
+    L.stage_n = chunk * per_el;
+  }
+  for (int el0 = 0; el0 < L.t.n_el; el0 += chunk) {
+    const int n = std::min(chunk, L.t.n_el - el0);
+    launch_from_wl(dev, L.stage, internal ? L.d_iid : L.d_ipos, el0, n, L.t.P, L.wl, c->stream);
+    ck_launch("from_wl");
+    ck(cudaMemcpyAsync(host + el0 * per_el, L.stage, n * per_el * sizeof(double), cudaMemcpyDeviceToHost, c->stream),
+       "d2h");
+  }
+}
+int64_t ref_size(const DevLevel& L) { return int64_t(L.t.n_el) * L.t.P * 4; }
+
 template <class F>
 int guard(F&& f) {
   try {
@@ -875,6 +1014,7 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
     c->rank = opt ? opt->rank : 0;
     c->world = opt ? std::max(1, opt->world) : 1;
     const bool want_mg = opt ? opt->build_hierarchy != 0 : true;
+    c->wl_allowed = !want_mg;  // wavefront layout only for contexts without a hierarchy
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
     if (c->world > 1) {
@@ -1019,28 +1159,33 @@ int stamg_vec_free(stamg_vec* v) {
   });
 }
 int stamg_vec_size(stamg_vec* v, int64_t* n) {
-  return guard([&] { *n = v->n; });
+  // host-visible length in the reference layout (device storage may be padded)
+  return guard([&] { *n = ref_size(level_of(v->ctx, v->level)); });
 }
 int stamg_vec_device_ptr(stamg_vec* v, double** p) {
   return guard([&] { *p = v->d; });
 }
 int stamg_vec_upload(stamg_ctx* c, stamg_vec* v, const double* host, int64_t n) {
   return guard([&] {
-    if (n != v->n) throw std::invalid_argument("vec_upload: layout mismatch");
-    ck(cudaMemcpyAsync(v->d, host, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+    DevLevel& L = level_of(c, v->level);
+    if (n != ref_size(L)) throw std::invalid_argument("vec_upload: layout mismatch");
+    host_to_vec(c, L, host, v->d, false);
     ck(cudaStreamSynchronize(c->stream), "sync");
   });
 }
 int stamg_vec_download(stamg_ctx* c, const stamg_vec* v, double* host, int64_t n) {
   return guard([&] {
-    if (n != v->n) throw std::invalid_argument("vec_download: layout mismatch");
-    ck(cudaMemcpyAsync(host, v->d, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    DevLevel& L = level_of(c, v->level);
+    if (n != ref_size(L)) throw std::invalid_argument("vec_download: layout mismatch");
+    vec_to_host(c, L, v->d, host, false);
     ck(cudaStreamSynchronize(c->stream), "sync");
   });
 }
 int stamg_vec_fill(stamg_ctx* c, stamg_vec* v, double value) {
   return guard([&] {
-    launch_fill(v->d, value, v->n, c->stream);
+    DevLevel& L = level_of(c, v->level);
+    if (L.wl.nd && value != 0.0) launch_wl_fill(v->d, value, L.t.n_el, L.t.P, L.wl, c->stream);
+    else launch_fill(v->d, value, v->n, c->stream);
     ck_launch("fill");
   });
 }
@@ -1141,8 +1286,8 @@ int stamg_mg_apply(stamg_ctx* c, const stamg_vec* r, stamg_vec* z) {
 int stamg_rhs(stamg_ctx* c, stamg_vec* f) {
   return guard([&] {
     need(f, c->outer, "assemble_rhs");
-    const auto v = assemble_rhs(c->pb, c->outer.t, c->tree);
-    ck(cudaMemcpyAsync(f->d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+    const auto v = assemble_rhs(c->pb, c->outer.t, c->tree);  // tables' (internal) patch order
+    host_to_vec(c, c->outer, v.data(), f->d, true);
     ck(cudaStreamSynchronize(c->stream), "sync");
   });
 }
@@ -1165,15 +1310,16 @@ int stamg_solve(stamg_ctx* c, int method, int precond, const stamg_vec* b, stamg
 int stamg_sweep_host(stamg_ctx* c, int level, const double* rhs, double* z, int64_t n) {
   return guard([&] {
     DevLevel& L = level_of(c, level);
-    if (n != L.n) throw std::invalid_argument("standard_sweep: layout mismatch");
-    if (c->hostio_n < n) {
+    if (n != ref_size(L)) throw std::invalid_argument("standard_sweep: layout mismatch");
+    if (c->hostio_n < L.n) {
       if (c->hostio) cudaFree(c->hostio);
-      c->hostio = dalloc<double>(n);
-      c->hostio_n = n;
+      c->hostio = dalloc<double>(L.n);
+      c->hostio_n = L.n;
+      ck(cudaMemsetAsync(c->hostio, 0, L.n * sizeof(double), c->stream), "memset");
     }
-    ck(cudaMemcpyAsync(c->hostio, rhs, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+    host_to_vec(c, L, rhs, c->hostio, false);
     op_sweep(c, L, c->hostio, c->hostio);
-    ck(cudaMemcpyAsync(z, c->hostio, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    vec_to_host(c, L, c->hostio, z, false);
     ck(cudaStreamSynchronize(c->stream), "sync");
   });
 }
@@ -1181,15 +1327,16 @@ int stamg_sweep_host(stamg_ctx* c, int level, const double* rhs, double* z, int6
 int stamg_solve_host(stamg_ctx* c, int method, int precond, const double* bh, double* xh, int64_t n, double tol,
                      int max_iter, int restart, stamg_report* rep) {
   return guard([&] {
-    if (n != c->outer.n) throw std::invalid_argument("solve: layout mismatch");
-    double* b = dalloc<double>(n);
-    double* x = dalloc<double>(n);
+    if (n != ref_size(c->outer)) throw std::invalid_argument("solve: layout mismatch");
+    double* b = dalloc<double>(c->outer.n);
+    double* x = dalloc<double>(c->outer.n);
+    ck(cudaMemsetAsync(b, 0, c->outer.n * sizeof(double), c->stream), "memset");
     try {
-      ck(cudaMemcpyAsync(b, bh, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+      host_to_vec(c, c->outer, bh, b, false);
       std::vector<double> hist;
       stamg_report r = method == 0 ? op_bicgstab(c, precond, b, x, tol, max_iter, hist)
                                    : op_gmres(c, precond, b, x, tol, max_iter, restart, hist);
-      ck(cudaMemcpyAsync(xh, x, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+      vec_to_host(c, c->outer, x, xh, false);
       ck(cudaStreamSynchronize(c->stream), "sync");
       if (rep) *rep = r;
     } catch (...) {
@@ -1203,8 +1350,8 @@ int stamg_solve_host(stamg_ctx* c, int method, int precond, const double* bh, do
 int stamg_scalar_flux(stamg_ctx* c, const stamg_vec* phi, double* out) {
   return guard([&] {
     need(phi, c->outer, "scalar_flux");
-    std::vector<double> h(phi->n);
-    ck(cudaMemcpyAsync(h.data(), phi->d, phi->n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    std::vector<double> h(ref_size(c->outer));
+    vec_to_host(c, c->outer, phi->d, h.data(), true);  // tables' (internal) patch order
     ck(cudaStreamSynchronize(c->stream), "sync");
     const auto& t = c->outer.t;
     const double vol = c->pb.h * c->pb.h;

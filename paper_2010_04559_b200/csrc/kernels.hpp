@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "common.cuh"
+
 namespace stamg_b200 {
 
 // Common per-level geometry of the wavefront / stencil kernels: direction
@@ -22,6 +24,10 @@ struct GroupGeom {
 struct SweepParams {
   GroupGeom g;                   // groups of g-width directions (4, or 8 when dirs == 8)
   int dirs = 4;
+  WLGeom wl;                     // wl.nd > 0: vectors in the wavefront layout (dirs == 8)
+  int mode = 0;                  // 0: z = [base +] L^{-1} rhs;  1: z = alpha*L rhs + beta*base (apply_L)
+  const double* Bfwd = nullptr;  // mode 1: forward blocks [n_mat][P][16]
+  double alpha = 1.0, beta = 0.0;
   double2* top = nullptr;        // dirs == 8: [n_groups][8][nx] strip-boundary trace scratch
   const double* rhs = nullptr;
   const double* base = nullptr;
@@ -48,6 +54,7 @@ void launch_apply_L(const ApplyLParams& p, cudaStream_t s);
 // src[el][h][i] = sig[mat(el)][h] * sum_j (sum_{q} X[q][h] phi[el][q][j]) N[j][i]
 // for h < Hused (zero above), on FP64 tensor cores.
 struct D2MParams {
+  WLGeom wl;                     // wl.nd > 0: phi in the wavefront layout (P = internal order)
   const double* phi = nullptr;
   double* src = nullptr;         // [n_el][Hp][4]
   const double* X = nullptr;     // [Pk][Hp]   (rows >= P are zero)
@@ -61,6 +68,7 @@ void launch_d2m(const D2MParams& p, cudaStream_t s);
 // M2D (scatter.cpp:132): y[el][q][i] = beta*y + scale * sum_h X[q][h] src[el][h][i]
 //   + (ext_q ? ext_q[el]/(4 pi) * area[q] * nsum[i] : 0)
 struct M2DParams {
+  WLGeom wl;                     // wl.nd > 0: y in the wavefront layout
   const double* src = nullptr;   // [n_el][Hp][4]
   double* y = nullptr;
   const double* XT = nullptr;    // [Hp][Pp]
@@ -75,9 +83,18 @@ void launch_m2d(const M2DParams& p, cudaStream_t s);
 // reflection-symmetry fold / unfold around the per-class moment GEMMs:
 // Phi[c][el][r][i] = sum_g chi_c(g) phi[el][orbit[r][g]][i];
 // y[el][orbit[r][g]][i] = beta*y + scale*sum_c chi_c(g) Y[c][el][r][i] (+ isotropic source)
-void launch_fold(const double* phi, double* Phi, const int* orbit, int n_el, int P, int R, int G, cudaStream_t s);
+void launch_fold(const double* phi, double* Phi, const int* orbit, int n_el, int P, int R, int G, const WLGeom& wl,
+                 cudaStream_t s);
 void launch_unfold(const double* Y, double* y, const int* orbit, int n_el, int P, int R, int G, double scale,
-                   double beta, const double* ext_q, const double* area, const double* nsum, cudaStream_t s);
+                   double beta, const double* ext_q, const double* area, const double* nsum, const WLGeom& wl,
+                   cudaStream_t s);
+// reference layout [el][q][4] (patch q mapped to internal k = perm[q]) <-> wavefront layout,
+// for elements [el0, el0 + n_el_chunk)
+void launch_to_wl(const double* ref, double* wlv, const int* perm, int el0, int n_el_chunk, int P, const WLGeom& wl,
+                  cudaStream_t s);
+void launch_from_wl(const double* wlv, double* ref, const int* perm, int el0, int n_el_chunk, int P,
+                    const WLGeom& wl, cudaStream_t s);
+void launch_wl_fill(double* dst, double v, int n_el, int P, const WLGeom& wl, cudaStream_t s);
 
 // transfers (multigrid.cpp:100-136), Const basis
 void launch_prolong(const double* coarse, double* fine, const int* up, const double* w, int n_el, int Pf,

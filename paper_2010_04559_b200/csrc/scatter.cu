@@ -37,16 +37,17 @@ __device__ __forceinline__ void load_tile_rows(double* sA, const double* src, in
   }
 }
 
-// D2M B tile: sB[k][e*4+i] = phi[((el0+e)*P + q0+k)*4 + i]
+// D2M B tile: sB[k][e*4+i] = phi[((el0+e)*P + q0+k)*4 + i] (or its wavefront-layout block)
 __device__ __forceinline__ void load_phi_tile(double* sB, const double* phi, int P, int n_el, int q0, int el0,
-                                              int tid) {
+                                              int tid, const WLGeom& wl) {
 #pragma unroll
   for (int it = 0; it < (BK * BN / 2) / kThreads; ++it) {
     const int chunk = tid + it * kThreads;       // 512 chunks: e (16) x k (16) x half (2)
     const int half = chunk & 1, k = (chunk >> 1) & (BK - 1), e = chunk >> 5;
     const bool ok = (el0 + e) < n_el && (q0 + k) < P;
-    const double* g = phi + (ok ? (((size_t)(el0 + e) * P + q0 + k) * 4 + half * 2) : 0);
-    cp_async16(sB + k * LDS + e * 4 + half * 2, g, ok);
+    size_t off = 0;
+    if (ok) off = wl.nd ? (size_t)wl_block(wl, el0 + e, q0 + k) * 4 : ((size_t)(el0 + e) * P + q0 + k) * 4;
+    cp_async16(sB + k * LDS + e * 4 + half * 2, phi + off + (ok ? half * 2 : 0), ok);
   }
 }
 
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kThreads) d2m_kernel(D2MParams p) {
     if (s < nk) {
       double* st = smem + s * kStageDoubles;
       load_tile_rows(st, p.X, p.Hp, s * BK, h0, Pk, tid);
-      load_phi_tile(st + BK * LDS, p.phi, p.P, p.n_el, s * BK, el0, tid);
+      load_phi_tile(st + BK * LDS, p.phi, p.P, p.n_el, s * BK, el0, tid, p.wl);
     }
     cp_async_commit();
   }
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(kThreads) d2m_kernel(D2MParams p) {
     if (nxt < nk) {
       double* st = smem + (nxt % NSTAGE) * kStageDoubles;
       load_tile_rows(st, p.X, p.Hp, nxt * BK, h0, Pk, tid);
-      load_phi_tile(st + BK * LDS, p.phi, p.P, p.n_el, nxt * BK, el0, tid);
+      load_phi_tile(st + BK * LDS, p.phi, p.P, p.n_el, nxt * BK, el0, tid, p.wl);
     }
     cp_async_commit();
     cp_async_wait<NSTAGE - 1>();
@@ -196,7 +197,7 @@ __global__ void __launch_bounds__(kThreads) m2d_kernel(M2DParams p) {
       const int el = el0 + e;
       if (el >= p.n_el) continue;
       const int i0 = (t & 1) * 2;
-      double* yp = p.y + ((size_t)el * p.P + q) * 4 + i0;
+      double* yp = p.y + (p.wl.nd ? (size_t)wl_block(p.wl, el, q) * 4 : ((size_t)el * p.P + q) * 4) + i0;
       double v0 = p.scale * acc[i][j][0], v1 = p.scale * acc[i][j][1];
       if (p.ext_q) {
         const double c = p.ext_q[el] * inv4pi * p.area[q];
@@ -232,14 +233,16 @@ __device__ __forceinline__ void wht(double (&v)[G][4]) {
 // Phi[c][el][r][i] = sum_g chi_c(g) phi[el][orbit[r][g]][i]
 template <int G>
 __global__ void fold_kernel(const double* __restrict__ phi, double* __restrict__ Phi, const int* __restrict__ orbit,
-                            int n_el, int P, int R) {
+                            int n_el, int P, int R, WLGeom wl) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n_el * R) return;
   const int el = int(idx / R), r = int(idx - (int64_t)el * R);
   double v[G][4];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    const double2* b = reinterpret_cast<const double2*>(phi + ((size_t)el * P + orbit[r * G + g]) * 4);
+    const int q = orbit[r * G + g];
+    const double2* b =
+        reinterpret_cast<const double2*>(phi + (wl.nd ? (size_t)wl_block(wl, el, q) * 4 : ((size_t)el * P + q) * 4));
     const double2 a0 = b[0], a1 = b[1];
     v[g][0] = a0.x, v[g][1] = a0.y, v[g][2] = a1.x, v[g][3] = a1.y;
   }
@@ -256,7 +259,7 @@ __global__ void fold_kernel(const double* __restrict__ phi, double* __restrict__
 template <int G>
 __global__ void unfold_kernel(const double* __restrict__ Y, double* __restrict__ y, const int* __restrict__ orbit,
                               int n_el, int P, int R, double scale, double beta, const double* __restrict__ ext_q,
-                              const double* __restrict__ area, double4 nsum) {
+                              const double* __restrict__ area, double4 nsum, WLGeom wl) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n_el * R) return;
   const int el = int(idx / R), r = int(idx - (int64_t)el * R);
@@ -272,7 +275,7 @@ __global__ void unfold_kernel(const double* __restrict__ Y, double* __restrict__
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const int q = orbit[r * G + g];
-    double2* o = reinterpret_cast<double2*>(y + ((size_t)el * P + q) * 4);
+    double2* o = reinterpret_cast<double2*>(y + (wl.nd ? (size_t)wl_block(wl, el, q) * 4 : ((size_t)el * P + q) * 4));
     double w0 = scale * v[g][0], w1 = scale * v[g][1], w2 = scale * v[g][2], w3 = scale * v[g][3];
     if (ext_q) {
       const double c = ext_q[el] * inv4pi * area[q];
@@ -287,28 +290,70 @@ __global__ void unfold_kernel(const double* __restrict__ Y, double* __restrict__
   }
 }
 
+// reference layout [el][q][4] (q -> internal k = perm[q]) <-> wavefront layout
+template <bool TO_WL>
+__global__ void wl_convert_kernel(const double* __restrict__ src, double* __restrict__ dst, const int* __restrict__ perm,
+                                  int el0, int n_el_chunk, int P, WLGeom wl) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (el, q) of the chunk
+  if (idx >= (int64_t)n_el_chunk * P) return;
+  const int e = int(idx / P), q = int(idx - (int64_t)e * P);
+  const size_t refo = (size_t)idx * 4;  // chunk-relative reference offset
+  const size_t wlo = (size_t)wl_block(wl, el0 + e, perm[q]) * 4;
+  const double2* a = reinterpret_cast<const double2*>(src + (TO_WL ? refo : wlo));
+  double2* b = reinterpret_cast<double2*>(dst + (TO_WL ? wlo : refo));
+  const double2 v0 = a[0], v1 = a[1];
+  b[0] = v0, b[1] = v1;
+}
+
+// fill the valid blocks of a wavefront-layout vector (padding stays zero)
+__global__ void wl_fill_kernel(double* __restrict__ dst, double v, int n_el, int P, WLGeom wl) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n_el * P) return;
+  const int el = int(idx / P), k = int(idx - (int64_t)el * P);
+  double2* b = reinterpret_cast<double2*>(dst + (size_t)wl_block(wl, el, k) * 4);
+  b[0] = make_double2(v, v), b[1] = make_double2(v, v);
+}
+
 }  // namespace
 
-void launch_fold(const double* phi, double* Phi, const int* orbit, int n_el, int P, int R, int G, cudaStream_t s) {
+void launch_wl_fill(double* dst, double v, int n_el, int P, const WLGeom& wl, cudaStream_t s) {
+  const int64_t n = (int64_t)n_el * P;
+  if (n > 0) wl_fill_kernel<<<int((n + 255) / 256), 256, 0, s>>>(dst, v, n_el, P, wl);
+}
+
+void launch_to_wl(const double* ref, double* wlv, const int* perm, int el0, int n_el_chunk, int P, const WLGeom& wl,
+                  cudaStream_t s) {
+  const int64_t n = (int64_t)n_el_chunk * P;
+  if (n > 0) wl_convert_kernel<true><<<int((n + 255) / 256), 256, 0, s>>>(ref, wlv, perm, el0, n_el_chunk, P, wl);
+}
+void launch_from_wl(const double* wlv, double* ref, const int* perm, int el0, int n_el_chunk, int P,
+                    const WLGeom& wl, cudaStream_t s) {
+  const int64_t n = (int64_t)n_el_chunk * P;
+  if (n > 0) wl_convert_kernel<false><<<int((n + 255) / 256), 256, 0, s>>>(wlv, ref, perm, el0, n_el_chunk, P, wl);
+}
+
+void launch_fold(const double* phi, double* Phi, const int* orbit, int n_el, int P, int R, int G, const WLGeom& wl,
+                 cudaStream_t s) {
   const int64_t n = (int64_t)n_el * R;
   const int blocks = int((n + 255) / 256);
   switch (G) {
-    case 2: fold_kernel<2><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, P, R); break;
-    case 4: fold_kernel<4><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, P, R); break;
-    case 8: fold_kernel<8><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, P, R); break;
+    case 2: fold_kernel<2><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, P, R, wl); break;
+    case 4: fold_kernel<4><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, P, R, wl); break;
+    case 8: fold_kernel<8><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, P, R, wl); break;
     default: break;
   }
 }
 
 void launch_unfold(const double* Y, double* y, const int* orbit, int n_el, int P, int R, int G, double scale,
-                   double beta, const double* ext_q, const double* area, const double* nsum, cudaStream_t s) {
+                   double beta, const double* ext_q, const double* area, const double* nsum, const WLGeom& wl,
+                   cudaStream_t s) {
   const int64_t n = (int64_t)n_el * R;
   const int blocks = int((n + 255) / 256);
   const double4 ns = make_double4(nsum[0], nsum[1], nsum[2], nsum[3]);
   switch (G) {
-    case 2: unfold_kernel<2><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns); break;
-    case 4: unfold_kernel<4><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns); break;
-    case 8: unfold_kernel<8><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns); break;
+    case 2: unfold_kernel<2><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl); break;
+    case 4: unfold_kernel<4><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl); break;
+    case 8: unfold_kernel<8><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl); break;
     default: break;
   }
 }

@@ -30,8 +30,10 @@ constexpr int NST = 4;
 // one 256-byte run (better DRAM efficiency than 128 B), and the strip-boundary
 // traces go through an L2-resident global scratch (TOPG) instead of shared
 // memory so the CTA still fits 3 per SM.
-template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG>
+template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY = false, int MODE = 0>
 __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepParams p) {
+  // WLAY: vectors in the wavefront layout (a step's R rows are consecutive slots).
+  // MODE 1: apply_L on the same skewed schedule (y = alpha*(B x + C x_up) + beta*f, traces of x).
   // TOPG (8-direction) variant: 4 CTAs/SM (<= 64 registers), B^-1 read from shared memory
   constexpr int NT = DIRS * R;
   constexpr int NW = NT / 32;
@@ -60,14 +62,15 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepPa
   for (int k = 0; k < 4; ++k) cx[k] = p.cxy[qq * 8 + k], cy[k] = p.cxy[qq * 8 + 4 + k];
   constexpr bool BSMEM = MULTI || TOPG;
   double Bi[16];
+  const double* Bsrc = MODE == 1 ? p.Bfwd : p.Binv;
   if constexpr (!BSMEM) {
 #pragma unroll
-    for (int k = 0; k < 16; ++k) Bi[k] = p.Binv[qq * 16 + k];
+    for (int k = 0; k < 16; ++k) Bi[k] = Bsrc[qq * 16 + k];
   } else {
     for (int idx = tid; idx < p.g.n_mat * DIRS * 16; idx += NT) {
       const int m = idx / (DIRS * 16), d = (idx / 16) % DIRS, k = idx & 15;
       const int qd = p.g.groups[grp * DIRS + d];
-      sB[(m * DIRS + d) * 17 + k] = qd >= 0 ? p.Binv[((size_t)m * P + qd) * 16 + k] : 0.0;
+      sB[(m * DIRS + d) * 17 + k] = qd >= 0 ? Bsrc[((size_t)m * P + qd) * 16 + k] : 0.0;
     }
   }
 
@@ -82,16 +85,26 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepPa
     el = gy * nx + gx;
     return qok && j < ny;
   };
+  // offset (doubles) of this thread's block for wavefront position k (cell el)
+  auto offset = [&](int k, int el) -> size_t {
+    if constexpr (WLAY) {
+      const int s = k / nx, i = k - s * nx;
+      return (((size_t)grp * p.wl.slots + wl_slot_frame(p.wl, i, s * R + r)) * DIRS + dir) * 4;
+    } else {
+      return ((size_t)el * P + qq) * 4;
+    }
+  };
   auto issue = [&](int t) {
     int el = 0;
     const int k = t - r;
     const bool ok = locate(k, el);
-    const double* src = p.rhs + (ok ? ((size_t)el * P + qq) * 4 : 0);
+    const size_t off = ok ? offset(k, el) : 0;
+    const double* src = p.rhs + off;
     double* dst = st_rhs + ((t % NST) * NT + tid) * 4;
     cp_async16(dst, src, ok);
     cp_async16(dst + 2, src + 2, ok);
     if constexpr (ACCUM) {
-      const double* sb = p.base + (ok ? ((size_t)el * P + qq) * 4 : 0);
+      const double* sb = p.base + off;
       double* db = st_base + ((t % NST) * NT + tid) * 4;
       cp_async16(db, sb, ok);
       cp_async16(db + 2, sb + 2, ok);
@@ -141,11 +154,6 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepPa
       if (m & 1) { double u = r0; r0 = r1; r1 = u; u = r2; r2 = r3; r3 = u; }
       if (m & 2) { double u = r0; r0 = r2; r2 = u; u = r1; r1 = r3; r3 = u; }
       if (i == 0) tx = make_double2(0.0, 0.0);
-      // upwind couplings: x-face rows {0,2} <- left trace, y-face rows {0,1} <- lower trace
-      r0 -= cx[0] * tx.x + cx[1] * tx.y;
-      r2 -= cx[2] * tx.x + cx[3] * tx.y;
-      r0 -= cy[0] * ty.x + cy[1] * ty.y;
-      r1 -= cy[2] * ty.x + cy[3] * ty.y;
       const double* B = Bi;
       double Bm[16];
       if constexpr (BSMEM) {
@@ -154,20 +162,50 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepPa
         for (int kk = 0; kk < 16; ++kk) Bm[kk] = sB[(mt * DIRS + dir) * 17 + kk];
         B = Bm;
       }
-      double z0 = B[0] * r0 + B[1] * r1 + B[2] * r2 + B[3] * r3;
-      double z1 = B[4] * r0 + B[5] * r1 + B[6] * r2 + B[7] * r3;
-      double z2 = B[8] * r0 + B[9] * r1 + B[10] * r2 + B[11] * r3;
-      double z3 = B[12] * r0 + B[13] * r1 + B[14] * r2 + B[15] * r3;
-      tx = make_double2(z1, z3);
-      tyout = make_double2(z2, z3);
+      double z0, z1, z2, z3;
+      if constexpr (MODE == 0) {
+        // upwind couplings: x-face rows {0,2} <- left trace, y-face rows {0,1} <- lower trace
+        r0 -= cx[0] * tx.x + cx[1] * tx.y;
+        r2 -= cx[2] * tx.x + cx[3] * tx.y;
+        r0 -= cy[0] * ty.x + cy[1] * ty.y;
+        r1 -= cy[2] * ty.x + cy[3] * ty.y;
+        z0 = B[0] * r0 + B[1] * r1 + B[2] * r2 + B[3] * r3;
+        z1 = B[4] * r0 + B[5] * r1 + B[6] * r2 + B[7] * r3;
+        z2 = B[8] * r0 + B[9] * r1 + B[10] * r2 + B[11] * r3;
+        z3 = B[12] * r0 + B[13] * r1 + B[14] * r2 + B[15] * r3;
+        tx = make_double2(z1, z3);
+        tyout = make_double2(z2, z3);
+      } else {  // apply_L (transport.cpp:72-87): y = B x + C_x x_left + C_y x_below
+        z0 = B[0] * r0 + B[1] * r1 + B[2] * r2 + B[3] * r3;
+        z1 = B[4] * r0 + B[5] * r1 + B[6] * r2 + B[7] * r3;
+        z2 = B[8] * r0 + B[9] * r1 + B[10] * r2 + B[11] * r3;
+        z3 = B[12] * r0 + B[13] * r1 + B[14] * r2 + B[15] * r3;
+        if (i > 0) {
+          z0 += cx[0] * tx.x + cx[1] * tx.y;
+          z2 += cx[2] * tx.x + cx[3] * tx.y;
+        }
+        if (s > 0 || r > 0) {
+          z0 += cy[0] * ty.x + cy[1] * ty.y;
+          z1 += cy[2] * ty.x + cy[3] * ty.y;
+        }
+        tx = make_double2(r1, r3);
+        tyout = make_double2(r2, r3);
+      }
       // frame -> physical
       if (m & 2) { double u = z0; z0 = z2; z2 = u; u = z1; z1 = z3; z3 = u; }
       if (m & 1) { double u = z0; z0 = z1; z1 = u; u = z2; z2 = z3; z3 = u; }
       if constexpr (ACCUM) {
         const double* bs = st_base + ((t % NST) * NT + tid) * 4;
-        z0 += bs[0], z1 += bs[1], z2 += bs[2], z3 += bs[3];
+        if constexpr (MODE == 0) {
+          z0 += bs[0], z1 += bs[1], z2 += bs[2], z3 += bs[3];
+        } else {
+          z0 = p.alpha * z0 + p.beta * bs[0], z1 = p.alpha * z1 + p.beta * bs[1];
+          z2 = p.alpha * z2 + p.beta * bs[2], z3 = p.alpha * z3 + p.beta * bs[3];
+        }
+      } else if constexpr (MODE == 1) {
+        z0 *= p.alpha, z1 *= p.alpha, z2 *= p.alpha, z3 *= p.alpha;
       }
-      double* out = p.z + ((size_t)el * P + q) * 4;
+      double* out = p.z + offset(k, el);
       reinterpret_cast<double2*>(out)[0] = make_double2(z0, z1);
       reinterpret_cast<double2*>(out)[1] = make_double2(z2, z3);
     }
@@ -183,23 +221,23 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepPa
   (void)RPW;
 }
 
-template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG>
+template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY = false, int MODE = 0>
 void launch_t(const SweepParams& p, cudaStream_t s) {
   constexpr int NT = DIRS * R;
   size_t smem = sizeof(double) * NST * NT * 4 * (ACCUM ? 2 : 1) +
                 sizeof(double2) * ((TOPG ? NST * DIRS : DIRS * p.g.nx) + 2 * (NT / 32) * DIRS) +
                 ((MULTI || TOPG) ? sizeof(double) * p.g.n_mat * DIRS * 17 : 0);
-  auto k = sweep_kernel<DIRS, R, MULTI, ACCUM, TOPG>;
+  auto k = sweep_kernel<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<p.g.n_groups, NT, smem, s>>>(p);
 }
 
-template <int DIRS, int R, bool TOPG>
+template <int DIRS, int R, bool TOPG, bool WLAY = false, int MODE = 0>
 void launch_r(const SweepParams& p, cudaStream_t s) {
   const bool multi = p.g.n_mat > 1;
   const bool acc = p.base != nullptr;
-  if (multi) acc ? launch_t<DIRS, R, true, true, TOPG>(p, s) : launch_t<DIRS, R, true, false, TOPG>(p, s);
-  else acc ? launch_t<DIRS, R, false, true, TOPG>(p, s) : launch_t<DIRS, R, false, false, TOPG>(p, s);
+  if (multi) acc ? launch_t<DIRS, R, true, true, TOPG, WLAY, MODE>(p, s) : launch_t<DIRS, R, true, false, TOPG, WLAY, MODE>(p, s);
+  else acc ? launch_t<DIRS, R, false, true, TOPG, WLAY, MODE>(p, s) : launch_t<DIRS, R, false, false, TOPG, WLAY, MODE>(p, s);
 }
 
 }  // namespace
@@ -216,7 +254,13 @@ void launch_sweep(const SweepParams& p, cudaStream_t s) {
   if (p.g.nx < 8) throw std::invalid_argument("sweep: nx must be >= 8 on the B200 path");
   if (p.dirs == 8) {  // 8-direction groups, R = 32, traces across strips through the L2 scratch
     if (p.g.nx < 32 + NST || p.g.ny < 32 || !p.top) throw std::invalid_argument("sweep: 8-direction groups need nx, ny >= 36");
-    launch_r<8, 32, true>(p, s);
+    if (p.wl.nd > 0) {
+      if (p.wl.R != 32) throw std::invalid_argument("sweep: wavefront layout strip height must be 32");
+      p.mode == 1 ? launch_r<8, 32, true, true, 1>(p, s) : launch_r<8, 32, true, true, 0>(p, s);
+    } else {
+      if (p.mode == 1) throw std::invalid_argument("sweep kernel apply_L mode needs the wavefront layout");
+      launch_r<8, 32, true>(p, s);
+    }
     return;
   }
   const int R = sweep_rows_for(p.g.nx, p.g.ny);
