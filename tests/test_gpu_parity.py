@@ -205,8 +205,9 @@ def test_sweep_8dir_groups(orc, stamg, k):
     assert rel(phi.numpy(), o.smoother(f, nr, phi0, level=l)) < 1e-12
 
 
+@pytest.mark.parametrize("wl", [True, False], ids=["wavefront", "reference"])
 @pytest.mark.parametrize("k", [5, 3])
-def test_wavefront_layout_context(orc, stamg, k):
+def test_wavefront_layout_context(orc, stamg, k, wl, monkeypatch):
     """A context without a hierarchy (the throughput path) stores vectors in the
     wavefront layout: upload/download round-trip exactly, and sweep, apply_L,
     scatter (folded), apply_A, rhs, scalar flux, the source iteration and a
@@ -215,6 +216,8 @@ def test_wavefront_layout_context(orc, stamg, k):
     st, mo = spec.kernel_arrays()
     spec.angular_level, spec.N, spec.n_levels = 5, 11, 1  # H = 144 >= 128: folded scatter
     spec.moments = mo[:, : spec.N + 1]
+    if wl:
+        monkeypatch.setenv("STAMG_WAVEFRONT_LAYOUT", "1")
     o = orc.Oracle(spec)
     g = stamg.Context(spec, build_hierarchy=False)
     x = rnd(o.size(), 31)
