@@ -249,3 +249,16 @@ def test_wavefront_layout_context(orc, stamg, k, wl, monkeypatch):
         assert rel(psi.numpy(), ref) < 1e-12
     ones = g.vec().fill(1.0)
     assert np.array_equal(ones.numpy(), np.ones(o.size()))
+
+
+@pytest.mark.parametrize("precond", ["mg", "sweep"])
+def test_bicgstab_parity(pair, precond):
+    """The reference's own Krylov method (krylov.cpp:9-93) on the device."""
+    spec, o, g = pair
+    if precond == "sweep" and spec.name in ("c3", "c4"):
+        pytest.skip("sweep-preconditioned BiCGSTAB needs hundreds of iterations at c = 0.999+")
+    xo, ro = o.solve("bicgstab", precond, max_iter=400)
+    xg, rg = g.solve(g.rhs(), "bicgstab", precond, max_iter=400)
+    assert ro["converged"] and rg["converged"]
+    assert abs(rg["iterations"] - ro["iterations"]) <= 1
+    assert rel(g.scalar_flux(xg), o.scalar_flux(xo)) < 1e-7
