@@ -78,27 +78,42 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepPa
   const int nk = nstrips * nx;
   const int T = nk + R - 1;
 
-  auto locate = [&](int k, int& el) -> bool {
-    if (k < 0 || k >= nk) return false;
-    const int s = k / nx, i = k - s * nx, j = s * R + r;
-    const int gx = xneg ? nx - 1 - i : i, gy = yneg ? ny - 1 - j : j;
-    el = gy * nx + gx;
-    return qok && j < ny;
+  // Cursor over this thread's wavefront positions k: strip s, column i, cell el and
+  // block offset, advanced incrementally (no integer division inside a strip).
+  struct Cursor {
+    int k, s, i, el;
+    bool ok, kin;
+    size_t off;
   };
-  // offset (doubles) of this thread's block for wavefront position k (cell el)
-  auto offset = [&](int k, int el) -> size_t {
-    if constexpr (WLAY) {
-      const int s = k / nx, i = k - s * nx;
-      return (((size_t)grp * p.wl.slots + wl_slot_frame(p.wl, i, s * R + r)) * DIRS + dir) * 4;
-    } else {
-      return ((size_t)el * P + qq) * 4;
+  const int dx = xneg ? -1 : 1;
+  auto fresh = [&](Cursor& c, int k) {
+    c.k = k;
+    c.kin = k >= 0 && k < nk;
+    if (!c.kin) {
+      c.ok = false, c.s = 0, c.i = 0, c.el = 0, c.off = 0;
+      return;
     }
+    c.s = k / nx, c.i = k - c.s * nx;
+    const int j = c.s * R + r;
+    c.ok = qok && j < ny;
+    const int gx = xneg ? nx - 1 - c.i : c.i, gy = yneg ? ny - 1 - j : (j < ny ? j : 0);
+    c.el = gy * nx + gx;
+    if constexpr (WLAY) c.off = (((size_t)grp * p.wl.slots + wl_slot_frame(p.wl, c.i, j)) * DIRS + dir) * 4;
+    else c.off = ((size_t)c.el * P + qq) * 4;
   };
-  auto issue = [&](int t) {
-    int el = 0;
-    const int k = t - r;
-    const bool ok = locate(k, el);
-    const size_t off = ok ? offset(k, el) : 0;
+  auto advance = [&](Cursor& c) {
+    const int k = c.k + 1;
+    if (k <= 0 || k >= nk || c.i + 1 == nx) {
+      fresh(c, k);
+      return;
+    }
+    c.k = k, c.i += 1, c.el += dx;
+    if constexpr (WLAY) c.off += (size_t)R * DIRS * 4;
+    else c.off += (size_t)dx * P * 4;
+  };
+  auto issue = [&](int t, const Cursor& c) {
+    const bool ok = c.ok;
+    const size_t off = ok ? c.off : 0;
     const double* src = p.rhs + off;
     double* dst = st_rhs + ((t % NST) * NT + tid) * 4;
     cp_async16(dst, src, ok);
@@ -111,28 +126,31 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepPa
     }
     if constexpr (TOPG) {  // row 0 of strip s >= 1 needs the trace row R-1 left in the scratch
       if (r == 0) {
-        const bool tk = k >= nx && k < nk;
-        const int i = tk ? k % nx : 0;
-        cp_async16(st_top + (t % NST) * DIRS + dir, gtop + (size_t)dir * nx + i, tk);
+        const bool tk = c.kin && c.s >= 1;
+        cp_async16(st_top + (t % NST) * DIRS + dir, gtop + (size_t)dir * nx + (tk ? c.i : 0), tk);
       }
     }
   };
+  Cursor ci, cc;  // issue cursor (k = t + NST - 1 - r) and compute cursor (k = t - r)
+  fresh(ci, -r);
+  fresh(cc, -r);
 #pragma unroll
   for (int t = 0; t < NST - 1; ++t) {
-    issue(t);
+    issue(t, ci);
     cp_async_commit();
+    advance(ci);
   }
   __syncthreads();
 
   const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
   double2 tx = make_double2(0.0, 0.0), typrev = make_double2(0.0, 0.0);
   for (int t = 0; t < T; ++t) {
-    issue(t + NST - 1);
+    issue(t + NST - 1, ci);
     cp_async_commit();
+    advance(ci);
     cp_async_wait<NST - 1>();
-    const int k = t - r;
-    const bool kin = k >= 0 && k < nk;
-    const int s = kin ? k / nx : 0, i = kin ? k - s * nx : 0;
+    const bool kin = cc.kin;
+    const int s = cc.s, i = cc.i;
     double2 ty;
     ty.x = __shfl_up_sync(0xffffffffu, typrev.x, DIRS);
     ty.y = __shfl_up_sync(0xffffffffu, typrev.y, DIRS);
@@ -146,8 +164,8 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepPa
       }
     }
     double2 tyout = make_double2(0.0, 0.0);
-    int el = 0;
-    if (locate(k, el)) {
+    const int el = cc.el;
+    if (cc.ok) {
       const double* rs = st_rhs + ((t % NST) * NT + tid) * 4;
       double r0 = rs[0], r1 = rs[1], r2 = rs[2], r3 = rs[3];
       // physical -> sweep frame (dof i -> i ^ m)
@@ -205,7 +223,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepPa
       } else if constexpr (MODE == 1) {
         z0 *= p.alpha, z1 *= p.alpha, z2 *= p.alpha, z3 *= p.alpha;
       }
-      double* out = p.z + offset(k, el);
+      double* out = p.z + cc.off;
       reinterpret_cast<double2*>(out)[0] = make_double2(z0, z1);
       reinterpret_cast<double2*>(out)[1] = make_double2(z2, z3);
     }
@@ -215,6 +233,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepPa
       else top[dir * nx + i] = tyout;
     }
     typrev = tyout;
+    advance(cc);
     __syncthreads();
   }
   cp_async_wait<0>();
