@@ -23,7 +23,7 @@ import numpy as np
 from .configs import ProblemSpec
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libstamg_b200.so")
+LIB_PATH = os.environ.get("STAMG_LIB") or os.path.join(_HERE, "libstamg_b200.so")  # override for A/B builds
 OUTER = -1
 
 dp = C.POINTER(C.c_double)
