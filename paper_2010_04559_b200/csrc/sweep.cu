@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepPa
     for (int idx = tid; idx < p.g.n_mat * DIRS * 16; idx += NT) {
       const int m = idx / (DIRS * 16), d = (idx / 16) % DIRS, k = idx & 15;
       const int qd = p.g.groups[grp * DIRS + d];
-      sB[(m * DIRS + d) * 18 + k] = qd >= 0 ? Bsrc[((size_t)m * P + qd) * 16 + k] : 0.0;
+      sB[(m * DIRS + d) * 17 + k] = qd >= 0 ? Bsrc[((size_t)m * P + qd) * 16 + k] : 0.0;
     }
   }
 
@@ -176,13 +176,8 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepPa
       double Bm[16];
       if constexpr (BSMEM) {
         const int mt = MULTI ? p.g.mat[el] : 0;
-        // row stride 18 doubles: 16-byte aligned and conflict-free across the 8 directions
-        const double2* b2 = reinterpret_cast<const double2*>(sB + (mt * DIRS + dir) * 18);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const double2 v = b2[kk];
-          Bm[2 * kk] = v.x, Bm[2 * kk + 1] = v.y;
-        }
+        for (int kk = 0; kk < 16; ++kk) Bm[kk] = sB[(mt * DIRS + dir) * 17 + kk];
         B = Bm;
       }
       double z0, z1, z2, z3;
@@ -250,7 +245,7 @@ void launch_t(const SweepParams& p, cudaStream_t s) {
   constexpr int NT = DIRS * R;
   size_t smem = sizeof(double) * NST * NT * 4 * (ACCUM ? 2 : 1) +
                 sizeof(double2) * ((TOPG ? NST * DIRS : DIRS * p.g.nx) + 2 * (NT / 32) * DIRS) +
-                ((MULTI || TOPG) ? sizeof(double) * p.g.n_mat * DIRS * 18 : 0);
+                ((MULTI || TOPG) ? sizeof(double) * p.g.n_mat * DIRS * 17 : 0);
   auto k = sweep_kernel<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<p.g.n_groups, NT, smem, s>>>(p);
