@@ -23,7 +23,13 @@
 namespace stamg_b200 {
 namespace {
 
-constexpr int NST = 4;
+#ifndef STAMG_SWEEP_NST
+#define STAMG_SWEEP_NST 4
+#endif
+#ifndef STAMG_SWEEP8_BREG
+#define STAMG_SWEEP8_BREG 0  // 1: 8-direction kernel keeps B^-1 in registers (2 CTAs/SM)
+#endif
+constexpr int NST = STAMG_SWEEP_NST;
 
 // DIRS directions x R rows per CTA (DIRS*R = 256 threads). thread = (dir, row):
 // dir = tid % DIRS, row = tid / DIRS. With DIRS = 8 a cell's 8 directions are
@@ -31,7 +37,7 @@ constexpr int NST = 4;
 // traces go through an L2-resident global scratch (TOPG) instead of shared
 // memory so the CTA still fits 3 per SM.
 template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY = false, int MODE = 0>
-__global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepParams p) {
+__global__ void __launch_bounds__(DIRS * R, (TOPG ? (STAMG_SWEEP8_BREG ? 2 : 4) : 1)) sweep_kernel(SweepParams p) {
   // WLAY: vectors in the wavefront layout (a step's R rows are consecutive slots).
   // MODE 1: apply_L on the same skewed schedule (y = alpha*(B x + C x_up) + beta*f, traces of x).
   // TOPG (8-direction) variant: 4 CTAs/SM (<= 64 registers), B^-1 read from shared memory
@@ -60,7 +66,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? 4 : 1)) sweep_kernel(SweepPa
   double cx[4], cy[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) cx[k] = p.cxy[qq * 8 + k], cy[k] = p.cxy[qq * 8 + 4 + k];
-  constexpr bool BSMEM = MULTI || TOPG;
+  constexpr bool BSMEM = MULTI || (TOPG && !STAMG_SWEEP8_BREG);
   double Bi[16];
   const double* Bsrc = MODE == 1 ? p.Bfwd : p.Binv;
   if constexpr (!BSMEM) {
