@@ -24,10 +24,10 @@ namespace stamg_b200 {
 namespace {
 
 #ifndef STAMG_SWEEP_NST
-#define STAMG_SWEEP_NST 4
+#define STAMG_SWEEP_NST 6
 #endif
 #ifndef STAMG_SWEEP8_BREG
-#define STAMG_SWEEP8_BREG 0  // 1: 8-direction kernel keeps B^-1 in registers (2 CTAs/SM)
+#define STAMG_SWEEP8_BREG 1  // 8-direction kernel keeps B^-1 in registers (2 CTAs/SM); A/B: 82.5 % vs 79 %
 #endif
 constexpr int NST = STAMG_SWEEP_NST;
 
