@@ -291,7 +291,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     L.d_ipos = dupload(L.ipos, s), L.d_iid = dupload(iid, s);
   }
   L.Hp = round_up(t.H, 64);
-  L.Pk = round_up(t.P, 16);
+  L.Pk = round_up(t.P, 32);  // X rows padded for any GEMM k-tile (16 or 32)
   L.Pp = round_up(t.P, 64);
   std::vector<double> X(size_t(L.Pk) * L.Hp, 0.0), XT(size_t(L.Hp) * L.Pp, 0.0), sig(size_t(t.n_mat) * L.Hp, 0.0);
   for (int q = 0; q < t.P; ++q)
@@ -396,7 +396,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
   if (t.n_sym_axes > 0 && t.H >= 128 && c->world == 1) {  // fold only where the GEMMs are big
     const int G = 1 << t.n_sym_axes, R = t.P / G;
     L.fold_G = G, L.fold_R = R, L.fold_Rp = round_up(R, 64);
-    const int Rk = round_up(R, 16);
+    const int Rk = round_up(R, 32);
     L.fold_hs.assign(G, {});
     for (int h = 0; h < t.H; ++h) L.fold_hs[t.hclass[h]].push_back(h);
     L.fold_hoff.assign(G + 1, 0);

@@ -18,7 +18,16 @@
 namespace stamg_b200 {
 namespace {
 
-constexpr int BM = 64, BN = 64, BK = 16, NSTAGE = 3;
+#ifndef STAMG_GEMM_BK
+#define STAMG_GEMM_BK 16
+#endif
+#ifndef STAMG_GEMM_NSTAGE
+#define STAMG_GEMM_NSTAGE 3
+#endif
+#ifndef STAMG_GEMM_SWAP
+#define STAMG_GEMM_SWAP 0  // 1: output-row tiles fastest in the grid (Phi / src panel reuse in L2)
+#endif
+constexpr int BM = 64, BN = 64, BK = STAMG_GEMM_BK, NSTAGE = STAMG_GEMM_NSTAGE;
 constexpr int LDS = BM + 4;  // padded row (conflict-free fragment loads)
 constexpr int kThreads = 128;
 constexpr int kStageDoubles = 2 * BK * LDS;
@@ -42,8 +51,8 @@ __device__ __forceinline__ void load_phi_tile(double* sB, const double* phi, int
                                               int tid, const WLGeom& wl) {
 #pragma unroll
   for (int it = 0; it < (BK * BN / 2) / kThreads; ++it) {
-    const int chunk = tid + it * kThreads;       // 512 chunks: e (16) x k (16) x half (2)
-    const int half = chunk & 1, k = (chunk >> 1) & (BK - 1), e = chunk >> 5;
+    const int chunk = tid + it * kThreads;       // e (16) x k (BK) x half (2)
+    const int half = chunk & 1, k = (chunk >> 1) & (BK - 1), e = chunk / (2 * BK);
     const bool ok = (el0 + e) < n_el && (q0 + k) < P;
     size_t off = 0;
     if (ok) off = wl.nd ? (size_t)wl_block(wl, el0 + e, q0 + k) * 4 : ((size_t)(el0 + e) * P + q0 + k) * 4;
@@ -57,7 +66,7 @@ __device__ __forceinline__ void load_src_tile(double* sB, const double* src, int
 #pragma unroll
   for (int it = 0; it < (BK * BN / 2) / kThreads; ++it) {
     const int chunk = tid + it * kThreads;
-    const int half = chunk & 1, k = (chunk >> 1) & (BK - 1), e = chunk >> 5;
+    const int half = chunk & 1, k = (chunk >> 1) & (BK - 1), e = chunk / (2 * BK);
     const bool ok = (el0 + e) < n_el;
     const double* g = src + (ok ? (((size_t)(el0 + e) * Hp + h0 + k) * 4 + half * 2) : 0);
     cp_async16(sB + k * LDS + e * 4 + half * 2, g, ok);
@@ -85,7 +94,8 @@ __global__ void __launch_bounds__(kThreads) d2m_kernel(D2MParams p) {
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;
-  const int el0 = blockIdx.x * (BN / 4), h0 = blockIdx.y * BM;
+  const int el0 = (STAMG_GEMM_SWAP ? blockIdx.y : blockIdx.x) * (BN / 4);
+  const int h0 = (STAMG_GEMM_SWAP ? blockIdx.x : blockIdx.y) * BM;
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -153,7 +163,8 @@ __global__ void __launch_bounds__(kThreads) m2d_kernel(M2DParams p) {
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;
-  const int el0 = blockIdx.x * (BN / 4), q0 = blockIdx.y * BM;
+  const int el0 = (STAMG_GEMM_SWAP ? blockIdx.y : blockIdx.x) * (BN / 4);
+  const int q0 = (STAMG_GEMM_SWAP ? blockIdx.x : blockIdx.y) * BM;
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -366,7 +377,8 @@ void launch_d2m(const D2MParams& p, cudaStream_t s) {
     cudaFuncSetAttribute(m2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
     init = true;
   }
-  dim3 grid((p.n_el + BN / 4 - 1) / (BN / 4), (p.Hused + BM - 1) / BM);
+  const unsigned ge = (p.n_el + BN / 4 - 1) / (BN / 4), gh = (p.Hused + BM - 1) / BM;
+  dim3 grid = STAMG_GEMM_SWAP ? dim3(gh, ge) : dim3(ge, gh);
   d2m_kernel<<<grid, kThreads, gemm_smem(), s>>>(p);
 }
 
@@ -378,7 +390,8 @@ void launch_m2d(const M2DParams& p, cudaStream_t s) {
     cudaFuncSetAttribute(m2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
     init = true;
   }
-  dim3 grid((p.n_el + BN / 4 - 1) / (BN / 4), (p.P + BM - 1) / BM);
+  const unsigned ge = (p.n_el + BN / 4 - 1) / (BN / 4), gq = (p.P + BM - 1) / BM;
+  dim3 grid = STAMG_GEMM_SWAP ? dim3(gq, ge) : dim3(ge, gq);
   m2d_kernel<<<grid, kThreads, gemm_smem(), s>>>(p);
 }
 
