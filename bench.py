@@ -147,6 +147,17 @@ class CpuSweepSampler:
                 return self.n_el * self.n_dirs * reps / dt, dt, reps
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference(args, world, rank, dist):
     from paper_2010_04559_b200 import configs as cf
     if rank != 0:
@@ -171,7 +182,8 @@ def run_reference(args, world, rank, dist):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "c5: 512x512 bilinear cells, uniform angular level 5 (8192 patches), fp64 sweep",
                        "sample": sample},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -320,6 +332,22 @@ def run_b200(args, world, rank, local, dist):
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"oracle standard_sweep over {smp.n_dirs} directions x {smp.n_el} cells, {reps} sweeps "
                          f"in {dt:.1f} s (config 5 grid, angular level 2 to bound host memory)"}
+        cpu["cpu_model"] = cpu_model()
+        # the same solves on the oracle (serial coarse GS like the reference, OpenMP elsewhere)
+        if not args.no_solve and "solve" in extras:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import pyoracle
+            for k in args.cpu_solve_configs:
+                key = f"c{k}"
+                if key not in extras["solve"]:
+                    continue
+                o = pyoracle.Oracle(cf.baseline_config(k))
+                t0 = time.perf_counter()
+                _, rep = o.solve("gmres", "mg")
+                extras["solve"][key]["cpu"] = {"wall_s": time.perf_counter() - t0, "iterations": rep["iterations"],
+                                               "final_residual": rep["final_residual"], "cores": threads,
+                                               "kind": "port"}
+                del o
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -351,6 +379,8 @@ def main():
     ap.add_argument("--no-si", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--cpu-solve-configs", type=int, nargs="*", default=[1],
+                    help="also time these solves on the CPU oracle (rank 0, N=1); c2 takes ~80 s on 8 cores")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

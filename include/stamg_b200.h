@@ -111,6 +111,12 @@ int stamg_level_order(stamg_ctx* ctx, int level, int* order);
 int stamg_vec_create(stamg_ctx* ctx, int level, stamg_vec** out);
 int stamg_vec_free(stamg_vec* v);
 int stamg_vec_size(stamg_vec* v, int64_t* n);
+/* Device storage order: the reference layout ((el*P+q)*D+d)*S+i, except on contexts
+ * without a hierarchy whose level qualifies for 8-direction groups, which store the
+ * "wavefront layout" (per 8-direction group, cells along the sweep's skewed
+ * anti-diagonals; STAMG_WAVEFRONT_LAYOUT=0 disables it). Upload,
+ * download, the host-buffer entry points and stamg_vec_size always use the
+ * reference layout; only the raw device pointer exposes the internal order. */
 int stamg_vec_device_ptr(stamg_vec* v, double** ptr);
 int stamg_vec_upload(stamg_ctx* ctx, stamg_vec* v, const double* host, int64_t n);
 int stamg_vec_download(stamg_ctx* ctx, const stamg_vec* v, double* host, int64_t n);

@@ -216,8 +216,7 @@ def test_wavefront_layout_context(orc, stamg, k, wl, monkeypatch):
     st, mo = spec.kernel_arrays()
     spec.angular_level, spec.N, spec.n_levels = 5, 11, 1  # H = 144 >= 128: folded scatter
     spec.moments = mo[:, : spec.N + 1]
-    if wl:
-        monkeypatch.setenv("STAMG_WAVEFRONT_LAYOUT", "1")
+    monkeypatch.setenv("STAMG_WAVEFRONT_LAYOUT", "1" if wl else "0")
     o = orc.Oracle(spec)
     g = stamg.Context(spec, build_hierarchy=False)
     x = rnd(o.size(), 31)
