@@ -206,7 +206,9 @@ def run_b200(args, world, rank, local, dist):
     from paper_2010_04559_b200 import configs as cf
     from paper_2010_04559_b200 import stamg
     spec = cf.baseline_config(5, args.n)
+    t_setup = time.perf_counter()
     g = make_context(stamg, spec, world, rank, local, dist, False)
+    setup_s = allmax(dist, time.perf_counter() - t_setup)  # host tables + device couplings + upload
     n_el, P_local, S, _ = g.layout()
     upd_local = n_el * P_local
     psi = g.vec().fill(1.0)
@@ -355,7 +357,8 @@ def run_b200(args, world, rank, local, dist):
                 "config": {"workload": f"c5: {spec.nx}x{spec.ny} bilinear cells, uniform angular level 5 "
                                        f"({P_local * world} patches), one in-place standard_sweep per step, "
                                        f"directions sharded over {world} rank(s)",
-                           "l2": f"input {spec.n_el * P_local * world * 4 * 8 / 2**30:.1f} GiB >> 126 MB L2 (no flush needed)", "wall_s": wall},
+                           "l2": f"input {spec.n_el * P_local * world * 4 * 8 / 2**30:.1f} GiB >> 126 MB L2 (no flush needed)", "wall_s": wall,
+                           "setup_s": setup_s},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                              "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
                              "kernel": "sweep_kernel", "bytes_per_update": BYTES_PER_UPDATE},

@@ -30,6 +30,43 @@ __device__ __forceinline__ double2 ld_stream(const double* p) {
 __device__ __forceinline__ void st_stream(double* p, double2 v) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
+// one 32-byte block (4 doubles = one DRAM sector) per thread: 256-bit LDG/STG (sm_100)
+#ifndef STAMG_V256
+#define STAMG_V256 1
+#endif
+struct dbl4 {
+  double x, y, z, w;
+};
+__device__ __forceinline__ dbl4 ld_block(const double* p) {
+  dbl4 v;
+#if STAMG_V256
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+#else
+  const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+  v.x = a.x, v.y = a.y, v.z = b.x, v.w = b.y;
+#endif
+  return v;
+}
+// the same for data the kernel itself writes (no read-only path)
+__device__ __forceinline__ dbl4 ld_block_rw(const double* p) {
+  dbl4 v;
+#if STAMG_V256
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p) : "memory");
+#else
+  const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+  v.x = a.x, v.y = a.y, v.z = b.x, v.w = b.y;
+#endif
+  return v;
+}
+__device__ __forceinline__ void st_block(double* p, const dbl4& v) {
+#if STAMG_V256
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+#else
+  reinterpret_cast<double2*>(p)[0] = make_double2(v.x, v.y);
+  reinterpret_cast<double2*>(p)[1] = make_double2(v.z, v.w);
+#endif
+}
+
 // L2-coherent (bypass L1) accesses for data produced by other CTAs of the same launch
 __device__ __forceinline__ double2 ld_cg2(const double* p) {
   double2 v;

@@ -406,7 +406,10 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     L.fold_hs.assign(G, {});
     for (int h = 0; h < t.H; ++h) L.fold_hs[t.hclass[h]].push_back(h);
     L.fold_hoff.assign(G + 1, 0);
-    for (int cl = 0; cl < G; ++cl) L.fold_hoff[cl + 1] = L.fold_hoff[cl] + round_up(std::max<int>(1, L.fold_hs[cl].size()), 64);
+    for (int cl = 0; cl < G; ++cl) {  // class region: whole D2M row tiles (d2m_row_tile)
+      const int hc = std::max<int>(1, L.fold_hs[cl].size()), bm = d2m_row_tile(hc, 1 << 30);
+      L.fold_hoff[cl + 1] = L.fold_hoff[cl] + round_up(hc, bm);
+    }
     L.fold_Hf = L.fold_hoff[G];
     std::vector<double> Xf(size_t(Rk) * L.fold_Hf, 0.0), XfT(size_t(L.fold_Hf) * L.fold_Rp, 0.0);
     std::vector<double> sigf(size_t(t.n_mat) * L.fold_Hf, 0.0);
@@ -487,7 +490,7 @@ void op_d2m(stamg_ctx* c, DevLevel& L, const double* phi, int order, double* out
   D2MParams p;
   p.wl = L.wl;
   p.phi = phi, p.src = out, p.X = L.X, p.sig = sig, p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
-  p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.Hused = (order + 1) * (order + 1);
+  p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.Hused = (order + 1) * (order + 1), p.Hrows = L.Hp;
   for (int k = 0; k < 16; ++k) p.N[k] = identity_N ? ((k % 5) == 0 ? 1.0 : 0.0) : L.t.Nmat[k];
   launch_d2m(p, c->stream);
   ck_launch("d2m");
@@ -539,7 +542,7 @@ void scatter_into(stamg_ctx* c, DevLevel& L, const double* phi, int order, doubl
     D2MParams p;
     p.phi = L.foldbuf + cl * cls, p.src = L.src + size_t(L.fold_hoff[cl]) * 4, p.X = L.Xf + L.fold_hoff[cl];
     p.sig = L.sigf + L.fold_hoff[cl], p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
-    p.n_el = n_el, p.P = R, p.Hp = L.fold_Hf, p.Hused = hu[cl];
+    p.n_el = n_el, p.P = R, p.Hp = L.fold_Hf, p.Hused = hu[cl], p.Hrows = L.fold_hoff[cl + 1] - L.fold_hoff[cl];
     for (int k = 0; k < 16; ++k) p.N[k] = L.t.Nmat[k];
     launch_d2m(p, c->stream);
     ck_launch("d2m");
@@ -1019,6 +1022,7 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
     auto c = std::make_unique<stamg_ctx>();
     c->pb = copy_problem(*prob);
     validate(c->pb);
+    c->pb.device_setup = std::getenv("STAMG_HOST_SETUP") == nullptr;  // couplings on the device
     c->device = opt ? opt->device : 0;
     c->rank = opt ? opt->rank : 0;
     c->world = opt ? std::max(1, opt->world) : 1;

@@ -61,9 +61,12 @@ struct D2MParams {
   const double* sig = nullptr;   // [n_mat][Hp]
   const int* mat = nullptr;
   int n_el = 0, P = 0, Hp = 0, Hused = 0;
+  int Hrows = 0;                 // rows of src this call may write (its region; >= Hused)
   double N[16];
 };
 void launch_d2m(const D2MParams& p, cudaStream_t s);
+// rows of the D2M output tile for `rows` harmonics inside a region of `limit` rows (0: none fits)
+int d2m_row_tile(int rows, int limit);
 
 // M2D (scatter.cpp:132): y[el][q][i] = beta*y + scale * sum_h X[q][h] src[el][h][i]
 //   + (ext_q ? ext_q[el]/(4 pi) * area[q] * nsum[i] : 0)

@@ -12,6 +12,8 @@
 // global->shared with cp.async (3 stages); each warp owns a 32x32 output
 // block = 4x4 m8n8k4 DMMA accumulators (tcgen05 has no f64 kind, so
 // mma.sync...f64 is the FP64 tensor path on sm_100a).
+#include <stdexcept>
+
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -29,76 +31,95 @@ namespace {
 #endif
 constexpr int BM = 64, BN = 64, BK = STAMG_GEMM_BK, NSTAGE = STAMG_GEMM_NSTAGE;
 constexpr int LDS = BM + 4;  // padded row (conflict-free fragment loads)
+constexpr int LDB = BN + 4;
 constexpr int kThreads = 128;
-constexpr int kStageDoubles = 2 * BK * LDS;
+constexpr int kStageDoubles = BK * (LDS + LDB);
+
+// Output-row tiling of the D2M GEMM (M = harmonics of the call): WM warp rows
+// x 2 warp columns, each warp MI x 4 m8n8k4 blocks, so BM = 8*MI*WM rows by
+// BN = 64 columns. The harmonic parity classes of the folded scatter have 153 /
+// 136 / 120 rows at N = 32: 64-row tiles pad them to 192 (71 % useful work);
+// 24-row warp strips cover them in one CTA tile of 168 / 144 / 120 rows.
+template <int MI, int WM>
+struct RowTile {
+  static constexpr int kBM = 8 * MI * WM, kLDA = kBM + 4, kThreads = 64 * WM;
+  static constexpr int kStage = BK * (kLDA + LDB);
+};
 
 // A tile: sA[k][m] = A_src[(k0+k) * lda + m0 + m]   (rows of k contiguous in m)
+template <int TBM, int TLDA, int TT>
 __device__ __forceinline__ void load_tile_rows(double* sA, const double* src, int lda, int k0, int m0, int krows,
                                                int tid) {
-  // BK x BM doubles = 512 16-byte chunks, 4 per thread
+  // BK x TBM doubles in 16-byte chunks
 #pragma unroll
-  for (int it = 0; it < (BK * BM / 2) / kThreads; ++it) {
-    const int chunk = tid + it * kThreads;
-    const int k = chunk / (BM / 2), mm = (chunk % (BM / 2)) * 2;
+  for (int it = 0; it < (BK * TBM / 2 + TT - 1) / TT; ++it) {
+    const int chunk = tid + it * TT;
+    if ((BK * TBM / 2) % TT != 0 && chunk >= BK * TBM / 2) break;
+    const int k = chunk / (TBM / 2), mm = (chunk % (TBM / 2)) * 2;
     const bool ok = (k0 + k) < krows;
     const double* g = src + (ok ? (size_t)(k0 + k) * lda + m0 + mm : 0);
-    cp_async16(sA + k * LDS + mm, g, ok);
+    cp_async16(sA + k * TLDA + mm, g, ok);
   }
 }
 
 // D2M B tile: sB[k][e*4+i] = phi[((el0+e)*P + q0+k)*4 + i] (or its wavefront-layout block)
+template <int TT>
 __device__ __forceinline__ void load_phi_tile(double* sB, const double* phi, int P, int n_el, int q0, int el0,
                                               int tid, const WLGeom& wl) {
 #pragma unroll
-  for (int it = 0; it < (BK * BN / 2) / kThreads; ++it) {
-    const int chunk = tid + it * kThreads;       // e (16) x k (BK) x half (2)
+  for (int it = 0; it < (BK * BN / 2 + TT - 1) / TT; ++it) {
+    const int chunk = tid + it * TT;             // e (16) x k (BK) x half (2)
+    if ((BK * BN / 2) % TT != 0 && chunk >= BK * BN / 2) break;
     const int half = chunk & 1, k = (chunk >> 1) & (BK - 1), e = chunk / (2 * BK);
     const bool ok = (el0 + e) < n_el && (q0 + k) < P;
     size_t off = 0;
     if (ok) off = wl.nd ? (size_t)wl_block(wl, el0 + e, q0 + k) * 4 : ((size_t)(el0 + e) * P + q0 + k) * 4;
-    cp_async16(sB + k * LDS + e * 4 + half * 2, phi + off + (ok ? half * 2 : 0), ok);
+    cp_async16(sB + k * LDB + e * 4 + half * 2, phi + off + (ok ? half * 2 : 0), ok);
   }
 }
 
-// M2D B tile: sB[k][e*4+i] = src[((el0+e)*Hp + h0+k)*4 + i]
+// M2D B tile: sB[k][e*4+i] = src[((el0+e)*Hp + h0+k)*4 + i], zero for h0+k >= krows
 __device__ __forceinline__ void load_src_tile(double* sB, const double* src, int Hp, int n_el, int h0, int el0,
-                                              int tid) {
+                                              int krows, int tid) {
 #pragma unroll
   for (int it = 0; it < (BK * BN / 2) / kThreads; ++it) {
     const int chunk = tid + it * kThreads;
     const int half = chunk & 1, k = (chunk >> 1) & (BK - 1), e = chunk / (2 * BK);
-    const bool ok = (el0 + e) < n_el;
+    const bool ok = (el0 + e) < n_el && (h0 + k) < krows;
     const double* g = src + (ok ? (((size_t)(el0 + e) * Hp + h0 + k) * 4 + half * 2) : 0);
-    cp_async16(sB + k * LDS + e * 4 + half * 2, g, ok);
+    cp_async16(sB + k * LDB + e * 4 + half * 2, g, ok);
   }
 }
 
-__device__ __forceinline__ void mma_stage(const double* sA, const double* sB, double (&acc)[4][4][2], int wm, int wn,
+template <int MI, int TLDA>
+__device__ __forceinline__ void mma_stage(const double* sA, const double* sB, double (&acc)[MI][4][2], int wm, int wn,
                                           int g, int t) {
 #pragma unroll
   for (int kk = 0; kk < BK; kk += 4) {
-    double a[4], b[4];
+    double a[MI], b[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) a[i] = sA[(kk + t) * LDS + wm * 32 + i * 8 + g];
+    for (int i = 0; i < MI; ++i) a[i] = sA[(kk + t) * TLDA + wm * (8 * MI) + i * 8 + g];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = sB[(kk + t) * LDS + wn * 32 + j * 8 + g];
+    for (int j = 0; j < 4; ++j) b[j] = sB[(kk + t) * LDB + wn * 32 + j * 8 + g];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
   }
 }
 
-// grid: x = element tiles (16 elements), y = harmonic tiles (64)
-__global__ void __launch_bounds__(kThreads) d2m_kernel(D2MParams p) {
+// grid: x = element tiles (16 elements), y = harmonic tiles (BM rows)
+template <int MI, int WM>
+__global__ void __launch_bounds__(RowTile<MI, WM>::kThreads) d2m_kernel(D2MParams p) {
+  using T = RowTile<MI, WM>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;
   const int el0 = (STAMG_GEMM_SWAP ? blockIdx.y : blockIdx.x) * (BN / 4);
-  const int h0 = (STAMG_GEMM_SWAP ? blockIdx.x : blockIdx.y) * BM;
-  double acc[4][4][2];
+  const int h0 = (STAMG_GEMM_SWAP ? blockIdx.x : blockIdx.y) * T::kBM;
+  double acc[MI][4][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -107,32 +128,33 @@ __global__ void __launch_bounds__(kThreads) d2m_kernel(D2MParams p) {
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
     if (s < nk) {
-      double* st = smem + s * kStageDoubles;
-      load_tile_rows(st, p.X, p.Hp, s * BK, h0, Pk, tid);
-      load_phi_tile(st + BK * LDS, p.phi, p.P, p.n_el, s * BK, el0, tid, p.wl);
+      double* st = smem + s * T::kStage;
+      load_tile_rows<T::kBM, T::kLDA, T::kThreads>(st, p.X, p.Hp, s * BK, h0, Pk, tid);
+      load_phi_tile<T::kThreads>(st + BK * T::kLDA, p.phi, p.P, p.n_el, s * BK, el0, tid, p.wl);
     }
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     const int nxt = kt + NSTAGE - 1;
     if (nxt < nk) {
-      double* st = smem + (nxt % NSTAGE) * kStageDoubles;
-      load_tile_rows(st, p.X, p.Hp, nxt * BK, h0, Pk, tid);
-      load_phi_tile(st + BK * LDS, p.phi, p.P, p.n_el, nxt * BK, el0, tid, p.wl);
+      double* st = smem + (nxt % NSTAGE) * T::kStage;
+      load_tile_rows<T::kBM, T::kLDA, T::kThreads>(st, p.X, p.Hp, nxt * BK, h0, Pk, tid);
+      load_phi_tile<T::kThreads>(st + BK * T::kLDA, p.phi, p.P, p.n_el, nxt * BK, el0, tid, p.wl);
     }
     cp_async_commit();
     cp_async_wait<NSTAGE - 1>();
     __syncthreads();
-    const double* st = smem + (kt % NSTAGE) * kStageDoubles;
-    mma_stage(st, st + BK * LDS, acc, wm, wn, g, t);
+    const double* st = smem + (kt % NSTAGE) * T::kStage;
+    mma_stage<MI, T::kLDA>(st, st + BK * T::kLDA, acc, wm, wn, g, t);
     __syncthreads();
   }
   cp_async_wait<0>();
 
   // epilogue: complete the element's 4 dofs from the partner lane, apply N and sigma
+  // (rows Hused <= h < h0 + BM of the call's region are written as zeros)
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int h = h0 + wm * 32 + i * 8 + g;
+  for (int i = 0; i < MI; ++i) {
+    const int h = h0 + wm * (8 * MI) + i * 8 + g;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const double o0 = __shfl_xor_sync(0xffffffffu, acc[i][j][0], 1);
@@ -143,7 +165,7 @@ __global__ void __launch_bounds__(kThreads) d2m_kernel(D2MParams p) {
       const int e = (wn * 32 + j * 8) / 4 + (t >> 1);
       const int el = el0 + e;
       const int i0 = (t & 1) * 2;
-      if (el < p.n_el && h < p.Hp) {
+      if (el < p.n_el && h < p.Hrows) {
         double s0 = 0.0, s1 = 0.0;
         if (h < p.Hused) {
           const int mt = p.mat ? p.mat[el] : 0;
@@ -176,8 +198,8 @@ __global__ void __launch_bounds__(kThreads) m2d_kernel(M2DParams p) {
   for (int s = 0; s < NSTAGE - 1; ++s) {
     if (s < nk) {
       double* st = smem + s * kStageDoubles;
-      load_tile_rows(st, p.XT, p.Pp, s * BK, q0, p.Hp, tid);
-      load_src_tile(st + BK * LDS, p.src, p.Hp, p.n_el, s * BK, el0, tid);
+      load_tile_rows<BM, LDS, kThreads>(st, p.XT, p.Pp, s * BK, q0, p.Hused, tid);
+      load_src_tile(st + BK * LDS, p.src, p.Hp, p.n_el, s * BK, el0, p.Hused, tid);
     }
     cp_async_commit();
   }
@@ -185,14 +207,14 @@ __global__ void __launch_bounds__(kThreads) m2d_kernel(M2DParams p) {
     const int nxt = kt + NSTAGE - 1;
     if (nxt < nk) {
       double* st = smem + (nxt % NSTAGE) * kStageDoubles;
-      load_tile_rows(st, p.XT, p.Pp, nxt * BK, q0, p.Hp, tid);
-      load_src_tile(st + BK * LDS, p.src, p.Hp, p.n_el, nxt * BK, el0, tid);
+      load_tile_rows<BM, LDS, kThreads>(st, p.XT, p.Pp, nxt * BK, q0, p.Hused, tid);
+      load_src_tile(st + BK * LDS, p.src, p.Hp, p.n_el, nxt * BK, el0, p.Hused, tid);
     }
     cp_async_commit();
     cp_async_wait<NSTAGE - 1>();
     __syncthreads();
     const double* st = smem + (kt % NSTAGE) * kStageDoubles;
-    mma_stage(st, st + BK * LDS, acc, wm, wn, g, t);
+    mma_stage<4, LDS>(st, st + BK * LDS, acc, wm, wn, g, t);
     __syncthreads();
   }
   cp_async_wait<0>();
@@ -223,7 +245,21 @@ __global__ void __launch_bounds__(kThreads) m2d_kernel(M2DParams p) {
   }
 }
 
-size_t gemm_smem() { return sizeof(double) * NSTAGE * kStageDoubles; }
+size_t gemm_smem() { return sizeof(double) * NSTAGE * BK * (LDS + LDB); }
+
+template <int MI, int WM>
+void launch_d2m_tile(const D2MParams& p, cudaStream_t s) {
+  using T = RowTile<MI, WM>;
+  const size_t smem = sizeof(double) * NSTAGE * T::kStage;
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(d2m_kernel<MI, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    init = true;
+  }
+  const unsigned ge = (p.n_el + BN / 4 - 1) / (BN / 4), gh = (p.Hused + T::kBM - 1) / T::kBM;
+  dim3 grid = STAMG_GEMM_SWAP ? dim3(gh, ge) : dim3(ge, gh);
+  d2m_kernel<MI, WM><<<grid, T::kThreads, smem, s>>>(p);
+}
 
 // Walsh-Hadamard transform over the G = 2^na members of an orbit (unnormalised):
 // out[c] = sum_g (-1)^popcount(c & g) in[g]
@@ -252,18 +288,12 @@ __global__ void fold_kernel(const double* __restrict__ phi, double* __restrict__
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const int q = orbit[r * G + g];
-    const double2* b =
-        reinterpret_cast<const double2*>(phi + (wl.nd ? (size_t)wl_block(wl, el, q) * 4 : ((size_t)el * P + q) * 4));
-    const double2 a0 = b[0], a1 = b[1];
-    v[g][0] = a0.x, v[g][1] = a0.y, v[g][2] = a1.x, v[g][3] = a1.y;
+    const dbl4 a = ld_block(phi + (wl.nd ? (size_t)wl_block(wl, el, q) * 4 : ((size_t)el * P + q) * 4));
+    v[g][0] = a.x, v[g][1] = a.y, v[g][2] = a.z, v[g][3] = a.w;
   }
   wht<G>(v);
 #pragma unroll
-  for (int c = 0; c < G; ++c) {
-    double2* o = reinterpret_cast<double2*>(Phi + (((size_t)c * n_el + el) * R + r) * 4);
-    o[0] = make_double2(v[c][0], v[c][1]);
-    o[1] = make_double2(v[c][2], v[c][3]);
-  }
+  for (int c = 0; c < G; ++c) st_block(Phi + (((size_t)c * n_el + el) * R + r) * 4, dbl4{v[c][0], v[c][1], v[c][2], v[c][3]});
 }
 
 // y[el][orbit[r][g]][i] = beta*y + scale * sum_c chi_c(g) Y[c][el][r][i] (+ isotropic source)
@@ -277,27 +307,26 @@ __global__ void unfold_kernel(const double* __restrict__ Y, double* __restrict__
   double v[G][4];
 #pragma unroll
   for (int c = 0; c < G; ++c) {
-    const double2* b = reinterpret_cast<const double2*>(Y + (((size_t)c * n_el + el) * R + r) * 4);
-    const double2 a0 = b[0], a1 = b[1];
-    v[c][0] = a0.x, v[c][1] = a0.y, v[c][2] = a1.x, v[c][3] = a1.y;
+    const dbl4 a = ld_block(Y + (((size_t)c * n_el + el) * R + r) * 4);
+    v[c][0] = a.x, v[c][1] = a.y, v[c][2] = a.z, v[c][3] = a.w;
   }
   wht<G>(v);
   constexpr double inv4pi = 0.07957747154594767;
+  const double qel = ext_q ? ext_q[el] * inv4pi : 0.0;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const int q = orbit[r * G + g];
-    double2* o = reinterpret_cast<double2*>(y + (wl.nd ? (size_t)wl_block(wl, el, q) * 4 : ((size_t)el * P + q) * 4));
+    double* o = y + (wl.nd ? (size_t)wl_block(wl, el, q) * 4 : ((size_t)el * P + q) * 4);
     double w0 = scale * v[g][0], w1 = scale * v[g][1], w2 = scale * v[g][2], w3 = scale * v[g][3];
     if (ext_q) {
-      const double c = ext_q[el] * inv4pi * area[q];
+      const double c = qel * area[q];
       w0 += c * nsum.x, w1 += c * nsum.y, w2 += c * nsum.z, w3 += c * nsum.w;
     }
     if (beta != 0.0) {
-      const double2 a0 = o[0], a1 = o[1];
-      w0 += beta * a0.x, w1 += beta * a0.y, w2 += beta * a1.x, w3 += beta * a1.y;
+      const dbl4 a = ld_block_rw(o);
+      w0 += beta * a.x, w1 += beta * a.y, w2 += beta * a.z, w3 += beta * a.w;
     }
-    o[0] = make_double2(w0, w1);
-    o[1] = make_double2(w2, w3);
+    st_block(o, dbl4{w0, w1, w2, w3});
   }
 }
 
@@ -310,10 +339,7 @@ __global__ void wl_convert_kernel(const double* __restrict__ src, double* __rest
   const int e = int(idx / P), q = int(idx - (int64_t)e * P);
   const size_t refo = (size_t)idx * 4;  // chunk-relative reference offset
   const size_t wlo = (size_t)wl_block(wl, el0 + e, perm[q]) * 4;
-  const double2* a = reinterpret_cast<const double2*>(src + (TO_WL ? refo : wlo));
-  double2* b = reinterpret_cast<double2*>(dst + (TO_WL ? wlo : refo));
-  const double2 v0 = a[0], v1 = a[1];
-  b[0] = v0, b[1] = v1;
+  st_block(dst + (TO_WL ? wlo : refo), ld_block(src + (TO_WL ? refo : wlo)));
 }
 
 // fill the valid blocks of a wavefront-layout vector (padding stays zero)
@@ -321,8 +347,7 @@ __global__ void wl_fill_kernel(double* __restrict__ dst, double v, int n_el, int
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n_el * P) return;
   const int el = int(idx / P), k = int(idx - (int64_t)el * P);
-  double2* b = reinterpret_cast<double2*>(dst + (size_t)wl_block(wl, el, k) * 4);
-  b[0] = make_double2(v, v), b[1] = make_double2(v, v);
+  st_block(dst + (size_t)wl_block(wl, el, k) * 4, dbl4{v, v, v, v});
 }
 
 }  // namespace
@@ -369,24 +394,40 @@ void launch_unfold(const double* Y, double* y, const int* orbit, int n_el, int P
   }
 }
 
+int d2m_row_tile(int rows, int limit) {
+  // candidate tiles: 64 rows (MI 4 x WM 2) and 24-row warp strips x 1..7 warp rows;
+  // cost = padded rows + 8 per tile (each extra tile re-reads the phi panel),
+  // restricted to tilings that stay inside the call's row region
+  static const int cand[] = {64, 24, 48, 72, 96, 120, 144, 168};
+  int best = 0, best_cost = 1 << 30;
+  for (int bm : cand) {
+    const int tiles = (rows + bm - 1) / bm, padded = tiles * bm;
+    if (padded > limit) continue;
+    const int cost = padded + 8 * tiles;
+    if (cost < best_cost) best = bm, best_cost = cost;
+  }
+  return best;
+}
+
 void launch_d2m(const D2MParams& p, cudaStream_t s) {
   if (p.n_el == 0 || p.Hused == 0) return;
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(d2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
-    cudaFuncSetAttribute(m2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
-    init = true;
+  switch (d2m_row_tile(p.Hused, p.Hrows)) {
+    case 24: launch_d2m_tile<3, 1>(p, s); break;
+    case 48: launch_d2m_tile<3, 2>(p, s); break;
+    case 72: launch_d2m_tile<3, 3>(p, s); break;
+    case 96: launch_d2m_tile<3, 4>(p, s); break;
+    case 120: launch_d2m_tile<3, 5>(p, s); break;
+    case 144: launch_d2m_tile<3, 6>(p, s); break;
+    case 168: launch_d2m_tile<3, 7>(p, s); break;
+    case 64: launch_d2m_tile<4, 2>(p, s); break;
+    default: throw std::invalid_argument("d2m: no row tiling fits the moment region");
   }
-  const unsigned ge = (p.n_el + BN / 4 - 1) / (BN / 4), gh = (p.Hused + BM - 1) / BM;
-  dim3 grid = STAMG_GEMM_SWAP ? dim3(gh, ge) : dim3(ge, gh);
-  d2m_kernel<<<grid, kThreads, gemm_smem(), s>>>(p);
 }
 
 void launch_m2d(const M2DParams& p, cudaStream_t s) {
   if (p.n_el == 0 || p.P == 0) return;
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(d2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
     cudaFuncSetAttribute(m2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
     init = true;
   }

@@ -230,10 +230,6 @@ const Rule1D& gauss01(int n) {  // Newton on P_n, mapped to [0,1] (quadrature.cp
   return cache.emplace(n, std::move(r)).first->second;
 }
 
-int patch_order(int level, int base) {  // quadrature.hpp:31-34
-  const int bump = level == 0 ? 20 : level == 1 ? 12 : 8;
-  return std::max(base, bump);
-}
 
 // Visit every node of the Duffy-collapsed rule of one patch
 // (quadrature.cpp:59-92): f(unit direction, weight).
@@ -261,6 +257,20 @@ void for_each_node(const SphereTree& t, int id, int order, F&& f) {
     }
   }
 }
+
+}  // namespace
+
+int patch_order(int level, int base) {  // quadrature.hpp:31-34
+  const int bump = level == 0 ? 20 : level == 1 ? 12 : 8;
+  return std::max(base, bump);
+}
+
+void gauss_rule01(int n, const double** x, const double** w) {
+  const Rule1D& r = gauss01(n);
+  *x = r.x.data(), *w = r.w.data();
+}
+
+namespace {
 
 // Real orthonormal spherical harmonics up to degree N, h = n^2 + n + o
 // (associated-Legendre recurrence along each order m; scatter.cpp:33-65).
@@ -404,6 +414,9 @@ LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool 
   L.cxy.resize(size_t(P) * 8);
   const int xorder_base = order > 12 ? 12 : 8;  // scatter.hpp:42
   std::vector<double> Y(H);
+  // the couplings are ~all of the setup time (1e9 harmonic evaluations at config 5): on the device
+  const bool device_X = pb.device_setup && device_couplings_supported(order);
+  if (device_X) device_couplings(t, L.leaf_id, order, xorder_base, L.X.data());
   for (int q = 0; q < P; ++q) {
     const int id = L.leaf_id[q];
     L.octant[q] = t.octant[id];
@@ -416,11 +429,13 @@ LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool 
     L.area[q] = M;
     for (int xi = 0; xi < 3; ++xi) L.Aflow[q * 3 + xi] = A[xi];
     // couplings X_q(h) = int_patch Y_h (scatter.cpp:74-99)
-    double* Xq = &L.X[size_t(q) * H];
-    for_each_node(t, id, patch_order(t.level[id], xorder_base), [&](const double* om, double w) {
-      harmonics(order, om, Y.data());
-      for (int h = 0; h < H; ++h) Xq[h] += w * Y[h];
-    });
+    if (!device_X) {
+      double* Xq = &L.X[size_t(q) * H];
+      for_each_node(t, id, patch_order(t.level[id], xorder_base), [&](const double* om, double w) {
+        harmonics(order, om, Y.data());
+        for (int h = 0; h < H; ++h) Xq[h] += w * Y[h];
+      });
+    }
     // fused blocks (transport.cpp:46-56)
     const int oct = t.octant[id];
     double sgn[2], Cq[2][16];

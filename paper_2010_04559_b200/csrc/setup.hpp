@@ -85,6 +85,7 @@ struct Problem {
   std::vector<double> q_el;
   int n_el = 0;
   double h = 0;
+  bool device_setup = false;  // build_couplings on the current CUDA device (couplings.cu)
 };
 
 Problem copy_problem(const stamg_problem& p);
@@ -111,6 +112,15 @@ std::vector<LevelTables> build_hierarchy(const Problem& pb, const SphereTree& fi
                                          const std::vector<std::vector<int>>* parts = nullptr);
 // assemble_rhs (transport.cpp:110-179 + cone beam EXTENSION)
 std::vector<double> assemble_rhs(const Problem& pb, const LevelTables& lev, const SphereTree& tree);
+
+// quadrature helpers (quadrature.hpp:31-34, quadrature.cpp:13-57): per-patch
+// 1D order, cached Gauss-Legendre rule on [0, 1]
+int patch_order(int level, int base);
+void gauss_rule01(int n, const double** x, const double** w);
+// build_couplings (scatter.cpp:74-99) on the current CUDA device: X [P][H] for
+// the given leaves, written to host memory; orders up to 32
+bool device_couplings_supported(int order);
+void device_couplings(const SphereTree& t, const std::vector<int>& leaf_id, int order, int xorder_base, double* X);
 
 // 4x4 helpers
 void inverse4(const double* A, double* Ainv);

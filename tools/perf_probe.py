@@ -51,6 +51,32 @@ def main():
         out["fp64_peaks_tflops"] = {"dmma": a, "dfma": b}
         del x, y
         g.close()
+    if "si" in which:  # one source iteration at config-5 physics on an n^2 grid, per kernel
+        spec = cf.baseline_config(5, int(os.environ.get("C5N", "256")))
+        t0 = time.perf_counter()
+        g = stamg.Context(spec, build_hierarchy=False)
+        setup = time.perf_counter() - t0
+        n_el, P, _, _ = g.layout()
+        psi = g.vec().fill(1.0)
+        g.source_iteration(psi, 1)
+        g.synchronize()
+        g.timing(True)
+        t0 = time.perf_counter()
+        g.source_iteration(psi, 2)
+        g.synchronize()
+        wall = (time.perf_counter() - t0) / 2
+        kt = {kk: g.timed(kk)[0] / 2 for kk in ("fold", "d2m", "m2d", "unfold", "sweep")}
+        g.timing(False)
+        H = (spec.N + 1) ** 2
+        fold = max(1, int(g.table("fold")[0]))
+        exe = 2.0 * H * P * 4 * n_el / fold
+        out["si"] = {"n": spec.nx, "setup_s": setup, "ms_per_iter": wall * 1e3, "kernels_ms": kt,
+                     "d2m_tflops_exec": exe / (kt["d2m"] * 1e-3) * 1e-12,
+                     "m2d_tflops_exec": exe / (kt["m2d"] * 1e-3) * 1e-12,
+                     "fold_gbs": 2 * n_el * P * 32 / (kt["fold"] * 1e-3) * 1e-9,
+                     "unfold_gbs": 2 * n_el * P * 32 / (kt["unfold"] * 1e-3) * 1e-9,
+                     "fp64_peaks": g.fp64_peaks()}
+        g.close()
     for k in (2, 3, 1):
         if f"c{k}" not in which:
             continue
