@@ -188,6 +188,83 @@ def run_reference(args, world, rank, dist):
     print(json.dumps(line), flush=True)
 
 
+SOLVE_KERNELS = ("coarse_gs", "sweep", "apply_L", "d2m", "m2d", "fold", "unfold", "restrict", "prolong")
+
+
+def kernel_rooflines(stamg, cf, dmma_peak):
+    """Per-kernel roofline at full config 4 (the largest solve config): the outer
+    apply_L / sweep / scatter GEMMs (N = 32), and the transfers and reduced-order
+    (nr = 8) GEMMs between the two finest MG levels, one call each after a warm
+    call, CUDA events on the context stream. Algorithmic bytes: apply_L and the
+    sweep 64 B per cell-direction; restrict V_f + V_c, prolongate V_c + V_f
+    (the API's non-accumulating form); GEMM flops 2*H*P*4 per cell each."""
+    hbm, _ = peaks()
+    spec = cf.baseline_config(4)
+    g = stamg.Context(spec)
+    out = {}
+    try:
+        n_el, P, _, _ = g.layout()
+        nlev, nr = g.levels()
+        x, y = g.vec().fill(1.0), g.vec()
+
+        def timed(name, fn):
+            fn()
+            g.synchronize()
+            g.timing(True)
+            fn()
+            g.synchronize()
+            ms, n = g.timed(name)
+            g.timing(False)
+            return ms / max(n, 1) * 1e-3
+
+        def hbm_row(name, fn, nbytes, kname=None):
+            t = timed(kname or name, fn)
+            out[name] = {"ms": t * 1e3, "bytes": nbytes, "achieved_gbs": nbytes / t * 1e-9, "frac": nbytes / t * 1e-9 / hbm,
+                         "bound": "hbm"}
+
+        upd = n_el * P
+        hbm_row("apply_L", lambda: g.apply_L_into(x, y), upd * 64)
+        hbm_row("sweep", lambda: g.standard_sweep(x, y), upd * 64)
+        fold = max(1, int(g.table("fold")[0]))
+        for kname in ("d2m", "m2d"):
+            t_all = None
+            g.apply_scatter_into(x, spec.N, 1.0, y)
+            g.synchronize()
+            g.timing(True)
+            g.apply_scatter_into(x, spec.N, 1.0, y)
+            g.synchronize()
+            t_all = g.timed(kname)[0] * 1e-3
+            g.timing(False)
+            flop = 2.0 * (spec.N + 1) ** 2 * P * 4 * n_el
+            out[f"{kname}_outer"] = {"ms": t_all * 1e3, "algorithmic_flop": flop, "fold_group_size": fold,
+                                     "achieved_tflops_executed": flop / fold / t_all * 1e-12,
+                                     "frac": flop / fold / t_all * 1e-12 / dmma_peak, "bound": "fp64_tensor"}
+        del x, y
+        lf = nlev - 1
+        vf, vc = g.vec(lf).fill(1.0), g.vec(lf - 1).fill(1.0)
+        _, Pf, _, _ = g.layout(lf)
+        _, Pc, _, _ = g.layout(lf - 1)
+        Vf, Vc = n_el * Pf * 32, n_el * Pc * 32
+        hbm_row("restrict", lambda: g.restrict_residual(lf, vf, vc), Vf + Vc)
+        hbm_row("prolongate", lambda: g.prolongate(lf, vc, vf), Vf + Vc, "prolong")
+        yf = g.vec(lf)
+        g.apply_scatter_into(vf, nr, 1.0, yf, level=lf)
+        g.synchronize()
+        g.timing(True)
+        g.apply_scatter_into(vf, nr, 1.0, yf, level=lf)
+        g.synchronize()
+        for kname in ("d2m", "m2d"):
+            t = g.timed(kname)[0] * 1e-3
+            flop = 2.0 * (nr + 1) ** 2 * Pf * 4 * n_el
+            out[f"{kname}_mg_nr{nr}"] = {"ms": t * 1e3, "algorithmic_flop": flop, "achieved_tflops": flop / t * 1e-12,
+                                        "frac": flop / t * 1e-12 / dmma_peak, "bound": "fp64_tensor"}
+        g.timing(False)
+        out["config"] = f"c4 full: {n_el} cells, outer P={P} (N={spec.N}), MG levels {lf}->{lf - 1}: P {Pf}->{Pc} (nr={nr})"
+    finally:
+        g.close()
+    return out
+
+
 def make_context(stamg, spec, world, rank, local, dist, build_hierarchy):
     """One context per rank; ranks > 1 share a fresh NCCL communicator (unique id
     from rank 0, broadcast over torch.distributed)."""
@@ -302,7 +379,10 @@ def run_b200(args, world, rank, local, dist):
         e2e = {"value": total_upd * k_e2e / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n * 8,
                "d2h_bytes_per_step": n * 8, "steps": k_e2e,
                "api": "stamg_sweep_host (include/stamg_b200.h), pinned host buffers"}
+    dmma_peak, _ = g.fp64_peaks()
     g.close()
+    if not args.no_kernels and world == 1:
+        extras["kernels"] = kernel_rooflines(stamg, cf, dmma_peak)
     # ---- extra: GMRES + AMG solve wall time to 1e-8 from a device-resident b
     # (directions sharded over the ranks, coarsest MG level replicated)
     if not args.no_solve:
@@ -323,6 +403,12 @@ def run_b200(args, world, rank, local, dist):
             solves[f"c{k}"] = {"wall_s": wall, "setup_s": setup, "iterations": rep["iterations"],
                                "final_residual": rep["final_residual"], "converged": rep["converged"],
                                "method": "GMRES(%d) right-preconditioned by one V(1,1) angular MG cycle" % sp.restart}
+            # where the time goes: the same solve once more with per-launch CUDA events
+            gs.timing(True)
+            gs.solve(b, "gmres", "mg")
+            gs.synchronize()
+            solves[f"c{k}"]["kernel_ms"] = {kk: round(gs.timed(kk)[0], 3) for kk in SOLVE_KERNELS}
+            gs.timing(False)
             gs.close()
         extras["solve"] = solves
     # ---- CPU baseline (oracle port) on rank 0 at N = 1
@@ -382,6 +468,7 @@ def main():
     ap.add_argument("--no-si", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel roofline section (config 4)")
     ap.add_argument("--cpu-solve-configs", type=int, nargs="*", default=[1],
                     help="also time these solves on the CPU oracle (rank 0, N=1); c2 takes ~80 s on 8 cores")
     ap.add_argument("--no-cpu", action="store_true")

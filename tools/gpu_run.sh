@@ -1,7 +1,11 @@
+# GPU session script (run under gpurun from the repo root); $1 = tag, $2 = mode
 set -x
 cd "${GRAFT_REPO_ROOT:-.}"; mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_golden.py tests/test_gpu_setup.py tests/test_gpu_fullsize.py -m gpu -x -q -s > gpurun_out/v2_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/v2_tests.log
-C5N=512 timeout 300 python tools/perf_probe.py si > gpurun_out/v2_si512.json 2>&1
-C5N=256 timeout 300 python tools/perf_probe.py si > gpurun_out/v2_si256.json 2>&1
-C5N=256 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"fold|d2m|unfold" -c 6 -o gpurun_out/v2_si256 python tools/perf_probe.py si > gpurun_out/v2_ncu.log 2>&1
+T=${1:-run}
+MODE=${2:-gs}
+if [ "$MODE" = gs ]; then
+  timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_golden.py tests/test_gpu_fullsize_golden.py -m gpu -x -q > gpurun_out/${T}_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_tests.log
+  for k in 1 2 3 4; do timeout 300 python tools/gs_probe.py $k 10 >> gpurun_out/${T}_gs.log 2>&1; done
+  timeout 900 python bench.py --steps 3 --warmup 3 --no-si --no-e2e --no-kernels --no-cpu --solve-configs 1 2 3 4 > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; echo "bench rc=$?"
+fi
 echo done
