@@ -277,7 +277,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     const auto& t0 = L.t;
-    if (c->wl_allowed && !t0.groups8.empty() && t0.nx >= 36 && t0.ny >= 32 &&
+    if (c->wl_allowed && !t0.groups8.empty() && !t0.groups8_padded && t0.nx >= 36 && t0.ny >= 32 &&
         int(t0.group8_oct.size()) >= 2 * sms && std::getenv("STAMG_SWEEP_DIRS4") == nullptr &&
         !env_is_zero("STAMG_WAVEFRONT_LAYOUT")) {
       // default for throughput contexts: every sweep step of a group touches one

@@ -180,7 +180,16 @@ __global__ void __launch_bounds__(RowTile<MI, WM>::kThreads) d2m_kernel(D2MParam
   }
 }
 
-// grid: x = element tiles (16), y = patch tiles (64)
+// output block of (patch q, element el, dof pair i0) in y
+__device__ __forceinline__ double* m2d_out(const M2DParams& p, int el, int q, int i0) {
+  return p.y + (p.wl.nd ? (size_t)wl_block(p.wl, el, q) * 4 : ((size_t)el * p.P + q) * 4) + i0;
+}
+
+// grid: x = element tiles (16), y = patch tiles (64). PRE (beta != 0): the old y
+// of the tile is loaded into registers before the k-loop, so the read-modify-write
+// epilogue does not expose a DRAM round trip (the MG levels' M2D has K = 25..81:
+// a few k-steps only)
+template <bool PRE>
 __global__ void __launch_bounds__(kThreads) m2d_kernel(M2DParams p) {
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -192,6 +201,19 @@ __global__ void __launch_bounds__(kThreads) m2d_kernel(M2DParams p) {
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  double2 oldv[PRE ? 4 : 1][PRE ? 4 : 1];
+  if constexpr (PRE) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int q = q0 + wm * 32 + i * 8 + g;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int el = el0 + (wn * 32 + j * 8) / 4 + (t >> 1);
+        oldv[i][j] = (q < p.P && el < p.n_el) ? *reinterpret_cast<const double2*>(m2d_out(p, el, q, (t & 1) * 2))
+                                               : make_double2(0.0, 0.0);
+      }
+    }
+  }
 
   const int nk = (p.Hused + BK - 1) / BK;
 #pragma unroll
@@ -230,13 +252,15 @@ __global__ void __launch_bounds__(kThreads) m2d_kernel(M2DParams p) {
       const int el = el0 + e;
       if (el >= p.n_el) continue;
       const int i0 = (t & 1) * 2;
-      double* yp = p.y + (p.wl.nd ? (size_t)wl_block(p.wl, el, q) * 4 : ((size_t)el * p.P + q) * 4) + i0;
+      double* yp = m2d_out(p, el, q, i0);
       double v0 = p.scale * acc[i][j][0], v1 = p.scale * acc[i][j][1];
       if (p.ext_q) {
         const double c = p.ext_q[el] * inv4pi * p.area[q];
         v0 += c * p.nsum[i0], v1 += c * p.nsum[i0 + 1];
       }
-      if (p.beta != 0.0) {
+      if constexpr (PRE) {
+        v0 += p.beta * oldv[i][j].x, v1 += p.beta * oldv[i][j].y;
+      } else if (p.beta != 0.0) {
         const double2 old = *reinterpret_cast<const double2*>(yp);
         v0 += p.beta * old.x, v1 += p.beta * old.y;
       }
@@ -428,12 +452,14 @@ void launch_m2d(const M2DParams& p, cudaStream_t s) {
   if (p.n_el == 0 || p.P == 0) return;
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(m2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
+    cudaFuncSetAttribute(m2d_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
+    cudaFuncSetAttribute(m2d_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
     init = true;
   }
   const unsigned ge = (p.n_el + BN / 4 - 1) / (BN / 4), gq = (p.P + BM - 1) / BM;
   dim3 grid = STAMG_GEMM_SWAP ? dim3(gq, ge) : dim3(ge, gq);
-  m2d_kernel<<<grid, kThreads, gemm_smem(), s>>>(p);
+  if (p.beta != 0.0) m2d_kernel<true><<<grid, kThreads, gemm_smem(), s>>>(p);
+  else m2d_kernel<false><<<grid, kThreads, gemm_smem(), s>>>(p);
 }
 
 }  // namespace stamg_b200

@@ -481,14 +481,18 @@ LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool 
     }
   }
   L.oct_ptr[8] = int(L.oct_patches.size());
-  bool by8 = true;
-  for (int oct = 0; oct < 8; ++oct) by8 = by8 && (L.oct_ptr[oct + 1] - L.oct_ptr[oct]) % 8 == 0;
-  if (by8)
-    for (int oct = 0; oct < 8; ++oct)
-      for (int k = L.oct_ptr[oct]; k < L.oct_ptr[oct + 1]; k += 8) {
-        for (int j = 0; j < 8; ++j) L.groups8.push_back(L.oct_patches[k + j]);
-        L.group8_oct.push_back(oct);
+  // 8-direction groups; an octant whose count is not a multiple of 8 (the config-4 cone
+  // mesh: 466 = 58*8 + 2) ends with a padded group (-1 lanes idle)
+  L.groups8_padded = false;
+  for (int oct = 0; oct < 8; ++oct)
+    for (int k = L.oct_ptr[oct]; k < L.oct_ptr[oct + 1]; k += 8) {
+      for (int j = 0; j < 8; ++j) {
+        const bool in = k + j < L.oct_ptr[oct + 1];
+        L.groups8.push_back(in ? L.oct_patches[k + j] : -1);
+        L.groups8_padded = L.groups8_padded || !in;
       }
+      L.group8_oct.push_back(oct);
+    }
   if (with_gs) {  // scatter-implicit blocks of the coarse solver (sweeps.cpp:60-72)
     L.sq.resize(size_t(L.n_mat) * P);
     L.BinvGS.resize(size_t(L.n_mat) * P * 16);

@@ -58,8 +58,9 @@ struct LevelTables {
   std::vector<double> Aflow;          // [P][3] A^x, A^y, A^z
   std::vector<int> groups;            // [n_groups][4] patch ids of equal octant (-1 pad)
   std::vector<int> group_oct;         // [n_groups]
-  std::vector<int> groups8;           // [n_groups8][8] equal-octant patches (empty if an octant's count % 8 != 0)
+  std::vector<int> groups8;           // [n_groups8][8] equal-octant patches (-1 pads an octant's last group)
   std::vector<int> group8_oct;
+  bool groups8_padded = false;        // some group holds -1 lanes (no wavefront layout then)
   std::vector<int> oct_patches;       // patches listed by octant (plan.patches)
   std::vector<int> oct_ptr;           // [9]
   // transfers to the next coarser level (multigrid.cpp:68-96); empty on level 0
