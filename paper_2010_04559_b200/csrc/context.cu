@@ -115,7 +115,7 @@ struct DevLevel {
   double* mom = nullptr;  // coarse GS moments
   int* gs_done = nullptr;
   double *gs_K = nullptr, *gs_Xo = nullptr, *gs_XoT = nullptr, *gs_G = nullptr;
-  int gs_blocks = 0, gs_cpw = 0, gs_kpad = 0, gs_max_np = 0, gs_rows = 0;
+  int gs_blocks = 0, gs_cpw = 0, gs_kpad = 0, gs_max_np = 0, gs_rows = 0, gs_mw = 0;
   double *tmp = nullptr, *cf = nullptr, *ce = nullptr;  // V-cycle workspace
   // reflection-symmetry folded scatter (setup.hpp find_symmetry)
   int fold_G = 0, fold_R = 0, fold_Rp = 0, fold_Hf = 0;
@@ -375,19 +375,27 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     L.gs_XoT = dupload(XoT, s);
     // static ownership: each warp owns a segment of gs_cpw consecutive cells of one row
     // row mode pays off once rows are long (measured: c2, c3 faster; c1 at 32^2 slower)
+    // many patches per octant (config 4: 64): a 4-warp CTA per row spreads the
+    // projections and moment updates (STAMG_GS_MW=0 keeps the one-warp kernels)
+    L.gs_mw = L.gs_max_np > 16 && !env_is_zero("STAMG_GS_MW") &&
+              coarse_gs_mw_ok(L.Hp, L.gs_kpad, t.n_mat, t.ny, L.gs_max_np);
     L.gs_rows = (std::getenv("STAMG_GS_SEGMENTS") || t.nx < 64)
                     ? 0
                     : coarse_gs_rows_wpb(L.Hp, L.gs_kpad, t.n_mat, t.nx, t.ny, L.gs_max_np);
-    const int max_warps = coarse_gs_max_warps(L.Hp, L.gs_kpad, t.n_mat, L.gs_max_np);
-    int seg = 1;
-    while (int64_t(t.n_el) / seg > max_warps || t.nx % seg != 0) {
-      if (seg >= t.nx) throw std::invalid_argument("coarse_scatter_sweep: grid too large for co-resident warps");
-      seg *= 2;
+    if (L.gs_mw) {  // one 4-warp CTA per grid row
+      L.gs_rows = 0, L.gs_cpw = t.nx, L.gs_blocks = t.ny;
+    } else {
+      const int max_warps = coarse_gs_max_warps(L.Hp, L.gs_kpad, t.n_mat, L.gs_max_np);
+      int seg = 1;
+      while (int64_t(t.n_el) / seg > max_warps || t.nx % seg != 0) {
+        if (seg >= t.nx) throw std::invalid_argument("coarse_scatter_sweep: grid too large for co-resident warps");
+        seg *= 2;
+      }
+      L.gs_cpw = seg;
+      const int W = t.n_el / seg;
+      const int wpb = coarse_gs_warps_per_block(L.Hp, L.gs_kpad, t.n_mat);
+      L.gs_blocks = (W + wpb - 1) / wpb;
     }
-    L.gs_cpw = seg;
-    const int W = t.n_el / seg;
-    const int wpb = coarse_gs_warps_per_block(L.Hp, L.gs_kpad, t.n_mat);
-    L.gs_blocks = (W + wpb - 1) / wpb;
     if (L.gs_rows) {  // row mode: a warp per grid row, CTAs of gs_rows consecutive rows
       L.gs_cpw = t.nx;
       L.gs_blocks = t.ny / L.gs_rows;
@@ -623,6 +631,7 @@ void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* 
   p.oct_patches = L.oct_patches, p.oct_ptr = L.oct_ptr, p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
   p.done = L.gs_done, p.K = L.gs_K, p.Xo = L.gs_Xo, p.XoT = L.gs_XoT, p.GS = L.gs_G, p.n_mat = L.t.n_mat;
   p.cells_per_warp = L.gs_cpw, p.kpad = L.gs_kpad, p.grid_blocks = L.gs_blocks, p.rows_mode = L.gs_rows;
+  p.multi_warp = L.gs_mw;
   p.xreg = std::getenv("STAMG_GS_XGLOBAL") ? 0 : 1;
   p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.H = L.t.H, p.nx = L.t.nx, p.ny = L.t.ny, p.nu = nu;
   for (int o = 0; o < 8; ++o)

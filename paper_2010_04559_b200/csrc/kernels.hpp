@@ -126,6 +126,7 @@ struct CoarseGSParams {
   int cells_per_warp = 0, kpad = 0, grid_blocks = 0;  // warp owns a row segment of cells_per_warp cells
   int xreg = 1;       // x-upwind traces inside a segment from registers (0: through global memory)
   int rows_mode = 0;  // > 0: warp owns a whole row, CTA = rows_mode consecutive rows (shared mailbox)
+  int multi_warp = 0; // 1: a CTA of 4 warps owns a whole row (projections / moment updates spread)
   int n_el = 0, P = 0, Hp = 0, H = 0, nx = 0, ny = 0, nu = 0, n_mat = 1;
   int max_patches_per_octant = 0;
   double N[16];
@@ -135,6 +136,7 @@ void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s);
 int coarse_gs_max_warps(int Hp, int kpad, int nmat, int max_np);
 int coarse_gs_warps_per_block(int Hp, int kpad, int nmat);
 int coarse_gs_rows_wpb(int Hp, int kpad, int nmat, int nx, int ny, int max_np);
+int coarse_gs_mw_ok(int Hp, int kpad, int nmat, int ny, int max_np);
 
 // BLAS-1 (deterministic reductions)
 void launch_fill(double* x, double v, int64_t n, cudaStream_t s);

@@ -411,6 +411,278 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
   }
 }
 
+// Multi-warp rows (many patches per octant: config 4 has 64). The one-warp item
+// is throughput-bound there (~12.7k warp instructions: projections t0 and the
+// running-moment update are np x H x 4 each). Here a CTA of GSW_MW warps owns one
+// grid row for the whole call and walks the same item sequence; per item
+//   1. all warps: t0_a = X_a sig mom (Lp threads per patch split the harmonics),
+//   2. warp 0: dependency wait, upwind fold, prologue and the sequential patch
+//      chain (as in the one-warp kernel, t from shared memory), publish,
+//   3. all warps: mom[h][i] += sum_a X_a[h] dz_a[i] (one output per thread, the
+//      reference's patch order).
+// Own rhs / previous iterate and the octant's G, B'^-1 are loaded by warp 0 before
+// step 1 so their latency hides behind it. Co-residency of the ny CTAs is required
+// (cooperative launch).
+constexpr int GSW_MW = 4;
+
+__host__ __device__ inline size_t gs_mw_doubles(int Hp, int kpad, int nmat) {
+  return size_t(Hp) * 8 + size_t(kpad) * 8 + size_t(nmat) * kpad * kpad + size_t(kpad) * (Hp + 1) + size_t(nmat) * Hp;
+}
+
+template <int NS>
+__global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSParams p) {
+  extern __shared__ __align__(16) double gsm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+  const unsigned full = 0xffffffffu;
+  const int n_el = p.n_el, nx = p.nx, ny = p.ny, P = p.P, Hp = p.Hp, H = p.H;
+  const int kpad = p.kpad, nmat = p.n_mat;
+  double* smom = gsm;                             // [2][Hp][4] double-buffered moments
+  double* sdz = smom + Hp * 8;                    // [kpad][4] chain output (sweep frame)
+  double* st0 = sdz + kpad * 4;                   // [kpad][4] projections (physical dofs)
+  double* sK = st0 + kpad * 4;                    // [n_mat][kpad][kpad]
+  double* sX = sK + (size_t)nmat * kpad * kpad;   // [kpad][Hp+1]
+  double* sS = sX + (size_t)kpad * (Hp + 1);      // [n_mat][Hp]
+  const int XS = Hp + 1;
+  for (int c = tid; c < nmat * Hp; c += nthr) sS[c] = p.sig[c];
+  const int gy = blockIdx.x;
+  const int seg = nx;
+  const int n_items = p.nu * 8 * seg;
+  auto cell_of = [&](int it) {
+    const int oct = (it / seg) & 7, j = it % seg;
+    return gy * nx + ((oct & 1) ? seg - 1 - j : j);
+  };
+  auto prefetch_mom = [&](int el, double* dst) {
+    const double* src = p.mom + (size_t)el * Hp * 4;
+    for (int c = tid; c < H * 2; c += nthr) cp_async16(dst + c * 2, src + c * 2, true);
+    cp_async_commit();
+  };
+  int cur = 0, k_oct = -1;
+  prefetch_mom(cell_of(0), smom);
+  cp_async_wait<0>();
+  __syncthreads();
+  double xtr[NS][2];  // warp 0: x-upwind traces from the previous cell of the row
+#pragma unroll
+  for (int sl = 0; sl < NS; ++sl) xtr[sl][0] = xtr[sl][1] = 0.0;
+  for (int it = 0; it < n_items; ++it) {
+    const int pass = it / (8 * seg), oct = (it / seg) & 7, jseg = it % seg;
+    const int el = cell_of(it);
+    const int el_next = it + 1 < n_items ? cell_of(it + 1) : -1;
+    const bool reuse = el_next == el;
+    if (el_next >= 0 && !reuse) prefetch_mom(el_next, smom + (cur ^ 1) * Hp * 4);
+    const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
+    const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
+    const int pbeg = p.oct_ptr[oct], np = p.oct_ptr[oct + 1] - pbeg;
+    const int gx = el - gy * nx;
+    const int ifr = xneg ? nx - 1 - gx : gx, jf = yneg ? ny - 1 - gy : gy;
+    const int sx = xneg ? -1 : 1, sy = yneg ? -nx : nx;
+    const int upx = ifr > 0 ? el - sx : -1, upy = jf > 0 ? el - sy : -1;
+    const int dnx = ifr < nx - 1 ? el + sx : -1, dny = jf < ny - 1 ? el + sy : -1;
+    const int mt = p.mat ? p.mat[el] : 0;
+    const double* mom = smom + cur * Hp * 4;
+    if (oct != k_oct) {  // stage this octant's K blocks and X rows once per (pass, octant)
+      for (int mm = 0; mm < nmat; ++mm)
+        for (int c = tid; c < np * kpad / 2; c += nthr)
+          cp_async16(sK + ((size_t)mm * kpad * kpad) + c * 2, p.K + ((size_t)mm * P + pbeg) * kpad + c * 2, true);
+      for (int c = tid; c < np * H; c += nthr) {
+        const int a = c / H, h = c - a * H;
+        cp_async8(sX + (size_t)a * XS + h, p.Xo + (size_t)(pbeg + a) * Hp + h, true);
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+      k_oct = oct;
+    }
+    const double* sg = sS + (size_t)mt * Hp;
+    // ---- warp 0: own data and the octant's blocks -> registers (latency hidden by step 1)
+    double r[NS][4], zo[NS][4], G[NS][16], Bq[NS][16];
+    int qs[NS];
+    if (warp == 0) {
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) {
+        const int a = lane + 32 * sl;
+        qs[sl] = a < np ? p.oct_patches[pbeg + a] : -1;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) r[sl][i] = zo[sl][i] = 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) G[sl][k] = Bq[sl][k] = 0.0;
+        if (qs[sl] >= 0) {
+          const double* rb = p.rhs + ((size_t)el * P + qs[sl]) * 4;
+          const double2 ra = __ldg(reinterpret_cast<const double2*>(rb)), rc = __ldg(reinterpret_cast<const double2*>(rb) + 1);
+          const double2 za = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4), zc = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4 + 2);
+          r[sl][0] = ra.x, r[sl][1] = ra.y, r[sl][2] = rc.x, r[sl][3] = rc.y;
+          zo[sl][0] = za.x, zo[sl][1] = za.y, zo[sl][2] = zc.x, zo[sl][3] = zc.y;
+          const double* Gq = p.GS + ((size_t)mt * P + qs[sl]) * 16;
+          const double* Bg = p.BinvGS + ((size_t)mt * P + qs[sl]) * 16;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) G[sl][k] = __ldg(Gq + k), Bq[sl][k] = __ldg(Bg + k);
+        }
+      }
+    }
+    // ---- step 1 (all warps): t0_a = X_a sig mom, Lp threads per patch
+    {
+      int Lp = 1;
+      while (Lp < 32 && Lp * 2 * np <= nthr) Lp *= 2;
+      const int a = tid / Lp, part = tid % Lp;
+      double u[4] = {0.0, 0.0, 0.0, 0.0};
+      if (a < np) {
+        const double* xr = sX + (size_t)a * XS;
+        for (int h = part; h < H; h += Lp) {
+          const double xs = xr[h] * sg[h];
+          const double2 ma = reinterpret_cast<const double2*>(mom)[2 * h], mb = reinterpret_cast<const double2*>(mom)[2 * h + 1];
+          u[0] += xs * ma.x, u[1] += xs * ma.y, u[2] += xs * mb.x, u[3] += xs * mb.y;
+        }
+      }
+      for (int o = Lp >> 1; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) u[i] += __shfl_xor_sync(full, u[i], o);
+      if (a < np && part == 0) {
+        reinterpret_cast<double2*>(st0)[2 * a] = make_double2(u[0], u[1]);
+        reinterpret_cast<double2*>(st0)[2 * a + 1] = make_double2(u[2], u[3]);
+      }
+    }
+    __syncthreads();
+    // ---- step 2 (warp 0): dependencies, upwind fold, chain, publish
+    if (warp == 0) {
+      double t[NS][4];
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) {
+        const int a = lane + 32 * sl;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) t[sl][i] = a < np ? st0[a * 4 + i] : 0.0;
+      }
+      const bool x_in_seg = upx >= 0 && jseg > 0;
+      {
+        const int* f = nullptr;
+        int need = 0;
+        const int* d = p.done + (size_t)oct * n_el;
+        if (lane == 0 && upx >= 0 && !x_in_seg) f = d + upx, need = pass + 1;
+        if (lane == 1 && upy >= 0) f = d + upy, need = pass + 1;
+        if (lane == 2 && pass > 0 && dnx >= 0 && jseg == seg - 1) f = d + dnx, need = pass;
+        if (lane == 3 && pass > 0 && dny >= 0) f = d + dny, need = pass;
+        bool ok = f == nullptr || ld_relaxed(f) >= need;
+        const bool any = __any_sync(full, f != nullptr);
+        while (!__all_sync(full, ok))
+          if (!ok) ok = ld_relaxed(f) >= need;
+        if (any) fence_acq_rel();
+      }
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) {
+        const int q = qs[sl];
+        if (q < 0) continue;
+        double ux[4] = {0, 0, 0, 0}, uy[4] = {0, 0, 0, 0};
+        if (upx >= 0 && !x_in_seg) {
+          const double2 a = ld_cg2(p.phi + ((size_t)upx * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upx * P + q) * 4 + 2);
+          ux[0] = a.x, ux[1] = a.y, ux[2] = b.x, ux[3] = b.y;
+          perm(m, ux[0], ux[1], ux[2], ux[3]);
+        } else if (x_in_seg) {
+          ux[1] = xtr[sl][0], ux[3] = xtr[sl][1];
+        }
+        if (upy >= 0) {
+          const double2 a = ld_cg2(p.phi + ((size_t)upy * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upy * P + q) * 4 + 2);
+          uy[0] = a.x, uy[1] = a.y, uy[2] = b.x, uy[3] = b.y;
+          perm(m, uy[0], uy[1], uy[2], uy[3]);
+        }
+        perm(m, r[sl][0], r[sl][1], r[sl][2], r[sl][3]);
+        perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
+        perm(m, t[sl][0], t[sl][1], t[sl][2], t[sl][3]);
+        const double* cxy = p.cxy + (size_t)q * 8;
+        if (upx >= 0) {
+          r[sl][0] -= cxy[0] * ux[1] + cxy[1] * ux[3];
+          r[sl][2] -= cxy[2] * ux[1] + cxy[3] * ux[3];
+        }
+        if (upy >= 0) {
+          r[sl][0] -= cxy[4] * uy[2] + cxy[5] * uy[3];
+          r[sl][1] -= cxy[6] * uy[2] + cxy[7] * uy[3];
+        }
+      }
+      const double* sKm = sK + (size_t)mt * kpad * kpad;
+      double e[NS][4];
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) {
+        if (qs[sl] < 0) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) e[sl][i] = 0.0;
+          continue;
+        }
+        const int a = lane + 32 * sl;
+        const double sq = sKm[(size_t)a * kpad + a];
+        double szo[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) szo[i] = sq * zo[sl][i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double c = Bq[sl][4 * i] * r[sl][0] + Bq[sl][4 * i + 1] * r[sl][1] + Bq[sl][4 * i + 2] * r[sl][2] +
+                           Bq[sl][4 * i + 3] * r[sl][3];
+          const double gz = G[sl][4 * i] * szo[0] + G[sl][4 * i + 1] * szo[1] + G[sl][4 * i + 2] * szo[2] +
+                            G[sl][4 * i + 3] * szo[3];
+          e[sl][i] = c - zo[sl][i] - gz;
+        }
+      }
+      for (int a = 0; a < np; ++a) {
+        const int sl = a >> 5, src = a & 31;
+        double dz[4];
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2)
+          if (s2 == sl)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dz[i] = e[s2][i] + (G[s2][4 * i] * t[s2][0] + G[s2][4 * i + 1] * t[s2][1] +
+                                  G[s2][4 * i + 2] * t[s2][2] + G[s2][4 * i + 3] * t[s2][3]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dz[i] = __shfl_sync(full, dz[i], src);
+#pragma unroll
+        for (int s2 = 0; s2 < NS; ++s2) {
+          const int b = lane + 32 * s2;
+          const double k = b > a ? sKm[(size_t)a * kpad + b] : 0.0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) t[s2][i] += k * dz[i];
+        }
+        if (lane == 0) {
+          reinterpret_cast<double2*>(sdz)[2 * a] = make_double2(dz[0], dz[1]);
+          reinterpret_cast<double2*>(sdz)[2 * a + 1] = make_double2(dz[2], dz[3]);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) {
+        const int a = lane + 32 * sl;
+        if (qs[sl] < 0) continue;
+        const double2 d0 = reinterpret_cast<const double2*>(sdz)[2 * a], d1 = reinterpret_cast<const double2*>(sdz)[2 * a + 1];
+        zo[sl][0] += d0.x, zo[sl][1] += d0.y, zo[sl][2] += d1.x, zo[sl][3] += d1.y;
+      }
+#pragma unroll
+      for (int sl = 0; sl < NS; ++sl) {
+        const int q = qs[sl];
+        xtr[sl][0] = zo[sl][1], xtr[sl][1] = zo[sl][3];
+        if (q < 0) continue;
+        perm(m, zo[sl][0], zo[sl][1], zo[sl][2], zo[sl][3]);
+        double* zb = p.phi + ((size_t)el * P + q) * 4;
+        st_cg2(zb, make_double2(zo[sl][0], zo[sl][1]));
+        st_cg2(zb + 2, make_double2(zo[sl][2], zo[sl][3]));
+      }
+      __syncwarp();
+      if (lane == 0) st_release(p.done + (size_t)oct * n_el + el, pass + 1);
+    }
+    __syncthreads();
+    // ---- step 3 (all warps): running moments, one (h, dof) output per thread, patches in order
+    {
+      double* mom_el = p.mom + (size_t)el * Hp * 4;
+      double* mw = const_cast<double*>(mom);
+      for (int o = tid; o < H * 4; o += nthr) {
+        const int h = o >> 2, i = o & 3, fi = i ^ m;  // physical dof i = frame dof i ^ m
+        double v = mom[o];
+        const double* xo = sX + h;
+        for (int a = 0; a < np; ++a) v += xo[(size_t)a * XS] * sdz[a * 4 + fi];
+        mom_el[o] = v;
+        if (reuse) mw[o] = v;
+      }
+    }
+    if (!reuse) cur ^= 1;
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+}
+
 size_t gs_smem(int Hp, int kpad, int nmat, int wpb, int rows_nx = 0) {
   return sizeof(double) * wpb * gs_warp_doubles(Hp, kpad, nmat) +
          (rows_nx ? sizeof(double2) * size_t(wpb) * 2 * rows_nx * kpad + sizeof(int) * 8 : 0);
@@ -481,8 +753,38 @@ int coarse_gs_max_warps(int Hp, int kpad, int nmat, int max_np) {
 }
 int coarse_gs_warps_per_block(int Hp, int kpad, int nmat) { return gs_wpb(Hp, kpad, nmat); }
 
+// multi-warp rows: whether the ny row-CTAs fit co-resident (0 = no)
+int coarse_gs_mw_ok(int Hp, int kpad, int nmat, int ny, int max_np) {
+  if (max_np > 64) return 0;
+  const size_t smem = sizeof(double) * gs_mw_doubles(Hp, kpad, nmat);
+  if (smem > 220 * 1024) return 0;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  auto k = max_np > 32 ? coarse_gs_mw_kernel<2> : coarse_gs_mw_kernel<1>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, GSW_MW * 32, smem);
+  return per_sm * sms >= ny ? 1 : 0;
+}
+
+template <int NS>
+void launch_gs_mw(const CoarseGSParams& p, cudaStream_t s) {
+  auto k = coarse_gs_mw_kernel<NS>;
+  const size_t smem = sizeof(double) * gs_mw_doubles(p.Hp, p.kpad, p.n_mat);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  CoarseGSParams q = p;
+  void* args[] = {&q};
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(p.ny), dim3(GSW_MW * 32), args, smem, s);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("coarse_gs cooperative launch: ") + cudaGetErrorString(e));
+}
+
 void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s) {
   if (p.nu <= 0 || p.n_el == 0) return;
+  if (p.multi_warp) {
+    if (p.max_patches_per_octant <= 32) launch_gs_mw<1>(p, s);
+    else launch_gs_mw<2>(p, s);
+    return;
+  }
   if (p.max_patches_per_octant <= 32) launch_gs2<1>(p, s);
   else launch_gs2<2>(p, s);
 }

@@ -36,8 +36,8 @@ constexpr int NST = STAMG_SWEEP_NST;
 // one 256-byte run (better DRAM efficiency than 128 B), and the strip-boundary
 // traces go through an L2-resident global scratch (TOPG) instead of shared
 // memory so the CTA still fits 3 per SM.
-template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY = false, int MODE = 0>
-__global__ void __launch_bounds__(DIRS * R, (TOPG ? (STAMG_SWEEP8_BREG ? 2 : 4) : 1)) sweep_kernel(SweepParams p) {
+template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY = false, int MODE = 0, bool BREG = true>
+__global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_kernel(SweepParams p) {
   // WLAY: vectors in the wavefront layout (a step's R rows are consecutive slots).
   // MODE 1: apply_L on the same skewed schedule (y = alpha*(B x + C x_up) + beta*f, traces of x).
   // TOPG (8-direction) variant: 4 CTAs/SM (<= 64 registers), B^-1 read from shared memory
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (STAMG_SWEEP8_BREG ? 2 : 4) 
   double cx[4], cy[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) cx[k] = p.cxy[qq * 8 + k], cy[k] = p.cxy[qq * 8 + 4 + k];
-  constexpr bool BSMEM = MULTI || (TOPG && !STAMG_SWEEP8_BREG);
+  constexpr bool BSMEM = MULTI || (TOPG && !BREG);
   double Bi[16];
   const double* Bsrc = MODE == 1 ? p.Bfwd : p.Binv;
   if constexpr (!BSMEM) {
@@ -246,15 +246,30 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (STAMG_SWEEP8_BREG ? 2 : 4) 
   (void)RPW;
 }
 
-template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY = false, int MODE = 0>
-void launch_t(const SweepParams& p, cudaStream_t s) {
+template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY, int MODE, bool BREG>
+void launch_tb(const SweepParams& p, cudaStream_t s) {
   constexpr int NT = DIRS * R;
   size_t smem = sizeof(double) * NST * NT * 4 * (ACCUM ? 2 : 1) +
                 sizeof(double2) * ((TOPG ? NST * DIRS : DIRS * p.g.nx) + 2 * (NT / 32) * DIRS) +
                 ((MULTI || TOPG) ? sizeof(double) * p.g.n_mat * DIRS * 17 : 0);
-  auto k = sweep_kernel<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE>;
+  auto k = sweep_kernel<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, BREG>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<p.g.n_groups, NT, smem, s>>>(p);
+}
+
+// 8-direction groups: B^-1 in registers gives 2 CTAs/SM (the faster kernel when the
+// grid is many waves, 82.5 % vs 79 % of HBM at config 5), B^-1 in shared memory 4.
+// A group count just above one 2-per-SM wave (config 4's cone mesh: 364 groups
+// for 296 slots) would leave a second, mostly empty wave of whole-grid sweeps:
+// there the 4-per-SM kernel runs everything in one wave.
+template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY = false, int MODE = 0>
+void launch_t(const SweepParams& p, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool breg = STAMG_SWEEP8_BREG && !(TOPG && p.g.n_groups > 2 * sms && p.g.n_groups <= 4 * sms);
+  if (breg) launch_tb<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, true>(p, s);
+  else launch_tb<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, false>(p, s);
 }
 
 template <int DIRS, int R, bool TOPG, bool WLAY = false, int MODE = 0>
