@@ -378,7 +378,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     // many patches per octant (config 4: 64): a 4-warp CTA per row spreads the
     // projections and moment updates (STAMG_GS_MW=0 keeps the one-warp kernels)
     L.gs_mw = L.gs_max_np > 16 && !env_is_zero("STAMG_GS_MW") &&
-              coarse_gs_mw_ok(L.Hp, L.gs_kpad, t.n_mat, t.ny, L.gs_max_np);
+              coarse_gs_mw_ok(L.Hp, t.H, L.gs_kpad, t.n_mat, t.ny, L.gs_max_np);
     L.gs_rows = (std::getenv("STAMG_GS_SEGMENTS") || t.nx < 64)
                     ? 0
                     : coarse_gs_rows_wpb(L.Hp, L.gs_kpad, t.n_mat, t.nx, t.ny, L.gs_max_np);

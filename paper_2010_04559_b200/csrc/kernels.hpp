@@ -136,7 +136,7 @@ void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s);
 int coarse_gs_max_warps(int Hp, int kpad, int nmat, int max_np);
 int coarse_gs_warps_per_block(int Hp, int kpad, int nmat);
 int coarse_gs_rows_wpb(int Hp, int kpad, int nmat, int nx, int ny, int max_np);
-int coarse_gs_mw_ok(int Hp, int kpad, int nmat, int ny, int max_np);
+int coarse_gs_mw_ok(int Hp, int H, int kpad, int nmat, int ny, int max_np);
 
 // BLAS-1 (deterministic reductions)
 void launch_fill(double* x, double v, int64_t n, cudaStream_t s);

@@ -412,22 +412,28 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
 }
 
 // Multi-warp rows (many patches per octant: config 4 has 64). The one-warp item
-// is throughput-bound there (~12.7k warp instructions: projections t0 and the
+// is throughput-bound there (~12.7k warp instructions: the projections t0 and the
 // running-moment update are np x H x 4 each). Here a CTA of GSW_MW warps owns one
-// grid row for the whole call and walks the same item sequence; per item
-//   1. all warps: t0_a = X_a sig mom (Lp threads per patch split the harmonics),
-//   2. warp 0: dependency wait, upwind fold, prologue and the sequential patch
-//      chain (as in the one-warp kernel, t from shared memory), publish,
-//   3. all warps: mom[h][i] += sum_a X_a[h] dz_a[i] (one output per thread, the
-//      reference's patch order).
-// Own rhs / previous iterate and the octant's G, B'^-1 are loaded by warp 0 before
-// step 1 so their latency hides behind it. Co-residency of the ny CTAs is required
-// (cooperative launch).
+// grid row for the whole call and walks the same item sequence, software-pipelined:
+// in iteration k
+//   warp 0      : item k - dependency wait, upwind fold, prologue, the sequential
+//                 patch chain (t0 from shared memory), publish;
+//   warps 1..3  : item k-1's running-moment update mom[h][i] += sum_a X_a[h] dz_a[i]
+//                 (patches in the reference's order), then item k+1's projections
+//                 t0_a = X_a sig mom, then the moment prefetch of item k+2.
+// At an octant boundary the next item is the same cell (its moments need item k's
+// update) and the octant's K / X tables change: the pipeline drains there (every
+// nx items). Moments use a 4-buffer ring (items k-1 .. k+2), t0 and dz two buffers.
+// Co-residency of the ny CTAs is required (cooperative launch).
 constexpr int GSW_MW = 4;
+constexpr int MW_BAR = 1;  // named barrier of warps 1..3
 
-__host__ __device__ inline size_t gs_mw_doubles(int Hp, int kpad, int nmat) {
-  return size_t(Hp) * 8 + size_t(kpad) * 8 + size_t(nmat) * kpad * kpad + size_t(kpad) * (Hp + 1) + size_t(nmat) * Hp;
+__host__ __device__ inline int gs_mw_xs(int H) { return (H % 2 == 0) ? H + 1 : H + 2; }  // odd X row stride
+__host__ __device__ inline size_t gs_mw_doubles(int Hp, int H, int kpad, int nmat) {
+  return size_t(Hp) * 16 + size_t(kpad) * 16 + size_t(nmat) * kpad * kpad + size_t(kpad) * gs_mw_xs(H) + size_t(nmat) * Hp;
 }
+
+__device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 template <int NS>
 __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSParams p) {
@@ -436,120 +442,147 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
   const unsigned full = 0xffffffffu;
   const int n_el = p.n_el, nx = p.nx, ny = p.ny, P = p.P, Hp = p.Hp, H = p.H;
   const int kpad = p.kpad, nmat = p.n_mat;
-  double* smom = gsm;                             // [2][Hp][4] double-buffered moments
-  double* sdz = smom + Hp * 8;                    // [kpad][4] chain output (sweep frame)
-  double* st0 = sdz + kpad * 4;                   // [kpad][4] projections (physical dofs)
-  double* sK = st0 + kpad * 4;                    // [n_mat][kpad][kpad]
+  double* smom = gsm;                             // [4][Hp][4] moments of items k-1 .. k+2 (ring)
+  double* sdz = smom + Hp * 16;                   // [2][kpad][4] chain outputs (sweep frame)
+  double* st0 = sdz + kpad * 8;                   // [2][kpad][4] projections (physical dofs)
+  double* sK = st0 + kpad * 8;                    // [n_mat][kpad][kpad]
   double* sX = sK + (size_t)nmat * kpad * kpad;   // [kpad][Hp+1]
-  double* sS = sX + (size_t)kpad * (Hp + 1);      // [n_mat][Hp]
-  const int XS = Hp + 1;
+  const int XS = gs_mw_xs(H);
+  double* sS = sX + (size_t)kpad * XS;            // [n_mat][Hp]
   for (int c = tid; c < nmat * Hp; c += nthr) sS[c] = p.sig[c];
   const int gy = blockIdx.x;
   const int seg = nx;
   const int n_items = p.nu * 8 * seg;
+  auto oct_of = [&](int it) { return (it / seg) & 7; };
   auto cell_of = [&](int it) {
     const int oct = (it / seg) & 7, j = it % seg;
     return gy * nx + ((oct & 1) ? seg - 1 - j : j);
   };
-  auto prefetch_mom = [&](int el, double* dst) {
-    const double* src = p.mom + (size_t)el * Hp * 4;
-    for (int c = tid; c < H * 2; c += nthr) cp_async16(dst + c * 2, src + c * 2, true);
+  auto mbuf = [&](int it) { return smom + (it & 3) * Hp * 4; };
+  // moments of item `it` -> its ring buffer (threads [t0, t0 + nt))
+  auto prefetch_mom = [&](int it, int t0, int nt) {
+    const double* src = p.mom + (size_t)cell_of(it) * Hp * 4;
+    double* dst = mbuf(it);
+    for (int c = tid - t0; c < H * 2; c += nt) cp_async16(dst + c * 2, src + c * 2, true);
     cp_async_commit();
   };
-  int cur = 0, k_oct = -1;
-  prefetch_mom(cell_of(0), smom);
+  auto stage_octant = [&](int oct) {  // all threads; caller synchronises
+    const int pbeg = p.oct_ptr[oct], np = p.oct_ptr[oct + 1] - pbeg;
+    for (int mm = 0; mm < nmat; ++mm)
+      for (int c = tid; c < np * kpad / 2; c += nthr)
+        cp_async16(sK + ((size_t)mm * kpad * kpad) + c * 2, p.K + ((size_t)mm * P + pbeg) * kpad + c * 2, true);
+    for (int c = tid; c < np * H; c += nthr) {
+      const int a = c / H, h = c - a * H;
+      cp_async8(sX + (size_t)a * XS + h, p.Xo + (size_t)(pbeg + a) * Hp + h, true);
+    }
+    cp_async_commit();
+  };
+  // t0 of item `it` by threads [t0, t0 + nt)
+  auto project = [&](int it, int t0, int nt) {
+    const int oct = oct_of(it), np = p.oct_ptr[oct + 1] - p.oct_ptr[oct];
+    const int el = cell_of(it);
+    const double* sg = sS + (size_t)(p.mat ? p.mat[el] : 0) * Hp;
+    const double* mom = mbuf(it);
+    double* out = st0 + (it & 1) * kpad * 4;
+    int Lp = 1;
+    while (Lp < 32 && Lp * 2 * np <= nt) Lp *= 2;
+    const int lt = tid - t0, a = lt / Lp, part = lt % Lp;
+    double u[4] = {0.0, 0.0, 0.0, 0.0};
+    if (a < np) {
+      const double* xr = sX + (size_t)a * XS;
+      for (int h = part; h < H; h += Lp) {
+        const double xs = xr[h] * sg[h];
+        const double2 ma = reinterpret_cast<const double2*>(mom)[2 * h], mb = reinterpret_cast<const double2*>(mom)[2 * h + 1];
+        u[0] += xs * ma.x, u[1] += xs * ma.y, u[2] += xs * mb.x, u[3] += xs * mb.y;
+      }
+    }
+    for (int o = Lp >> 1; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) u[i] += __shfl_xor_sync(full, u[i], o);
+    if (a < np && part == 0) {
+      reinterpret_cast<double2*>(out)[2 * a] = make_double2(u[0], u[1]);
+      reinterpret_cast<double2*>(out)[2 * a + 1] = make_double2(u[2], u[3]);
+    }
+  };
+  // running moments of item `it` (threads [t0, t0 + nt)); with `into` also the ring buffer of item it+1
+  auto update = [&](int it, int t0, int nt, bool into_next) {
+    const int oct = oct_of(it), np = p.oct_ptr[oct + 1] - p.oct_ptr[oct];
+    const int m = (oct & 1) | (oct & 2);
+    double* mom_el = p.mom + (size_t)cell_of(it) * Hp * 4;
+    const double* mom = mbuf(it);
+    double* nxt = mbuf(it + 1);
+    const double* dz = sdz + (it & 1) * kpad * 4;
+    for (int o = tid - t0; o < H * 4; o += nt) {
+      const int h = o >> 2, fi = (o & 3) ^ m;  // physical dof i = frame dof i ^ m
+      double v = mom[o];
+      const double* xo = sX + h;
+      for (int a = 0; a < np; ++a) v += xo[(size_t)a * XS] * dz[a * 4 + fi];
+      mom_el[o] = v;
+      if (into_next) nxt[o] = v;
+    }
+  };
+
+  // ---- prologue: octant of item 0, moments of items 0 and 1, t0 of item 0
+  stage_octant(oct_of(0));
+  if (warp > 0) {
+    prefetch_mom(0, 32, nthr - 32);
+    if (n_items > 1 && cell_of(1) != cell_of(0)) prefetch_mom(1, 32, nthr - 32);
+  }
   cp_async_wait<0>();
   __syncthreads();
-  double xtr[NS][2];  // warp 0: x-upwind traces from the previous cell of the row
+  project(0, 0, nthr);
+  __syncthreads();
+  bool drained = true;  // item k-1's update already done (octant boundary drain)
+  double xtr[NS][2];    // warp 0: x-upwind traces from the previous cell of the row
 #pragma unroll
   for (int sl = 0; sl < NS; ++sl) xtr[sl][0] = xtr[sl][1] = 0.0;
+  int g_oct = -1, g_mt = -1;  // warp 0: octant / material of the cached G, B'^-1
+  double G[NS][16], Bq[NS][16];
+  int qs[NS];
   for (int it = 0; it < n_items; ++it) {
-    const int pass = it / (8 * seg), oct = (it / seg) & 7, jseg = it % seg;
+    const int pass = it / (8 * seg), oct = oct_of(it), jseg = it % seg;
     const int el = cell_of(it);
-    const int el_next = it + 1 < n_items ? cell_of(it + 1) : -1;
-    const bool reuse = el_next == el;
-    if (el_next >= 0 && !reuse) prefetch_mom(el_next, smom + (cur ^ 1) * Hp * 4);
-    const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
-    const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
+    const bool boundary = it + 1 < n_items && oct_of(it + 1) != oct;  // next item: same cell, new octant
     const int pbeg = p.oct_ptr[oct], np = p.oct_ptr[oct + 1] - pbeg;
-    const int gx = el - gy * nx;
-    const int ifr = xneg ? nx - 1 - gx : gx, jf = yneg ? ny - 1 - gy : gy;
-    const int sx = xneg ? -1 : 1, sy = yneg ? -nx : nx;
-    const int upx = ifr > 0 ? el - sx : -1, upy = jf > 0 ? el - sy : -1;
-    const int dnx = ifr < nx - 1 ? el + sx : -1, dny = jf < ny - 1 ? el + sy : -1;
-    const int mt = p.mat ? p.mat[el] : 0;
-    const double* mom = smom + cur * Hp * 4;
-    if (oct != k_oct) {  // stage this octant's K blocks and X rows once per (pass, octant)
-      for (int mm = 0; mm < nmat; ++mm)
-        for (int c = tid; c < np * kpad / 2; c += nthr)
-          cp_async16(sK + ((size_t)mm * kpad * kpad) + c * 2, p.K + ((size_t)mm * P + pbeg) * kpad + c * 2, true);
-      for (int c = tid; c < np * H; c += nthr) {
-        const int a = c / H, h = c - a * H;
-        cp_async8(sX + (size_t)a * XS + h, p.Xo + (size_t)(pbeg + a) * Hp + h, true);
-      }
-      cp_async_commit();
-      cp_async_wait<0>();
-      __syncthreads();
-      k_oct = oct;
-    }
-    const double* sg = sS + (size_t)mt * Hp;
-    // ---- warp 0: own data and the octant's blocks -> registers (latency hidden by step 1)
-    double r[NS][4], zo[NS][4], G[NS][16], Bq[NS][16];
-    int qs[NS];
     if (warp == 0) {
+      // ---------------- item `it`: dependencies, upwind fold, chain, publish
+      const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
+      const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
+      const int gx = el - gy * nx;
+      const int ifr = xneg ? nx - 1 - gx : gx, jf = yneg ? ny - 1 - gy : gy;
+      const int sx = xneg ? -1 : 1, sy = yneg ? -nx : nx;
+      const int upx = ifr > 0 ? el - sx : -1, upy = jf > 0 ? el - sy : -1;
+      const int dnx = ifr < nx - 1 ? el + sx : -1, dny = jf < ny - 1 ? el + sy : -1;
+      const int mt = p.mat ? p.mat[el] : 0;
+      double r[NS][4], zo[NS][4], t[NS][4];
+      const bool reload = oct != g_oct || mt != g_mt;
 #pragma unroll
       for (int sl = 0; sl < NS; ++sl) {
         const int a = lane + 32 * sl;
-        qs[sl] = a < np ? p.oct_patches[pbeg + a] : -1;
+        if (reload) qs[sl] = a < np ? p.oct_patches[pbeg + a] : -1;
 #pragma unroll
         for (int i = 0; i < 4; ++i) r[sl][i] = zo[sl][i] = 0.0;
-#pragma unroll
-        for (int k = 0; k < 16; ++k) G[sl][k] = Bq[sl][k] = 0.0;
         if (qs[sl] >= 0) {
           const double* rb = p.rhs + ((size_t)el * P + qs[sl]) * 4;
           const double2 ra = __ldg(reinterpret_cast<const double2*>(rb)), rc = __ldg(reinterpret_cast<const double2*>(rb) + 1);
           const double2 za = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4), zc = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4 + 2);
           r[sl][0] = ra.x, r[sl][1] = ra.y, r[sl][2] = rc.x, r[sl][3] = rc.y;
           zo[sl][0] = za.x, zo[sl][1] = za.y, zo[sl][2] = zc.x, zo[sl][3] = zc.y;
-          const double* Gq = p.GS + ((size_t)mt * P + qs[sl]) * 16;
-          const double* Bg = p.BinvGS + ((size_t)mt * P + qs[sl]) * 16;
+          if (reload) {
+            const double* Gq = p.GS + ((size_t)mt * P + qs[sl]) * 16;
+            const double* Bg = p.BinvGS + ((size_t)mt * P + qs[sl]) * 16;
 #pragma unroll
-          for (int k = 0; k < 16; ++k) G[sl][k] = __ldg(Gq + k), Bq[sl][k] = __ldg(Bg + k);
+            for (int k = 0; k < 16; ++k) G[sl][k] = __ldg(Gq + k), Bq[sl][k] = __ldg(Bg + k);
+          }
+        } else if (reload) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) G[sl][k] = Bq[sl][k] = 0.0;
         }
-      }
-    }
-    // ---- step 1 (all warps): t0_a = X_a sig mom, Lp threads per patch
-    {
-      int Lp = 1;
-      while (Lp < 32 && Lp * 2 * np <= nthr) Lp *= 2;
-      const int a = tid / Lp, part = tid % Lp;
-      double u[4] = {0.0, 0.0, 0.0, 0.0};
-      if (a < np) {
-        const double* xr = sX + (size_t)a * XS;
-        for (int h = part; h < H; h += Lp) {
-          const double xs = xr[h] * sg[h];
-          const double2 ma = reinterpret_cast<const double2*>(mom)[2 * h], mb = reinterpret_cast<const double2*>(mom)[2 * h + 1];
-          u[0] += xs * ma.x, u[1] += xs * ma.y, u[2] += xs * mb.x, u[3] += xs * mb.y;
-        }
-      }
-      for (int o = Lp >> 1; o > 0; o >>= 1)
+        const double* t0b = st0 + (it & 1) * kpad * 4;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) u[i] += __shfl_xor_sync(full, u[i], o);
-      if (a < np && part == 0) {
-        reinterpret_cast<double2*>(st0)[2 * a] = make_double2(u[0], u[1]);
-        reinterpret_cast<double2*>(st0)[2 * a + 1] = make_double2(u[2], u[3]);
+        for (int i = 0; i < 4; ++i) t[sl][i] = a < np ? t0b[a * 4 + i] : 0.0;
       }
-    }
-    __syncthreads();
-    // ---- step 2 (warp 0): dependencies, upwind fold, chain, publish
-    if (warp == 0) {
-      double t[NS][4];
-#pragma unroll
-      for (int sl = 0; sl < NS; ++sl) {
-        const int a = lane + 32 * sl;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) t[sl][i] = a < np ? st0[a * 4 + i] : 0.0;
-      }
+      g_oct = oct, g_mt = mt;
       const bool x_in_seg = upx >= 0 && jseg > 0;
       {
         const int* f = nullptr;
@@ -618,6 +651,7 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
           e[sl][i] = c - zo[sl][i] - gz;
         }
       }
+      double* dzb = sdz + (it & 1) * kpad * 4;
       for (int a = 0; a < np; ++a) {
         const int sl = a >> 5, src = a & 31;
         double dz[4];
@@ -638,8 +672,8 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
           for (int i = 0; i < 4; ++i) t[s2][i] += k * dz[i];
         }
         if (lane == 0) {
-          reinterpret_cast<double2*>(sdz)[2 * a] = make_double2(dz[0], dz[1]);
-          reinterpret_cast<double2*>(sdz)[2 * a + 1] = make_double2(dz[2], dz[3]);
+          reinterpret_cast<double2*>(dzb)[2 * a] = make_double2(dz[0], dz[1]);
+          reinterpret_cast<double2*>(dzb)[2 * a + 1] = make_double2(dz[2], dz[3]);
         }
       }
       __syncwarp();
@@ -647,7 +681,7 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
       for (int sl = 0; sl < NS; ++sl) {
         const int a = lane + 32 * sl;
         if (qs[sl] < 0) continue;
-        const double2 d0 = reinterpret_cast<const double2*>(sdz)[2 * a], d1 = reinterpret_cast<const double2*>(sdz)[2 * a + 1];
+        const double2 d0 = reinterpret_cast<const double2*>(dzb)[2 * a], d1 = reinterpret_cast<const double2*>(dzb)[2 * a + 1];
         zo[sl][0] += d0.x, zo[sl][1] += d0.y, zo[sl][2] += d1.x, zo[sl][3] += d1.y;
       }
 #pragma unroll
@@ -662,25 +696,34 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
       }
       __syncwarp();
       if (lane == 0) st_release(p.done + (size_t)oct * n_el + el, pass + 1);
-    }
-    __syncthreads();
-    // ---- step 3 (all warps): running moments, one (h, dof) output per thread, patches in order
-    {
-      double* mom_el = p.mom + (size_t)el * Hp * 4;
-      double* mw = const_cast<double*>(mom);
-      for (int o = tid; o < H * 4; o += nthr) {
-        const int h = o >> 2, i = o & 3, fi = i ^ m;  // physical dof i = frame dof i ^ m
-        double v = mom[o];
-        const double* xo = sX + h;
-        for (int a = 0; a < np; ++a) v += xo[(size_t)a * XS] * sdz[a * 4 + fi];
-        mom_el[o] = v;
-        if (reuse) mw[o] = v;
+    } else {
+      // ---------------- warps 1..3: update of item it-1, projections of item it+1
+      if (it >= 1 && !drained) update(it - 1, 32, nthr - 32, false);
+      if (it + 1 < n_items && !boundary) {
+        cp_async_wait<0>();  // this thread's part of item it+1's moments
+        bar_named(MW_BAR, nthr - 32);
+        project(it + 1, 32, nthr - 32);
       }
     }
-    if (!reuse) cur ^= 1;
-    cp_async_wait<0>();
     __syncthreads();
+    drained = false;
+    if (boundary) {  // drain: item it's update (into item it+1's buffer: same cell), new octant, t0 of it+1
+      update(it, 0, nthr, true);
+      __syncthreads();  // X / K of the old octant no longer read
+      stage_octant(oct_of(it + 1));
+      cp_async_wait<0>();
+      __syncthreads();
+      project(it + 1, 0, nthr);
+      drained = true;
+      __syncthreads();
+    }
+    // moments of item it+2 (its cell is not item it's or it+1's; reuse: written by the drain)
+    if (warp > 0 && it + 2 < n_items && cell_of(it + 2) != cell_of(it + 1)) prefetch_mom(it + 2, 32, nthr - 32);
   }
+  if (!drained && n_items >= 1) {  // last item's update
+    update(n_items - 1, 0, nthr, false);
+  }
+  cp_async_wait<0>();
 }
 
 size_t gs_smem(int Hp, int kpad, int nmat, int wpb, int rows_nx = 0) {
@@ -754,9 +797,9 @@ int coarse_gs_max_warps(int Hp, int kpad, int nmat, int max_np) {
 int coarse_gs_warps_per_block(int Hp, int kpad, int nmat) { return gs_wpb(Hp, kpad, nmat); }
 
 // multi-warp rows: whether the ny row-CTAs fit co-resident (0 = no)
-int coarse_gs_mw_ok(int Hp, int kpad, int nmat, int ny, int max_np) {
+int coarse_gs_mw_ok(int Hp, int H, int kpad, int nmat, int ny, int max_np) {
   if (max_np > 64) return 0;
-  const size_t smem = sizeof(double) * gs_mw_doubles(Hp, kpad, nmat);
+  const size_t smem = sizeof(double) * gs_mw_doubles(Hp, H, kpad, nmat);
   if (smem > 220 * 1024) return 0;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
@@ -770,7 +813,7 @@ int coarse_gs_mw_ok(int Hp, int kpad, int nmat, int ny, int max_np) {
 template <int NS>
 void launch_gs_mw(const CoarseGSParams& p, cudaStream_t s) {
   auto k = coarse_gs_mw_kernel<NS>;
-  const size_t smem = sizeof(double) * gs_mw_doubles(p.Hp, p.kpad, p.n_mat);
+  const size_t smem = sizeof(double) * gs_mw_doubles(p.Hp, p.H, p.kpad, p.n_mat);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   CoarseGSParams q = p;
   void* args[] = {&q};
