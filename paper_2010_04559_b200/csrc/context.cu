@@ -375,9 +375,11 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     L.gs_XoT = dupload(XoT, s);
     // static ownership: each warp owns a segment of gs_cpw consecutive cells of one row
     // row mode pays off once rows are long (measured: c2, c3 faster; c1 at 32^2 slower)
-    // many patches per octant (config 4: 64): a 4-warp CTA per row spreads the
-    // projections and moment updates (STAMG_GS_MW=0 keeps the one-warp kernels)
-    L.gs_mw = L.gs_max_np > 16 && !env_is_zero("STAMG_GS_MW") &&
+    // a 4-warp CTA per grid row, software-pipelined (projections and moment updates of
+    // the neighbouring items beside the chain); measured faster on every BASELINE config
+    // (10 passes: c1 12.8 -> 10.4 ms, c2 26.7 -> 20.7, c3 55.7 -> 36.8, c4 640 -> 337).
+    // STAMG_GS_MW=0 keeps the one-warp kernels
+    L.gs_mw = !env_is_zero("STAMG_GS_MW") &&
               coarse_gs_mw_ok(L.Hp, t.H, L.gs_kpad, t.n_mat, t.ny, L.gs_max_np);
     L.gs_rows = (std::getenv("STAMG_GS_SEGMENTS") || t.nx < 64)
                     ? 0

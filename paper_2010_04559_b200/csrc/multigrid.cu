@@ -430,7 +430,7 @@ constexpr int MW_BAR = 1;  // named barrier of warps 1..3
 
 __host__ __device__ inline int gs_mw_xs(int H) { return (H % 2 == 0) ? H + 1 : H + 2; }  // odd X row stride
 __host__ __device__ inline size_t gs_mw_doubles(int Hp, int H, int kpad, int nmat) {
-  return size_t(Hp) * 16 + size_t(kpad) * 16 + size_t(nmat) * kpad * kpad + size_t(kpad) * gs_mw_xs(H) + size_t(nmat) * Hp;
+  return size_t(Hp) * 16 + size_t(kpad) * 32 + size_t(nmat) * kpad * kpad + size_t(kpad) * gs_mw_xs(H) + size_t(nmat) * Hp;
 }
 
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -445,7 +445,8 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
   double* smom = gsm;                             // [4][Hp][4] moments of items k-1 .. k+2 (ring)
   double* sdz = smom + Hp * 16;                   // [2][kpad][4] chain outputs (sweep frame)
   double* st0 = sdz + kpad * 8;                   // [2][kpad][4] projections (physical dofs)
-  double* sK = st0 + kpad * 8;                    // [n_mat][kpad][kpad]
+  double* srz = st0 + kpad * 8;                   // [2][kpad][8] warp 0: rhs | iterate of the next item
+  double* sK = srz + kpad * 16;                   // [n_mat][kpad][kpad]
   double* sX = sK + (size_t)nmat * kpad * kpad;   // [kpad][Hp+1]
   const int XS = gs_mw_xs(H);
   double* sS = sX + (size_t)kpad * XS;            // [n_mat][Hp]
@@ -537,6 +538,7 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
 #pragma unroll
   for (int sl = 0; sl < NS; ++sl) xtr[sl][0] = xtr[sl][1] = 0.0;
   int g_oct = -1, g_mt = -1;  // warp 0: octant / material of the cached G, B'^-1
+  bool rz_next = false;       // warp 0: the next item's rhs / iterate are in srz
   double G[NS][16], Bq[NS][16];
   int qs[NS];
   for (int it = 0; it < n_items; ++it) {
@@ -556,6 +558,11 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
       const int mt = p.mat ? p.mat[el] : 0;
       double r[NS][4], zo[NS][4], t[NS][4];
       const bool reload = oct != g_oct || mt != g_mt;
+      const bool rz_pf = rz_next;
+      if (rz_pf) {
+        cp_async_wait<0>();
+        __syncwarp();
+      }
 #pragma unroll
       for (int sl = 0; sl < NS; ++sl) {
         const int a = lane + 32 * sl;
@@ -563,11 +570,18 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
 #pragma unroll
         for (int i = 0; i < 4; ++i) r[sl][i] = zo[sl][i] = 0.0;
         if (qs[sl] >= 0) {
-          const double* rb = p.rhs + ((size_t)el * P + qs[sl]) * 4;
-          const double2 ra = __ldg(reinterpret_cast<const double2*>(rb)), rc = __ldg(reinterpret_cast<const double2*>(rb) + 1);
-          const double2 za = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4), zc = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4 + 2);
-          r[sl][0] = ra.x, r[sl][1] = ra.y, r[sl][2] = rc.x, r[sl][3] = rc.y;
-          zo[sl][0] = za.x, zo[sl][1] = za.y, zo[sl][2] = zc.x, zo[sl][3] = zc.y;
+          if (rz_pf) {  // prefetched by the previous item (same octant)
+            const double2* d = reinterpret_cast<const double2*>(srz + ((it & 1) * kpad + a) * 8);
+            const double2 ra = d[0], rc = d[1], za = d[2], zc = d[3];
+            r[sl][0] = ra.x, r[sl][1] = ra.y, r[sl][2] = rc.x, r[sl][3] = rc.y;
+            zo[sl][0] = za.x, zo[sl][1] = za.y, zo[sl][2] = zc.x, zo[sl][3] = zc.y;
+          } else {
+            const double* rb = p.rhs + ((size_t)el * P + qs[sl]) * 4;
+            const double2 ra = __ldg(reinterpret_cast<const double2*>(rb)), rc = __ldg(reinterpret_cast<const double2*>(rb) + 1);
+            const double2 za = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4), zc = ld_cg2(p.phi + ((size_t)el * P + qs[sl]) * 4 + 2);
+            r[sl][0] = ra.x, r[sl][1] = ra.y, r[sl][2] = rc.x, r[sl][3] = rc.y;
+            zo[sl][0] = za.x, zo[sl][1] = za.y, zo[sl][2] = zc.x, zo[sl][3] = zc.y;
+          }
           if (reload) {
             const double* Gq = p.GS + ((size_t)mt * P + qs[sl]) * 16;
             const double* Bg = p.BinvGS + ((size_t)mt * P + qs[sl]) * 16;
@@ -696,6 +710,21 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
       }
       __syncwarp();
       if (lane == 0) st_release(p.done + (size_t)oct * n_el + el, pass + 1);
+      // rhs / previous iterate of the next item of this octant (its iterate was written by
+      // this warp one octant sweep ago): hidden behind the barrier and the next wait
+      rz_next = it + 1 < n_items && !boundary;
+      if (rz_next) {
+        const size_t eln = (size_t)cell_of(it + 1) * P;
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) {
+          if (qs[sl] < 0) continue;
+          double* d = srz + (((it + 1) & 1) * kpad + lane + 32 * sl) * 8;
+          const size_t off = (eln + qs[sl]) * 4;
+          cp_async16(d, p.rhs + off, true), cp_async16(d + 2, p.rhs + off + 2, true);
+          cp_async16(d + 4, p.phi + off, true), cp_async16(d + 6, p.phi + off + 2, true);
+        }
+        cp_async_commit();
+      }
     } else {
       // ---------------- warps 1..3: update of item it-1, projections of item it+1
       if (it >= 1 && !drained) update(it - 1, 32, nthr - 32, false);
