@@ -430,7 +430,8 @@ constexpr int MW_BAR = 1;  // named barrier of warps 1..3
 
 __host__ __device__ inline int gs_mw_xs(int H) { return (H % 2 == 0) ? H + 1 : H + 2; }  // odd X row stride
 __host__ __device__ inline size_t gs_mw_doubles(int Hp, int H, int kpad, int nmat) {
-  return size_t(Hp) * 16 + size_t(kpad) * 32 + size_t(nmat) * kpad * kpad + size_t(kpad) * gs_mw_xs(H) + size_t(nmat) * Hp;
+  return size_t(Hp) * 16 + size_t(kpad) * 32 + size_t(nmat) * kpad * kpad + size_t(kpad) * gs_mw_xs(H) + size_t(nmat) * Hp +
+         8;  // + oct_ptr
 }
 
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -454,17 +455,29 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
   const int gy = blockIdx.x;
   const int seg = nx;
   const int n_items = p.nu * 8 * seg;
-  auto oct_of = [&](int it) { return (it / seg) & 7; };
-  auto cell_of = [&](int it) {
-    const int oct = (it / seg) & 7, j = it % seg;
-    return gy * nx + ((oct & 1) ? seg - 1 - j : j);
+  // item descriptors advanced incrementally (no integer division per item)
+  struct Item {
+    int it, pass, oct, j, el;
+  };
+  int* sOptr = reinterpret_cast<int*>(sS + (size_t)nmat * Hp);  // oct_ptr[0..8] in shared memory
+  if (tid < 9) sOptr[tid] = p.oct_ptr[tid];
+  auto cell = [&](int oct, int j) { return gy * nx + ((oct & 1) ? seg - 1 - j : j); };
+  auto advance = [&](const Item& c) {
+    Item n = c;
+    n.it += 1, n.j += 1;
+    if (n.j == seg) {
+      n.j = 0, n.oct += 1;
+      if (n.oct == 8) n.oct = 0, n.pass += 1;
+    }
+    n.el = cell(n.oct, n.j);
+    return n;
   };
   auto mbuf = [&](int it) { return smom + (it & 3) * Hp * 4; };
-  // moments of item `it` -> its ring buffer (threads [t0, t0 + nt))
-  auto prefetch_mom = [&](int it, int t0, int nt) {
-    const double* src = p.mom + (size_t)cell_of(it) * Hp * 4;
-    double* dst = mbuf(it);
-    for (int c = tid - t0; c < H * 2; c += nt) cp_async16(dst + c * 2, src + c * 2, true);
+  // moments of item c -> its ring buffer (threads [t0, t0 + nt))
+  auto prefetch_mom = [&](const Item& c, int t0, int nt) {
+    const double* src = p.mom + (size_t)c.el * Hp * 4;
+    double* dst = mbuf(c.it);
+    for (int q = tid - t0; q < H * 2; q += nt) cp_async16(dst + q * 2, src + q * 2, true);
     cp_async_commit();
   };
   auto stage_octant = [&](int oct) {  // all threads; caller synchronises
@@ -478,16 +491,14 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
     }
     cp_async_commit();
   };
-  // t0 of item `it` by threads [t0, t0 + nt)
-  auto project = [&](int it, int t0, int nt) {
-    const int oct = oct_of(it), np = p.oct_ptr[oct + 1] - p.oct_ptr[oct];
-    const int el = cell_of(it);
-    const double* sg = sS + (size_t)(p.mat ? p.mat[el] : 0) * Hp;
-    const double* mom = mbuf(it);
-    double* out = st0 + (it & 1) * kpad * 4;
-    int Lp = 1;
-    while (Lp < 32 && Lp * 2 * np <= nt) Lp *= 2;
-    const int lt = tid - t0, a = lt / Lp, part = lt % Lp;
+  // t0 of item c by threads [t0, t0 + nt): Lp = largest power of two <= 32 with Lp * np <= nt
+  auto project = [&](const Item& c, int t0, int nt) {
+    const int np = sOptr[c.oct + 1] - sOptr[c.oct];
+    const double* sg = sS + (size_t)(p.mat ? p.mat[c.el] : 0) * Hp;
+    const double* mom = mbuf(c.it);
+    double* out = st0 + (c.it & 1) * kpad * 4;
+    const int Lp = min(32, 1 << (31 - __clz(max(1, nt / np))));
+    const int lt = tid - t0, a = lt / Lp, part = lt & (Lp - 1);
     double u[4] = {0.0, 0.0, 0.0, 0.0};
     if (a < np) {
       const double* xr = sX + (size_t)a * XS;
@@ -505,14 +516,14 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
       reinterpret_cast<double2*>(out)[2 * a + 1] = make_double2(u[2], u[3]);
     }
   };
-  // running moments of item `it` (threads [t0, t0 + nt)); with `into` also the ring buffer of item it+1
-  auto update = [&](int it, int t0, int nt, bool into_next) {
-    const int oct = oct_of(it), np = p.oct_ptr[oct + 1] - p.oct_ptr[oct];
-    const int m = (oct & 1) | (oct & 2);
-    double* mom_el = p.mom + (size_t)cell_of(it) * Hp * 4;
-    const double* mom = mbuf(it);
-    double* nxt = mbuf(it + 1);
-    const double* dz = sdz + (it & 1) * kpad * 4;
+  // running moments of item c (threads [t0, t0 + nt)); with into_next also the ring buffer of item c.it+1
+  auto update = [&](const Item& c, int t0, int nt, bool into_next) {
+    const int np = sOptr[c.oct + 1] - sOptr[c.oct];
+    const int m = (c.oct & 1) | (c.oct & 2);
+    double* mom_el = p.mom + (size_t)c.el * Hp * 4;
+    const double* mom = mbuf(c.it);
+    double* nxt = mbuf(c.it + 1);
+    const double* dz = sdz + (c.it & 1) * kpad * 4;
     for (int o = tid - t0; o < H * 4; o += nt) {
       const int h = o >> 2, fi = (o & 3) ^ m;  // physical dof i = frame dof i ^ m
       double v = mom[o];
@@ -524,14 +535,17 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
   };
 
   // ---- prologue: octant of item 0, moments of items 0 and 1, t0 of item 0
-  stage_octant(oct_of(0));
+  Item prv{-1, 0, 0, 0, 0}, cur{0, 0, 0, 0, cell(0, 0)};
+  Item n1 = advance(cur), n2 = advance(n1);
+  stage_octant(0);
+  __syncthreads();  // sOptr
   if (warp > 0) {
-    prefetch_mom(0, 32, nthr - 32);
-    if (n_items > 1 && cell_of(1) != cell_of(0)) prefetch_mom(1, 32, nthr - 32);
+    prefetch_mom(cur, 32, nthr - 32);
+    if (n_items > 1 && n1.el != cur.el) prefetch_mom(n1, 32, nthr - 32);
   }
   cp_async_wait<0>();
   __syncthreads();
-  project(0, 0, nthr);
+  project(cur, 0, nthr);
   __syncthreads();
   bool drained = true;  // item k-1's update already done (octant boundary drain)
   double xtr[NS][2];    // warp 0: x-upwind traces from the previous cell of the row
@@ -542,10 +556,10 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
   double G[NS][16], Bq[NS][16];
   int qs[NS];
   for (int it = 0; it < n_items; ++it) {
-    const int pass = it / (8 * seg), oct = oct_of(it), jseg = it % seg;
-    const int el = cell_of(it);
-    const bool boundary = it + 1 < n_items && oct_of(it + 1) != oct;  // next item: same cell, new octant
-    const int pbeg = p.oct_ptr[oct], np = p.oct_ptr[oct + 1] - pbeg;
+    const int pass = cur.pass, oct = cur.oct, jseg = cur.j;
+    const int el = cur.el;
+    const bool boundary = it + 1 < n_items && n1.oct != oct;  // next item: same cell, new octant
+    const int pbeg = sOptr[oct], np = sOptr[oct + 1] - pbeg;
     if (warp == 0) {
       // ---------------- item `it`: dependencies, upwind fold, chain, publish
       const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
@@ -714,7 +728,7 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
       // this warp one octant sweep ago): hidden behind the barrier and the next wait
       rz_next = it + 1 < n_items && !boundary;
       if (rz_next) {
-        const size_t eln = (size_t)cell_of(it + 1) * P;
+        const size_t eln = (size_t)n1.el * P;
 #pragma unroll
         for (int sl = 0; sl < NS; ++sl) {
           if (qs[sl] < 0) continue;
@@ -727,30 +741,31 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
       }
     } else {
       // ---------------- warps 1..3: update of item it-1, projections of item it+1
-      if (it >= 1 && !drained) update(it - 1, 32, nthr - 32, false);
+      if (it >= 1 && !drained) update(prv, 32, nthr - 32, false);
       if (it + 1 < n_items && !boundary) {
         cp_async_wait<0>();  // this thread's part of item it+1's moments
         bar_named(MW_BAR, nthr - 32);
-        project(it + 1, 32, nthr - 32);
+        project(n1, 32, nthr - 32);
       }
     }
     __syncthreads();
     drained = false;
     if (boundary) {  // drain: item it's update (into item it+1's buffer: same cell), new octant, t0 of it+1
-      update(it, 0, nthr, true);
+      update(cur, 0, nthr, true);
       __syncthreads();  // X / K of the old octant no longer read
-      stage_octant(oct_of(it + 1));
+      stage_octant(n1.oct);
       cp_async_wait<0>();
       __syncthreads();
-      project(it + 1, 0, nthr);
+      project(n1, 0, nthr);
       drained = true;
       __syncthreads();
     }
     // moments of item it+2 (its cell is not item it's or it+1's; reuse: written by the drain)
-    if (warp > 0 && it + 2 < n_items && cell_of(it + 2) != cell_of(it + 1)) prefetch_mom(it + 2, 32, nthr - 32);
+    if (warp > 0 && it + 2 < n_items && n2.el != n1.el) prefetch_mom(n2, 32, nthr - 32);
+    prv = cur, cur = n1, n1 = n2, n2 = advance(n2);
   }
   if (!drained && n_items >= 1) {  // last item's update
-    update(n_items - 1, 0, nthr, false);
+    update(prv, 0, nthr, false);
   }
   cp_async_wait<0>();
 }

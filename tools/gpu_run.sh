@@ -17,6 +17,14 @@ if [ "$MODE" = gsab ]; then
   for k in 1 2 3; do STAMG_GS_MW=1 timeout 300 python tools/gs_probe.py $k 10 >> gpurun_out/${T}_gs_mw.log 2>&1; done
   STAMG_GS_MW=1 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "coarse or mg_apply or solve" > gpurun_out/${T}_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_tests.log
 fi
+if [ "$MODE" = gsprofmw ]; then
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:coarse_gs -c 1 -o gpurun_out/${T}_gs_c3 python tools/gs_probe.py 3 1 > gpurun_out/${T}_ncu3.log 2>&1
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:coarse_gs -c 1 -o gpurun_out/${T}_gs_c4 python tools/gs_probe.py 4 1 > gpurun_out/${T}_ncu4.log 2>&1
+fi
+if [ "$MODE" = gst ]; then
+  timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_golden.py tests/test_gpu_fullsize_golden.py -m gpu -x -q > gpurun_out/${T}_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_tests.log
+  for k in 1 2 3 4; do timeout 300 python tools/gs_probe.py $k 10 >> gpurun_out/${T}_gs.log 2>&1; done
+fi
 if [ "$MODE" = quick ]; then
   timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -m gpu -x -q > gpurun_out/${T}_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_tests.log
   timeout 900 python bench.py --steps 3 --no-si --no-e2e --no-cpu --solve-configs 1 2 3 4 > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; echo "bench rc=$?"
