@@ -378,7 +378,9 @@ def run_b200(args, world, rank, local, dist):
         e2e_s = allmax(dist, time.perf_counter() - t0)
         e2e = {"value": total_upd * k_e2e / e2e_s, "unit": UNIT, "h2d_bytes_per_step": n * 8,
                "d2h_bytes_per_step": n * 8, "steps": k_e2e,
-               "api": "stamg_sweep_host (include/stamg_b200.h), pinned host buffers"}
+               "api": "stamg_sweep_host (include/stamg_b200.h), pinned host buffers",
+               "pipeline_chunks": g.host_pipeline_chunks()}
+        stamg.host_free(host)
     dmma_peak, _ = g.fp64_peaks()
     g.close()
     if not args.no_kernels and world == 1:

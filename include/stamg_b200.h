@@ -154,7 +154,9 @@ int stamg_solve(stamg_ctx* ctx, int method, int precond, const stamg_vec* b, sta
                 int max_iter, int restart, stamg_report* rep, double* history, int history_cap);
 
 /* Host-buffer entry points (what a reference-side FFI binds): copy in, run,
- * copy out. */
+ * copy out. stamg_sweep_host pipelines the copies with the sweep over chunks of
+ * direction groups (host->device, sweep and device->host of different chunks
+ * run concurrently); rhs and z may be the same buffer. */
 int stamg_sweep_host(stamg_ctx* ctx, int level, const double* rhs, double* z, int64_t n);
 int stamg_solve_host(stamg_ctx* ctx, int method, int precond, const double* b, double* x, int64_t n,
                      double tol, int max_iter, int restart, stamg_report* rep);
@@ -176,6 +178,8 @@ int stamg_bench_fp64_peaks(stamg_ctx* ctx, double* dmma_tflops, double* dfma_tfl
 /* pinned host buffers for the host-buffer entry points */
 int stamg_host_alloc(int64_t bytes, void** out);
 int stamg_host_free(void* p);
+/* chunks the last stamg_sweep_host was pipelined over (0: serial copy-sweep-copy) */
+int stamg_host_pipeline_chunks(stamg_ctx* ctx, int* n);
 /* kernel launches issued by this context since creation (for bench) */
 int stamg_launch_count(stamg_ctx* ctx, int64_t* n);
 /* per-kernel device time accounting: enable and read (ms) */

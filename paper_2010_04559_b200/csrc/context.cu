@@ -115,13 +115,13 @@ struct DevLevel {
   double* mom = nullptr;  // coarse GS moments
   int* gs_done = nullptr;
   double *gs_K = nullptr, *gs_Xo = nullptr, *gs_XoT = nullptr, *gs_G = nullptr;
-  int gs_blocks = 0, gs_cpw = 0, gs_kpad = 0, gs_max_np = 0, gs_rows = 0, gs_mw = 0;
+  int gs_blocks = 0, gs_cpw = 0, gs_kpad = 0, gs_max_np = 0, gs_rows = 0, gs_mw = 0, gs_cluster = 0;
   double *tmp = nullptr, *cf = nullptr, *ce = nullptr;  // V-cycle workspace
   // reflection-symmetry folded scatter (setup.hpp find_symmetry)
   int fold_G = 0, fold_R = 0, fold_Rp = 0, fold_Hf = 0;
   std::vector<int> fold_hoff;                 // [G+1] class column offsets
   std::vector<std::vector<int>> fold_hs;      // per class: ascending original harmonics
-  double *Xf = nullptr, *XfT = nullptr, *sigf = nullptr, *foldbuf = nullptr;
+  double *Xf = nullptr, *XfT = nullptr, *sigf = nullptr;
   int* orbit = nullptr;
   std::vector<void*> owned;
 };
@@ -147,6 +147,14 @@ struct stamg_ctx {
   // host-buffer entry points
   double *hostio = nullptr;
   int64_t hostio_n = 0;
+  // pipelined host-buffer sweep: copy streams, staging ring, events
+  cudaStream_t io_h2d = nullptr, io_d2h = nullptr;
+  double* pipe[3] = {nullptr, nullptr, nullptr};
+  int64_t pipe_n = 0;
+  cudaEvent_t pev[10] = {};
+  int last_host_chunks = 0;  // chunks of the last stamg_sweep_host (0: unpipelined path)
+  double* foldbuf = nullptr;  // reflection-fold workspace shared by all levels
+  int64_t foldbuf_n = 0;
   int64_t launches = 0;
   bool timing = false;
   std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -386,6 +394,11 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
                     : coarse_gs_rows_wpb(L.Hp, L.gs_kpad, t.n_mat, t.nx, t.ny, L.gs_max_np);
     if (L.gs_mw) {  // one 4-warp CTA per grid row
       L.gs_rows = 0, L.gs_cpw = t.nx, L.gs_blocks = t.ny;
+      // rows grouped in thread-block clusters: y-hops inside a cluster through DSMEM
+      // mailboxes (STAMG_GS_CLUSTER=0 keeps every hop in global memory)
+      L.gs_cluster = env_is_zero("STAMG_GS_CLUSTER")
+                         ? 0
+                         : coarse_gs_cluster_rows(L.Hp, t.H, L.gs_kpad, t.n_mat, t.nx, t.ny, L.gs_max_np);
     } else {
       const int max_warps = coarse_gs_max_warps(L.Hp, L.gs_kpad, t.n_mat, L.gs_max_np);
       int seg = 1;
@@ -409,7 +422,10 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     L.child_ptr = dupload(t.child_ptr, s), L.child_idx = dupload(t.child_idx, s);
   }
   size_t src_rows = L.Hp;
-  if (t.n_sym_axes > 0 && t.H >= 128 && c->world == 1) {  // fold only where the GEMMs are big
+  // fold only where the GEMMs are big enough to pay for the two streaming passes
+  int fold_min_h = 128;
+  if (const char* e = std::getenv("STAMG_FOLD_MIN_H")) fold_min_h = std::atoi(e);
+  if (t.n_sym_axes > 0 && t.H >= fold_min_h && c->world == 1) {
     const int G = 1 << t.n_sym_axes, R = t.P / G;
     L.fold_G = G, L.fold_R = R, L.fold_Rp = round_up(R, 64);
     const int Rk = round_up(R, 32);
@@ -444,7 +460,7 @@ void free_level(DevLevel& L) {
                   (void*)L.oct_patches, (void*)L.oct_ptr, (void*)L.up, (void*)L.child_ptr, (void*)L.child_idx,
                   (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_K, (void*)L.gs_Xo, (void*)L.gs_XoT, (void*)L.gs_G, (void*)L.Xf, (void*)L.XfT, (void*)L.groups8, (void*)L.group8_oct, (void*)L.sweep_top,
                   (void*)L.d_ipos, (void*)L.d_iid, (void*)L.stage,
-                  (void*)L.sigf, (void*)L.foldbuf, (void*)L.orbit, (void*)L.tmp, (void*)L.cf,
+                  (void*)L.sigf, (void*)L.orbit, (void*)L.tmp, (void*)L.cf,
                   (void*)L.ce})
     if (p) cudaFree(p);
 }
@@ -535,11 +551,18 @@ void scatter_into(stamg_ctx* c, DevLevel& L, const double* phi, int order, doubl
     return;
   }
   const int G = L.fold_G, R = L.fold_R, n_el = L.t.n_el;
-  if (!L.foldbuf) L.foldbuf = dalloc<double>(size_t(n_el) * L.t.P * 4);
+  // one fold workspace per context, shared by the levels (used only inside this call)
+  const int64_t need = int64_t(n_el) * L.t.P * 4;
+  if (c->foldbuf_n < need) {
+    if (c->foldbuf) cudaFree(c->foldbuf);
+    c->foldbuf = dalloc<double>(need);
+    c->foldbuf_n = need;
+  }
+  double* const fb = c->foldbuf;
   const size_t cls = size_t(n_el) * R * 4;
   {
     Timed tm(c, "fold");
-    launch_fold(phi, L.foldbuf, L.orbit, n_el, L.t.P, R, G, L.wl, c->stream);
+    launch_fold(phi, fb, L.orbit, n_el, L.t.P, R, G, L.wl, c->stream);
     ck_launch("fold");
     c->launches += 1;
   }
@@ -550,7 +573,7 @@ void scatter_into(stamg_ctx* c, DevLevel& L, const double* phi, int order, doubl
     if (hu[cl] == 0) continue;
     Timed tm(c, "d2m");
     D2MParams p;
-    p.phi = L.foldbuf + cl * cls, p.src = L.src + size_t(L.fold_hoff[cl]) * 4, p.X = L.Xf + L.fold_hoff[cl];
+    p.phi = fb + cl * cls, p.src = L.src + size_t(L.fold_hoff[cl]) * 4, p.X = L.Xf + L.fold_hoff[cl];
     p.sig = L.sigf + L.fold_hoff[cl], p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
     p.n_el = n_el, p.P = R, p.Hp = L.fold_Hf, p.Hused = hu[cl], p.Hrows = L.fold_hoff[cl + 1] - L.fold_hoff[cl];
     for (int k = 0; k < 16; ++k) p.N[k] = L.t.Nmat[k];
@@ -560,7 +583,7 @@ void scatter_into(stamg_ctx* c, DevLevel& L, const double* phi, int order, doubl
   }
   if (L.sharded) op_allreduce(c, L.src, size_t(n_el) * L.fold_Hf * 4);
   for (int cl = 0; cl < G; ++cl) {
-    double* Yc = L.foldbuf + cl * cls;
+    double* Yc = fb + cl * cls;
     if (hu[cl] == 0) {
       launch_fill(Yc, 0.0, int64_t(cls), c->stream);
       c->launches += 1;
@@ -577,7 +600,7 @@ void scatter_into(stamg_ctx* c, DevLevel& L, const double* phi, int order, doubl
     c->launches += 1;
   }
   Timed tm(c, "unfold");
-  launch_unfold(L.foldbuf, y, L.orbit, n_el, L.t.P, R, G, scale, beta, ext, L.area, c->nsum, L.wl, c->stream);
+  launch_unfold(fb, y, L.orbit, n_el, L.t.P, R, G, scale, beta, ext, L.area, c->nsum, L.wl, c->stream);
   ck_launch("unfold");
   c->launches += 1;
 }
@@ -634,6 +657,7 @@ void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* 
   p.done = L.gs_done, p.K = L.gs_K, p.Xo = L.gs_Xo, p.XoT = L.gs_XoT, p.GS = L.gs_G, p.n_mat = L.t.n_mat;
   p.cells_per_warp = L.gs_cpw, p.kpad = L.gs_kpad, p.grid_blocks = L.gs_blocks, p.rows_mode = L.gs_rows;
   p.multi_warp = L.gs_mw;
+  p.cluster = L.gs_cluster, p.mb_np = L.gs_max_np;
   p.xreg = std::getenv("STAMG_GS_XGLOBAL") ? 0 : 1;
   p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.H = L.t.H, p.nx = L.t.nx, p.ny = L.t.ny, p.nu = nu;
   for (int o = 0; o < 8; ++o)
@@ -1096,9 +1120,15 @@ int stamg_destroy(stamg_ctx* c) {
     for (auto& L : c->mg) free_level(L);
     for (double* v : c->V) cudaFree(v);
     for (void* p : {(void*)c->z, (void*)c->u, (void*)c->partial, (void*)c->dots, (void*)c->coef, (void*)c->mat,
-                    (void*)c->q_el, (void*)c->hostio})
+                    (void*)c->q_el, (void*)c->hostio, (void*)c->foldbuf})
       if (p) cudaFree(p);
     if (c->hbuf) cudaFreeHost(c->hbuf);
+    for (double* p : c->pipe)
+      if (p) cudaFree(p);
+    for (cudaEvent_t e : c->pev)
+      if (e) cudaEventDestroy(e);
+    if (c->io_h2d) cudaStreamDestroy(c->io_h2d);
+    if (c->io_d2h) cudaStreamDestroy(c->io_d2h);
     if (c->comm) nccl().commDestroy(c->comm);
     cudaStreamDestroy(c->stream);
     delete c;
@@ -1331,10 +1361,101 @@ int stamg_solve(stamg_ctx* c, int method, int precond, const stamg_vec* b, stamg
   });
 }
 
+// Host-buffer sweep pipelined over chunks of 8-direction groups (the sweep is
+// independent per direction, sweeps.cpp:28): chunk k's host->device copy, chunk
+// k-1's sweep and chunk k-2's device->host copy run at once on three streams, so
+// both PCIe directions stream concurrently. A chunk's directions are a contiguous
+// run of reference patch columns, moved by one strided 2D copy ([n_el] rows of
+// w*32 bytes at a host pitch of P*32) into a [n_el][w][4] staging buffer that the
+// sweep reads and writes in place. Returns false (caller falls back to the
+// serial path) when the level has no 8-direction groups or a chunk's patches are
+// not a contiguous reference range.
+static bool sweep_host_pipelined(stamg_ctx* c, DevLevel& L, const double* rhs, double* z) {
+  if (!L.sweep_top || env_is_zero("STAMG_E2E_PIPELINE")) return false;
+  const LevelTables& t = L.t;
+  const int ng = int(t.group8_oct.size());
+  // reference column of internal patch k (wavefront contexts reorder the tables)
+  std::vector<int> ref_of(t.P, -1);
+  if (L.wl.nd) {
+    for (int q = 0; q < t.P; ++q) ref_of[L.ipos[q]] = q;
+  }
+  auto col = [&](int k) { return L.wl.nd ? ref_of[k] : k; };
+  int chunk_dirs = 512;
+  if (const char* e = std::getenv("STAMG_E2E_CHUNK_DIRS")) chunk_dirs = std::max(8, std::atoi(e));
+  const int cg = std::max(1, std::min(chunk_dirs / 8, (ng + 3) / 4));  // >= 4 chunks when possible
+  const int nch = (ng + cg - 1) / cg;
+  std::vector<int> k0(nch), q0(nch), w(nch);
+  for (int ch = 0; ch < nch; ++ch) {
+    const int g0 = ch * cg, g1 = std::min(ng, g0 + cg);
+    k0[ch] = t.groups8[size_t(g0) * 8], w[ch] = (g1 - g0) * 8;
+    if (k0[ch] < 0) return false;
+    q0[ch] = col(k0[ch]);
+    for (int j = 0; j < w[ch]; ++j) {
+      const int k = t.groups8[size_t(g0) * 8 + j];
+      if (k != k0[ch] + j || col(k) != q0[ch] + j) return false;
+    }
+  }
+  const int64_t per = int64_t(t.n_el) * cg * 8 * 4;
+  if (c->pipe_n < per) {
+    for (double*& p : c->pipe) {
+      if (p) cudaFree(p);
+      p = nullptr;
+    }
+    for (double*& p : c->pipe) p = dalloc<double>(per);
+    c->pipe_n = per;
+  }
+  if (!c->io_h2d) {
+    ck(cudaStreamCreateWithFlags(&c->io_h2d, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&c->io_d2h, cudaStreamNonBlocking), "stream");
+    for (cudaEvent_t& e : c->pev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  }
+  cudaEvent_t* ev_h2d = c->pev;      // [3]
+  cudaEvent_t* ev_sw = c->pev + 3;   // [3]
+  cudaEvent_t* ev_d2h = c->pev + 6;  // [3]
+  cudaEvent_t ev_go = c->pev[9];
+  ck(cudaEventRecord(ev_go, c->stream), "event");  // after earlier work on the context stream
+  ck(cudaStreamWaitEvent(c->io_h2d, ev_go, 0), "wait");
+  const size_t hpitch = size_t(t.P) * 32;
+  for (int ch = 0; ch < nch; ++ch) {
+    const int b = ch % 3;
+    double* buf = c->pipe[b];
+    const size_t wb = size_t(w[ch]) * 32;
+    if (ch >= 3) ck(cudaStreamWaitEvent(c->io_h2d, ev_d2h[b], 0), "wait");
+    ck(cudaMemcpy2DAsync(buf, wb, rhs + size_t(q0[ch]) * 4, hpitch, wb, t.n_el, cudaMemcpyHostToDevice, c->io_h2d),
+       "h2d");
+    ck(cudaEventRecord(ev_h2d[b], c->io_h2d), "event");
+    ck(cudaStreamWaitEvent(c->stream, ev_h2d[b], 0), "wait");
+    {
+      Timed tm(c, "sweep");
+      SweepParams p;
+      p.g = geom(c, L);
+      p.dirs = 8, p.top = L.sweep_top;  // reference layout in the staging buffer (wl.nd = 0)
+      p.g.groups = L.groups8, p.g.group_oct = L.group8_oct, p.g.n_groups = w[ch] / 8;
+      p.grp0 = ch * cg, p.data_P = w[ch], p.data_q0 = k0[ch];
+      p.rhs = buf, p.z = buf, p.Binv = L.Binv, p.cxy = L.cxy;
+      launch_sweep(p, c->stream);
+      ck_launch("sweep");
+      c->launches += 1;
+    }
+    ck(cudaEventRecord(ev_sw[b], c->stream), "event");
+    ck(cudaStreamWaitEvent(c->io_d2h, ev_sw[b], 0), "wait");
+    ck(cudaMemcpy2DAsync(z + size_t(q0[ch]) * 4, hpitch, buf, wb, wb, t.n_el, cudaMemcpyDeviceToHost, c->io_d2h),
+       "d2h");
+    ck(cudaEventRecord(ev_d2h[b], c->io_d2h), "event");
+  }
+  ck(cudaEventRecord(ev_go, c->io_d2h), "event");
+  ck(cudaStreamWaitEvent(c->stream, ev_go, 0), "wait");
+  ck(cudaStreamSynchronize(c->stream), "sync");
+  c->last_host_chunks = nch;
+  return true;
+}
+
 int stamg_sweep_host(stamg_ctx* c, int level, const double* rhs, double* z, int64_t n) {
   return guard([&] {
     DevLevel& L = level_of(c, level);
     if (n != ref_size(L)) throw std::invalid_argument("standard_sweep: layout mismatch");
+    if (sweep_host_pipelined(c, L, rhs, z)) return;
+    c->last_host_chunks = 0;
     if (c->hostio_n < L.n) {
       if (c->hostio) cudaFree(c->hostio);
       c->hostio = dalloc<double>(L.n);
@@ -1421,6 +1542,7 @@ int stamg_get_table(stamg_ctx* c, int level, const char* name, double* out, int6
     std::vector<double> v;
     const std::string nm(name);
     if (nm == "fold") v = {double(L.fold_G), double(L.fold_R), double(L.fold_Hf)};
+    else if (nm == "gs_mode") v = {double(L.gs_mw), double(L.gs_cluster), double(L.gs_rows)};
     else if (nm == "X") v = t.X;
     else if (nm == "B") v = t.B;
     else if (nm == "Binv") v = t.Binv;
@@ -1441,6 +1563,9 @@ int stamg_get_table(stamg_ctx* c, int level, const char* name, double* out, int6
 
 int stamg_synchronize(stamg_ctx* c) {
   return guard([&] { ck(cudaStreamSynchronize(c->stream), "sync"); });
+}
+int stamg_host_pipeline_chunks(stamg_ctx* c, int* n) {
+  return guard([&] { *n = c->last_host_chunks; });
 }
 int stamg_launch_count(stamg_ctx* c, int64_t* n) {
   return guard([&] { *n = c->launches; });

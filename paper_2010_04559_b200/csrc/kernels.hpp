@@ -34,6 +34,10 @@ struct SweepParams {
   double* z = nullptr;
   const double* Binv = nullptr;  // [n_mat][P][16]
   const double* cxy = nullptr;   // [P][8]
+  // group sub-range and staged data (host-buffer pipeline): CTA b sweeps group grp0 + b;
+  // with data_P > 0 (reference-layout vectors only) the data of patch k sits at column
+  // k - data_q0 of a [n_el][data_P][4] buffer
+  int grp0 = 0, data_P = 0, data_q0 = 0;
 };
 void launch_sweep(const SweepParams& p, cudaStream_t s);
 
@@ -127,6 +131,8 @@ struct CoarseGSParams {
   int xreg = 1;       // x-upwind traces inside a segment from registers (0: through global memory)
   int rows_mode = 0;  // > 0: warp owns a whole row, CTA = rows_mode consecutive rows (shared mailbox)
   int multi_warp = 0; // 1: a CTA of 4 warps owns a whole row (projections / moment updates spread)
+  int cluster = 0;    // multi_warp: > 1 = rows per thread-block cluster (DSMEM y-mailboxes)
+  int mb_np = 0;      // mailbox patches per slot (max patches per octant)
   int n_el = 0, P = 0, Hp = 0, H = 0, nx = 0, ny = 0, nu = 0, n_mat = 1;
   int max_patches_per_octant = 0;
   double N[16];
@@ -137,6 +143,8 @@ int coarse_gs_max_warps(int Hp, int kpad, int nmat, int max_np);
 int coarse_gs_warps_per_block(int Hp, int kpad, int nmat);
 int coarse_gs_rows_wpb(int Hp, int kpad, int nmat, int nx, int ny, int max_np);
 int coarse_gs_mw_ok(int Hp, int H, int kpad, int nmat, int ny, int max_np);
+// multi-warp rows in clusters: rows per cluster (16, 8, 4 or 2) whose clusters all fit co-resident, 0 if none
+int coarse_gs_cluster_rows(int Hp, int H, int kpad, int nmat, int nx, int ny, int max_np);
 
 // BLAS-1 (deterministic reductions)
 void launch_fill(double* x, double v, int64_t n, cudaStream_t s);

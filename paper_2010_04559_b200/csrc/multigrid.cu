@@ -435,11 +435,74 @@ __host__ __device__ inline size_t gs_mw_doubles(int Hp, int H, int kpad, int nma
 }
 
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+constexpr int MAIN_BAR = 2;  // named barrier of the GSW_MW item warps (the publisher warp stays out)
 
-template <int NS>
-__global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSParams p) {
+// Cluster mode (CL): the ny row-CTAs form clusters of p.cluster consecutive rows. Inside a
+// cluster the y-upwind traces (2 doubles per patch, sweep frame) are pushed into the
+// consumer row's shared-memory mailbox with st.async (distributed shared memory), each
+// slot completing an mbarrier transaction: a y-hop costs one DSMEM write instead of a
+// global store + release fence + flag poll + acquire + L2 reload. Mailbox slot of item
+// (pass, oct, j): direction yneg, slot (oct & 1) * nx + j, use 2 * pass + (oct >= 4). A
+// row never runs more than one octant pair ahead of its y-downwind neighbour (the next
+// pair runs the other y-direction, which waits on that neighbour), so 2 nx slots per
+// direction never overrun and need no credits. Rows at a cluster edge exchange with
+// the neighbouring cluster through global memory as before; their done flags are
+// published by a fifth warp (fence + flag stores), off the item warp's chain.
+__host__ __device__ inline size_t gs_mw_cl_doubles(int nx, int mbnp) {
+  return size_t(8) * nx * mbnp + size_t(4) * nx + 2;  // mailbox [2][2nx][mbnp][2], mbarriers [2][2nx], s_pub
+}
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(unsigned bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arm(unsigned bar, unsigned bytes) {  // this CTA's arrival + expected bytes
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1;\n}" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_done(unsigned bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ unsigned cluster_map(unsigned addr, unsigned rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async2(unsigned raddr, double a, double b, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr), "d"(a),
+               "d"(b), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_release_cta_smem(int* p, int v) {
+  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cta_smem(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(int* p, int v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int NS, bool CL = false>
+__global__ void __launch_bounds__(GSW_MW * 32 + (CL ? 32 : 0), 2) coarse_gs_mw_kernel(CoarseGSParams p) {
   extern __shared__ __align__(16) double gsm[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = GSW_MW * 32;
   const unsigned full = 0xffffffffu;
   const int n_el = p.n_el, nx = p.nx, ny = p.ny, P = p.P, Hp = p.Hp, H = p.H;
   const int kpad = p.kpad, nmat = p.n_mat;
@@ -451,7 +514,8 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
   double* sX = sK + (size_t)nmat * kpad * kpad;   // [kpad][Hp+1]
   const int XS = gs_mw_xs(H);
   double* sS = sX + (size_t)kpad * XS;            // [n_mat][Hp]
-  for (int c = tid; c < nmat * Hp; c += nthr) sS[c] = p.sig[c];
+  if (tid < nthr)
+    for (int c = tid; c < nmat * Hp; c += nthr) sS[c] = p.sig[c];
   const int gy = blockIdx.x;
   const int seg = nx;
   const int n_items = p.nu * 8 * seg;
@@ -460,6 +524,48 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
     int it, pass, oct, j, el;
   };
   int* sOptr = reinterpret_cast<int*>(sS + (size_t)nmat * Hp);  // oct_ptr[0..8] in shared memory
+  // cluster mode: mailbox, its mbarriers and the publish counter after the tables
+  const int CS = CL ? p.cluster : 1, crank = CL ? int(cluster_rank()) : 0, mbnp = p.mb_np;
+  double* sMail = sS + (size_t)nmat * Hp + 8;                                     // [2][2nx][mbnp][2]
+  unsigned long long* sBar = reinterpret_cast<unsigned long long*>(sMail + (size_t)8 * nx * mbnp);  // [2][2nx]
+  int* sPub = reinterpret_cast<int*>(sBar + 4 * nx);
+  // a row at a cluster edge with a y-neighbour in the next cluster publishes global done flags
+  const bool edge_pub = CL && ((crank == 0 && gy > 0) || (crank == CS - 1 && gy < ny - 1));
+  if constexpr (CL) {
+    if (warp == 0) {
+      for (int b = lane; b < 4 * nx; b += 32) mbar_init(smem_addr(sBar + b), 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      __syncwarp();
+      for (int b = lane; b < 4 * nx; b += 32) {  // first use: octant pair (0,1) / (2,3)
+        const int dir = b / (2 * nx), o = (b % (2 * nx)) / nx + 2 * dir;
+        mbar_arm(smem_addr(sBar + b), 16u * unsigned(p.oct_ptr[o + 1] - p.oct_ptr[o]));
+      }
+      if (lane == 0) *sPub = 0;
+    }
+    cluster_sync_all();
+    if (warp == GSW_MW) {  // publisher: done flags of this edge row, fenced in batches
+      if (edge_pub && lane == 0) {
+        int pass = 0, oct = 0, j = 0;
+        for (int done_items = 0; done_items < p.nu * 8 * nx;) {
+          const int avail = ld_acquire_cta_smem(sPub);
+          if (avail == done_items) {  // shares an issue slot with warp 0: poll gently
+            __nanosleep(32);
+            continue;
+          }
+          fence_acq_rel();
+          for (; done_items < avail; ++done_items) {
+            const int el = gy * nx + ((oct & 1) ? nx - 1 - j : j);
+            st_relaxed(p.done + (size_t)oct * n_el + el, pass + 1);
+            if (++j == nx) {
+              j = 0;
+              if (++oct == 8) oct = 0, ++pass;
+            }
+          }
+        }
+      }
+    }
+  }
+  if (!CL || warp < GSW_MW) {
   if (tid < 9) sOptr[tid] = p.oct_ptr[tid];
   auto cell = [&](int oct, int j) { return gy * nx + ((oct & 1) ? seg - 1 - j : j); };
   auto advance = [&](const Item& c) {
@@ -538,15 +644,15 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
   Item prv{-1, 0, 0, 0, 0}, cur{0, 0, 0, 0, cell(0, 0)};
   Item n1 = advance(cur), n2 = advance(n1);
   stage_octant(0);
-  __syncthreads();  // sOptr
+  bar_named(MAIN_BAR, nthr);  // sOptr
   if (warp > 0) {
     prefetch_mom(cur, 32, nthr - 32);
     if (n_items > 1 && n1.el != cur.el) prefetch_mom(n1, 32, nthr - 32);
   }
   cp_async_wait<0>();
-  __syncthreads();
+  bar_named(MAIN_BAR, nthr);
   project(cur, 0, nthr);
-  __syncthreads();
+  bar_named(MAIN_BAR, nthr);
   bool drained = true;  // item k-1's update already done (octant boundary drain)
   double xtr[NS][2];    // warp 0: x-upwind traces from the previous cell of the row
 #pragma unroll
@@ -612,19 +718,36 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
       }
       g_oct = oct, g_mt = mt;
       const bool x_in_seg = upx >= 0 && jseg > 0;
+      // cluster mode: y-neighbours inside the cluster exchange through the mailbox
+      const bool up_mail = CL && upy >= 0 && (yneg ? crank < CS - 1 : crank > 0);
+      const bool dn_mail = CL && dny >= 0 && (yneg ? crank > 0 : crank < CS - 1);
+      const int mslot = yneg * 2 * nx + (oct & 1) * nx + jseg;  // [dir][slot]
       {
         const int* f = nullptr;
         int need = 0;
         const int* d = p.done + (size_t)oct * n_el;
         if (lane == 0 && upx >= 0 && !x_in_seg) f = d + upx, need = pass + 1;
-        if (lane == 1 && upy >= 0) f = d + upy, need = pass + 1;
+        if (lane == 1 && upy >= 0 && !up_mail) f = d + upy, need = pass + 1;
         if (lane == 2 && pass > 0 && dnx >= 0 && jseg == seg - 1) f = d + dnx, need = pass;
-        if (lane == 3 && pass > 0 && dny >= 0) f = d + dny, need = pass;
+        if (lane == 3 && pass > 0 && dny >= 0 && !dn_mail) f = d + dny, need = pass;
         bool ok = f == nullptr || ld_relaxed(f) >= need;
         const bool any = __any_sync(full, f != nullptr);
         while (!__all_sync(full, ok))
           if (!ok) ok = ld_relaxed(f) >= need;
         if (any) fence_acq_rel();
+        if constexpr (CL) {
+          if (up_mail) {
+            const unsigned bar = smem_addr(sBar + mslot);
+            const unsigned par = unsigned(2 * pass + (oct >= 4 ? 1 : 0)) & 1u;
+            while (!mbar_done(bar, par)) {
+            }
+            __syncwarp();
+            if (lane == 0) {  // arm the slot's next use: same column, octant oct ^ 4
+              const int o2 = oct ^ 4;
+              mbar_arm(bar, 16u * unsigned(sOptr[o2 + 1] - sOptr[o2]));
+            }
+          }
+        }
       }
 #pragma unroll
       for (int sl = 0; sl < NS; ++sl) {
@@ -638,7 +761,10 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
         } else if (x_in_seg) {
           ux[1] = xtr[sl][0], ux[3] = xtr[sl][1];
         }
-        if (upy >= 0) {
+        if (up_mail) {  // frame traces pushed by the upwind row
+          const double2 v = reinterpret_cast<const double2*>(sMail)[(size_t)mslot * mbnp + lane + 32 * sl];
+          uy[2] = v.x, uy[3] = v.y;
+        } else if (upy >= 0) {
           const double2 a = ld_cg2(p.phi + ((size_t)upy * P + q) * 4), b = ld_cg2(p.phi + ((size_t)upy * P + q) * 4 + 2);
           uy[0] = a.x, uy[1] = a.y, uy[2] = b.x, uy[3] = b.y;
           perm(m, uy[0], uy[1], uy[2], uy[3]);
@@ -712,6 +838,18 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
         const double2 d0 = reinterpret_cast<const double2*>(dzb)[2 * a], d1 = reinterpret_cast<const double2*>(dzb)[2 * a + 1];
         zo[sl][0] += d0.x, zo[sl][1] += d0.y, zo[sl][2] += d1.x, zo[sl][3] += d1.y;
       }
+      if constexpr (CL) {
+        if (dn_mail) {  // push the top traces into the downwind row's mailbox
+          const unsigned rk = unsigned(yneg ? crank - 1 : crank + 1);
+          const unsigned rbar = cluster_map(smem_addr(sBar + mslot), rk);
+#pragma unroll
+          for (int sl = 0; sl < NS; ++sl) {
+            if (qs[sl] < 0) continue;
+            const unsigned dst = cluster_map(smem_addr(sMail + ((size_t)mslot * mbnp + lane + 32 * sl) * 2), rk);
+            st_async2(dst, zo[sl][2], zo[sl][3], rbar);
+          }
+        }
+      }
 #pragma unroll
       for (int sl = 0; sl < NS; ++sl) {
         const int q = qs[sl];
@@ -723,7 +861,11 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
         st_cg2(zb + 2, make_double2(zo[sl][2], zo[sl][3]));
       }
       __syncwarp();
-      if (lane == 0) st_release(p.done + (size_t)oct * n_el + el, pass + 1);
+      if constexpr (CL) {
+        if (edge_pub && lane == 0) st_release_cta_smem(sPub, it + 1);  // the publisher warp fences and flags
+      } else {
+        if (lane == 0) st_release(p.done + (size_t)oct * n_el + el, pass + 1);
+      }
       // rhs / previous iterate of the next item of this octant (its iterate was written by
       // this warp one octant sweep ago): hidden behind the barrier and the next wait
       rz_next = it + 1 < n_items && !boundary;
@@ -748,17 +890,17 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
         project(n1, 32, nthr - 32);
       }
     }
-    __syncthreads();
+    bar_named(MAIN_BAR, nthr);
     drained = false;
     if (boundary) {  // drain: item it's update (into item it+1's buffer: same cell), new octant, t0 of it+1
       update(cur, 0, nthr, true);
-      __syncthreads();  // X / K of the old octant no longer read
+      bar_named(MAIN_BAR, nthr);  // X / K of the old octant no longer read
       stage_octant(n1.oct);
       cp_async_wait<0>();
-      __syncthreads();
+      bar_named(MAIN_BAR, nthr);
       project(n1, 0, nthr);
       drained = true;
-      __syncthreads();
+      bar_named(MAIN_BAR, nthr);
     }
     // moments of item it+2 (its cell is not item it's or it+1's; reuse: written by the drain)
     if (warp > 0 && it + 2 < n_items && n2.el != n1.el) prefetch_mom(n2, 32, nthr - 32);
@@ -768,6 +910,8 @@ __global__ void __launch_bounds__(GSW_MW * 32, 2) coarse_gs_mw_kernel(CoarseGSPa
     update(prv, 0, nthr, false);
   }
   cp_async_wait<0>();
+  }  // item warps
+  if constexpr (CL) cluster_sync_all();  // no CTA leaves while a neighbour may still write its mailbox
 }
 
 size_t gs_smem(int Hp, int kpad, int nmat, int wpb, int rows_nx = 0) {
@@ -854,8 +998,55 @@ int coarse_gs_mw_ok(int Hp, int H, int kpad, int nmat, int ny, int max_np) {
   return per_sm * sms >= ny ? 1 : 0;
 }
 
+size_t gs_mw_cl_smem(int Hp, int H, int kpad, int nmat, int nx, int mbnp) {
+  return sizeof(double) * (gs_mw_doubles(Hp, H, kpad, nmat) + gs_mw_cl_doubles(nx, mbnp));
+}
+
+template <int NS>
+cudaLaunchConfig_t gs_cl_config(const CoarseGSParams& p, cudaLaunchAttribute* at, size_t smem, int rows, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.ny), cfg.blockDim = dim3((GSW_MW + 1) * 32), cfg.dynamicSmemBytes = smem, cfg.stream = s;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = rows, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+  cfg.attrs = at, cfg.numAttrs = 1;
+  auto k = coarse_gs_mw_kernel<NS, true>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  return cfg;
+}
+
+template <int NS>
+int gs_cluster_rows_t(int Hp, int H, int kpad, int nmat, int nx, int ny, int max_np) {
+  const size_t smem = gs_mw_cl_smem(Hp, H, kpad, nmat, nx, max_np);
+  if (smem > 110 * 1024) return 0;  // keep two row-CTAs per SM
+  for (int rows : {16, 8, 4, 2}) {
+    if (ny % rows != 0 || ny / rows < 2) continue;
+    CoarseGSParams p;
+    p.ny = ny;
+    cudaLaunchAttribute at[1];
+    cudaLaunchConfig_t cfg = gs_cl_config<NS>(p, at, smem, rows, nullptr);
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, coarse_gs_mw_kernel<NS, true>, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (nclusters >= ny / rows) return rows;
+  }
+  return 0;
+}
+
+template <int NS>
+void launch_gs_mw_cluster(const CoarseGSParams& p, cudaStream_t s) {
+  const size_t smem = gs_mw_cl_smem(p.Hp, p.H, p.kpad, p.n_mat, p.nx, p.mb_np);
+  cudaLaunchAttribute at[1];
+  cudaLaunchConfig_t cfg = gs_cl_config<NS>(p, at, smem, p.cluster, s);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, coarse_gs_mw_kernel<NS, true>, p);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("coarse_gs cluster launch: ") + cudaGetErrorString(e));
+}
+
 template <int NS>
 void launch_gs_mw(const CoarseGSParams& p, cudaStream_t s) {
+  if (p.cluster > 1) return launch_gs_mw_cluster<NS>(p, s);
   auto k = coarse_gs_mw_kernel<NS>;
   const size_t smem = sizeof(double) * gs_mw_doubles(p.Hp, p.H, p.kpad, p.n_mat);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -863,6 +1054,12 @@ void launch_gs_mw(const CoarseGSParams& p, cudaStream_t s) {
   void* args[] = {&q};
   const cudaError_t e = cudaLaunchCooperativeKernel((const void*)k, dim3(p.ny), dim3(GSW_MW * 32), args, smem, s);
   if (e != cudaSuccess) throw std::runtime_error(std::string("coarse_gs cooperative launch: ") + cudaGetErrorString(e));
+}
+
+int coarse_gs_cluster_rows(int Hp, int H, int kpad, int nmat, int nx, int ny, int max_np) {
+  if (max_np > 64) return 0;
+  return max_np > 32 ? gs_cluster_rows_t<2>(Hp, H, kpad, nmat, nx, ny, max_np)
+                     : gs_cluster_rows_t<1>(Hp, H, kpad, nmat, nx, ny, max_np);
 }
 
 void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s) {

@@ -54,11 +54,12 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
   double* sB = reinterpret_cast<double*>(xw + 2 * NW * DIRS);
 
   const int tid = threadIdx.x, dir = tid % DIRS, r = tid / DIRS, lane = tid & 31, warp = tid >> 5;
-  const int grp = blockIdx.x;
+  const int grp = blockIdx.x + p.grp0;
   const int q = p.g.groups[grp * DIRS + dir];
   const int oct = p.g.group_oct[grp];
   const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
   const int nx = p.g.nx, ny = p.g.ny, P = p.g.P;
+  const int DP = p.data_P > 0 ? p.data_P : P, DQ0 = p.data_P > 0 ? p.data_q0 : 0;
   const bool qok = q >= 0;
   const int qq = qok ? q : 0;
   double2* gtop = p.top + (size_t)grp * DIRS * nx;  // TOPG scratch of this group
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
     const int gx = xneg ? nx - 1 - c.i : c.i, gy = yneg ? ny - 1 - j : (j < ny ? j : 0);
     c.el = gy * nx + gx;
     if constexpr (WLAY) c.off = (((size_t)grp * p.wl.slots + wl_slot_frame(p.wl, c.i, j)) * DIRS + dir) * 4;
-    else c.off = ((size_t)c.el * P + qq) * 4;
+    else c.off = ((size_t)c.el * DP + (qq - DQ0)) * 4;
   };
   auto advance = [&](Cursor& c) {
     const int k = c.k + 1;
@@ -115,7 +116,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
     }
     c.k = k, c.i += 1, c.el += dx;
     if constexpr (WLAY) c.off += (size_t)R * DIRS * 4;
-    else c.off += (size_t)dx * P * 4;
+    else c.off += (ptrdiff_t)dx * DP * 4;
   };
   auto issue = [&](int t, const Cursor& c) {
     const bool ok = c.ok;

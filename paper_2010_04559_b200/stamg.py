@@ -217,6 +217,11 @@ class Context:
     def synchronize(self):
         _check(lib().stamg_synchronize(self.h))
 
+    def host_pipeline_chunks(self):
+        n = C.c_int()
+        _check(lib().stamg_host_pipeline_chunks(self.h, C.byref(n)))
+        return n.value
+
     def launch_count(self):
         n = C.c_int64()
         _check(lib().stamg_launch_count(self.h, C.byref(n)))
@@ -372,3 +377,8 @@ def host_alloc(n_doubles: int) -> np.ndarray:
     _check(lib().stamg_host_alloc(C.c_int64(n_doubles * 8), C.byref(p)))
     arr = np.ctypeslib.as_array(C.cast(p, dp), shape=(n_doubles,))
     return arr
+
+
+def host_free(arr: np.ndarray) -> None:
+    """Release a buffer from host_alloc (the array must not be used afterwards)."""
+    _check(lib().stamg_host_free(C.c_void_p(arr.ctypes.data)))

@@ -41,4 +41,18 @@ if [ "$MODE" = gsprof4 ]; then
   timeout 300 python tools/gs_probe.py 4 1 > gpurun_out/${T}_gs.log 2>&1
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:coarse_gs -c 1 -o gpurun_out/${T}_gs_c4 python tools/gs_probe.py 4 1 > gpurun_out/${T}_ncu.log 2>&1
 fi
+if [ "$MODE" = e2e ]; then
+  timeout 600 python -m pytest tests/test_gpu_fullsize.py -m gpu -x -q -k "sweep_host" > gpurun_out/${T}_e2etest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_e2etest.log
+  for cd in 256 512 1024; do STAMG_E2E_CHUNK_DIRS=$cd timeout 600 python bench.py --steps 3 --no-si --no-solve --no-kernels --no-cpu > gpurun_out/${T}_e2e_$cd.json 2>> gpurun_out/${T}_e2e.err; done
+  STAMG_E2E_PIPELINE=0 timeout 600 python bench.py --steps 3 --no-si --no-solve --no-kernels --no-cpu > gpurun_out/${T}_e2e_serial.json 2>> gpurun_out/${T}_e2e.err
+  timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${T}_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_tests.log
+fi
+if [ "$MODE" = cl ]; then
+  timeout 300 python -m pytest tests/test_gpu_coarse_cluster.py -m gpu -x -q > gpurun_out/${T}_cltest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_cltest.log
+  for k in 1 2 3 4; do timeout 120 python tools/gs_probe.py $k 10 >> gpurun_out/${T}_gs.log 2>&1; done
+  for k in 1 2 3; do STAMG_GS_CLUSTER=0 timeout 120 python tools/gs_probe.py $k 10 >> gpurun_out/${T}_gs0.log 2>&1; done
+  timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "coarse or mg_apply or gmres or bicgstab" > gpurun_out/${T}_ptest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_ptest.log
+  timeout 600 python bench.py --steps 3 --no-si --no-e2e --no-cpu --no-kernels --solve-configs 1 2 3 > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; echo "bench rc=$?"
+  STAMG_FOLD_MIN_H=16 timeout 600 python bench.py --steps 3 --no-si --no-e2e --no-cpu --no-kernels --solve-configs 2 3 > gpurun_out/${T}_bench_fold.json 2> gpurun_out/${T}_bench_fold.err; echo "bench rc=$?"
+fi
 echo done
