@@ -55,4 +55,11 @@ if [ "$MODE" = cl ]; then
   timeout 600 python bench.py --steps 3 --no-si --no-e2e --no-cpu --no-kernels --solve-configs 1 2 3 > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; echo "bench rc=$?"
   STAMG_FOLD_MIN_H=16 timeout 600 python bench.py --steps 3 --no-si --no-e2e --no-cpu --no-kernels --solve-configs 2 3 > gpurun_out/${T}_bench_fold.json 2> gpurun_out/${T}_bench_fold.err; echo "bench rc=$?"
 fi
+if [ "$MODE" = gsprofcl ]; then
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:coarse_gs -c 1 -o gpurun_out/${T}_gs_c3 python tools/gs_probe.py 3 2 > gpurun_out/${T}_ncu3.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:coarse_gs -c 1 -o gpurun_out/${T}_gs_c2 python tools/gs_probe.py 2 2 > gpurun_out/${T}_ncu2.log 2>&1
+fi
+if [ "$MODE" = gsprof4mw ]; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:coarse_gs -c 1 -o gpurun_out/${T}_gs_c4 python tools/gs_probe.py 4 1 > gpurun_out/${T}_ncu4.log 2>&1
+fi
 echo done
