@@ -32,6 +32,7 @@ if [ "$MODE" = final ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 2 --warmup 3 --no-si --no-e2e --no-solve --no-kernels --no-cpu > gpurun_out/${T}_ncu_launch.log 2>&1
   C5N=256 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"d2m|m2d|unfold|fold" -c 4 -o gpurun_out/${T}_si256 python tools/perf_probe.py si > gpurun_out/${T}_ncu_si.log 2>&1
   C5N=128 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep_kernel" -c 2 -o gpurun_out/${T}_sweep128 python tools/perf_probe.py c5s > gpurun_out/${T}_ncu_sweep.log 2>&1
+  timeout 900 python bench.py --steps 3 --no-si --no-e2e --no-cpu --no-kernels --solve-configs 4 > gpurun_out/${T}_bench_c4.json 2> gpurun_out/${T}_bench_c4.err
 fi
 if [ "$MODE" = quick ]; then
   timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -m gpu -x -q > gpurun_out/${T}_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_tests.log
