@@ -63,4 +63,8 @@ fi
 if [ "$MODE" = gsprof4mw ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:coarse_gs -c 1 -o gpurun_out/${T}_gs_c4 python tools/gs_probe.py 4 1 > gpurun_out/${T}_ncu4.log 2>&1
 fi
+if [ "$MODE" = c4fold ]; then
+  STAMG_FOLD_MIN_H=16 timeout 900 python bench.py --steps 3 --no-si --no-e2e --no-cpu --no-kernels --solve-configs 4 > gpurun_out/${T}_bench_c4fold.json 2> gpurun_out/${T}_bench_c4fold.err
+  STAMG_FOLD_MIN_H=16 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "scatter or mg_apply or gmres or smoother" > gpurun_out/${T}_ptest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_ptest.log
+fi
 echo done
