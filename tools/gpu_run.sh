@@ -67,4 +67,10 @@ if [ "$MODE" = c4fold ]; then
   STAMG_FOLD_MIN_H=16 timeout 900 python bench.py --steps 3 --no-si --no-e2e --no-cpu --no-kernels --solve-configs 4 > gpurun_out/${T}_bench_c4fold.json 2> gpurun_out/${T}_bench_c4fold.err
   STAMG_FOLD_MIN_H=16 timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "scatter or mg_apply or gmres or smoother" > gpurun_out/${T}_ptest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_ptest.log
 fi
+if [ "$MODE" = chain ]; then
+  timeout 300 python -m pytest tests/test_gpu_coarse_cluster.py -m gpu -x -q > gpurun_out/${T}_cltest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_cltest.log
+  for k in 1 2 3 4; do timeout 120 python tools/gs_probe.py $k 10 >> gpurun_out/${T}_gs.log 2>&1; done
+  timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "coarse or mg_apply or gmres or bicgstab" > gpurun_out/${T}_ptest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_ptest.log
+  STAMG_FOLD_MIN_H=16 timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "scatter or mg_apply or smoother" > gpurun_out/${T}_ftest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_ftest.log
+fi
 echo done
