@@ -116,6 +116,7 @@ struct DevLevel {
   int* gs_done = nullptr;
   double *gs_K = nullptr, *gs_Xo = nullptr, *gs_XoT = nullptr, *gs_G = nullptr;
   int gs_blocks = 0, gs_cpw = 0, gs_kpad = 0, gs_max_np = 0, gs_rows = 0, gs_mw = 0, gs_cluster = 0;
+  int gs_mb_slots = 0, gs_mb_credit = 0;
   double *tmp = nullptr, *cf = nullptr, *ce = nullptr;  // V-cycle workspace
   // reflection-symmetry folded scatter (setup.hpp find_symmetry)
   int fold_G = 0, fold_R = 0, fold_Rp = 0, fold_Hf = 0;
@@ -396,9 +397,10 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
       L.gs_rows = 0, L.gs_cpw = t.nx, L.gs_blocks = t.ny;
       // rows grouped in thread-block clusters: y-hops inside a cluster through DSMEM
       // mailboxes (STAMG_GS_CLUSTER=0 keeps every hop in global memory)
-      L.gs_cluster = env_is_zero("STAMG_GS_CLUSTER")
+      const int cl = env_is_zero("STAMG_GS_CLUSTER")
                          ? 0
                          : coarse_gs_cluster_rows(L.Hp, t.H, L.gs_kpad, t.n_mat, t.nx, t.ny, L.gs_max_np);
+      L.gs_cluster = cl & 127, L.gs_mb_credit = (cl >> 7) & 1, L.gs_mb_slots = cl >> 8;
     } else {
       const int max_warps = coarse_gs_max_warps(L.Hp, L.gs_kpad, t.n_mat, L.gs_max_np);
       int seg = 1;
@@ -659,7 +661,8 @@ void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* 
   p.done = L.gs_done, p.K = L.gs_K, p.Xo = L.gs_Xo, p.XoT = L.gs_XoT, p.GS = L.gs_G, p.n_mat = L.t.n_mat;
   p.cells_per_warp = L.gs_cpw, p.kpad = L.gs_kpad, p.grid_blocks = L.gs_blocks, p.rows_mode = L.gs_rows;
   p.multi_warp = L.gs_mw;
-  p.cluster = L.gs_cluster, p.mb_np = L.gs_max_np;
+  p.cluster = L.gs_cluster, p.mb_np = L.gs_max_np, p.mb_slots = L.gs_mb_slots, p.mb_credit = L.gs_mb_credit;
+  p.mom_stride = L.gs_mb_credit ? (L.t.H + 1) / 2 * 2 : 0;
   p.xreg = std::getenv("STAMG_GS_XGLOBAL") ? 0 : 1;
   p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.H = L.t.H, p.nx = L.t.nx, p.ny = L.t.ny, p.nu = nu;
   for (int o = 0; o < 8; ++o)
@@ -1544,7 +1547,8 @@ int stamg_get_table(stamg_ctx* c, int level, const char* name, double* out, int6
     std::vector<double> v;
     const std::string nm(name);
     if (nm == "fold") v = {double(L.fold_G), double(L.fold_R), double(L.fold_Hf)};
-    else if (nm == "gs_mode") v = {double(L.gs_mw), double(L.gs_cluster), double(L.gs_rows)};
+    else if (nm == "gs_mode")
+      v = {double(L.gs_mw), double(L.gs_cluster), double(L.gs_rows), double(L.gs_mb_slots), double(L.gs_mb_credit)};
     else if (nm == "X") v = t.X;
     else if (nm == "B") v = t.B;
     else if (nm == "Binv") v = t.Binv;

@@ -133,6 +133,9 @@ struct CoarseGSParams {
   int multi_warp = 0; // 1: a CTA of 4 warps owns a whole row (projections / moment updates spread)
   int cluster = 0;    // multi_warp: > 1 = rows per thread-block cluster (DSMEM y-mailboxes)
   int mb_np = 0;      // mailbox patches per slot (max patches per octant)
+  int mb_slots = 0;   // mailbox slots per y-direction: 2 nx, or a power of two with credits
+  int mb_credit = 0;  // 1: the downwind row returns slots (ring smaller than two octants of a row)
+  int mom_stride = 0; // multi-warp: shared moment ring row stride (0 = Hp; H rounded to even with rings)
   int n_el = 0, P = 0, Hp = 0, H = 0, nx = 0, ny = 0, nu = 0, n_mat = 1;
   int max_patches_per_octant = 0;
   double N[16];
@@ -143,7 +146,8 @@ int coarse_gs_max_warps(int Hp, int kpad, int nmat, int max_np);
 int coarse_gs_warps_per_block(int Hp, int kpad, int nmat);
 int coarse_gs_rows_wpb(int Hp, int kpad, int nmat, int nx, int ny, int max_np);
 int coarse_gs_mw_ok(int Hp, int H, int kpad, int nmat, int ny, int max_np);
-// multi-warp rows in clusters: rows per cluster (16, 8, 4 or 2) whose clusters all fit co-resident, 0 if none
+// multi-warp rows in clusters: (mailbox slots << 8) | (credit << 7) | rows per cluster (16, 8, 4 or 2)
+// for the largest mailbox whose clusters all fit co-resident, 0 if none
 int coarse_gs_cluster_rows(int Hp, int H, int kpad, int nmat, int nx, int ny, int max_np);
 
 // BLAS-1 (deterministic reductions)

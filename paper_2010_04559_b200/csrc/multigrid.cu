@@ -15,6 +15,7 @@
 // warp (lane owns harmonics lane, lane+32, ...). Results are bitwise
 // reproducible run to run.
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -426,12 +427,13 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
 // nx items). Moments use a 4-buffer ring (items k-1 .. k+2), t0 and dz two buffers.
 // Co-residency of the ny CTAs is required (cooperative launch).
 constexpr int GSW_MW = 4;
+
 constexpr int MW_BAR = 1;  // named barrier of warps 1..3
 
 __host__ __device__ inline int gs_mw_xs(int H) { return (H % 2 == 0) ? H + 1 : H + 2; }  // odd X row stride
-__host__ __device__ inline size_t gs_mw_doubles(int Hp, int H, int kpad, int nmat) {
-  return size_t(Hp) * 16 + size_t(kpad) * 32 + size_t(nmat) * kpad * kpad + size_t(kpad) * gs_mw_xs(H) + size_t(nmat) * Hp +
-         8;  // + oct_ptr
+__host__ __device__ inline size_t gs_mw_doubles(int Hp, int H, int kpad, int nmat, int hs = 0) {
+  return size_t(hs > 0 ? hs : Hp) * 16 + size_t(kpad) * 32 + size_t(nmat) * kpad * kpad + size_t(kpad) * gs_mw_xs(H) +
+         size_t(nmat) * Hp + 8;  // + oct_ptr
 }
 
 __device__ __forceinline__ void bar_named(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -448,8 +450,13 @@ constexpr int MAIN_BAR = 2;  // named barrier of the GSW_MW item warps (the publ
 // direction never overrun and need no credits. Rows at a cluster edge exchange with
 // the neighbouring cluster through global memory as before; their done flags are
 // published by a fifth warp (fence + flag stores), off the item warp's chain.
-__host__ __device__ inline size_t gs_mw_cl_doubles(int nx, int mbnp) {
-  return size_t(8) * nx * mbnp + size_t(4) * nx + 2;  // mailbox [2][2nx][mbnp][2], mbarriers [2][2nx], s_pub
+__host__ __device__ inline size_t gs_mw_cl_doubles(int nslots, int mbnp) {
+  return size_t(4) * nslots * mbnp + size_t(2) * nslots + 2;  // mailbox [2][nslots][mbnp][2], mbarriers [2][nslots], s_pub + credits
+}
+// octant of the n-th item of y-direction d (0: +y octants 0,1,4,5; 1: -y octants 2,3,6,7) of a row
+__host__ __device__ inline int gs_cls_oct(int n, int d, int nx) {
+  const int pi = n / (2 * nx), r = n - pi * 2 * nx;
+  return (pi & 1) * 4 + d * 2 + (r >= nx ? 1 : 0);
 }
 __device__ __forceinline__ unsigned smem_addr(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(unsigned bar, int count) {
@@ -495,19 +502,34 @@ __device__ __forceinline__ int ld_acquire_cta_smem(const int* p) {
   asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
   return v;
 }
+__device__ __forceinline__ void st_release_cluster_remote(unsigned raddr, int v) {
+  asm volatile("st.release.cluster.shared::cluster.s32 [%0], %1;" ::"r"(raddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cluster_smem(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cluster.shared::cta.s32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_relaxed(int* p, int v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-template <int NS, bool CL = false>
-__global__ void __launch_bounds__(GSW_MW * 32 + (CL ? 32 : 0), 2) coarse_gs_mw_kernel(CoarseGSParams p) {
+// PUBW: a fifth warp publishes the edge rows' done flags (one-slot kernel); the 64-patch
+// kernel (NS = 2) needs all 255 registers of a 128-thread CTA, so helper warp 3 publishes
+// the previous item's flag at the top of each iteration instead (the helpers have slack there)
+template <int NS, bool CL>
+constexpr bool gs_pubw() { return CL && NS == 1; }
+template <int NS, bool CL = false, bool RING = false>
+__global__ void __launch_bounds__(GSW_MW * 32 + (gs_pubw<NS, CL>() ? 32 : 0), 2) coarse_gs_mw_kernel(CoarseGSParams p) {
+  constexpr bool PUBW = gs_pubw<NS, CL>();
   extern __shared__ __align__(16) double gsm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = GSW_MW * 32;
   const unsigned full = 0xffffffffu;
   const int n_el = p.n_el, nx = p.nx, ny = p.ny, P = p.P, Hp = p.Hp, H = p.H;
   const int kpad = p.kpad, nmat = p.n_mat;
   double* smom = gsm;                             // [4][Hp][4] moments of items k-1 .. k+2 (ring)
-  double* sdz = smom + Hp * 16;                   // [2][kpad][4] chain outputs (sweep frame)
+  const int HS = p.mom_stride > 0 ? p.mom_stride : Hp;  // moment ring stride (Hp; H rounded up to even for rings)
+  double* sdz = smom + HS * 16;                   // [2][kpad][4] chain outputs (sweep frame)
   double* st0 = sdz + kpad * 8;                   // [2][kpad][4] projections (physical dofs)
   double* srz = st0 + kpad * 8;                   // [2][kpad][8] warp 0: rhs | iterate of the next item
   double* sK = srz + kpad * 16;                   // [n_mat][kpad][kpad]
@@ -526,24 +548,27 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (CL ? 32 : 0), 2) coarse_gs_mw_k
   int* sOptr = reinterpret_cast<int*>(sS + (size_t)nmat * Hp);  // oct_ptr[0..8] in shared memory
   // cluster mode: mailbox, its mbarriers and the publish counter after the tables
   const int CS = CL ? p.cluster : 1, crank = CL ? int(cluster_rank()) : 0, mbnp = p.mb_np;
-  double* sMail = sS + (size_t)nmat * Hp + 8;                                     // [2][2nx][mbnp][2]
-  unsigned long long* sBar = reinterpret_cast<unsigned long long*>(sMail + (size_t)8 * nx * mbnp);  // [2][2nx]
-  int* sPub = reinterpret_cast<int*>(sBar + 4 * nx);
+  const int NSL = p.mb_slots;  // mailbox slots per direction: 2 nx (no credits) or a power of two (credits)
+  constexpr bool credit = RING;  // mailbox ring with credits (p.mb_credit)
+  double* sMail = sS + (size_t)nmat * Hp + 8;                                     // [2][NSL][mbnp][2]
+  unsigned long long* sBar = reinterpret_cast<unsigned long long*>(sMail + (size_t)4 * NSL * mbnp);  // [2][NSL]
+  int* sPub = reinterpret_cast<int*>(sBar + 2 * NSL);
+  int* sCred = sPub + 1;  // [2] items of each direction the downwind row has consumed (written remotely)
   // a row at a cluster edge with a y-neighbour in the next cluster publishes global done flags
   const bool edge_pub = CL && ((crank == 0 && gy > 0) || (crank == CS - 1 && gy < ny - 1));
   if constexpr (CL) {
     if (warp == 0) {
-      for (int b = lane; b < 4 * nx; b += 32) mbar_init(smem_addr(sBar + b), 1);
+      for (int b = lane; b < 2 * NSL; b += 32) mbar_init(smem_addr(sBar + b), 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       __syncwarp();
-      for (int b = lane; b < 4 * nx; b += 32) {  // first use: octant pair (0,1) / (2,3)
-        const int dir = b / (2 * nx), o = (b % (2 * nx)) / nx + 2 * dir;
+      for (int b = lane; b < 2 * NSL; b += 32) {  // first use of slot b: the direction's item b
+        const int dir = b / NSL, o = gs_cls_oct(b - dir * NSL, dir, nx);
         mbar_arm(smem_addr(sBar + b), 16u * unsigned(p.oct_ptr[o + 1] - p.oct_ptr[o]));
       }
-      if (lane == 0) *sPub = 0;
+      if (lane == 0) *sPub = 0, sCred[0] = 0, sCred[1] = 0;
     }
     cluster_sync_all();
-    if (warp == GSW_MW) {  // publisher: done flags of this edge row, fenced in batches
+    if (PUBW && warp == GSW_MW) {  // publisher: done flags of this edge row, fenced in batches
       if (edge_pub && lane == 0) {
         int pass = 0, oct = 0, j = 0;
         for (int done_items = 0; done_items < p.nu * 8 * nx;) {
@@ -565,7 +590,7 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (CL ? 32 : 0), 2) coarse_gs_mw_k
       }
     }
   }
-  if (!CL || warp < GSW_MW) {
+  if (!PUBW || warp < GSW_MW) {
   if (tid < 9) sOptr[tid] = p.oct_ptr[tid];
   auto cell = [&](int oct, int j) { return gy * nx + ((oct & 1) ? seg - 1 - j : j); };
   auto advance = [&](const Item& c) {
@@ -578,7 +603,7 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (CL ? 32 : 0), 2) coarse_gs_mw_k
     n.el = cell(n.oct, n.j);
     return n;
   };
-  auto mbuf = [&](int it) { return smom + (it & 3) * Hp * 4; };
+  auto mbuf = [&](int it) { return smom + (it & 3) * HS * 4; };
   // moments of item c -> its ring buffer (threads [t0, t0 + nt))
   auto prefetch_mom = [&](const Item& c, int t0, int nt) {
     const double* src = p.mom + (size_t)c.el * Hp * 4;
@@ -721,7 +746,17 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (CL ? 32 : 0), 2) coarse_gs_mw_k
       // cluster mode: y-neighbours inside the cluster exchange through the mailbox
       const bool up_mail = CL && upy >= 0 && (yneg ? crank < CS - 1 : crank > 0);
       const bool dn_mail = CL && dny >= 0 && (yneg ? crank > 0 : crank < CS - 1);
-      const int mslot = yneg * 2 * nx + (oct & 1) * nx + jseg;  // [dir][slot]
+      // the item's index among this row's items of its y-direction, its slot and slot use
+      // (2 nx slots: slot (oct & 1) nx + j, use 2 pass + (oct >= 4); a ring: ncls mod / div NSL)
+      int mslot = 0, muse = 0, ncls = 0;
+      if constexpr (CL) {
+        if (credit) {
+          ncls = ((pass * 2 + (oct >= 4 ? 1 : 0)) * 2 + (oct & 1)) * nx + jseg;
+          mslot = yneg * NSL + (ncls & (NSL - 1)), muse = ncls >> (31 - __clz(NSL));
+        } else {
+          mslot = yneg * NSL + (oct & 1) * nx + jseg, muse = pass * 2 + (oct >= 4 ? 1 : 0);
+        }
+      }
       {
         const int* f = nullptr;
         int need = 0;
@@ -738,12 +773,17 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (CL ? 32 : 0), 2) coarse_gs_mw_k
         if constexpr (CL) {
           if (up_mail) {
             const unsigned bar = smem_addr(sBar + mslot);
-            const unsigned par = unsigned(2 * pass + (oct >= 4 ? 1 : 0)) & 1u;
-            while (!mbar_done(bar, par)) {
+            while (!mbar_done(bar, unsigned(muse) & 1u)) {
             }
             __syncwarp();
-            if (lane == 0) {  // arm the slot's next use: same column, octant oct ^ 4
-              const int o2 = oct ^ 4;
+            if (lane == 0) {  // arm the slot's next use: this direction's item ncls + NSL
+              int o2 = oct ^ 4;   // 2 nx slots: the same column of the next octant pair
+              if (credit) {       // ring (NSL < 2 nx): NSL items further in this direction
+                int r = (oct & 1) * nx + jseg + NSL;
+                const int wrap = r >= 2 * nx ? 1 : 0;
+                r -= wrap * 2 * nx;
+                o2 = (((oct >= 4 ? 1 : 0) ^ wrap) * 4) + yneg * 2 + (r >= nx ? 1 : 0);
+              }
               mbar_arm(bar, 16u * unsigned(sOptr[o2 + 1] - sOptr[o2]));
             }
           }
@@ -805,6 +845,14 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (CL ? 32 : 0), 2) coarse_gs_mw_k
           e[sl][i] = c - zo[sl][i] - gz;
         }
       }
+      if constexpr (CL) {
+        if (up_mail && credit) {  // slot data read (in registers): hand the slot back to the upwind row
+          __syncwarp();
+          if (lane == 0)
+            st_release_cluster_remote(cluster_map(smem_addr(sCred + yneg), unsigned(yneg ? crank + 1 : crank - 1)),
+                                      ncls + 1);
+        }
+      }
       double* dzb = sdz + (it & 1) * kpad * 4;
       for (int a = 0; a < np; ++a) {
         const int sl = a >> 5, src = a & 31;
@@ -841,6 +889,9 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (CL ? 32 : 0), 2) coarse_gs_mw_k
       if constexpr (CL) {
         if (dn_mail) {  // push the top traces into the downwind row's mailbox
           const unsigned rk = unsigned(yneg ? crank - 1 : crank + 1);
+          if (credit && ncls >= NSL)  // the slot's previous use must have been read
+            while (ld_acquire_cluster_smem(sCred + yneg) < ncls - NSL + 1) {
+            }
           const unsigned rbar = cluster_map(smem_addr(sBar + mslot), rk);
 #pragma unroll
           for (int sl = 0; sl < NS; ++sl) {
@@ -861,8 +912,10 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (CL ? 32 : 0), 2) coarse_gs_mw_k
         st_cg2(zb + 2, make_double2(zo[sl][2], zo[sl][3]));
       }
       __syncwarp();
-      if constexpr (CL) {
+      if constexpr (PUBW) {
         if (edge_pub && lane == 0) st_release_cta_smem(sPub, it + 1);  // the publisher warp fences and flags
+      } else if constexpr (CL) {
+        // helper warp 3 publishes this item's flag at the top of the next iteration
       } else {
         if (lane == 0) st_release(p.done + (size_t)oct * n_el + el, pass + 1);
       }
@@ -883,6 +936,12 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (CL ? 32 : 0), 2) coarse_gs_mw_k
       }
     } else {
       // ---------------- warps 1..3: update of item it-1, projections of item it+1
+      if constexpr (CL && !PUBW) {
+        if (edge_pub && it >= 1 && tid == 96) {  // item it-1's stores precede the last CTA barrier
+          fence_acq_rel();
+          st_relaxed(p.done + (size_t)prv.oct * n_el + prv.el, prv.pass + 1);
+        }
+      }
       if (it >= 1 && !drained) update(prv, 32, nthr - 32, false);
       if (it + 1 < n_items && !boundary) {
         cp_async_wait<0>();  // this thread's part of item it+1's moments
@@ -908,6 +967,12 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (CL ? 32 : 0), 2) coarse_gs_mw_k
   }
   if (!drained && n_items >= 1) {  // last item's update
     update(prv, 0, nthr, false);
+  }
+  if constexpr (CL && !PUBW) {
+    if (edge_pub && n_items >= 1 && tid == 96) {
+      fence_acq_rel();
+      st_relaxed(p.done + (size_t)prv.oct * n_el + prv.el, prv.pass + 1);
+    }
   }
   cp_async_wait<0>();
   }  // item warps
@@ -998,49 +1063,70 @@ int coarse_gs_mw_ok(int Hp, int H, int kpad, int nmat, int ny, int max_np) {
   return per_sm * sms >= ny ? 1 : 0;
 }
 
-size_t gs_mw_cl_smem(int Hp, int H, int kpad, int nmat, int nx, int mbnp) {
-  return sizeof(double) * (gs_mw_doubles(Hp, H, kpad, nmat) + gs_mw_cl_doubles(nx, mbnp));
+size_t gs_mw_cl_smem(int Hp, int H, int kpad, int nmat, int nslots, int mbnp, int hs) {
+  return sizeof(double) * (gs_mw_doubles(Hp, H, kpad, nmat, hs) + gs_mw_cl_doubles(nslots, mbnp));
 }
+int gs_ring_hs(int H) { return (H + 1) & ~1; }  // rings: the compact moment ring makes room for the mailbox
 
-template <int NS>
+template <int NS, bool RING>
 cudaLaunchConfig_t gs_cl_config(const CoarseGSParams& p, cudaLaunchAttribute* at, size_t smem, int rows, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(p.ny), cfg.blockDim = dim3((GSW_MW + 1) * 32), cfg.dynamicSmemBytes = smem, cfg.stream = s;
+  cfg.gridDim = dim3(p.ny), cfg.blockDim = dim3((GSW_MW + (gs_pubw<NS, true>() ? 1 : 0)) * 32);
+  cfg.dynamicSmemBytes = smem, cfg.stream = s;
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = rows, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
   cfg.attrs = at, cfg.numAttrs = 1;
-  auto k = coarse_gs_mw_kernel<NS, true>;
+  auto k = coarse_gs_mw_kernel<NS, true, RING>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return cfg;
 }
 
+// rows per cluster and mailbox slots per direction (slots << 8 | credit << 7 | rows), 0 if none
 template <int NS>
 int gs_cluster_rows_t(int Hp, int H, int kpad, int nmat, int nx, int ny, int max_np) {
-  const size_t smem = gs_mw_cl_smem(Hp, H, kpad, nmat, nx, max_np);
-  if (smem > 110 * 1024) return 0;  // keep two row-CTAs per SM
-  for (int rows : {16, 8, 4, 2}) {
-    if (ny % rows != 0 || ny / rows < 2) continue;
-    CoarseGSParams p;
-    p.ny = ny;
-    cudaLaunchAttribute at[1];
-    cudaLaunchConfig_t cfg = gs_cl_config<NS>(p, at, smem, rows, nullptr);
-    int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, coarse_gs_mw_kernel<NS, true>, &cfg) != cudaSuccess) {
-      cudaGetLastError();
-      continue;
+  // rings with credits (for mailboxes of two octants that do not fit) are opt-in: at config 4
+  // (64 patches per octant, 4-slot ring) they measured 0.319 s per coarse solve against 0.311 s
+  // for the global-memory kernel
+  const bool rings = std::getenv("STAMG_GS_MAILBOX_RING") != nullptr;
+  for (int nslots : {2 * nx, 16, 8, 4}) {
+    const bool credit = nslots != 2 * nx;
+    if (credit && !rings) break;
+    if (credit && nslots >= 2 * nx) continue;
+    const size_t smem = gs_mw_cl_smem(Hp, H, kpad, nmat, nslots, max_np, credit ? gs_ring_hs(H) : 0);
+    if (smem > 112 * 1024) continue;  // keep two row-CTAs per SM
+    for (int rows : {16, 8, 4, 2}) {
+      if (ny % rows != 0 || ny / rows < 2) continue;
+      CoarseGSParams p;
+      p.ny = ny;
+      cudaLaunchAttribute at[1];
+      cudaLaunchConfig_t cfg = credit ? gs_cl_config<NS, true>(p, at, smem, rows, nullptr)
+                                      : gs_cl_config<NS, false>(p, at, smem, rows, nullptr);
+      int nclusters = 0;
+      const cudaError_t e = credit ? cudaOccupancyMaxActiveClusters(&nclusters, coarse_gs_mw_kernel<NS, true, true>, &cfg)
+                                   : cudaOccupancyMaxActiveClusters(&nclusters, coarse_gs_mw_kernel<NS, true, false>, &cfg);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        continue;
+      }
+      if (nclusters >= ny / rows) return (nslots << 8) | (credit ? 128 : 0) | rows;
     }
-    if (nclusters >= ny / rows) return rows;
   }
   return 0;
 }
 
 template <int NS>
 void launch_gs_mw_cluster(const CoarseGSParams& p, cudaStream_t s) {
-  const size_t smem = gs_mw_cl_smem(p.Hp, p.H, p.kpad, p.n_mat, p.nx, p.mb_np);
+  const size_t smem = gs_mw_cl_smem(p.Hp, p.H, p.kpad, p.n_mat, p.mb_slots, p.mb_np, p.mom_stride);
   cudaLaunchAttribute at[1];
-  cudaLaunchConfig_t cfg = gs_cl_config<NS>(p, at, smem, p.cluster, s);
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, coarse_gs_mw_kernel<NS, true>, p);
+  cudaError_t e;
+  if (p.mb_credit) {
+    cudaLaunchConfig_t cfg = gs_cl_config<NS, true>(p, at, smem, p.cluster, s);
+    e = cudaLaunchKernelEx(&cfg, coarse_gs_mw_kernel<NS, true, true>, p);
+  } else {
+    cudaLaunchConfig_t cfg = gs_cl_config<NS, false>(p, at, smem, p.cluster, s);
+    e = cudaLaunchKernelEx(&cfg, coarse_gs_mw_kernel<NS, true, false>, p);
+  }
   if (e != cudaSuccess) throw std::runtime_error(std::string("coarse_gs cluster launch: ") + cudaGetErrorString(e));
 }
 

@@ -10,12 +10,19 @@ from paper_2010_04559_b200 import configs as cf
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("k,n", [(1, None), (2, None), (3, None), (2, 16), (3, 16)])
+@pytest.mark.parametrize("k,n", [(1, None), (2, None), (3, None), (4, None), (2, 16), (3, 16), (4, 16)])
 def test_cluster_coarse_gs_bitwise(stamg, monkeypatch, k, n):
+    """Config 4's coarsest level (64 patches per octant) only fits a 4-slot mailbox ring
+    with credits (the downwind row hands slots back; opt-in, STAMG_GS_MAILBOX_RING);
+    configs 1-3 hold two octants of a row (no credits)."""
     spec = cf.baseline_config(k, n)
+    if k == 4:
+        monkeypatch.setenv("STAMG_GS_MAILBOX_RING", "1")
     g = stamg.Context(spec)
-    mw, cluster, _ = (int(v) for v in g.table("gs_mode", level=0))
+    monkeypatch.delenv("STAMG_GS_MAILBOX_RING", raising=False)
+    mw, cluster, _, slots, credit = (int(v) for v in g.table("gs_mode", level=0))
     assert mw == 1 and cluster > 1, "cluster mode expected on this grid"
+    assert slots >= 4 and credit == (1 if k == 4 else 0)
     monkeypatch.setenv("STAMG_GS_CLUSTER", "0")
     g0 = stamg.Context(spec)
     assert int(g0.table("gs_mode", level=0)[1]) == 0

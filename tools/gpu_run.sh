@@ -73,4 +73,10 @@ if [ "$MODE" = chain ]; then
   timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "coarse or mg_apply or gmres or bicgstab" > gpurun_out/${T}_ptest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_ptest.log
   STAMG_FOLD_MIN_H=16 timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "scatter or mg_apply or smoother" > gpurun_out/${T}_ftest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_ftest.log
 fi
+if [ "$MODE" = abgs ]; then
+  for r in 1 2 3; do for v in old new; do for k in 1 2 3 4; do
+    STAMG_LIB=ablib/lib_$v.so timeout 120 python tools/gs_probe.py $k 10 2>&1 | tail -1 | sed "s/^/$v /" >> gpurun_out/${T}_ab.log
+  done; done; done
+  timeout 300 python -m pytest tests/test_gpu_coarse_cluster.py -m gpu -x -q > gpurun_out/${T}_cltest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_cltest.log
+fi
 echo done
