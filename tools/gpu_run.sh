@@ -79,4 +79,12 @@ if [ "$MODE" = abgs ]; then
   done; done; done
   timeout 300 python -m pytest tests/test_gpu_coarse_cluster.py -m gpu -x -q > gpurun_out/${T}_cltest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_cltest.log
 fi
+if [ "$MODE" = ramp ]; then
+  timeout 600 python -m pytest tests/test_gpu_fullsize.py -m gpu -x -q -k "sweep_host" > gpurun_out/${T}_e2etest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_e2etest.log
+  for r in 1 2; do
+  timeout 600 python bench.py --steps 3 --no-si --no-solve --no-kernels --no-cpu > gpurun_out/${T}_e2e_ramp$r.json 2>> gpurun_out/${T}_e2e.err
+  STAMG_E2E_RAMP=0 timeout 600 python bench.py --steps 3 --no-si --no-solve --no-kernels --no-cpu > gpurun_out/${T}_e2e_flat$r.json 2>> gpurun_out/${T}_e2e.err
+  done
+  STAMG_E2E_CHUNK_DIRS=1024 timeout 600 python bench.py --steps 3 --no-si --no-solve --no-kernels --no-cpu > gpurun_out/${T}_e2e_ramp1024.json 2>> gpurun_out/${T}_e2e.err
+fi
 echo done
