@@ -103,6 +103,9 @@ struct DevLevel {
   int *groups = nullptr, *group_oct = nullptr, *oct_patches = nullptr, *oct_ptr = nullptr;
   int *groups8 = nullptr, *group8_oct = nullptr;
   double2* sweep_top = nullptr;  // 8-direction sweep: strip-boundary trace scratch
+  int sweep_xb = 1;               // column blocks per group (sweep_kernel XBLK)
+  int* sweep_xflag = nullptr;
+  double2* sweep_xtrace = nullptr;
   // wavefront layout (contexts without a hierarchy): tables in internal (group-major)
   // patch order; vectors padded to n_groups8 * slots * 8 blocks
   WLGeom wl;                      // wl.nd == 0: reference layout
@@ -275,6 +278,18 @@ std::vector<int> apply_internal_order(LevelTables& t) {
   return ipos;
 }
 
+// Solve contexts use 8-direction groups only with enough of them to give every SM two
+// CTAs (configs 2-3 are faster with the 4-direction kernel's doubled CTA count).
+// Throughput contexts (config 5, sharded over N GPUs) always use them, with the
+// wavefront layout: rank 0's sweep of a 1/N slice on one GPU (tools/shard_probe.py)
+// takes 6.04 / 3.71 ms at N = 4 / 8 against 9.03 / 5.32 ms with 4-direction groups
+// (3.9x / 6.3x instead of 2.6x / 4.4x over one GPU's 23.4 ms).
+// STAMG_SWEEP8_MIN_GROUPS overrides the threshold.
+int sweep8_min_groups(const stamg_ctx* c, int sms) {
+  if (const char* e = std::getenv("STAMG_SWEEP8_MIN_GROUPS")) return std::atoi(e);
+  return c->wl_allowed ? 1 : 2 * sms;
+}
+
 bool env_is_zero(const char* name) {
   const char* v = std::getenv(name);
   return v != nullptr && v[0] == '0' && v[1] == 0;
@@ -287,7 +302,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     const auto& t0 = L.t;
     if (c->wl_allowed && !t0.groups8.empty() && !t0.groups8_padded && t0.nx >= 36 && t0.ny >= 32 &&
-        int(t0.group8_oct.size()) >= 2 * sms && std::getenv("STAMG_SWEEP_DIRS4") == nullptr &&
+        int(t0.group8_oct.size()) >= sweep8_min_groups(c, sms) && std::getenv("STAMG_SWEEP_DIRS4") == nullptr &&
         !env_is_zero("STAMG_WAVEFRONT_LAYOUT")) {
       // default for throughput contexts: every sweep step of a group touches one
       // contiguous 8 KB run (90 % of measured HBM bandwidth at 512^2 x 8192 against
@@ -333,10 +348,18 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
   // small levels keep the 4-direction kernels (twice the CTAs, latency-bound anyway)
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  if (!t.groups8.empty() && t.nx >= 36 && t.ny >= 32 && int(t.group8_oct.size()) >= 2 * sms &&
+  if (!t.groups8.empty() && t.nx >= 36 && t.ny >= 32 && int(t.group8_oct.size()) >= sweep8_min_groups(c, sms) &&
       std::getenv("STAMG_SWEEP_DIRS4") == nullptr) {
     L.groups8 = dupload(t.groups8, s), L.group8_oct = dupload(t.group8_oct, s);
     L.sweep_top = dalloc<double2>(t.group8_oct.size() * 8 * size_t(t.nx));
+    // fewer groups than SMs (config 5 sharded over 8 GPUs: 128 per rank): two column blocks per
+    // group so the wavefronts cover twice the SMs (STAMG_SWEEP_XBLOCKS=0 keeps one block)
+    const int ng = int(t.group8_oct.size());
+    if (c->wl_allowed && ng <= sms && t.nx % 2 == 0 && t.nx / 2 >= 38 && !env_is_zero("STAMG_SWEEP_XBLOCKS")) {
+      L.sweep_xb = 2;
+      L.sweep_xflag = dalloc<int>(size_t(ng) * L.sweep_xb);
+      L.sweep_xtrace = dalloc<double2>(size_t(ng) * L.sweep_xb * t.ny * 8);
+    }
   }
   if (L.wl.nd) {
     if (!L.groups8) throw std::logic_error("wavefront layout needs the 8-direction groups");
@@ -462,7 +485,7 @@ void free_level(DevLevel& L) {
   for (void* p : {(void*)L.X, (void*)L.XT, (void*)L.sig, (void*)L.ones, (void*)L.B, (void*)L.Binv, (void*)L.cxy,
                   (void*)L.BinvGS, (void*)L.sq, (void*)L.area, (void*)L.up_w, (void*)L.groups, (void*)L.group_oct,
                   (void*)L.oct_patches, (void*)L.oct_ptr, (void*)L.up, (void*)L.child_ptr, (void*)L.child_idx,
-                  (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_K, (void*)L.gs_Xo, (void*)L.gs_XoT, (void*)L.gs_G, (void*)L.Xf, (void*)L.XfT, (void*)L.groups8, (void*)L.group8_oct, (void*)L.sweep_top,
+                  (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_K, (void*)L.gs_Xo, (void*)L.gs_XoT, (void*)L.gs_G, (void*)L.Xf, (void*)L.XfT, (void*)L.groups8, (void*)L.group8_oct, (void*)L.sweep_top, (void*)L.sweep_xflag, (void*)L.sweep_xtrace,
                   (void*)L.d_ipos, (void*)L.d_iid, (void*)L.stage,
                   (void*)L.sigf, (void*)L.orbit, (void*)L.tmp, (void*)L.cf,
                   (void*)L.ce})
@@ -483,6 +506,7 @@ void need(const stamg_vec* v, const DevLevel& L, const char* what) {
 // ------------------------------------------------------------------ operators
 void op_allreduce(stamg_ctx* c, double* buf, size_t n) {
   if (c->world <= 1) return;
+  if (!c->comm) throw std::logic_error("allreduce: no communicator (STAMG_SHARD_PROBE context)");
   const int ncclDouble = 8, ncclSum = 0;
   if (nccl().allReduce(buf, buf, n, ncclDouble, ncclSum, c->comm, c->stream) != 0)
     throw NcclError("ncclAllReduce failed");
@@ -497,7 +521,7 @@ void op_apply_L(stamg_ctx* c, DevLevel& L, const double* x, double* y, double al
     p.dirs = 8, p.top = L.sweep_top, p.wl = L.wl, p.mode = 1;
     p.g.groups = L.groups8, p.g.group_oct = L.group8_oct, p.g.n_groups = int(L.t.group8_oct.size());
     p.rhs = x, p.z = y, p.base = (f && beta != 0.0) ? f : nullptr, p.alpha = alpha, p.beta = beta;
-    p.Bfwd = L.B, p.Binv = L.Binv, p.cxy = L.cxy;
+    p.Bfwd = L.B, p.Binv = L.Binv, p.cxy = L.cxy, p.prefer_breg = true;
     launch_sweep(p, c->stream);
     ck_launch("apply_L");
     c->launches += 1;
@@ -636,6 +660,15 @@ void op_sweep(stamg_ctx* c, DevLevel& L, const double* rhs, double* z, const dou
     p.g.groups = L.groups8, p.g.group_oct = L.group8_oct, p.g.n_groups = int(L.t.group8_oct.size());
   }
   p.rhs = rhs, p.z = z, p.base = base, p.Binv = L.Binv, p.cxy = L.cxy;
+  // wavefront-layout (throughput) contexts keep B^-1 in registers at two CTAs per SM even
+  // when the groups would fit one wave at four: rank 0 of 2 (512 groups) sweeps in 12.5 ms
+  // against 14.6 ms (tools/shard_probe.py); solve contexts (config 4's 364 cone-mesh
+  // groups) keep the one-wave choice
+  p.prefer_breg = L.wl.nd > 0 || std::getenv("STAMG_SWEEP8_PREFER_BREG") != nullptr;
+  if (L.sweep_xb > 1 && !base) {
+    p.xb = L.sweep_xb, p.xflag = L.sweep_xflag, p.xtrace = L.sweep_xtrace;
+    ck(cudaMemsetAsync(L.sweep_xflag, 0, sizeof(int) * L.t.group8_oct.size() * L.sweep_xb, c->stream), "memset");
+  }
   launch_sweep(p, c->stream);
   ck_launch("sweep");
   c->launches += 1;
@@ -1070,7 +1103,8 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
     c->wl_allowed = !want_mg;  // wavefront layout only for contexts without a hierarchy
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
-    if (c->world > 1) {
+    const bool probe = std::getenv("STAMG_SHARD_PROBE") != nullptr;  // one rank's slice, no communicator
+    if (c->world > 1 && !(probe && !opt->nccl_id)) {
       if (!opt->nccl_id) throw std::invalid_argument("world > 1 needs an nccl id");
       if (!nccl().load()) throw NcclError("libnccl.so.2 not loadable");
       UniqueId uid;

@@ -38,6 +38,10 @@ struct SweepParams {
   // with data_P > 0 (reference-layout vectors only) the data of patch k sits at column
   // k - data_q0 of a [n_el][data_P][4] buffer
   int grp0 = 0, data_P = 0, data_q0 = 0;
+  bool prefer_breg = false;  // 8-direction groups: keep B^-1 in registers (2 CTAs/SM) even for 2-4 CTAs per SM of groups
+  int xb = 1;                // > 1: column blocks per group (wavefront layout, plain sweep)
+  int* xflag = nullptr;      // [n_groups][xb] strips published by each block (zeroed per launch)
+  double2* xtrace = nullptr; // [n_groups][xb][ny][8] x-traces at the block edges
 };
 void launch_sweep(const SweepParams& p, cudaStream_t s);
 

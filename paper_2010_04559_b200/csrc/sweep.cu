@@ -36,7 +36,13 @@ constexpr int NST = STAMG_SWEEP_NST;
 // one 256-byte run (better DRAM efficiency than 128 B), and the strip-boundary
 // traces go through an L2-resident global scratch (TOPG) instead of shared
 // memory so the CTA still fits 3 per SM.
-template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY = false, int MODE = 0, bool BREG = true>
+// XBLK: each group's grid is split into p.xb column blocks swept by consecutive CTAs
+// (KBA-style): block b starts a strip once block b-1 has published that strip's
+// x-traces at their common edge (global scratch + one flag per strip), so a group's
+// wavefront runs on xb SMs. Used when there are fewer groups than SMs (config 5
+// sharded over 8 GPUs: 128 groups per rank); all CTAs are co-resident.
+template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY = false, int MODE = 0, bool BREG = true,
+          bool XBLK = false>
 __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_kernel(SweepParams p) {
   // WLAY: vectors in the wavefront layout (a step's R rows are consecutive slots).
   // MODE 1: apply_L on the same skewed schedule (y = alpha*(B x + C x_up) + beta*f, traces of x).
@@ -54,12 +60,18 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
   double* sB = reinterpret_cast<double*>(xw + 2 * NW * DIRS);
 
   const int tid = threadIdx.x, dir = tid % DIRS, r = tid / DIRS, lane = tid & 31, warp = tid >> 5;
-  const int grp = blockIdx.x + p.grp0;
+  const int xb = XBLK ? p.xb : 1;
+  const int gb = XBLK ? int(blockIdx.x) / xb : int(blockIdx.x);
+  const int xblk = XBLK ? int(blockIdx.x) - gb * xb : 0;
+  const int grp = gb + p.grp0;
   const int q = p.g.groups[grp * DIRS + dir];
   const int oct = p.g.group_oct[grp];
   const bool xneg = oct & 1, yneg = (oct >> 1) & 1;
   const int nx = p.g.nx, ny = p.g.ny, P = p.g.P;
   const int DP = p.data_P > 0 ? p.data_P : P, DQ0 = p.data_P > 0 ? p.data_q0 : 0;
+  const int nxl = XBLK ? nx / xb : nx;  // columns of this CTA's block, frame columns i0 ..
+  const int i0 = xblk * nxl;
+  double2* sxin = reinterpret_cast<double2*>(sB + ((MULTI || (TOPG && !BREG)) ? p.g.n_mat * DIRS * 17 : 0));  // XBLK: [NT]
   const bool qok = q >= 0;
   const int qq = qok ? q : 0;
   double2* gtop = p.top + (size_t)grp * DIRS * nx;  // TOPG scratch of this group
@@ -82,8 +94,11 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
   }
 
   const int nstrips = (ny + R - 1) / R;
-  const int nk = nstrips * nx;
+  const int nk = nstrips * nxl;
   const int T = nk + R - 1;
+  // XBLK: traces at the block edges, [groups][xb][ny][DIRS], and per-(group, block) strip flags
+  const double2* xin = XBLK && xblk > 0 ? p.xtrace + ((size_t)(grp * xb + xblk - 1) * ny) * DIRS : nullptr;
+  double2* xout = XBLK && xblk < xb - 1 ? p.xtrace + ((size_t)(grp * xb + xblk) * ny) * DIRS : nullptr;
 
   // Cursor over this thread's wavefront positions k: strip s, column i, cell el and
   // block offset, advanced incrementally (no integer division inside a strip).
@@ -100,17 +115,17 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
       c.ok = false, c.s = 0, c.i = 0, c.el = 0, c.off = 0;
       return;
     }
-    c.s = k / nx, c.i = k - c.s * nx;
-    const int j = c.s * R + r;
+    c.s = k / nxl, c.i = k - c.s * nxl;
+    const int j = c.s * R + r, fi = i0 + c.i;
     c.ok = qok && j < ny;
-    const int gx = xneg ? nx - 1 - c.i : c.i, gy = yneg ? ny - 1 - j : (j < ny ? j : 0);
+    const int gx = xneg ? nx - 1 - fi : fi, gy = yneg ? ny - 1 - j : (j < ny ? j : 0);
     c.el = gy * nx + gx;
-    if constexpr (WLAY) c.off = (((size_t)grp * p.wl.slots + wl_slot_frame(p.wl, c.i, j)) * DIRS + dir) * 4;
+    if constexpr (WLAY) c.off = (((size_t)grp * p.wl.slots + wl_slot_frame(p.wl, fi, j)) * DIRS + dir) * 4;
     else c.off = ((size_t)c.el * DP + (qq - DQ0)) * 4;
   };
   auto advance = [&](Cursor& c) {
     const int k = c.k + 1;
-    if (k <= 0 || k >= nk || c.i + 1 == nx) {
+    if (k <= 0 || k >= nk || c.i + 1 == nxl) {
       fresh(c, k);
       return;
     }
@@ -134,10 +149,31 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
     if constexpr (TOPG) {  // row 0 of strip s >= 1 needs the trace row R-1 left in the scratch
       if (r == 0) {
         const bool tk = c.kin && c.s >= 1;
-        cp_async16(st_top + (t % NST) * DIRS + dir, gtop + (size_t)dir * nx + (tk ? c.i : 0), tk);
+        cp_async16(st_top + (t % NST) * DIRS + dir, gtop + (size_t)dir * nx + (tk ? i0 + c.i : 0), tk);
+      }
+    }
+    if constexpr (XBLK) {  // the block's first column of a strip: x-trace from the upwind block
+      if (xin && c.kin && c.i == 0) {
+        const int j = c.s * R + r;
+        cp_async16(sxin + tid, xin + (size_t)(j < ny ? j : 0) * DIRS + dir, j < ny);
       }
     }
   };
+  // XBLK: strip s of the upwind block must be complete before this block issues its loads
+  int wait_s = 0, wait_t = 0, pub_s = 0, pub_t = (nxl - 1) + (R - 1);
+  auto wait_strip = [&]() {
+    if (tid == 0) {
+      const int* f = p.xflag + grp * xb + xblk - 1;
+      while (ld_relaxed(f) < wait_s + 1) {
+      }
+      fence_acq_rel();
+    }
+    __syncthreads();
+    ++wait_s, wait_t = wait_s * nxl - (NST - 1);
+  };
+  if constexpr (XBLK) {
+    if (xin) wait_strip();
+  }
   Cursor ci, cc;  // issue cursor (k = t + NST - 1 - r) and compute cursor (k = t - r)
   fresh(ci, -r);
   fresh(cc, -r);
@@ -152,6 +188,9 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
   const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
   double2 tx = make_double2(0.0, 0.0), typrev = make_double2(0.0, 0.0);
   for (int t = 0; t < T; ++t) {
+    if constexpr (XBLK) {
+      if (xin && wait_s < nstrips && t == wait_t) wait_strip();
+    }
     issue(t + NST - 1, ci);
     cp_async_commit();
     advance(ci);
@@ -178,7 +217,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
       // physical -> sweep frame (dof i -> i ^ m)
       if (m & 1) { double u = r0; r0 = r1; r1 = u; u = r2; r2 = r3; r3 = u; }
       if (m & 2) { double u = r0; r0 = r2; r2 = u; u = r1; r1 = r3; r3 = u; }
-      if (i == 0) tx = make_double2(0.0, 0.0);
+      if (i == 0) tx = (XBLK && xin) ? sxin[tid] : make_double2(0.0, 0.0);
       const double* B = Bi;
       double Bm[16];
       if constexpr (BSMEM) {
@@ -200,6 +239,9 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
         z3 = B[12] * r0 + B[13] * r1 + B[14] * r2 + B[15] * r3;
         tx = make_double2(z1, z3);
         tyout = make_double2(z2, z3);
+        if constexpr (XBLK) {
+          if (xout && i == nxl - 1) reinterpret_cast<double2*>(xout)[(size_t)(s * R + r) * DIRS + dir] = tx;
+        }
       } else {  // apply_L (transport.cpp:72-87): y = B x + C_x x_left + C_y x_below
         z0 = B[0] * r0 + B[1] * r1 + B[2] * r2 + B[3] * r3;
         z1 = B[4] * r0 + B[5] * r1 + B[6] * r2 + B[7] * r3;
@@ -236,26 +278,35 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
     }
     if (lane >= 32 - DIRS) xw[(t & 1) * NW * DIRS + warp * DIRS + dir] = tyout;
     if (r == R - 1 && kin) {
-      if constexpr (TOPG) reinterpret_cast<double2*>(gtop)[(size_t)dir * nx + i] = tyout;
+      if constexpr (TOPG) reinterpret_cast<double2*>(gtop)[(size_t)dir * nx + i0 + i] = tyout;
       else top[dir * nx + i] = tyout;
     }
     typrev = tyout;
     advance(cc);
     __syncthreads();
+    if constexpr (XBLK) {  // strip pub_s's last column is done by every row: publish its edge traces
+      if (xout && t == pub_t) {
+        if (tid == 0) {
+          __threadfence();
+          st_release(p.xflag + grp * xb + xblk, pub_s + 1);
+        }
+        ++pub_s, pub_t += nxl;
+      }
+    }
   }
   cp_async_wait<0>();
   (void)RPW;
 }
 
-template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY, int MODE, bool BREG>
+template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY, int MODE, bool BREG, bool XBLK = false>
 void launch_tb(const SweepParams& p, cudaStream_t s) {
   constexpr int NT = DIRS * R;
   size_t smem = sizeof(double) * NST * NT * 4 * (ACCUM ? 2 : 1) +
                 sizeof(double2) * ((TOPG ? NST * DIRS : DIRS * p.g.nx) + 2 * (NT / 32) * DIRS) +
-                ((MULTI || TOPG) ? sizeof(double) * p.g.n_mat * DIRS * 17 : 0);
-  auto k = sweep_kernel<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, BREG>;
+                ((MULTI || TOPG) ? sizeof(double) * p.g.n_mat * DIRS * 17 : 0) + (XBLK ? sizeof(double2) * NT : 0);
+  auto k = sweep_kernel<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, BREG, XBLK>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  k<<<p.g.n_groups, NT, smem, s>>>(p);
+  k<<<p.g.n_groups * (XBLK ? p.xb : 1), NT, smem, s>>>(p);
 }
 
 // 8-direction groups: B^-1 in registers gives 2 CTAs/SM (the faster kernel when the
@@ -268,7 +319,8 @@ void launch_t(const SweepParams& p, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const bool breg = STAMG_SWEEP8_BREG && !(TOPG && p.g.n_groups > 2 * sms && p.g.n_groups <= 4 * sms);
+  const bool one_wave4 = TOPG && p.g.n_groups > 2 * sms && p.g.n_groups <= 4 * sms && !p.prefer_breg;
+  const bool breg = STAMG_SWEEP8_BREG && !one_wave4;
   if (breg) launch_tb<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, true>(p, s);
   else launch_tb<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, false>(p, s);
 }
@@ -297,6 +349,13 @@ void launch_sweep(const SweepParams& p, cudaStream_t s) {
     if (p.g.nx < 32 + NST || p.g.ny < 32 || !p.top) throw std::invalid_argument("sweep: 8-direction groups need nx, ny >= 36");
     if (p.wl.nd > 0) {
       if (p.wl.R != 32) throw std::invalid_argument("sweep: wavefront layout strip height must be 32");
+      if (p.xb > 1) {  // column blocks (plain sweep, wavefront layout, B^-1 in registers)
+        if (p.mode != 0 || p.base || !p.xflag || !p.xtrace || p.g.nx % p.xb || p.g.nx / p.xb < 32 + NST)
+          throw std::invalid_argument("sweep: column blocks need a plain sweep and nx / xb >= 38");
+        if (p.g.n_mat > 1) launch_tb<8, 32, true, false, true, true, 0, true, true>(p, s);
+        else launch_tb<8, 32, false, false, true, true, 0, true, true>(p, s);
+        return;
+      }
       p.mode == 1 ? launch_r<8, 32, true, true, 1>(p, s) : launch_r<8, 32, true, true, 0>(p, s);
     } else {
       if (p.mode == 1) throw std::invalid_argument("sweep kernel apply_L mode needs the wavefront layout");

@@ -87,4 +87,17 @@ if [ "$MODE" = ramp ]; then
   done
   STAMG_E2E_CHUNK_DIRS=1024 timeout 600 python bench.py --steps 3 --no-si --no-solve --no-kernels --no-cpu > gpurun_out/${T}_e2e_ramp1024.json 2>> gpurun_out/${T}_e2e.err
 fi
+if [ "$MODE" = shard ]; then
+  timeout 600 python tools/shard_probe.py > gpurun_out/${T}_shard_default.log 2>&1
+  STAMG_SWEEP8_MIN_GROUPS=1 timeout 600 python tools/shard_probe.py 1 2 4 8 > gpurun_out/${T}_shard_8dir.log 2>&1
+fi
+if [ "$MODE" = shard2 ]; then
+  timeout 600 python tools/shard_probe.py 1 2 4 8 > gpurun_out/${T}_shard_default.log 2>&1
+  STAMG_SWEEP8_PREFER_BREG=1 timeout 600 python tools/shard_probe.py 2 > gpurun_out/${T}_shard_breg.log 2>&1
+fi
+if [ "$MODE" = xblk ]; then
+  timeout 300 python -m pytest tests/test_gpu_shard_sweep.py -m gpu -x -q > gpurun_out/${T}_xtest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_xtest.log
+  timeout 600 python tools/shard_probe.py 1 2 4 8 > gpurun_out/${T}_shard.log 2>&1
+  STAMG_SWEEP_XBLOCKS=0 timeout 600 python tools/shard_probe.py 8 > gpurun_out/${T}_shard_noxb.log 2>&1
+fi
 echo done
