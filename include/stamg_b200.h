@@ -103,6 +103,10 @@ int stamg_patch_list(stamg_ctx* ctx, int level, int* out, int cap, int* n);
  * level, replicated) and, for level >= 1, each patch's parent position in the coarser
  * level's list held by the same rank */
 int stamg_partition(const stamg_problem* prob, int rank, int world, int level, int* qpos, int* up, int cap, int* n);
+/* Host-only: the directions (global leaf positions, ascending) rank `rank` of `world` owns
+ * in a context without a hierarchy: whole orbits of the mesh's reflection symmetry, so
+ * every rank folds its own scatter (contiguous slices of 4 patches without symmetry). */
+int stamg_shard_patches(const stamg_problem* prob, int rank, int world, int* out, int cap, int* n);
 int stamg_n_levels(stamg_ctx* ctx, int* n_levels, int* nr);
 /* scatter order of a level's coupling table (ops.kernel.N) */
 int stamg_level_order(stamg_ctx* ctx, int level, int* order);

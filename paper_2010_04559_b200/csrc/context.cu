@@ -452,7 +452,8 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
   if (const char* e = std::getenv("STAMG_FOLD_MIN_H")) fold_min_h = std::atoi(e);
   // (orbit classes of fewer than 64 patches are below the GEMM tile sizes the folded
   // path is validated for: config 1's 128-patch level folds to 16 and is off by 1e-10)
-  if (t.n_sym_axes > 0 && t.H >= fold_min_h && c->world == 1 && (t.P >> t.n_sym_axes) >= 64) {
+  // (sharded: throughput contexts, whose shards are whole orbits; the folded moments are allreduced)
+  if (t.n_sym_axes > 0 && t.H >= fold_min_h && (c->world == 1 || c->wl_allowed) && (t.P >> t.n_sym_axes) >= 64) {
     const int G = 1 << t.n_sym_axes, R = t.P / G;
     L.fold_G = G, L.fold_R = R, L.fold_Rp = round_up(R, 64);
     const int Rk = round_up(R, 32);
@@ -506,7 +507,10 @@ void need(const stamg_vec* v, const DevLevel& L, const char* what) {
 // ------------------------------------------------------------------ operators
 void op_allreduce(stamg_ctx* c, double* buf, size_t n) {
   if (c->world <= 1) return;
-  if (!c->comm) throw std::logic_error("allreduce: no communicator (STAMG_SHARD_PROBE context)");
+  if (!c->comm) {  // STAMG_SHARD_PROBE: one rank's slice timed alone; partial sums are left as they are
+    if (std::getenv("STAMG_SHARD_PROBE")) return;
+    throw std::logic_error("allreduce: no communicator");
+  }
   const int ncclDouble = 8, ncclSum = 0;
   if (nccl().allReduce(buf, buf, n, ncclDouble, ncclSum, c->comm, c->stream) != 0)
     throw NcclError("ncclAllReduce failed");
@@ -1120,12 +1124,8 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
       // sharded hierarchy: subtrees of the coarsest level per rank, coarsest replicated
       parts = partition_levels(c->tree, s.n_levels, c->rank, c->world);
       c->outer.t = build_level(c->pb, c->tree, s.N, false, &parts.back());
-    } else {  // direction sharding: contiguous slices of the leaf order, multiples of 4 patches
-      const int Pg = int(c->tree.leaves.size());
-      const int quads = (Pg + 3) / 4;
-      const int q0 = std::min(Pg, 4 * int((int64_t(quads) * c->rank) / c->world));
-      const int q1 = std::min(Pg, 4 * int((int64_t(quads) * (c->rank + 1)) / c->world));
-      const auto sub = range_subset(q0, q1);
+    } else {  // direction sharding: whole reflection orbits per rank (each rank folds its scatter)
+      const auto sub = throughput_shard(c->tree, c->rank, c->world);
       c->outer.t = build_level(c->pb, c->tree, s.N, false, &sub);
     }
     c->outer.sharded = c->world > 1;
@@ -1214,6 +1214,19 @@ int stamg_partition(const stamg_problem* prob, int rank, int world, int level, i
         up[k] = it == pos.end() ? -1 : it->second;
       }
     }
+  });
+}
+
+int stamg_shard_patches(const stamg_problem* prob, int rank, int world, int* out, int cap, int* n) {
+  return guard([&] {
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("shard: bad rank / world");
+    Problem pb = copy_problem(*prob);
+    validate(pb);
+    const auto& s = pb.spec;
+    SphereTree tree = make_sphere(s.angular_kind, s.angular_level, s.cone_levels, s.cone_half_angle_deg);
+    const auto sub = throughput_shard(tree, rank, world);
+    *n = int(sub.size());
+    for (int k = 0; k < *n && k < cap; ++k) out[k] = sub[k];
   });
 }
 

@@ -512,6 +512,62 @@ LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool 
   return L;
 }
 
+std::vector<int> throughput_shard(const SphereTree& t, int rank, int world) {
+  const int Pg = int(t.leaves.size());
+  using Key = std::array<std::int64_t, 9>;
+  auto key_of = [](std::array<std::int64_t, 9> f) {
+    std::array<std::array<std::int64_t, 3>, 3> v{{{f[0], f[1], f[2]}, {f[3], f[4], f[5]}, {f[6], f[7], f[8]}}};
+    std::sort(v.begin(), v.end());
+    Key k;
+    for (int i = 0; i < 3; ++i)
+      for (int r = 0; r < 3; ++r) k[3 * i + r] = v[i][r];
+    return k;
+  };
+  std::map<Key, int> pos;
+  for (int q = 0; q < Pg; ++q) pos[key_of(t.flat[t.leaves[q]])] = q;
+  std::vector<int> axes;
+  std::vector<std::vector<int>> mirror;
+  for (int axis = 0; axis < 3; ++axis) {
+    std::vector<int> mq(Pg, -1);
+    bool ok = true;
+    for (int q = 0; ok && q < Pg; ++q) {
+      auto f = t.flat[t.leaves[q]];
+      for (int v = 0; v < 3; ++v) f[3 * v + axis] = -f[3 * v + axis];
+      auto it = pos.find(key_of(f));
+      if (it == pos.end()) ok = false;
+      else mq[q] = it->second;
+    }
+    if (ok) axes.push_back(axis), mirror.push_back(mq);
+  }
+  std::vector<int> reps;  // orbit representatives: octant bits 0 on every symmetric axis
+  for (int q = 0; q < Pg; ++q) {
+    bool rep = true;
+    for (int axis : axes)
+      if ((t.octant[t.leaves[q]] >> axis) & 1) rep = false;
+    if (rep) reps.push_back(q);
+  }
+  const int G = 1 << int(axes.size());
+  if (axes.empty() || int(reps.size()) * G != Pg) {  // no reflection symmetry: contiguous slices of 4
+    const int quads = (Pg + 3) / 4;
+    const int q0 = std::min(Pg, 4 * int((int64_t(quads) * rank) / world));
+    const int q1 = std::min(Pg, 4 * int((int64_t(quads) * (rank + 1)) / world));
+    return range_subset(q0, q1);
+  }
+  // whole orbits, in slices of 8 representatives when possible (full 8-direction groups per octant)
+  const int R = int(reps.size()), unit = R % (8 * world) == 0 ? 8 : 1, units = R / unit;
+  const int r0 = unit * int((int64_t(units) * rank) / world), r1 = unit * int((int64_t(units) * (rank + 1)) / world);
+  std::vector<int> out;
+  for (int r = r0; r < r1; ++r)
+    for (int g = 0; g < G; ++g) {
+      int m = reps[r];
+      for (size_t k = 0; k < axes.size(); ++k)
+        if ((g >> k) & 1) m = mirror[k][m];
+      out.push_back(m);
+    }
+  std::sort(out.begin(), out.end());
+  return out;
+}
+
 void find_symmetry(LevelTables& L, const SphereTree& t) {
   // key of a patch: its three lattice vertices, sorted
   using Key = std::array<std::int64_t, 9>;
@@ -529,7 +585,7 @@ void find_symmetry(LevelTables& L, const SphereTree& t) {
   L.n_sym_axes = 0;
   for (int axis = 0; axis < 3; ++axis) {
     std::vector<int> mq(L.P, -1);
-    bool ok = L.P_global == L.P;  // a rank's slice is not closed under reflections
+    bool ok = true;  // a rank's slice must be closed under the reflection (lookup among its own patches)
     for (int q = 0; ok && q < L.P; ++q) {
       auto f = t.flat[L.leaf_id[q]];
       for (int v = 0; v < 3; ++v) f[3 * v + axis] = -f[3 * v + axis];

@@ -99,6 +99,10 @@ LevelTables build_level(const Problem& pb, const SphereTree& tree, int order, bo
                         const std::vector<int>* subset = nullptr);
 // contiguous leaf-order range [q_begin, q_end) as a subset
 std::vector<int> range_subset(int q_begin, int q_end);
+// Direction shard of `rank` for contexts without a hierarchy (config 5): whole orbits of
+// the mesh's reflection symmetry group (so each rank can fold its scatter), balanced in
+// slices of 8 orbit representatives; contiguous slices of 4 patches without symmetry.
+std::vector<int> throughput_shard(const SphereTree& tree, int rank, int world);
 
 // Direction sharding of a hierarchy: rank r owns whole subtrees rooted at the
 // coarsest used level's patches (contiguous roots, balanced by the number of

@@ -365,6 +365,17 @@ def partition(spec: ProblemSpec, rank: int, world: int, level: int):
     return qpos, up
 
 
+def shard_patches(spec: ProblemSpec, rank: int, world: int) -> np.ndarray:
+    """Host-only: global leaf positions (ascending) of `rank`'s directions in a context
+    without a hierarchy (whole reflection orbits; stamg_shard_patches)."""
+    pr, keep = _problem_struct(spec)
+    n = C.c_int()
+    _check(lib().stamg_shard_patches(C.byref(pr), rank, world, None, 0, C.byref(n)))
+    out = np.empty(n.value, dtype=np.int32)
+    _check(lib().stamg_shard_patches(C.byref(pr), rank, world, out.ctypes.data_as(ip), n.value, C.byref(n)))
+    return out
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().stamg_nccl_unique_id(buf))

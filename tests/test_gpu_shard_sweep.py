@@ -38,3 +38,28 @@ def test_column_blocks_bitwise(stamg, monkeypatch, world, rank, n):
     assert np.array_equal(v.numpy(), a)
     g.close()
     g1.close()
+
+
+@pytest.mark.parametrize("world,rank", [(2, 1), (8, 6)])
+def test_sharded_folded_scatter(stamg, monkeypatch, world, rank):
+    """A rank's shard is whole reflection orbits, so its scatter folds (|G| = 8); without
+    a communicator its moments are the partial sums over its own directions, i.e. the
+    unsharded operator applied to the vector restricted to those directions."""
+    spec = cf.baseline_config(5, 64)
+    g1 = stamg.Context(spec, build_hierarchy=False)
+    monkeypatch.setenv("STAMG_SHARD_PROBE", "1")
+    gr = stamg.Context(spec, build_hierarchy=False, rank=rank, world=world)
+    assert int(gr.table("fold")[0]) == 8
+    mine = stamg.shard_patches(spec, rank, world)
+    n_el, P, S, _ = g1.layout()
+    x = rnd(g1.vec().n, 21).reshape(n_el, P, S)
+    xr = np.zeros_like(x)
+    xr[:, mine] = x[:, mine]
+    y1 = g1.vec()
+    g1.apply_scatter_into(g1.vec(data=xr.ravel()), spec.N, 1.0, y1)
+    yr = gr.vec()
+    gr.apply_scatter_into(gr.vec(data=np.ascontiguousarray(x[:, mine]).ravel()), spec.N, 1.0, yr)
+    ref = y1.numpy().reshape(n_el, P, S)[:, mine].ravel()
+    assert np.linalg.norm(yr.numpy() - ref) < 1e-12 * np.linalg.norm(ref)
+    g1.close()
+    gr.close()

@@ -100,4 +100,8 @@ if [ "$MODE" = xblk ]; then
   timeout 600 python tools/shard_probe.py 1 2 4 8 > gpurun_out/${T}_shard.log 2>&1
   STAMG_SWEEP_XBLOCKS=0 timeout 600 python tools/shard_probe.py 8 > gpurun_out/${T}_shard_noxb.log 2>&1
 fi
+if [ "$MODE" = orbit ]; then
+  timeout 600 python -m pytest tests/test_gpu_shard_sweep.py tests/test_gpu_fullsize.py -m gpu -x -q > gpurun_out/${T}_test.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_test.log
+  timeout 900 python tools/shard_probe.py 1 2 4 8 > gpurun_out/${T}_shard.log 2>&1
+fi
 echo done

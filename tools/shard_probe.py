@@ -9,6 +9,7 @@ the N-GPU job's time; speed-up = t(1) / t(N).
 import json
 import os
 import sys
+import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -35,9 +36,16 @@ def main():
         ms, k = g.timed("sweep")
         g.timing(False)
         t = ms / k
+        g.source_iteration(psi, 1)  # warm
+        g.synchronize()
+        t0 = time.perf_counter()
+        g.source_iteration(psi, 2)
+        g.synchronize()
+        si_ms = (time.perf_counter() - t0) / 2 * 1e3  # rank-local (no allreduce without a communicator)
         t1 = t if n == 1 else t1
         out[n] = {"directions": P, "ms_per_sweep": t, "updates_per_s_job": n_el * P * n / (t * 1e-3),
-                  "speedup_vs_1": (t1 / t) if t1 else None, "hbm_frac_rank": n_el * P * 64 / (t * 1e-3) / 6455.3e9}
+                  "speedup_vs_1": (t1 / t) if t1 else None, "si_ms_per_iter_rank_local": si_ms,
+                  "fold_group": int(g.table("fold")[0]), "hbm_frac_rank": n_el * P * 64 / (t * 1e-3) / 6455.3e9}
         print(json.dumps({n: out[n]}), flush=True)
         psi.free()
         g.close()
