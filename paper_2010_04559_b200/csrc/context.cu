@@ -357,6 +357,11 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     const int ng = int(t.group8_oct.size());
     if (c->wl_allowed && ng <= sms && t.nx % 2 == 0 && t.nx / 2 >= 38 && !env_is_zero("STAMG_SWEEP_XBLOCKS")) {
       L.sweep_xb = 2;
+      if (const char* e = std::getenv("STAMG_SWEEP_XB")) {  // A/B: more blocks (all must stay co-resident)
+        const int xb = std::atoi(e);
+        const int slots = (std::getenv("STAMG_SWEEP_XB_SMEMB") ? 4 : 2) * sms;
+        if (xb >= 1 && t.nx % xb == 0 && t.nx / xb >= 38 && ng * xb <= slots) L.sweep_xb = xb;
+      }
       L.sweep_xflag = dalloc<int>(size_t(ng) * L.sweep_xb);
       L.sweep_xtrace = dalloc<double2>(size_t(ng) * L.sweep_xb * t.ny * 8);
     }
@@ -671,6 +676,7 @@ void op_sweep(stamg_ctx* c, DevLevel& L, const double* rhs, double* z, const dou
   p.prefer_breg = L.wl.nd > 0 || std::getenv("STAMG_SWEEP8_PREFER_BREG") != nullptr;
   if (L.sweep_xb > 1 && !base) {
     p.xb = L.sweep_xb, p.xflag = L.sweep_xflag, p.xtrace = L.sweep_xtrace;
+    p.xb_smemb = std::getenv("STAMG_SWEEP_XB_SMEMB") != nullptr;
     ck(cudaMemsetAsync(L.sweep_xflag, 0, sizeof(int) * L.t.group8_oct.size() * L.sweep_xb, c->stream), "memset");
   }
   launch_sweep(p, c->stream);

@@ -104,4 +104,11 @@ if [ "$MODE" = orbit ]; then
   timeout 600 python -m pytest tests/test_gpu_shard_sweep.py tests/test_gpu_fullsize.py -m gpu -x -q > gpurun_out/${T}_test.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_test.log
   timeout 900 python tools/shard_probe.py 1 2 4 8 > gpurun_out/${T}_shard.log 2>&1
 fi
+if [ "$MODE" = xbab ]; then
+  timeout 300 python tools/shard_probe.py 8 > gpurun_out/${T}_xb2.log 2>&1
+  STAMG_SWEEP_XB_SMEMB=1 timeout 300 python tools/shard_probe.py 8 > gpurun_out/${T}_xb2s.log 2>&1
+  STAMG_SWEEP_XB=4 STAMG_SWEEP_XB_SMEMB=1 timeout 300 python tools/shard_probe.py 8 > gpurun_out/${T}_xb4s.log 2>&1
+  STAMG_SWEEP_XB=4 STAMG_SWEEP_XB_SMEMB=1 timeout 300 python tools/shard_probe.py 4 > gpurun_out/${T}_xb4s_n4.log 2>&1
+  STAMG_SWEEP_XB=4 STAMG_SWEEP_XB_SMEMB=1 STAMG_SHARD_PROBE=1 timeout 300 python -m pytest tests/test_gpu_shard_sweep.py -m gpu -x -q -k column > gpurun_out/${T}_xt.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_xt.log
+fi
 echo done
