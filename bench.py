@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
 """Benchmark: transport-sweep throughput (cell.direction updates/s) on
 BASELINE.json config 5 (512x512 bilinear cells, 8192 angular patches, fp64),
-directions sharded across ranks, plus GMRES+AMG solve wall time (config 2)
+directions sharded across ranks, plus GMRES+AMG solve wall time (configs 1-3)
 and source-iteration throughput as extra keys.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
@@ -444,7 +444,7 @@ def run_b200(args, world, rank, local, dist):
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": f"c5: {spec.nx}x{spec.ny} bilinear cells, uniform angular level 5 "
                                        f"({P_local * world} patches), one in-place standard_sweep per step, "
-                                       f"directions sharded over {world} rank(s)",
+                                       f"directions sharded over {world} rank(s) (whole reflection orbits per rank)",
                            "l2": f"input {spec.n_el * P_local * world * 4 * 8 / 2**30:.1f} GiB >> 126 MB L2 (no flush needed)", "wall_s": wall,
                            "setup_s": setup_s},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
