@@ -111,4 +111,12 @@ if [ "$MODE" = xbab ]; then
   STAMG_SWEEP_XB=4 STAMG_SWEEP_XB_SMEMB=1 timeout 300 python tools/shard_probe.py 4 > gpurun_out/${T}_xb4s_n4.log 2>&1
   STAMG_SWEEP_XB=4 STAMG_SWEEP_XB_SMEMB=1 STAMG_SHARD_PROBE=1 timeout 300 python -m pytest tests/test_gpu_shard_sweep.py -m gpu -x -q -k column > gpurun_out/${T}_xt.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_xt.log
 fi
+if [ "$MODE" = ab8 ]; then
+  for r in 1 2; do for v in old new; do for k in 1 2 3; do
+    STAMG_LIB=ablib/lib_$v.so timeout 120 python tools/gs_probe.py $k 10 2>&1 | tail -1 | sed "s/^/$v /" >> gpurun_out/${T}_ab.log
+  done; done; done
+  timeout 300 python -m pytest tests/test_gpu_coarse_cluster.py -m gpu -x -q > gpurun_out/${T}_cltest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_cltest.log
+  timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "coarse or mg_apply or gmres or bicgstab" > gpurun_out/${T}_ptest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_ptest.log
+  timeout 600 python bench.py --steps 3 --no-si --no-e2e --no-cpu --no-kernels --solve-configs 1 2 3 > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err
+fi
 echo done
