@@ -19,7 +19,10 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
 import pyoracle  # noqa: E402
 from paper_2010_04559_b200 import configs as cf  # noqa: E402
 
-CASES = {"c1n8": (1, 8), "c2n8": (2, 8), "c3n8": (3, 8)}
+CASES = {"c1n8": (1, 8), "c2n8": (2, 8), "c3n8": (3, 8), "c4n8": (4, 8), "c5n8": (5, 8)}
+# configs whose BASELINE entry is a throughput workload (no MG hierarchy, no
+# solve): frozen operators plus one source iteration at the full angular mesh
+THROUGHPUT = {"c5n8"}
 SAMPLE = 61  # larger cases keep every 61st entry plus the L2 norm of each vector
 
 
@@ -31,25 +34,31 @@ def seeded_coarse(k, size):
     return np.random.default_rng(2000 + k).uniform(-1, 1, size)
 
 
-def main():
+def throughput_case(o, spec, x):
+    """Operators of a hierarchy-free context and one source iteration
+    psi <- L^-1 (q + S psi) (sweeps.cpp:106-113 with the full-order kernel)."""
+    return dict(
+        apply_L=o.apply_L(x),
+        apply_A=o.apply_A(x, spec.N),
+        scatter_full=o.apply_scatter(x, spec.N, 1.0),
+        sweep=o.sweep(x),
+        rhs=o.rhs(),
+        source_iteration=o.sweep(o.rhs() + o.apply_scatter(np.abs(x), spec.N, 1.0)),
+    )
+
+
+def main(only=None):
     for name, (k, n) in CASES.items():
+        if only and name not in only:
+            continue
         spec = cf.baseline_config(k, n)
         o = pyoracle.Oracle(spec)
         size = o.size()
         x = seeded_input(k, size)
-        nlev, nr = o.levels()
-        xs, rep = o.solve("gmres", "mg")
-        full = dict(
-            apply_L=o.apply_L(x),
-            apply_A=o.apply_A(x, spec.N),
-            scatter_full=o.apply_scatter(x, spec.N, 1.0),
-            sweep=o.sweep(x),
-            mg_apply=o.mg_apply(x),
-            rhs=o.rhs(),
-            solve_scalar_flux=o.scalar_flux(xs),
-            solve_iterations=np.array([rep["iterations"]]),
-            coarse_gs_nu1=o.coarse_gs(seeded_coarse(k, o.size(0)), 1, np.zeros(o.size(0)), level=0),
-        )
+        if name in THROUGHPUT:
+            full, rep = throughput_case(o, spec, x), {"iterations": "-"}
+        else:
+            full, rep = solve_case(o, spec, k, x)
         out = {}
         for key, v in full.items():
             v = np.asarray(v, dtype=np.float64)
@@ -64,5 +73,20 @@ def main():
         print(name, size, rep["iterations"])
 
 
+def solve_case(o, spec, k, x):
+    xs, rep = o.solve("gmres", "mg")
+    return dict(
+        apply_L=o.apply_L(x),
+        apply_A=o.apply_A(x, spec.N),
+        scatter_full=o.apply_scatter(x, spec.N, 1.0),
+        sweep=o.sweep(x),
+        mg_apply=o.mg_apply(x),
+        rhs=o.rhs(),
+        solve_scalar_flux=o.scalar_flux(xs),
+        solve_iterations=np.array([rep["iterations"]]),
+        coarse_gs_nu1=o.coarse_gs(seeded_coarse(k, o.size(0)), 1, np.zeros(o.size(0)), level=0),
+    ), rep
+
+
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:] or None)
