@@ -109,8 +109,11 @@ __device__ __forceinline__ void mma_stage(const double* sA, const double* sB, do
 }
 
 // grid: x = element tiles (16 elements), y = harmonic tiles (BM rows)
+#ifndef STAMG_D2M_MINB
+#define STAMG_D2M_MINB 1  // A/B knob: resident CTAs per SM the register budget is sized for
+#endif
 template <int MI, int WM>
-__global__ void __launch_bounds__(RowTile<MI, WM>::kThreads) d2m_kernel(D2MParams p) {
+__global__ void __launch_bounds__(RowTile<MI, WM>::kThreads, STAMG_D2M_MINB) d2m_kernel(D2MParams p) {
   using T = RowTile<MI, WM>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -418,6 +421,9 @@ void launch_unfold(const double* Y, double* y, const int* orbit, int n_el, int P
   }
 }
 
+#ifndef STAMG_D2M_MAXBM
+#define STAMG_D2M_MAXBM 168  // A/B knob: largest D2M row tile (smaller -> more, lighter CTAs per SM)
+#endif
 int d2m_row_tile(int rows, int limit) {
   // candidate tiles: 64 rows (MI 4 x WM 2) and 24-row warp strips x 1..7 warp rows;
   // cost = padded rows + 8 per tile (each extra tile re-reads the phi panel),
@@ -426,7 +432,7 @@ int d2m_row_tile(int rows, int limit) {
   int best = 0, best_cost = 1 << 30;
   for (int bm : cand) {
     const int tiles = (rows + bm - 1) / bm, padded = tiles * bm;
-    if (padded > limit) continue;
+    if (padded > limit || bm > STAMG_D2M_MAXBM) continue;
     const int cost = padded + 8 * tiles;
     if (cost < best_cost) best = bm, best_cost = cost;
   }

@@ -120,3 +120,11 @@ if [ "$MODE" = ab8 ]; then
   timeout 600 python bench.py --steps 3 --no-si --no-e2e --no-cpu --no-kernels --solve-configs 1 2 3 > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err
 fi
 echo done
+if [ "$MODE" = ab ]; then
+  # A/B of library variants built by tools/ab_build.py (abl/<name>.so), interleaved; $3 = variant names
+  timeout 600 python -m pytest tests/test_golden.py -m gpu -x -q > gpurun_out/${T}_golden.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_golden.log
+  for rep in 1 2; do for v in ${3:-base}; do
+    echo "== $v rep $rep" >> gpurun_out/${T}_ab.log
+    STAMG_LIB=abl/$v.so C5N=${C5N:-512} timeout 300 python tools/perf_probe.py si >> gpurun_out/${T}_ab.log 2>&1
+  done; done
+fi
