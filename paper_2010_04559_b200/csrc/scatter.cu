@@ -33,7 +33,6 @@ constexpr int BM = 64, BN = 64, BK = STAMG_GEMM_BK, NSTAGE = STAMG_GEMM_NSTAGE;
 constexpr int LDS = BM + 4;  // padded row (conflict-free fragment loads)
 constexpr int LDB = BN + 4;
 constexpr int kThreads = 128;
-constexpr int kStageDoubles = BK * (LDS + LDB);
 
 // Output-row tiling of the D2M GEMM (M = harmonics of the call): WM warp rows
 // x 2 warp columns, each warp MI x 4 m8n8k4 blocks, so BM = 8*MI*WM rows by
@@ -79,11 +78,12 @@ __device__ __forceinline__ void load_phi_tile(double* sB, const double* phi, int
 }
 
 // M2D B tile: sB[k][e*4+i] = src[((el0+e)*Hp + h0+k)*4 + i], zero for h0+k >= krows
+template <int TT>
 __device__ __forceinline__ void load_src_tile(double* sB, const double* src, int Hp, int n_el, int h0, int el0,
                                               int krows, int tid) {
 #pragma unroll
-  for (int it = 0; it < (BK * BN / 2) / kThreads; ++it) {
-    const int chunk = tid + it * kThreads;
+  for (int it = 0; it < (BK * BN / 2) / TT; ++it) {
+    const int chunk = tid + it * TT;
     const int half = chunk & 1, k = (chunk >> 1) & (BK - 1), e = chunk / (2 * BK);
     const bool ok = (el0 + e) < n_el && (h0 + k) < krows;
     const double* g = src + (ok ? (((size_t)(el0 + e) * Hp + h0 + k) * 4 + half * 2) : 0);
@@ -110,7 +110,7 @@ __device__ __forceinline__ void mma_stage(const double* sA, const double* sB, do
 
 // grid: x = element tiles (16 elements), y = harmonic tiles (BM rows)
 #ifndef STAMG_D2M_MINB
-#define STAMG_D2M_MINB 1  // A/B knob: resident CTAs per SM the register budget is sized for
+#define STAMG_D2M_MINB 2  // resident CTAs per SM the register budget is sized for (A/B at c5: 1 -> 2 = D2M -19 %)
 #endif
 template <int MI, int WM>
 __global__ void __launch_bounds__(RowTile<MI, WM>::kThreads, STAMG_D2M_MINB) d2m_kernel(D2MParams p) {
@@ -192,13 +192,19 @@ __device__ __forceinline__ double* m2d_out(const M2DParams& p, int el, int q, in
 // of the tile is loaded into registers before the k-loop, so the read-modify-write
 // epilogue does not expose a DRAM round trip (the MG levels' M2D has K = 25..81:
 // a few k-steps only)
+#ifndef STAMG_M2D_WM
+#define STAMG_M2D_WM 2  // A/B knob: warp rows of the M2D tile (32 patch rows each); c5 A/B: 1 / 2 / 4 = 97.0 / 83.7 / 88.4 ms
+#endif
+constexpr int M2D_BM = 32 * STAMG_M2D_WM, M2D_LDA = M2D_BM + 4, M2D_THREADS = 64 * STAMG_M2D_WM;
+constexpr int M2D_STAGE = BK * (M2D_LDA + LDB);
+
 template <bool PRE>
-__global__ void __launch_bounds__(kThreads) m2d_kernel(M2DParams p) {
+__global__ void __launch_bounds__(M2D_THREADS) m2d_kernel(M2DParams p) {
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;
   const int el0 = (STAMG_GEMM_SWAP ? blockIdx.y : blockIdx.x) * (BN / 4);
-  const int q0 = (STAMG_GEMM_SWAP ? blockIdx.x : blockIdx.y) * BM;
+  const int q0 = (STAMG_GEMM_SWAP ? blockIdx.x : blockIdx.y) * M2D_BM;
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -222,24 +228,24 @@ __global__ void __launch_bounds__(kThreads) m2d_kernel(M2DParams p) {
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
     if (s < nk) {
-      double* st = smem + s * kStageDoubles;
-      load_tile_rows<BM, LDS, kThreads>(st, p.XT, p.Pp, s * BK, q0, p.Hused, tid);
-      load_src_tile(st + BK * LDS, p.src, p.Hp, p.n_el, s * BK, el0, p.Hused, tid);
+      double* st = smem + s * M2D_STAGE;
+      load_tile_rows<M2D_BM, M2D_LDA, M2D_THREADS>(st, p.XT, p.Pp, s * BK, q0, p.Hused, tid);
+      load_src_tile<M2D_THREADS>(st + BK * M2D_LDA, p.src, p.Hp, p.n_el, s * BK, el0, p.Hused, tid);
     }
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
     const int nxt = kt + NSTAGE - 1;
     if (nxt < nk) {
-      double* st = smem + (nxt % NSTAGE) * kStageDoubles;
-      load_tile_rows<BM, LDS, kThreads>(st, p.XT, p.Pp, nxt * BK, q0, p.Hused, tid);
-      load_src_tile(st + BK * LDS, p.src, p.Hp, p.n_el, nxt * BK, el0, p.Hused, tid);
+      double* st = smem + (nxt % NSTAGE) * M2D_STAGE;
+      load_tile_rows<M2D_BM, M2D_LDA, M2D_THREADS>(st, p.XT, p.Pp, nxt * BK, q0, p.Hused, tid);
+      load_src_tile<M2D_THREADS>(st + BK * M2D_LDA, p.src, p.Hp, p.n_el, nxt * BK, el0, p.Hused, tid);
     }
     cp_async_commit();
     cp_async_wait<NSTAGE - 1>();
     __syncthreads();
-    const double* st = smem + (kt % NSTAGE) * kStageDoubles;
-    mma_stage<4, LDS>(st, st + BK * LDS, acc, wm, wn, g, t);
+    const double* st = smem + (kt % NSTAGE) * M2D_STAGE;
+    mma_stage<4, M2D_LDA>(st, st + BK * M2D_LDA, acc, wm, wn, g, t);
     __syncthreads();
   }
   cp_async_wait<0>();
@@ -272,7 +278,7 @@ __global__ void __launch_bounds__(kThreads) m2d_kernel(M2DParams p) {
   }
 }
 
-size_t gemm_smem() { return sizeof(double) * NSTAGE * BK * (LDS + LDB); }
+size_t gemm_smem() { return sizeof(double) * NSTAGE * M2D_STAGE; }
 
 template <int MI, int WM>
 void launch_d2m_tile(const D2MParams& p, cudaStream_t s) {
@@ -462,10 +468,11 @@ void launch_m2d(const M2DParams& p, cudaStream_t s) {
     cudaFuncSetAttribute(m2d_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
     init = true;
   }
-  const unsigned ge = (p.n_el + BN / 4 - 1) / (BN / 4), gq = (p.P + BM - 1) / BM;
+  if (p.Pp % M2D_BM != 0) throw std::invalid_argument("m2d: X^T row pitch is not a multiple of the patch tile");
+  const unsigned ge = (p.n_el + BN / 4 - 1) / (BN / 4), gq = (p.P + M2D_BM - 1) / M2D_BM;
   dim3 grid = STAMG_GEMM_SWAP ? dim3(gq, ge) : dim3(ge, gq);
-  if (p.beta != 0.0) m2d_kernel<true><<<grid, kThreads, gemm_smem(), s>>>(p);
-  else m2d_kernel<false><<<grid, kThreads, gemm_smem(), s>>>(p);
+  if (p.beta != 0.0) m2d_kernel<true><<<grid, M2D_THREADS, gemm_smem(), s>>>(p);
+  else m2d_kernel<false><<<grid, M2D_THREADS, gemm_smem(), s>>>(p);
 }
 
 }  // namespace stamg_b200
