@@ -30,7 +30,7 @@ if [ "$MODE" = final ]; then
   timeout 900 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; echo "bench rc=$?"
   timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${T}_ref.json 2> gpurun_out/${T}_ref.err
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 2 --warmup 3 --no-si --no-e2e --no-solve --no-kernels --no-cpu > gpurun_out/${T}_ncu_launch.log 2>&1
-  C5N=256 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"d2m|m2d|unfold|fold" -c 4 -o gpurun_out/${T}_si256 python tools/perf_probe.py si > gpurun_out/${T}_ncu_si.log 2>&1
+  C5N=256 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"d2m|m2d|unfold|fold" -c 18 -o gpurun_out/${T}_si256 python tools/perf_probe.py si > gpurun_out/${T}_ncu_si.log 2>&1
   C5N=128 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep_kernel" -c 2 -o gpurun_out/${T}_sweep128 python tools/perf_probe.py c5s > gpurun_out/${T}_ncu_sweep.log 2>&1
   timeout 900 python bench.py --steps 3 --no-si --no-e2e --no-cpu --no-kernels --solve-configs 4 > gpurun_out/${T}_bench_c4.json 2> gpurun_out/${T}_bench_c4.err
 fi
