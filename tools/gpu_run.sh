@@ -128,3 +128,22 @@ if [ "$MODE" = ab ]; then
     STAMG_LIB=abl/$v.so C5N=${C5N:-512} timeout 300 python tools/perf_probe.py si >> gpurun_out/${T}_ab.log 2>&1
   done; done
 fi
+if [ "$MODE" = final2 ]; then
+  # the final set with size-bounded outputs (gpurun copies back <= 64 MiB): ncu
+  # reports are exported to CSV on the box and only kept when small
+  timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/${T}_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_tests.log
+  timeout 900 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; echo "bench rc=$?"
+  timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${T}_ref.json 2> gpurun_out/${T}_ref.err
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${T}_launches.csv python bench.py --steps 2 --warmup 3 --no-si --no-e2e --no-solve --no-kernels --no-cpu > gpurun_out/${T}_ncu_launch.log 2>&1
+  C5N=256 timeout 900 ncu --set full --clock-control none -k regex:"d2m|m2d|unfold|fold" -c 18 -o /tmp/${T}_si256 python tools/perf_probe.py si > gpurun_out/${T}_ncu_si.log 2>&1
+  ncu -i /tmp/${T}_si256.ncu-rep --page raw --csv > gpurun_out/${T}_si256_raw.csv 2>&1
+  C5N=128 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sweep_kernel" -c 2 -o /tmp/${T}_sweep128 python tools/perf_probe.py c5s > gpurun_out/${T}_ncu_sweep.log 2>&1
+  ncu -i /tmp/${T}_sweep128.ncu-rep --page raw --csv > gpurun_out/${T}_sweep128_raw.csv 2>&1
+  ncu -i /tmp/${T}_sweep128.ncu-rep --page details > gpurun_out/${T}_sweep128_details.txt 2>&1
+  timeout 900 python bench.py --steps 3 --no-si --no-e2e --no-cpu --no-kernels --solve-configs 4 > gpurun_out/${T}_bench_c4.json 2> gpurun_out/${T}_bench_c4.err
+  for rep in 1 2; do for v in ${3:-}; do
+    echo "== $v rep $rep" >> gpurun_out/${T}_ab.log
+    STAMG_LIB=abl/$v.so C5N=512 timeout 300 python tools/perf_probe.py si >> gpurun_out/${T}_ab.log 2>&1
+  done; done
+  du -sh gpurun_out
+fi
