@@ -317,11 +317,16 @@ __global__ void fold_kernel(const double* __restrict__ phi, double* __restrict__
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n_el * R) return;
   const int el = int(idx / R), r = int(idx - (int64_t)el * R);
-  double v[G][4];
+  const double* src[G];  // member addresses first, then the G block loads back to back
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const int q = orbit[r * G + g];
-    const dbl4 a = ld_block(phi + (wl.nd ? (size_t)wl_block(wl, el, q) * 4 : ((size_t)el * P + q) * 4));
+    src[g] = phi + (wl.nd ? (size_t)wl_block(wl, el, q) * 4 : ((size_t)el * P + q) * 4);
+  }
+  double v[G][4];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const dbl4 a = ld_block(src[g]);
     v[g][0] = a.x, v[g][1] = a.y, v[g][2] = a.z, v[g][3] = a.w;
   }
   wht<G>(v);
@@ -337,6 +342,16 @@ __global__ void unfold_kernel(const double* __restrict__ Y, double* __restrict__
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n_el * R) return;
   const int el = int(idx / R), r = int(idx - (int64_t)el * R);
+  // orbit members and their source weights first: the block stores below are
+  // ordered asm (memory clobber), so loads left between them would serialise
+  double* o[G];
+  double ar[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int q = orbit[r * G + g];
+    o[g] = y + (wl.nd ? (size_t)wl_block(wl, el, q) * 4 : ((size_t)el * P + q) * 4);
+    ar[g] = ext_q ? area[q] : 0.0;
+  }
   double v[G][4];
 #pragma unroll
   for (int c = 0; c < G; ++c) {
@@ -346,21 +361,22 @@ __global__ void unfold_kernel(const double* __restrict__ Y, double* __restrict__
   wht<G>(v);
   constexpr double inv4pi = 0.07957747154594767;
   const double qel = ext_q ? ext_q[el] * inv4pi : 0.0;
+  // all reads of the old y before the first store (same reason as above)
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    const int q = orbit[r * G + g];
-    double* o = y + (wl.nd ? (size_t)wl_block(wl, el, q) * 4 : ((size_t)el * P + q) * 4);
     double w0 = scale * v[g][0], w1 = scale * v[g][1], w2 = scale * v[g][2], w3 = scale * v[g][3];
     if (ext_q) {
-      const double c = qel * area[q];
+      const double c = qel * ar[g];
       w0 += c * nsum.x, w1 += c * nsum.y, w2 += c * nsum.z, w3 += c * nsum.w;
     }
     if (beta != 0.0) {
-      const dbl4 a = ld_block_rw(o);
+      const dbl4 a = ld_block_rw(o[g]);
       w0 += beta * a.x, w1 += beta * a.y, w2 += beta * a.z, w3 += beta * a.w;
     }
-    st_block(o, dbl4{w0, w1, w2, w3});
+    v[g][0] = w0, v[g][1] = w1, v[g][2] = w2, v[g][3] = w3;
   }
+#pragma unroll
+  for (int g = 0; g < G; ++g) st_block(o[g], dbl4{v[g][0], v[g][1], v[g][2], v[g][3]});
 }
 
 // reference layout [el][q][4] (q -> internal k = perm[q]) <-> wavefront layout
