@@ -31,6 +31,9 @@ __device__ __forceinline__ void st_stream(double* p, double2 v) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 // one 32-byte block (4 doubles = one DRAM sector) per thread: 256-bit LDG/STG (sm_100)
+#ifndef STAMG_ST_CLOBBER
+#define STAMG_ST_CLOBBER 1  // A/B knob: "memory" clobber on the 256-bit block store
+#endif
 #ifndef STAMG_V256
 #define STAMG_V256 1
 #endif
@@ -60,7 +63,11 @@ __device__ __forceinline__ dbl4 ld_block_rw(const double* p) {
 }
 __device__ __forceinline__ void st_block(double* p, const dbl4& v) {
 #if STAMG_V256
+#if STAMG_ST_CLOBBER
   asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+#else  // streaming stores: volatile keeps them ordered with the block loads; other loads may move across
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w));
+#endif
 #else
   reinterpret_cast<double2*>(p)[0] = make_double2(v.x, v.y);
   reinterpret_cast<double2*>(p)[1] = make_double2(v.z, v.w);

@@ -311,8 +311,11 @@ __device__ __forceinline__ void wht(double (&v)[G][4]) {
 }
 
 // Phi[c][el][r][i] = sum_g chi_c(g) phi[el][orbit[r][g]][i]
+#ifndef STAMG_FOLD_MINB
+#define STAMG_FOLD_MINB 1  // A/B knob: resident 256-thread CTAs per SM the fold/unfold registers are sized for
+#endif
 template <int G>
-__global__ void fold_kernel(const double* __restrict__ phi, double* __restrict__ Phi, const int* __restrict__ orbit,
+__global__ void __launch_bounds__(256, STAMG_FOLD_MINB) fold_kernel(const double* __restrict__ phi, double* __restrict__ Phi, const int* __restrict__ orbit,
                             int n_el, int P, int R, WLGeom wl) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n_el * R) return;
@@ -335,8 +338,8 @@ __global__ void fold_kernel(const double* __restrict__ phi, double* __restrict__
 }
 
 // y[el][orbit[r][g]][i] = beta*y + scale * sum_c chi_c(g) Y[c][el][r][i] (+ isotropic source)
-template <int G>
-__global__ void unfold_kernel(const double* __restrict__ Y, double* __restrict__ y, const int* __restrict__ orbit,
+template <int G, bool BETA>
+__global__ void __launch_bounds__(256, STAMG_FOLD_MINB) unfold_kernel(const double* __restrict__ Y, double* __restrict__ y, const int* __restrict__ orbit,
                               int n_el, int P, int R, double scale, double beta, const double* __restrict__ ext_q,
                               const double* __restrict__ area, double4 nsum, WLGeom wl) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -369,7 +372,7 @@ __global__ void unfold_kernel(const double* __restrict__ Y, double* __restrict__
       const double c = qel * ar[g];
       w0 += c * nsum.x, w1 += c * nsum.y, w2 += c * nsum.z, w3 += c * nsum.w;
     }
-    if (beta != 0.0) {
+    if constexpr (BETA) {
       const dbl4 a = ld_block_rw(o[g]);
       w0 += beta * a.x, w1 += beta * a.y, w2 += beta * a.z, w3 += beta * a.w;
     }
@@ -429,16 +432,103 @@ void launch_fold(const double* phi, double* Phi, const int* orbit, int n_el, int
   }
 }
 
+#ifndef STAMG_UNFOLD_SPLIT
+#define STAMG_UNFOLD_SPLIT 0  // A/B knob: two threads per orbit representative (one dof pair each, 16-byte accesses)
+#endif
+// unfold_kernel with the four dofs split over a lane pair: half the registers per
+// thread (8 x 2 doubles), the pair still covers each 32-byte block in one access
+template <int G, bool BETA>
+__global__ void __launch_bounds__(256) unfold2_kernel(const double* __restrict__ Y, double* __restrict__ y,
+                                                      const int* __restrict__ orbit, int n_el, int P, int R,
+                                                      double scale, double beta, const double* __restrict__ ext_q,
+                                                      const double* __restrict__ area, double4 nsum, WLGeom wl) {
+  const int64_t idx2 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx2 >= (int64_t)n_el * R * 2) return;
+  const int half = int(idx2 & 1);
+  const int64_t idx = idx2 >> 1;
+  const int el = int(idx / R), r = int(idx - (int64_t)el * R);
+  double* o[G];
+  double ar[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int q = orbit[r * G + g];
+    o[g] = y + (wl.nd ? (size_t)wl_block(wl, el, q) * 4 : ((size_t)el * P + q) * 4) + half * 2;
+    ar[g] = ext_q ? area[q] : 0.0;
+  }
+  double v[G][2];
+#pragma unroll
+  for (int c = 0; c < G; ++c) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(Y + (((size_t)c * n_el + el) * R + r) * 4 + half * 2));
+    v[c][0] = a.x, v[c][1] = a.y;
+  }
+#pragma unroll
+  for (int bit = 1; bit < G; bit <<= 1)
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (!(g & bit))
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const double a = v[g][i], b = v[g | bit][i];
+          v[g][i] = a + b, v[g | bit][i] = a - b;
+        }
+  constexpr double inv4pi = 0.07957747154594767;
+  const double qel = ext_q ? ext_q[el] * inv4pi : 0.0;
+  const double n0 = half ? nsum.z : nsum.x, n1 = half ? nsum.w : nsum.y;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    double w0 = scale * v[g][0], w1 = scale * v[g][1];
+    if (ext_q) {
+      const double c = qel * ar[g];
+      w0 += c * n0, w1 += c * n1;
+    }
+    if constexpr (BETA) {
+      const double2 a = *reinterpret_cast<const double2*>(o[g]);
+      w0 += beta * a.x, w1 += beta * a.y;
+    }
+    v[g][0] = w0, v[g][1] = w1;
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) *reinterpret_cast<double2*>(o[g]) = make_double2(v[g][0], v[g][1]);
+}
+
 void launch_unfold(const double* Y, double* y, const int* orbit, int n_el, int P, int R, int G, double scale,
                    double beta, const double* ext_q, const double* area, const double* nsum, const WLGeom& wl,
                    cudaStream_t s) {
   const int64_t n = (int64_t)n_el * R;
   const int blocks = int((n + 255) / 256);
   const double4 ns = make_double4(nsum[0], nsum[1], nsum[2], nsum[3]);
+  if (STAMG_UNFOLD_SPLIT) {
+    const int b2 = int((2 * n + 255) / 256);
+    switch (G) {
+      case 2:
+        if (beta != 0.0) unfold2_kernel<2, true><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+        else unfold2_kernel<2, false><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+        break;
+      case 4:
+        if (beta != 0.0) unfold2_kernel<4, true><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+        else unfold2_kernel<4, false><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+        break;
+      case 8:
+        if (beta != 0.0) unfold2_kernel<8, true><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+        else unfold2_kernel<8, false><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+        break;
+      default: break;
+    }
+    return;
+  }
   switch (G) {
-    case 2: unfold_kernel<2><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl); break;
-    case 4: unfold_kernel<4><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl); break;
-    case 8: unfold_kernel<8><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl); break;
+    case 2:
+      if (beta != 0.0) unfold_kernel<2, true><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+      else unfold_kernel<2, false><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+      break;
+    case 4:
+      if (beta != 0.0) unfold_kernel<4, true><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+      else unfold_kernel<4, false><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+      break;
+    case 8:
+      if (beta != 0.0) unfold_kernel<8, true><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+      else unfold_kernel<8, false><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+      break;
     default: break;
   }
 }
