@@ -198,8 +198,13 @@ __device__ __forceinline__ double* m2d_out(const M2DParams& p, int el, int q, in
 constexpr int M2D_BM = 32 * STAMG_M2D_WM, M2D_LDA = M2D_BM + 4, M2D_THREADS = 64 * STAMG_M2D_WM;
 constexpr int M2D_STAGE = BK * (M2D_LDA + LDB);
 
+#ifndef STAMG_M2D_MINB
+#define STAMG_M2D_MINB 1  // A/B knob: resident CTAs per SM the beta != 0 M2D registers are sized for
+#endif
+template <bool PRE_>
+constexpr int m2d_minb() { return PRE_ ? STAMG_M2D_MINB : 1; }
 template <bool PRE>
-__global__ void __launch_bounds__(M2D_THREADS) m2d_kernel(M2DParams p) {
+__global__ void __launch_bounds__(M2D_THREADS, m2d_minb<PRE>()) m2d_kernel(M2DParams p) {
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;

@@ -147,3 +147,11 @@ if [ "$MODE" = final2 ]; then
   done; done
   du -sh gpurun_out
 fi
+if [ "$MODE" = abk ]; then
+  # A/B of library variants on the bench's config-4 kernel roofline section
+  for rep in 1 2; do for v in ${3:-}; do
+    echo "== $v rep $rep" >> gpurun_out/${T}_abk.log
+    STAMG_LIB=abl/$v.so timeout 400 python bench.py --steps 3 --no-si --no-e2e --no-cpu --no-solve >> gpurun_out/${T}_abk.log 2>&1
+  done; done
+  STAMG_LIB=abl/m2dm3.so timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_golden.py -m gpu -x -q -k "scatter or apply_A or mg_apply or gmres or golden" > gpurun_out/${T}_tests.log 2>&1; echo rc=$? >> gpurun_out/${T}_tests.log
+fi
