@@ -68,11 +68,25 @@ typedef struct {
   double coarse_tol;
 } stamg_problem;
 
+/* Host-side collective: sum n doubles element-wise across all ranks, in place.
+ * buf is pinned host memory owned by the context; the context's stream is
+ * synchronised before the call and the result is copied back after it.
+ * Return 0 on success (anything else fails the operator with STAMG_ENCCL).
+ * For in-process multi-rank emulation, tests and custom transports; the
+ * production multi-GPU path is NCCL (nccl_id). */
+typedef int (*stamg_allreduce_fn)(void* user, double* buf, int64_t n);
+
 typedef struct {
   int device;            /* CUDA device ordinal */
   int rank, world;       /* direction sharding; world = 1 for one GPU */
   const void* nccl_id;   /* 128-byte ncclUniqueId when world > 1, else NULL */
   int build_hierarchy;   /* 0: outer level only (sweep/scatter throughput) */
+  /* world > 1 needs exactly one of: nccl_id, allreduce, shard_probe */
+  stamg_allreduce_fn allreduce;  /* host collective (see above), or NULL */
+  void* allreduce_user;          /* passed to allreduce */
+  int shard_probe;       /* timing only: this rank's slice runs alone and every
+                            collective is skipped, so scatter moments, dots and
+                            the scalar flux are partial sums (tools/shard_probe.py) */
 } stamg_options;
 
 typedef struct {

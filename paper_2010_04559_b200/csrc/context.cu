@@ -51,6 +51,12 @@ T* dalloc(size_t n) {
   return static_cast<T*>(p);
 }
 template <class T>
+T* dalloc_zero(size_t n, cudaStream_t s) {
+  T* p = dalloc<T>(n);
+  if (p) ck(cudaMemsetAsync(p, 0, n * sizeof(T), s), "memset");
+  return p;
+}
+template <class T>
 T* dupload(const std::vector<T>& v, cudaStream_t s) {
   T* p = dalloc<T>(v.size());
   if (p) ck(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "upload");
@@ -164,6 +170,12 @@ struct stamg_ctx {
   std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   std::map<std::string, std::pair<double, int64_t>> timed;
   void* comm = nullptr;
+  // host collective (stamg_options.allreduce) and its pinned staging buffer
+  stamg_allreduce_fn host_allreduce = nullptr;
+  void* host_allreduce_user = nullptr;
+  double* coll_host = nullptr;
+  int64_t coll_host_n = 0;
+  bool shard_probe = false;
 };
 
 struct stamg_vec {
@@ -301,7 +313,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     const auto& t0 = L.t;
-    if (c->wl_allowed && !t0.groups8.empty() && !t0.groups8_padded && t0.nx >= 36 && t0.ny >= 32 &&
+    if (c->wl_allowed && !t0.groups8.empty() && !t0.groups8_padded && t0.nx >= kSweep8MinNx && t0.ny >= kSweep8MinNy &&
         int(t0.group8_oct.size()) >= sweep8_min_groups(c, sms) && std::getenv("STAMG_SWEEP_DIRS4") == nullptr &&
         !env_is_zero("STAMG_WAVEFRONT_LAYOUT")) {
       // default for throughput contexts: every sweep step of a group touches one
@@ -348,19 +360,19 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
   // small levels keep the 4-direction kernels (twice the CTAs, latency-bound anyway)
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  if (!t.groups8.empty() && t.nx >= 36 && t.ny >= 32 && int(t.group8_oct.size()) >= sweep8_min_groups(c, sms) &&
+  if (!t.groups8.empty() && t.nx >= kSweep8MinNx && t.ny >= kSweep8MinNy && int(t.group8_oct.size()) >= sweep8_min_groups(c, sms) &&
       std::getenv("STAMG_SWEEP_DIRS4") == nullptr) {
     L.groups8 = dupload(t.groups8, s), L.group8_oct = dupload(t.group8_oct, s);
     L.sweep_top = dalloc<double2>(t.group8_oct.size() * 8 * size_t(t.nx));
     // fewer groups than SMs (config 5 sharded over 8 GPUs: 128 per rank): two column blocks per
     // group so the wavefronts cover twice the SMs (STAMG_SWEEP_XBLOCKS=0 keeps one block)
     const int ng = int(t.group8_oct.size());
-    if (c->wl_allowed && ng <= sms && t.nx % 2 == 0 && t.nx / 2 >= 38 && !env_is_zero("STAMG_SWEEP_XBLOCKS")) {
+    if (c->wl_allowed && ng <= sms && t.nx % 2 == 0 && t.nx / 2 >= kSweep8MinNx && !env_is_zero("STAMG_SWEEP_XBLOCKS")) {
       L.sweep_xb = 2;
       if (const char* e = std::getenv("STAMG_SWEEP_XB")) {  // A/B: more blocks (all must stay co-resident)
         const int xb = std::atoi(e);
         const int slots = (std::getenv("STAMG_SWEEP_XB_SMEMB") ? 4 : 2) * sms;
-        if (xb >= 1 && t.nx % xb == 0 && t.nx / xb >= 38 && ng * xb <= slots) L.sweep_xb = xb;
+        if (xb >= 1 && t.nx % xb == 0 && t.nx / xb >= kSweep8MinNx && ng * xb <= slots) L.sweep_xb = xb;
       }
       L.sweep_xflag = dalloc<int>(size_t(ng) * L.sweep_xb);
       L.sweep_xtrace = dalloc<double2>(size_t(ng) * L.sweep_xb * t.ny * 8);
@@ -455,10 +467,13 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
   // fold only where the GEMMs are big enough to pay for the two streaming passes
   int fold_min_h = 128;
   if (const char* e = std::getenv("STAMG_FOLD_MIN_H")) fold_min_h = std::atoi(e);
-  // (orbit classes of fewer than 64 patches are below the GEMM tile sizes the folded
-  // path is validated for: config 1's 128-patch level folds to 16 and is off by 1e-10)
-  // (sharded: throughput contexts, whose shards are whole orbits; the folded moments are allreduced)
-  if (t.n_sym_axes > 0 && t.H >= fold_min_h && (c->world == 1 || c->wl_allowed) && (t.P >> t.n_sym_axes) >= 64) {
+  // exactness: the coupling table must satisfy the reflection identity (sym_defect, measured
+  // in find_symmetry; config 1's level-2 mesh misses it by 2.2e-9 and never folds).
+  // size: orbit classes of >= 64 patches (smaller class GEMMs do not pay for the two
+  // streaming passes). sharded: throughput contexts, whose shards are whole orbits; the
+  // folded moments are allreduced
+  const bool fold_exact = t.n_sym_axes > 0 && t.sym_defect <= kFoldMaxDefect;
+  if (fold_exact && t.H >= fold_min_h && (c->world == 1 || c->wl_allowed) && (t.P >> t.n_sym_axes) >= 64) {
     const int G = 1 << t.n_sym_axes, R = t.P / G;
     L.fold_G = G, L.fold_R = R, L.fold_Rp = round_up(R, 64);
     const int Rk = round_up(R, 32);
@@ -511,11 +526,23 @@ void need(const stamg_vec* v, const DevLevel& L, const char* what) {
 
 // ------------------------------------------------------------------ operators
 void op_allreduce(stamg_ctx* c, double* buf, size_t n) {
-  if (c->world <= 1) return;
-  if (!c->comm) {  // STAMG_SHARD_PROBE: one rank's slice timed alone; partial sums are left as they are
-    if (std::getenv("STAMG_SHARD_PROBE")) return;
-    throw std::logic_error("allreduce: no communicator");
+  if (c->world <= 1 || n == 0) return;
+  if (c->shard_probe) return;  // explicit timing option (stamg_options.shard_probe): partial sums
+  if (c->host_allreduce) {     // host collective: device -> pinned host, callback, host -> device
+    if (c->coll_host_n < int64_t(n)) {
+      if (c->coll_host) cudaFreeHost(c->coll_host);
+      c->coll_host = nullptr, c->coll_host_n = 0;
+      ck(cudaMallocHost(&c->coll_host, n * sizeof(double)), "cudaMallocHost");
+      c->coll_host_n = int64_t(n);
+    }
+    ck(cudaMemcpyAsync(c->coll_host, buf, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (c->host_allreduce(c->host_allreduce_user, c->coll_host, int64_t(n)) != 0)
+      throw NcclError("host allreduce callback failed");
+    ck(cudaMemcpyAsync(buf, c->coll_host, n * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
+    return;
   }
+  if (!c->comm) throw std::logic_error("allreduce: no communicator");
   const int ncclDouble = 8, ncclSum = 0;
   if (nccl().allReduce(buf, buf, n, ncclDouble, ncclSum, c->comm, c->stream) != 0)
     throw NcclError("ncclAllReduce failed");
@@ -686,7 +713,7 @@ void op_sweep(stamg_ctx* c, DevLevel& L, const double* rhs, double* z, const dou
 
 // smoother_step (sweeps.cpp:106-113): phi += L^{-1}(f - A phi), the add fused into the sweep
 void op_smoother(stamg_ctx* c, DevLevel& L, const double* f, int order, double* phi) {
-  if (!L.tmp) L.tmp = dalloc<double>(L.n);
+  if (!L.tmp) L.tmp = dalloc_zero<double>(L.n, c->stream);
   op_residual(c, L, f, phi, order, L.tmp);
   op_sweep(c, L, L.tmp, phi, phi);
 }
@@ -745,7 +772,7 @@ void op_vcycle(stamg_ctx* c, int l, const double* f, double* phi) {
   const auto& spec = c->pb.spec;
   if (l == 0) {
     if (spec.coarse_tol > 0) {
-      if (!L.tmp) L.tmp = dalloc<double>(L.n);
+      if (!L.tmp) L.tmp = dalloc_zero<double>(L.n, c->stream);
       const double fnorm = std::sqrt(op_dot(c, f, f, L.n, L.sharded));
       for (int s = 0; s < 200; ++s) {
         op_coarse_gs(c, L, f, 1, phi);
@@ -758,8 +785,8 @@ void op_vcycle(stamg_ctx* c, int l, const double* f, double* phi) {
     return;
   }
   DevLevel& Cl = c->mg[l - 1];
-  if (!L.tmp) L.tmp = dalloc<double>(L.n);
-  if (!Cl.cf) Cl.cf = dalloc<double>(Cl.n), Cl.ce = dalloc<double>(Cl.n);
+  if (!L.tmp) L.tmp = dalloc_zero<double>(L.n, c->stream);
+  if (!Cl.cf) Cl.cf = dalloc_zero<double>(Cl.n, c->stream), Cl.ce = dalloc_zero<double>(Cl.n, c->stream);
   for (int s = 0; s < spec.nu_pre; ++s) op_smoother(c, L, f, c->nr, phi);
   op_residual(c, L, f, phi, c->nr, L.tmp);
   op_restrict(c, l, L.tmp, Cl.cf);
@@ -788,6 +815,11 @@ void ensure_krylov(stamg_ctx* c, int restart) {
   for (int k = 0; k <= restart; ++k) c->V.push_back(dalloc<double>(n));
   c->z = dalloc<double>(n);
   c->u = dalloc<double>(n);
+  // zeroed once: wavefront-layout vectors have padding slots that the operators never
+  // write but the dot products and axpys run over (padding must stay 0, never NaN)
+  for (double* v : c->V) ck(cudaMemsetAsync(v, 0, n * sizeof(double), c->stream), "memset");
+  ck(cudaMemsetAsync(c->z, 0, n * sizeof(double), c->stream), "memset");
+  ck(cudaMemsetAsync(c->u, 0, n * sizeof(double), c->stream), "memset");
   c->restart_alloc = restart;
 }
 
@@ -1084,6 +1116,26 @@ int guard(F&& f) {
   }
 }
 
+// every context-taking entry point binds the context's device first: kernels,
+// allocations and per-device function attributes then land on the right GPU
+// even when one host thread drives contexts on several devices
+template <class F>
+int guard_ctx(stamg_ctx* c, F&& f) {
+  if (!c) {
+    g_err = "invalid_argument: null context";
+    return STAMG_EINVAL;
+  }
+  int cur = -1;
+  if (cudaGetDevice(&cur) != cudaSuccess || cur != c->device) {
+    const cudaError_t e = cudaSetDevice(c->device);
+    if (e != cudaSuccess) {
+      g_err = std::string("cuda: cudaSetDevice: ") + cudaGetErrorString(e);
+      return STAMG_ECUDA;
+    }
+  }
+  return guard(std::forward<F>(f));
+}
+
 }  // namespace
 
 // ====================================================================== C ABI
@@ -1113,9 +1165,18 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
     c->wl_allowed = !want_mg;  // wavefront layout only for contexts without a hierarchy
     ck(cudaSetDevice(c->device), "cudaSetDevice");
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
-    const bool probe = std::getenv("STAMG_SHARD_PROBE") != nullptr;  // one rank's slice, no communicator
-    if (c->world > 1 && !(probe && !opt->nccl_id)) {
-      if (!opt->nccl_id) throw std::invalid_argument("world > 1 needs an nccl id");
+    if (c->world > 1) {
+      if (!opt) throw std::invalid_argument("world > 1 needs options");
+      if (c->rank < 0 || c->rank >= c->world) throw std::invalid_argument("stamg_create: rank out of range");
+      const int kinds = (opt->nccl_id != nullptr) + (opt->allreduce != nullptr) + (opt->shard_probe != 0);
+      if (kinds != 1)
+        throw std::invalid_argument("world > 1 needs exactly one of nccl_id, allreduce, shard_probe");
+    }
+    if (c->world > 1 && opt->allreduce) {
+      c->host_allreduce = opt->allreduce, c->host_allreduce_user = opt->allreduce_user;
+    } else if (c->world > 1 && opt->shard_probe) {
+      c->shard_probe = true;
+    } else if (c->world > 1) {
       if (!nccl().load()) throw NcclError("libnccl.so.2 not loadable");
       UniqueId uid;
       std::memcpy(uid.internal, opt->nccl_id, 128);
@@ -1160,6 +1221,7 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
 int stamg_destroy(stamg_ctx* c) {
   return guard([&] {
     if (!c) return;
+    cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     free_level(c->outer);
     for (auto& L : c->mg) free_level(L);
@@ -1168,6 +1230,7 @@ int stamg_destroy(stamg_ctx* c) {
                     (void*)c->q_el, (void*)c->hostio, (void*)c->foldbuf})
       if (p) cudaFree(p);
     if (c->hbuf) cudaFreeHost(c->hbuf);
+    if (c->coll_host) cudaFreeHost(c->coll_host);
     for (double* p : c->pipe)
       if (p) cudaFree(p);
     for (cudaEvent_t e : c->pev)
@@ -1181,13 +1244,13 @@ int stamg_destroy(stamg_ctx* c) {
 }
 
 int stamg_layout(stamg_ctx* c, int level, int out4[4]) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, level);
     out4[0] = L.t.n_el, out4[1] = L.t.P, out4[2] = 4, out4[3] = 1;
   });
 }
 int stamg_patch_range(stamg_ctx* c, int level, int* q0, int* q1) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, level);
     *q0 = L.t.P ? L.t.qpos.front() : 0, *q1 = L.t.P ? L.t.qpos.back() + 1 : 0;
   });
@@ -1237,24 +1300,24 @@ int stamg_shard_patches(const stamg_problem* prob, int rank, int world, int* out
 }
 
 int stamg_patch_list(stamg_ctx* c, int level, int* out, int cap, int* n) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, level);
     *n = L.t.P;
     for (int q = 0; out && q < L.t.P && q < cap; ++q) out[q] = L.t.qpos[q];
   });
 }
 int stamg_n_levels(stamg_ctx* c, int* n, int* nr) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     *n = int(c->mg.size());
     *nr = c->nr;
   });
 }
 int stamg_level_order(stamg_ctx* c, int level, int* order) {
-  return guard([&] { *order = level_of(c, level).t.order; });
+  return guard_ctx(c, [&] { *order = level_of(c, level).t.order; });
 }
 
 int stamg_vec_create(stamg_ctx* c, int level, stamg_vec** out) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, level);
     auto v = std::make_unique<stamg_vec>();
     v->ctx = c, v->level = level, v->n = L.n, v->d = dalloc<double>(L.n);
@@ -1265,6 +1328,7 @@ int stamg_vec_create(stamg_ctx* c, int level, stamg_vec** out) {
 int stamg_vec_free(stamg_vec* v) {
   return guard([&] {
     if (!v) return;
+    cudaSetDevice(v->ctx->device);
     cudaStreamSynchronize(v->ctx->stream);
     cudaFree(v->d);
     delete v;
@@ -1272,13 +1336,13 @@ int stamg_vec_free(stamg_vec* v) {
 }
 int stamg_vec_size(stamg_vec* v, int64_t* n) {
   // host-visible length in the reference layout (device storage may be padded)
-  return guard([&] { *n = ref_size(level_of(v->ctx, v->level)); });
+  return guard_ctx(v ? v->ctx : nullptr, [&] { *n = ref_size(level_of(v->ctx, v->level)); });
 }
 int stamg_vec_device_ptr(stamg_vec* v, double** p) {
-  return guard([&] { *p = v->d; });
+  return guard_ctx(v ? v->ctx : nullptr, [&] { *p = v->d; });
 }
 int stamg_vec_upload(stamg_ctx* c, stamg_vec* v, const double* host, int64_t n) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, v->level);
     if (n != ref_size(L)) throw std::invalid_argument("vec_upload: layout mismatch");
     host_to_vec(c, L, host, v->d, false);
@@ -1286,7 +1350,7 @@ int stamg_vec_upload(stamg_ctx* c, stamg_vec* v, const double* host, int64_t n) 
   });
 }
 int stamg_vec_download(stamg_ctx* c, const stamg_vec* v, double* host, int64_t n) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, v->level);
     if (n != ref_size(L)) throw std::invalid_argument("vec_download: layout mismatch");
     vec_to_host(c, L, v->d, host, false);
@@ -1294,7 +1358,7 @@ int stamg_vec_download(stamg_ctx* c, const stamg_vec* v, double* host, int64_t n
   });
 }
 int stamg_vec_fill(stamg_ctx* c, stamg_vec* v, double value) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, v->level);
     if (L.wl.nd && value != 0.0) launch_wl_fill(v->d, value, L.t.n_el, L.t.P, L.wl, c->stream);
     else launch_fill(v->d, value, v->n, c->stream);
@@ -1302,20 +1366,20 @@ int stamg_vec_fill(stamg_ctx* c, stamg_vec* v, double value) {
   });
 }
 int stamg_vec_copy(stamg_ctx* c, const stamg_vec* a, stamg_vec* b) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     if (a->n != b->n) throw std::invalid_argument("vec_copy: layout mismatch");
     ck(cudaMemcpyAsync(b->d, a->d, a->n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "copy");
   });
 }
 int stamg_vec_axpy(stamg_ctx* c, double a, const stamg_vec* x, stamg_vec* y) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     if (x->n != y->n) throw std::invalid_argument("vec_axpy: layout mismatch");
     launch_axpy(a, x->d, y->d, x->n, c->stream);
     ck_launch("axpy");
   });
 }
 int stamg_vec_dot(stamg_ctx* c, const stamg_vec* x, const stamg_vec* y, double* out) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     if (x->n != y->n) throw std::invalid_argument("vec_dot: layout mismatch");
     const DevLevel& L = level_of(c, x->level);
     *out = op_dot(c, x->d, y->d, x->n, L.sharded);
@@ -1323,7 +1387,7 @@ int stamg_vec_dot(stamg_ctx* c, const stamg_vec* x, const stamg_vec* y, double* 
 }
 
 int stamg_apply_L(stamg_ctx* c, int level, const stamg_vec* phi, stamg_vec* y) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, level);
     need(phi, L, "apply_L"), need(y, L, "apply_L");
     if (phi->d == y->d) throw std::invalid_argument("apply_L: y must not alias phi");
@@ -1331,14 +1395,14 @@ int stamg_apply_L(stamg_ctx* c, int level, const stamg_vec* phi, stamg_vec* y) {
   });
 }
 int stamg_apply_scatter(stamg_ctx* c, int level, const stamg_vec* phi, int order, double scale, stamg_vec* y) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, level);
     need(phi, L, "apply_scatter"), need(y, L, "apply_scatter");
     op_scatter(c, L, phi->d, order, scale, y->d);
   });
 }
 int stamg_apply_A(stamg_ctx* c, int level, const stamg_vec* phi, int order, stamg_vec* y) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, level);
     need(phi, L, "apply_A"), need(y, L, "apply_A");
     if (phi->d == y->d) throw std::invalid_argument("apply_A: y must not alias phi");
@@ -1346,49 +1410,49 @@ int stamg_apply_A(stamg_ctx* c, int level, const stamg_vec* phi, int order, stam
   });
 }
 int stamg_sweep(stamg_ctx* c, int level, const stamg_vec* rhs, stamg_vec* z) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, level);
     need(rhs, L, "standard_sweep"), need(z, L, "standard_sweep");
     op_sweep(c, L, rhs->d, z->d);
   });
 }
 int stamg_coarse_gs(stamg_ctx* c, int level, const stamg_vec* rhs, int nu, stamg_vec* phi) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, level);
     need(rhs, L, "coarse_scatter_sweep"), need(phi, L, "coarse_scatter_sweep");
     op_coarse_gs(c, L, rhs->d, nu, phi->d);
   });
 }
 int stamg_smoother_step(stamg_ctx* c, int level, const stamg_vec* f, int order, stamg_vec* phi) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, level);
     need(f, L, "smoother_step"), need(phi, L, "smoother_step");
     op_smoother(c, L, f->d, order, phi->d);
   });
 }
 int stamg_prolongate(stamg_ctx* c, int l, const stamg_vec* coarse, stamg_vec* fine) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     if (!c->have_mg || l < 1 || l >= int(c->mg.size())) throw std::invalid_argument("prolongate: level out of range");
     need(coarse, c->mg[l - 1], "prolongate"), need(fine, c->mg[l], "prolongate");
     op_prolong(c, l, coarse->d, fine->d, false);
   });
 }
 int stamg_restrict(stamg_ctx* c, int l, const stamg_vec* fine, stamg_vec* coarse) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     if (!c->have_mg || l < 1 || l >= int(c->mg.size())) throw std::invalid_argument("restrict_residual: level out of range");
     need(fine, c->mg[l], "restrict_residual"), need(coarse, c->mg[l - 1], "restrict_residual");
     op_restrict(c, l, fine->d, coarse->d);
   });
 }
 int stamg_vcycle(stamg_ctx* c, int l, const stamg_vec* f, stamg_vec* phi) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, l);
     need(f, L, "lmg_vcycle"), need(phi, L, "lmg_vcycle");
     op_vcycle(c, l, f->d, phi->d);
   });
 }
 int stamg_mg_apply(stamg_ctx* c, const stamg_vec* r, stamg_vec* z) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     if (!c->have_mg) throw std::invalid_argument("multigrid hierarchy was not built for this context");
     need(r, c->mg.back(), "mg_apply"), need(z, c->mg.back(), "mg_apply");
     if (r->d == z->d) throw std::invalid_argument("mg_apply: z must not alias r");
@@ -1396,7 +1460,7 @@ int stamg_mg_apply(stamg_ctx* c, const stamg_vec* r, stamg_vec* z) {
   });
 }
 int stamg_rhs(stamg_ctx* c, stamg_vec* f) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     need(f, c->outer, "assemble_rhs");
     const auto v = assemble_rhs(c->pb, c->outer.t, c->tree);  // tables' (internal) patch order
     host_to_vec(c, c->outer, v.data(), f->d, true);
@@ -1406,7 +1470,7 @@ int stamg_rhs(stamg_ctx* c, stamg_vec* f) {
 
 int stamg_solve(stamg_ctx* c, int method, int precond, const stamg_vec* b, stamg_vec* x, double tol, int max_iter,
                 int restart, stamg_report* rep, double* history, int cap) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     need(b, c->outer, "solve"), need(x, c->outer, "solve");
     if (precond == 1 && !c->have_mg) throw std::invalid_argument("multigrid hierarchy was not built for this context");
     if (precond < 0 || precond > 2) throw std::invalid_argument("solve: unknown preconditioner");
@@ -1509,7 +1573,7 @@ static bool sweep_host_pipelined(stamg_ctx* c, DevLevel& L, const double* rhs, d
 }
 
 int stamg_sweep_host(stamg_ctx* c, int level, const double* rhs, double* z, int64_t n) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, level);
     if (n != ref_size(L)) throw std::invalid_argument("standard_sweep: layout mismatch");
     if (sweep_host_pipelined(c, L, rhs, z)) return;
@@ -1529,11 +1593,12 @@ int stamg_sweep_host(stamg_ctx* c, int level, const double* rhs, double* z, int6
 
 int stamg_solve_host(stamg_ctx* c, int method, int precond, const double* bh, double* xh, int64_t n, double tol,
                      int max_iter, int restart, stamg_report* rep) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     if (n != ref_size(c->outer)) throw std::invalid_argument("solve: layout mismatch");
     double* b = dalloc<double>(c->outer.n);
     double* x = dalloc<double>(c->outer.n);
     ck(cudaMemsetAsync(b, 0, c->outer.n * sizeof(double), c->stream), "memset");
+    ck(cudaMemsetAsync(x, 0, c->outer.n * sizeof(double), c->stream), "memset");
     try {
       host_to_vec(c, c->outer, bh, b, false);
       std::vector<double> hist;
@@ -1551,7 +1616,7 @@ int stamg_solve_host(stamg_ctx* c, int method, int precond, const double* bh, do
 }
 
 int stamg_scalar_flux(stamg_ctx* c, const stamg_vec* phi, double* out) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     need(phi, c->outer, "scalar_flux");
     std::vector<double> h(ref_size(c->outer));
     vec_to_host(c, c->outer, phi->d, h.data(), true);  // tables' (internal) patch order
@@ -1582,7 +1647,7 @@ int stamg_scalar_flux(stamg_ctx* c, const stamg_vec* phi, double* out) {
 // of the new psi (D2M, allreduced over ranks). psi holds the angular flux on
 // entry and exit; the moments live in the level's src buffer.
 int stamg_source_iteration(stamg_ctx* c, stamg_vec* psi, int n_iter) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     DevLevel& O = c->outer;
     need(psi, O, "source_iteration");
     const int order = c->pb.spec.N;
@@ -1594,12 +1659,12 @@ int stamg_source_iteration(stamg_ctx* c, stamg_vec* psi, int n_iter) {
 }
 
 int stamg_get_table(stamg_ctx* c, int level, const char* name, double* out, int64_t cap, int64_t* n) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     const DevLevel& L = level_of(c, level);
     const LevelTables& t = L.t;
     std::vector<double> v;
     const std::string nm(name);
-    if (nm == "fold") v = {double(L.fold_G), double(L.fold_R), double(L.fold_Hf)};
+    if (nm == "fold") v = {double(L.fold_G), double(L.fold_R), double(L.fold_Hf), t.sym_defect, double(t.n_sym_axes)};
     else if (nm == "gs_mode")
       v = {double(L.gs_mw), double(L.gs_cluster), double(L.gs_rows), double(L.gs_mb_slots), double(L.gs_mb_credit)};
     else if (nm == "X") v = t.X;
@@ -1621,23 +1686,23 @@ int stamg_get_table(stamg_ctx* c, int level, const char* name, double* out, int6
 }
 
 int stamg_synchronize(stamg_ctx* c) {
-  return guard([&] { ck(cudaStreamSynchronize(c->stream), "sync"); });
+  return guard_ctx(c, [&] { ck(cudaStreamSynchronize(c->stream), "sync"); });
 }
 int stamg_host_pipeline_chunks(stamg_ctx* c, int* n) {
-  return guard([&] { *n = c->last_host_chunks; });
+  return guard_ctx(c, [&] { *n = c->last_host_chunks; });
 }
 int stamg_launch_count(stamg_ctx* c, int64_t* n) {
-  return guard([&] { *n = c->launches; });
+  return guard_ctx(c, [&] { *n = c->launches; });
 }
 int stamg_timing_enable(stamg_ctx* c, int on) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     if (!on) resolve_timing(c);
     c->timing = on != 0;
     if (on) c->timed.clear();
   });
 }
 int stamg_timing_read(stamg_ctx* c, const char* kernel, double* ms, int64_t* launches) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     resolve_timing(c);
     auto it = c->timed.find(kernel);
     *ms = it == c->timed.end() ? 0.0 : it->second.first;
@@ -1647,7 +1712,7 @@ int stamg_timing_read(stamg_ctx* c, const char* kernel, double* ms, int64_t* lau
 
 // FP64 throughput probes (roofline denominators, measured on the box)
 int stamg_bench_fp64_peaks(stamg_ctx* c, double* dmma_tflops, double* dfma_tflops) {
-  return guard([&] {
+  return guard_ctx(c, [&] {
     *dmma_tflops = bench_dmma_tflops(c->device, c->stream);
     *dfma_tflops = bench_dfma_tflops(c->device, c->stream);
   });
@@ -1655,7 +1720,7 @@ int stamg_bench_fp64_peaks(stamg_ctx* c, double* dmma_tflops, double* dfma_tflop
 
 // access-pattern probe: GB/s of an in-place 128-byte-chunk read+write over a vector
 int stamg_bench_chunk_rw(stamg_ctx* c, stamg_vec* v, int64_t stride_chunks, int mode, double* gbs) {
-  return guard([&] { *gbs = bench_chunk_rw_gbs(v->d, v->n, stride_chunks, mode, c->stream); });
+  return guard_ctx(c, [&] { *gbs = bench_chunk_rw_gbs(v->d, v->n, stride_chunks, mode, c->stream); });
 }
 
 // pinned host memory for the host-buffer entry points

@@ -6,7 +6,17 @@
 
 #include "common.cuh"
 
+#ifndef STAMG_SWEEP_NST
+#define STAMG_SWEEP_NST 6  // sweep rhs staging depth (steps issued ahead)
+#endif
+
 namespace stamg_b200 {
+
+// Smallest nx (and the strip height 32 as smallest ny) for 8-direction sweep groups:
+// the strip hand-off of the trace scratch needs nx >= R + NST - 1 with R = 32, plus
+// one step of slack. upload_level and launch_sweep use the same constant.
+constexpr int kSweep8MinNx = 32 + STAMG_SWEEP_NST;
+constexpr int kSweep8MinNy = 32;
 
 // Common per-level geometry of the wavefront / stencil kernels: direction
 // groups of up to 4 equal-octant patches (-1 = padding).

@@ -289,11 +289,8 @@ template <int MI, int WM>
 void launch_d2m_tile(const D2MParams& p, cudaStream_t s) {
   using T = RowTile<MI, WM>;
   const size_t smem = sizeof(double) * NSTAGE * T::kStage;
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(d2m_kernel<MI, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    init = true;
-  }
+  // per launch: the attribute is per device (contexts may live on different GPUs)
+  cudaFuncSetAttribute(d2m_kernel<MI, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   const unsigned ge = (p.n_el + BN / 4 - 1) / (BN / 4), gh = (p.Hused + T::kBM - 1) / T::kBM;
   dim3 grid = STAMG_GEMM_SWAP ? dim3(gh, ge) : dim3(ge, gh);
   d2m_kernel<MI, WM><<<grid, T::kThreads, smem, s>>>(p);
@@ -573,12 +570,9 @@ void launch_d2m(const D2MParams& p, cudaStream_t s) {
 
 void launch_m2d(const M2DParams& p, cudaStream_t s) {
   if (p.n_el == 0 || p.P == 0) return;
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(m2d_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
-    cudaFuncSetAttribute(m2d_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
-    init = true;
-  }
+  // per launch: the attribute is per device (contexts may live on different GPUs)
+  if (p.beta != 0.0) cudaFuncSetAttribute(m2d_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
+  else cudaFuncSetAttribute(m2d_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(gemm_smem()));
   if (p.Pp % M2D_BM != 0) throw std::invalid_argument("m2d: X^T row pitch is not a multiple of the patch tile");
   const unsigned ge = (p.n_el + BN / 4 - 1) / (BN / 4), gq = (p.P + M2D_BM - 1) / M2D_BM;
   dim3 grid = STAMG_GEMM_SWAP ? dim3(gq, ge) : dim3(ge, gq);

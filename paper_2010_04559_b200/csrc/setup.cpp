@@ -632,6 +632,22 @@ void find_symmetry(LevelTables& L, const SphereTree& t) {
       for (int k = 0; k < L.n_sym_axes; ++k) c |= par[L.sym_axes[k]] << k;
       L.hclass[n * n + n + o] = c;
     }
+  // the fold's exactness is a property of the coupling table, not only of the lattice:
+  // measure the reflection defect of X over every orbit member and harmonic
+  double xmax = 0, dmax = 0;
+  for (double v : L.X) xmax = std::max(xmax, std::abs(v));
+  const int R = L.P / G;
+  for (int r = 0; r < R; ++r) {
+    const double* Xr = &L.X[size_t(L.orbit[size_t(r) * G]) * L.H];
+    for (int g = 1; g < G; ++g) {
+      const double* Xg = &L.X[size_t(L.orbit[size_t(r) * G + g]) * L.H];
+      for (int h = 0; h < L.H; ++h) {
+        const double chi = (__builtin_popcount(unsigned(g) & unsigned(L.hclass[h])) & 1) ? -1.0 : 1.0;
+        dmax = std::max(dmax, std::abs(Xg[h] - chi * Xr[h]));
+      }
+    }
+  }
+  L.sym_defect = xmax > 0 ? dmax / xmax : 0.0;
 }
 
 std::vector<std::vector<int>> partition_levels(const SphereTree& fine, int nlev, int rank, int world) {

@@ -73,10 +73,18 @@ struct LevelTables {
   int sym_axes[3] = {0, 0, 0};
   std::vector<int> orbit;             // [R][|G|] patch index of member g of orbit r (r = representative)
   std::vector<int> hclass;            // [H] parity class of each harmonic under the symmetric axes
+  // max_{r,g,h} |X[orbit(r,g)][h] - chi_h(g) X[orbit(r,0)][h]| / max|X|: how far the
+  // coupling table is from the exact reflection identity the fold relies on
+  double sym_defect = 0.0;
 };
 
+// The folded scatter is used only when the coupling table satisfies the
+// reflection identity to this relative accuracy (the quadrature of build_couplings
+// is exact only up to its order; level-2 meshes miss it by ~2e-9).
+constexpr double kFoldMaxDefect = 1e-14;
+
 // Reflections (x, y, z) that map the leaf set onto itself; fills n_sym_axes,
-// sym_axes, orbit and hclass (an empty orbit table means no folding).
+// sym_axes, orbit, hclass and sym_defect (an empty orbit table means no folding).
 void find_symmetry(LevelTables& L, const SphereTree& tree);
 
 struct Problem {

@@ -23,9 +23,6 @@
 namespace stamg_b200 {
 namespace {
 
-#ifndef STAMG_SWEEP_NST
-#define STAMG_SWEEP_NST 6
-#endif
 #ifndef STAMG_SWEEP8_BREG
 #define STAMG_SWEEP8_BREG 1  // 8-direction kernel keeps B^-1 in registers (2 CTAs/SM); A/B: 82.5 % vs 79 %
 #endif
@@ -346,11 +343,13 @@ void launch_sweep(const SweepParams& p, cudaStream_t s) {
   if (p.g.n_groups == 0) return;
   if (p.g.nx < 8) throw std::invalid_argument("sweep: nx must be >= 8 on the B200 path");
   if (p.dirs == 8) {  // 8-direction groups, R = 32, traces across strips through the L2 scratch
-    if (p.g.nx < 32 + NST || p.g.ny < 32 || !p.top) throw std::invalid_argument("sweep: 8-direction groups need nx, ny >= 36");
+    if (p.g.nx < kSweep8MinNx || p.g.ny < kSweep8MinNy || !p.top)
+      throw std::invalid_argument("sweep: 8-direction groups need nx >= " + std::to_string(kSweep8MinNx) +
+                                  " and ny >= " + std::to_string(kSweep8MinNy));
     if (p.wl.nd > 0) {
       if (p.wl.R != 32) throw std::invalid_argument("sweep: wavefront layout strip height must be 32");
       if (p.xb > 1) {  // column blocks (plain sweep, wavefront layout, B^-1 in registers)
-        if (p.mode != 0 || p.base || !p.xflag || !p.xtrace || p.g.nx % p.xb || p.g.nx / p.xb < 32 + NST)
+        if (p.mode != 0 || p.base || !p.xflag || !p.xtrace || p.g.nx % p.xb || p.g.nx / p.xb < kSweep8MinNx)
           throw std::invalid_argument("sweep: column blocks need a plain sweep and nx / xb >= 38");
         if (p.xb_smemb) {  // B^-1 in shared memory: 4 CTAs per SM (more blocks co-resident)
           if (p.g.n_mat > 1) launch_tb<8, 32, true, false, true, true, 0, false, true>(p, s);

@@ -63,9 +63,13 @@ class _Problem(C.Structure):
                 ("nu_post", C.c_int), ("coarse_sweeps", C.c_int), ("coarse_tol", C.c_double)]
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, dp, C.c_int64)
+
+
 class _Options(C.Structure):
     _fields_ = [("device", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("nccl_id", C.c_void_p),
-                ("build_hierarchy", C.c_int)]
+                ("build_hierarchy", C.c_int), ("allreduce", ALLREDUCE_FN), ("allreduce_user", C.c_void_p),
+                ("shard_probe", C.c_int)]
 
 
 class Report(C.Structure):
@@ -155,7 +159,11 @@ class Context:
     (ProblemOperators / SweepPlan / MgHierarchy of the reference)."""
 
     def __init__(self, spec: ProblemSpec, device: int = 0, build_hierarchy: bool = True, rank: int = 0,
-                 world: int = 1, nccl_id: bytes | None = None):
+                 world: int = 1, nccl_id: bytes | None = None, allreduce=None, shard_probe: bool = False):
+        """world > 1 takes exactly one of: ``nccl_id`` (NCCL, one GPU per rank),
+        ``allreduce`` (a host collective ``f(buf: np.ndarray) -> None`` summing
+        ``buf`` in place across ranks, stamg_allreduce_fn) or ``shard_probe``
+        (timing only: collectives skipped, partial sums)."""
         self.spec = spec
         self.h = None
         self._vecs = weakref.WeakSet()
@@ -171,8 +179,21 @@ class Context:
                       spec.y0, spec.y1, spec.nr, spec.n_levels, spec.nu_pre, spec.nu_post, spec.coarse_sweeps,
                       spec.coarse_tol)
         self._nccl_buf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        self._allreduce_cb = None
+        if allreduce is not None:
+            def _cb(user, buf, n, _f=allreduce):
+                try:
+                    _f(np.ctypeslib.as_array(buf, shape=(n,)))
+                    return 0
+                except Exception:  # noqa: BLE001 - reported to the library as a failed collective
+                    import traceback
+                    traceback.print_exc()
+                    return 1
+            self._allreduce_cb = ALLREDUCE_FN(_cb)
         opt = _Options(device, rank, world, C.cast(self._nccl_buf, C.c_void_p) if self._nccl_buf else None,
-                       1 if build_hierarchy else 0)
+                       1 if build_hierarchy else 0,
+                       self._allreduce_cb if self._allreduce_cb is not None else ALLREDUCE_FN(), None,
+                       1 if shard_probe else 0)
         h = C.c_void_p()
         _check(lib().stamg_create(C.byref(pr), C.byref(opt), C.byref(h)))
         self.h = h

@@ -1,5 +1,5 @@
 """Sweep of one rank's direction slice (config 5 sharded over N GPUs, rank r alone on
-one GPU, no communicator: STAMG_SHARD_PROBE). With fewer 8-direction groups than SMs
+one GPU, no communicator: the shard_probe option). With fewer 8-direction groups than SMs
 the sweep splits every group's grid into two column blocks (sweep_kernel XBLK: the
 upwind block publishes each strip's edge x-traces, the downwind block waits for
 them); the result must be bitwise the one-block sweep and must invert apply_L."""
@@ -17,11 +17,10 @@ def rnd(n, seed):
 
 @pytest.mark.parametrize("world,rank,n", [(8, 0, 128), (8, 5, 128), (8, 3, 96), (4, 1, 96)])
 def test_column_blocks_bitwise(stamg, monkeypatch, world, rank, n):
-    monkeypatch.setenv("STAMG_SHARD_PROBE", "1")
     spec = cf.baseline_config(5, n)
-    g = stamg.Context(spec, build_hierarchy=False, rank=rank, world=world)
+    g = stamg.Context(spec, build_hierarchy=False, rank=rank, world=world, shard_probe=True)
     monkeypatch.setenv("STAMG_SWEEP_XBLOCKS", "0")
-    g1 = stamg.Context(spec, build_hierarchy=False, rank=rank, world=world)
+    g1 = stamg.Context(spec, build_hierarchy=False, rank=rank, world=world, shard_probe=True)
     monkeypatch.delenv("STAMG_SWEEP_XBLOCKS")
     x = rnd(g.vec().n, 11 + rank)
     z, z1 = g.vec(), g1.vec()
@@ -47,8 +46,7 @@ def test_sharded_folded_scatter(stamg, monkeypatch, world, rank):
     unsharded operator applied to the vector restricted to those directions."""
     spec = cf.baseline_config(5, 64)
     g1 = stamg.Context(spec, build_hierarchy=False)
-    monkeypatch.setenv("STAMG_SHARD_PROBE", "1")
-    gr = stamg.Context(spec, build_hierarchy=False, rank=rank, world=world)
+    gr = stamg.Context(spec, build_hierarchy=False, rank=rank, world=world, shard_probe=True)
     assert int(gr.table("fold")[0]) == 8
     mine = stamg.shard_patches(spec, rank, world)
     n_el, P, S, _ = g1.layout()

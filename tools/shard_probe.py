@@ -1,7 +1,7 @@
 """Per-rank sweep time of config 5 when its 8192 directions are sharded over N
 GPUs, measured on one GPU: rank 0's slice (P/N directions, the contiguous leaf
 range the library gives it) swept alone, without a communicator
-(STAMG_SHARD_PROBE). The sweep has no collective, so a rank's device time is
+(stamg_options.shard_probe). The sweep has no collective, so a rank's device time is
 the N-GPU job's time; speed-up = t(1) / t(N).
 
     python tools/shard_probe.py [N ...]      (default 1 2 4 8)
@@ -13,7 +13,6 @@ import time
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["STAMG_SHARD_PROBE"] = "1"
 from paper_2010_04559_b200 import configs as cf  # noqa: E402
 from paper_2010_04559_b200 import stamg  # noqa: E402
 
@@ -23,7 +22,7 @@ def main():
     spec = cf.baseline_config(5, int(os.environ.get("C5N", "512")))
     out, t1 = {}, None
     for n in ns:
-        g = stamg.Context(spec, build_hierarchy=False, rank=0, world=n)
+        g = stamg.Context(spec, build_hierarchy=False, rank=0, world=n, shard_probe=n > 1)
         n_el, P, _, _ = g.layout()
         psi = g.vec().fill(1.0)
         for _ in range(3):
