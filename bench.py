@@ -85,6 +85,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def fp64_peaks_with_clocks(g, local):
+    """The DMMA / DFMA throughput probes (FP64 roofline denominators: not in
+    MEASURED_PEAKS.json) with the SM clocks sampled while they run."""
+    with ClockSampler(local) as clk:
+        dmma, dfma = g.fp64_peaks()
+        dmma2, dfma2 = g.fp64_peaks()  # >= 2 samples of the clock inside the probe window
+    return max(dmma, dmma2), max(dfma, dfma2), clk.summary()
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -343,7 +352,7 @@ def run_b200(args, world, rank, local, dist):
         gemm_flop = 2.0 * H * P_local * 4 * n_el * args.si_iters  # per contraction, all iterations (algorithmic)
         fold_g = max(1, int(g.table("fold")[0]))  # reflection-symmetry fold: executed = algorithmic / |G|
         exe_flop = gemm_flop / fold_g
-        dmma_peak, dfma_peak = g.fp64_peaks()
+        dmma_peak, dfma_peak, probe_clk = fp64_peaks_with_clocks(g, local)
         extras["source_iteration"] = {
             "value": total_upd * args.si_iters / si_wall, "unit": UNIT, "iterations": args.si_iters,
             "ms_per_iter": si_wall / args.si_iters * 1e3,
@@ -353,6 +362,7 @@ def run_b200(args, world, rank, local, dist):
                               "d2m_achieved": exe_flop / (d2m_ms * 1e-3) * 1e-12,
                               "m2d_achieved": exe_flop / (m2d_ms * 1e-3) * 1e-12,
                               "peak": dmma_peak, "peak_kind": "measured DMMA m8n8k4 probe on this GPU",
+                              "peak_probe_clocks": probe_clk,
                               "dfma_peak": dfma_peak,
                               "frac": (2 * exe_flop / ((d2m_ms + m2d_ms) * 1e-3) * 1e-12) / dmma_peak,
                               "achieved_basis": "executed flops (algorithmic / fold group size)",
@@ -381,10 +391,12 @@ def run_b200(args, world, rank, local, dist):
                "api": "stamg_sweep_host (include/stamg_b200.h), pinned host buffers",
                "pipeline_chunks": g.host_pipeline_chunks()}
         stamg.host_free(host)
-    dmma_peak, _ = g.fp64_peaks()
+    dmma_peak, _, probe_clk = fp64_peaks_with_clocks(g, local)
     g.close()
     if not args.no_kernels and world == 1:
         extras["kernels"] = kernel_rooflines(stamg, cf, dmma_peak)
+        extras["kernels"]["dmma_peak_tflops"] = dmma_peak
+        extras["kernels"]["dmma_peak_probe_clocks"] = probe_clk
     # ---- extra: GMRES + AMG solve wall time to 1e-8 from a device-resident b
     # (directions sharded over the ranks, coarsest MG level replicated)
     if not args.no_solve:
@@ -401,8 +413,8 @@ def run_b200(args, world, rank, local, dist):
             t0 = time.perf_counter()
             x, rep = gs.solve(b, "gmres", "mg")
             gs.synchronize()
-            wall = allmax(dist, time.perf_counter() - t0)
-            solves[f"c{k}"] = {"wall_s": wall, "setup_s": setup, "iterations": rep["iterations"],
+            solve_wall = allmax(dist, time.perf_counter() - t0)
+            solves[f"c{k}"] = {"wall_s": solve_wall, "setup_s": setup, "iterations": rep["iterations"],
                                "final_residual": rep["final_residual"], "converged": rep["converged"],
                                "method": "GMRES(%d) right-preconditioned by one V(1,1) angular MG cycle" % sp.restart}
             # where the time goes: the same solve once more with per-launch CUDA events
@@ -471,8 +483,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--no-kernels", action="store_true", help="skip the per-kernel roofline section (config 4)")
-    ap.add_argument("--cpu-solve-configs", type=int, nargs="*", default=[1],
-                    help="also time these solves on the CPU oracle (rank 0, N=1); c2 takes ~80 s on 8 cores")
+    ap.add_argument("--cpu-solve-configs", type=int, nargs="*", default=[1, 2],
+                    help="also time these solves on the CPU oracle (rank 0, N=1); c2 takes ~100 s on 8 cores")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -19,3 +19,19 @@ psi = h.vec().fill(1.0)
 h.source_iteration(psi, 1)
 g.synchronize(); h.synchronize()
 print("sanitize run ok", rep["iterations"])
+# coarse GS in its clustered multi-warp row kernel (DSMEM mailboxes, spin flags): c2 physics at 32^2
+c2 = cf.baseline_config(2, 32)
+g2 = stamg.Context(c2)
+print("c2 32^2 coarse GS mode [mw, cluster, rows, slots, credit]:", g2.table("gs_mode", 0)[:5].tolist())
+f0 = g2.vec(0).fill(1e-3)
+phi0 = g2.vec(0)
+g2.coarse_scatter_sweep(f0, 2, phi0, level=0)
+g2.synchronize()
+# sweep with two column blocks per group (XBLK: strip flags + L2 trace scratch): rank 0 of 8, 80^2
+c5 = cf.baseline_config(5, 80)
+g5 = stamg.Context(c5, build_hierarchy=False, rank=0, world=8, shard_probe=True)
+v5 = g5.vec().fill(1.0)
+g5.standard_sweep(v5, v5)
+g5.standard_sweep(v5, v5)
+g5.synchronize()
+print("sanitize run (coarse GS cluster + XBLK sweep) ok")
