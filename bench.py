@@ -326,10 +326,11 @@ def run_b200(args, world, rank, local, dist):
     achieved = upd_local * BYTES_PER_UPDATE / (sweep_ms * 1e-3 / max(sweep_n, 1)) / 1e9
     traffic = None
     try:
-        # ncu --set full capture (profiles/sweep_ncu_traffic.json): dram read+write per launch
-        # at 128^2 cells x 8192 directions, scaled by its ratio to the algorithmic bytes
-        with open(os.path.join(ROOT, "profiles", "sweep_ncu_traffic.json")) as f:
-            traffic = json.load(f)["traffic_over_algorithmic"] * upd_local * BYTES_PER_UPDATE
+        # ncu --set full capture of this exact launch (config 5 at full size, one GPU):
+        # dram__bytes_read.sum + dram__bytes_write.sum per launch (profiles/r02_sweep_c5_ncu_traffic.json)
+        if world == 1 and args.n is None:
+            with open(os.path.join(ROOT, "profiles", "r02_sweep_c5_ncu_traffic.json")) as f:
+                traffic = json.load(f)["dram_bytes_per_launch"]
     except Exception:
         pass
     extras = {}
@@ -460,7 +461,8 @@ def run_b200(args, world, rank, local, dist):
                            "l2": f"input {spec.n_el * P_local * world * 4 * 8 / 2**30:.1f} GiB >> 126 MB L2 (no flush needed)", "wall_s": wall,
                            "setup_s": setup_s},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                             "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                             "frac": achieved / hbm, "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram read + write)",
+                             "algorithmic_bytes_per_launch": upd_local * BYTES_PER_UPDATE, "peak_kind": peak_kind,
                              "kernel": "sweep_kernel", "bytes_per_update": BYTES_PER_UPDATE},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}
         line.update(extras)

@@ -73,6 +73,7 @@ struct Nccl {
   int (*commInitRank)(void**, int, const void*, int) = nullptr;
   int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*commDestroy)(void*) = nullptr;
+  int (*commSplit)(void*, int, int, void**, void*) = nullptr;  // ncclCommSplit (NCCL >= 2.18), optional
   bool load() {
     if (h) return true;
     for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
@@ -84,6 +85,7 @@ struct Nccl {
     commInitRank = reinterpret_cast<int (*)(void**, int, const void*, int)>(dlsym(h, "ncclCommInitRank"));
     allReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(dlsym(h, "ncclAllReduce"));
     commDestroy = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommDestroy"));
+    commSplit = reinterpret_cast<int (*)(void*, int, int, void**, void*)>(dlsym(h, "ncclCommSplit"));
     return getUniqueId && commInitRank && allReduce && commDestroy;
   }
 };
@@ -170,12 +172,26 @@ struct stamg_ctx {
   std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   std::map<std::string, std::pair<double, int64_t>> timed;
   void* comm = nullptr;
+  // scatter-moment allreduce overlapped with the GEMMs: a second communicator (split from
+  // comm) driven from its own stream, per-chunk events
+  void* comm_ar = nullptr;
+  cudaStream_t ar_stream = nullptr;
+  std::vector<cudaEvent_t> ev_d2m, ev_ar;
+  int ar_chunks_used = 0;
   // host collective (stamg_options.allreduce) and its pinned staging buffer
   stamg_allreduce_fn host_allreduce = nullptr;
   void* host_allreduce_user = nullptr;
   double* coll_host = nullptr;
   int64_t coll_host_n = 0;
   bool shard_probe = false;
+  // CUDA graphs of mg_apply (one per (r, z) pair; the V-cycle is device-only)
+  struct MgGraph {
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;
+  };
+  std::map<std::pair<const double*, double*>, MgGraph> mg_graphs;
+  bool mg_warm = false, graphs_off = false;
+  int64_t graph_replays = 0;
 };
 
 struct stamg_vec {
@@ -470,10 +486,11 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
   // exactness: the coupling table must satisfy the reflection identity (sym_defect, measured
   // in find_symmetry; config 1's level-2 mesh misses it by 2.2e-9 and never folds).
   // size: orbit classes of >= 64 patches (smaller class GEMMs do not pay for the two
-  // streaming passes). sharded: throughput contexts, whose shards are whole orbits; the
-  // folded moments are allreduced
+  // streaming passes). sharded levels fold when the rank's patch set is closed under the
+  // reflections (throughput shards and orbit-partitioned hierarchies are; find_symmetry
+  // checks closure among the rank's own patches); the folded moments are allreduced
   const bool fold_exact = t.n_sym_axes > 0 && t.sym_defect <= kFoldMaxDefect;
-  if (fold_exact && t.H >= fold_min_h && (c->world == 1 || c->wl_allowed) && (t.P >> t.n_sym_axes) >= 64) {
+  if (fold_exact && t.H >= fold_min_h && (t.P >> t.n_sym_axes) >= 64) {
     const int G = 1 << t.n_sym_axes, R = t.P / G;
     L.fold_G = G, L.fold_R = R, L.fold_Rp = round_up(R, 64);
     const int Rk = round_up(R, 32);
@@ -587,34 +604,103 @@ void op_d2m(stamg_ctx* c, DevLevel& L, const double* phi, int order, double* out
   c->launches += 1;
 }
 
-void op_m2d(stamg_ctx* c, DevLevel& L, int order, double scale, double beta, double* y, const double* ext) {
-  Timed tm(c, "m2d");
-  M2DParams p;
-  p.wl = L.wl;
-  p.src = L.src, p.y = y, p.XT = L.XT, p.n_el = L.t.n_el, p.P = L.t.P, p.Pp = L.Pp, p.Hp = L.Hp;
-  p.Hused = (order + 1) * (order + 1), p.scale = scale, p.beta = beta, p.ext_q = ext, p.area = L.area;
-  for (int i = 0; i < 4; ++i) p.nsum[i] = c->nsum[i];
-  launch_m2d(p, c->stream);
-  ck_launch("m2d");
-  c->launches += 1;
+
+// element-range chunks of a sharded scatter: D2M of chunk k+1 overlaps the moment
+// allreduce of chunk k, which overlaps the M2D of chunk k-1 (STAMG_AR_CHUNKS overrides;
+// one chunk for unsharded levels, the shard probe, or without a second communicator)
+int scatter_chunks(stamg_ctx* c, const DevLevel& L) {
+  if (!L.sharded || c->world <= 1 || c->shard_probe) return 1;
+  int k = c->comm_ar ? 8 : 1;
+  if (const char* e = std::getenv("STAMG_AR_CHUNKS")) k = std::max(1, std::atoi(e));
+  if (!c->comm_ar && !c->host_allreduce) k = 1;
+  return std::max(1, std::min({k, 64, L.t.n_el}));
+}
+
+void ensure_ar_events(stamg_ctx* c, int k) {
+  while (int(c->ev_d2m.size()) < k) {
+    cudaEvent_t a, b;
+    ck(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "event");
+    c->ev_d2m.push_back(a), c->ev_ar.push_back(b);
+  }
+}
+
+// allreduce of one moment chunk on the comm stream (second communicator), after the
+// chunk's D2M; the chunk's M2D waits for ev_ar[k]
+void allreduce_chunk_async(stamg_ctx* c, double* buf, size_t n, int k) {
+  ck(cudaEventRecord(c->ev_d2m[k], c->stream), "event");
+  ck(cudaStreamWaitEvent(c->ar_stream, c->ev_d2m[k], 0), "wait");
+  const int ncclDouble = 8, ncclSum = 0;
+  if (nccl().allReduce(buf, buf, n, ncclDouble, ncclSum, c->comm_ar, c->ar_stream) != 0)
+    throw NcclError("ncclAllReduce (moment chunk) failed");
+  ck(cudaEventRecord(c->ev_ar[k], c->ar_stream), "event");
 }
 
 // y = beta*y + scale * S_order phi (+ isotropic source): apply_scatter_into
 // (scatter.cpp:110-135) as D2M -> [allreduce] -> M2D. With a reflection
 // symmetry group G the patches are folded over their orbits (Walsh-Hadamard),
 // each harmonic parity class is one GEMM with K = P/|G|, and the result is
-// unfolded: the same algebra with |G| times fewer flops.
+// unfolded: the same algebra with |G| times fewer flops. Sharded levels run
+// element-range chunks so the moment allreduce overlaps the GEMMs.
 void scatter_into(stamg_ctx* c, DevLevel& L, const double* phi, int order, double scale, double beta, double* y,
                   const double* ext) {
   if (order > L.t.order) throw std::invalid_argument("sigma_by_harmonic: max_order exceeds kernel order");
   const int Hu = (order + 1) * (order + 1);
+  const int n_el = L.t.n_el;
+  const int K = scatter_chunks(c, L);
+  c->ar_chunks_used = K;
+  const bool async_ar = K > 1 && c->comm_ar != nullptr;
+  if (async_ar) ensure_ar_events(c, K);
+  auto chunk = [&](int k, int& e0, int& e1) {
+    e0 = int(int64_t(n_el) * k / K), e1 = int(int64_t(n_el) * (k + 1) / K);
+  };
+  const size_t Hrow = L.fold_G == 0 ? size_t(L.Hp) : size_t(L.fold_Hf);  // src row pitch
+  // moments of chunk k: after its D2M, before its M2D
+  auto reduce_chunk = [&](int k, bool issue) {
+    if (!L.sharded) return;
+    int e0, e1;
+    chunk(k, e0, e1);
+    double* buf = L.src + size_t(e0) * Hrow * 4;
+    const size_t n = size_t(e1 - e0) * Hrow * 4;
+    if (async_ar) {
+      if (issue) allreduce_chunk_async(c, buf, n, k);
+      else ck(cudaStreamWaitEvent(c->stream, c->ev_ar[k], 0), "wait");
+    } else if (!issue) {
+      op_allreduce(c, buf, n);
+    }
+  };
   if (L.fold_G == 0) {
-    op_d2m(c, L, phi, order, L.src, L.sig, false);
-    if (L.sharded) op_allreduce(c, L.src, size_t(L.t.n_el) * L.Hp * 4);
-    op_m2d(c, L, order, scale, beta, y, ext);
+    for (int k = 0; k < K; ++k) {
+      int e0, e1;
+      chunk(k, e0, e1);
+      Timed tm(c, "d2m");
+      D2MParams p;
+      p.wl = L.wl;
+      p.phi = phi, p.src = L.src, p.X = L.X, p.sig = L.sig, p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
+      p.n_el = e1 - e0, p.el_base = e0, p.P = L.t.P, p.Hp = L.Hp, p.Hused = Hu, p.Hrows = L.Hp;
+      for (int i = 0; i < 16; ++i) p.N[i] = L.t.Nmat[i];
+      launch_d2m(p, c->stream);
+      ck_launch("d2m");
+      c->launches += 1;
+      reduce_chunk(k, true);
+    }
+    for (int k = 0; k < K; ++k) {
+      int e0, e1;
+      chunk(k, e0, e1);
+      reduce_chunk(k, false);
+      Timed tm(c, "m2d");
+      M2DParams p;
+      p.wl = L.wl;
+      p.src = L.src, p.y = y, p.XT = L.XT, p.n_el = e1 - e0, p.el_base = e0, p.P = L.t.P, p.Pp = L.Pp, p.Hp = L.Hp;
+      p.Hused = Hu, p.scale = scale, p.beta = beta, p.ext_q = ext, p.area = L.area;
+      for (int i = 0; i < 4; ++i) p.nsum[i] = c->nsum[i];
+      launch_m2d(p, c->stream);
+      ck_launch("m2d");
+      c->launches += 1;
+    }
     return;
   }
-  const int G = L.fold_G, R = L.fold_R, n_el = L.t.n_el;
+  const int G = L.fold_G, R = L.fold_R;
   // one fold workspace per context, shared by the levels (used only inside this call)
   const int64_t need = int64_t(n_el) * L.t.P * 4;
   if (c->foldbuf_n < need) {
@@ -624,49 +710,59 @@ void scatter_into(stamg_ctx* c, DevLevel& L, const double* phi, int order, doubl
   }
   double* const fb = c->foldbuf;
   const size_t cls = size_t(n_el) * R * 4;
-  {
-    Timed tm(c, "fold");
-    launch_fold(phi, fb, L.orbit, n_el, L.t.P, R, G, L.wl, c->stream);
-    ck_launch("fold");
-    c->launches += 1;
-  }
   std::vector<int> hu(G, 0);
   for (int cl = 0; cl < G; ++cl)
     for (int h : L.fold_hs[cl]) hu[cl] += h < Hu ? 1 : 0;
-  for (int cl = 0; cl < G; ++cl) {
-    if (hu[cl] == 0) continue;
-    Timed tm(c, "d2m");
-    D2MParams p;
-    p.phi = fb + cl * cls, p.src = L.src + size_t(L.fold_hoff[cl]) * 4, p.X = L.Xf + L.fold_hoff[cl];
-    p.sig = L.sigf + L.fold_hoff[cl], p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
-    p.n_el = n_el, p.P = R, p.Hp = L.fold_Hf, p.Hused = hu[cl], p.Hrows = L.fold_hoff[cl + 1] - L.fold_hoff[cl];
-    for (int k = 0; k < 16; ++k) p.N[k] = L.t.Nmat[k];
-    launch_d2m(p, c->stream);
-    ck_launch("d2m");
-    c->launches += 1;
-  }
-  if (L.sharded) op_allreduce(c, L.src, size_t(n_el) * L.fold_Hf * 4);
-  for (int cl = 0; cl < G; ++cl) {
-    double* Yc = fb + cl * cls;
-    if (hu[cl] == 0) {
-      launch_fill(Yc, 0.0, int64_t(cls), c->stream);
+  for (int k = 0; k < K; ++k) {
+    int e0, e1;
+    chunk(k, e0, e1);
+    {
+      Timed tm(c, "fold");
+      launch_fold(phi, fb, L.orbit, n_el, e0, e1, L.t.P, R, G, L.wl, c->stream);
+      ck_launch("fold");
       c->launches += 1;
-      continue;
     }
-    Timed tm(c, "m2d");
-    M2DParams p;
-    p.src = L.src + size_t(L.fold_hoff[cl]) * 4, p.y = Yc, p.XT = L.XfT + size_t(L.fold_hoff[cl]) * L.fold_Rp;
-    p.n_el = n_el, p.P = R, p.Pp = L.fold_Rp, p.Hp = L.fold_Hf, p.Hused = hu[cl];
-    p.scale = 1.0, p.beta = 0.0, p.ext_q = nullptr, p.area = L.area;
-    for (int i = 0; i < 4; ++i) p.nsum[i] = c->nsum[i];
-    launch_m2d(p, c->stream);
-    ck_launch("m2d");
+    for (int cl = 0; cl < G; ++cl) {
+      if (hu[cl] == 0) continue;
+      Timed tm(c, "d2m");
+      D2MParams p;
+      p.phi = fb + cl * cls, p.src = L.src + size_t(L.fold_hoff[cl]) * 4, p.X = L.Xf + L.fold_hoff[cl];
+      p.sig = L.sigf + L.fold_hoff[cl], p.mat = L.t.n_mat > 1 ? c->mat : nullptr;
+      p.n_el = e1 - e0, p.el_base = e0, p.P = R, p.Hp = L.fold_Hf, p.Hused = hu[cl];
+      p.Hrows = L.fold_hoff[cl + 1] - L.fold_hoff[cl];
+      for (int i = 0; i < 16; ++i) p.N[i] = L.t.Nmat[i];
+      launch_d2m(p, c->stream);
+      ck_launch("d2m");
+      c->launches += 1;
+    }
+    reduce_chunk(k, true);
+  }
+  for (int k = 0; k < K; ++k) {
+    int e0, e1;
+    chunk(k, e0, e1);
+    reduce_chunk(k, false);
+    for (int cl = 0; cl < G; ++cl) {
+      double* Yc = fb + cl * cls;
+      if (hu[cl] == 0) {
+        launch_fill(Yc + size_t(e0) * R * 4, 0.0, int64_t(e1 - e0) * R * 4, c->stream);
+        c->launches += 1;
+        continue;
+      }
+      Timed tm(c, "m2d");
+      M2DParams p;
+      p.src = L.src + size_t(L.fold_hoff[cl]) * 4, p.y = Yc, p.XT = L.XfT + size_t(L.fold_hoff[cl]) * L.fold_Rp;
+      p.n_el = e1 - e0, p.el_base = e0, p.P = R, p.Pp = L.fold_Rp, p.Hp = L.fold_Hf, p.Hused = hu[cl];
+      p.scale = 1.0, p.beta = 0.0, p.ext_q = nullptr, p.area = L.area;
+      for (int i = 0; i < 4; ++i) p.nsum[i] = c->nsum[i];
+      launch_m2d(p, c->stream);
+      ck_launch("m2d");
+      c->launches += 1;
+    }
+    Timed tm(c, "unfold");
+    launch_unfold(fb, y, L.orbit, n_el, e0, e1, L.t.P, R, G, scale, beta, ext, L.area, c->nsum, L.wl, c->stream);
+    ck_launch("unfold");
     c->launches += 1;
   }
-  Timed tm(c, "unfold");
-  launch_unfold(fb, y, L.orbit, n_el, L.t.P, R, G, scale, beta, ext, L.area, c->nsum, L.wl, c->stream);
-  ck_launch("unfold");
-  c->launches += 1;
 }
 
 void op_scatter(stamg_ctx* c, DevLevel& L, const double* phi, int order, double scale, double* y) {
@@ -804,6 +900,60 @@ void op_mg_apply(stamg_ctx* c, const double* r, double* z) {
   op_vcycle(c, top, r, z);
 }
 
+// mg_apply through a CUDA graph: the V-cycle is a fixed sequence of
+// ~10-100 launches with no host round trip (coarse_tol = 0, one rank), so after one eager
+// call (which allocates the level workspaces) it is captured once per (r, z) pair and
+// replayed. Timing mode (per-launch events), host collectives and the coarse_tol loop
+// (host dot products) stay eager; STAMG_GRAPHS=0 disables graphs. A capture the driver
+// rejects turns graphs off for the context and runs eagerly.
+void op_mg_apply_graph(stamg_ctx* c, const double* r, double* z) {
+  const bool ok = !c->graphs_off && c->world == 1 && c->pb.spec.coarse_tol <= 0 && !c->timing &&
+                  !env_is_zero("STAMG_GRAPHS");
+  if (!ok || !c->mg_warm) {
+    op_mg_apply(c, r, z);
+    c->mg_warm = true;
+    return;
+  }
+  const auto key = std::make_pair(r, z);
+  auto it = c->mg_graphs.find(key);
+  if (it == c->mg_graphs.end()) {
+    if (c->mg_graphs.size() >= 64) {  // bounded cache (ABI callers may pass many vectors)
+      for (auto& kv : c->mg_graphs) cudaGraphExecDestroy(kv.second.exec);
+      c->mg_graphs.clear();
+    }
+    const int64_t l0 = c->launches;
+    cudaGraph_t graph = nullptr;
+    ck(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+      op_mg_apply(c, r, z);
+    } catch (...) {
+      cudaStreamEndCapture(c->stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      c->launches = l0;
+      c->graphs_off = true;
+      op_mg_apply(c, r, z);
+      return;
+    }
+    const cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+    stamg_ctx::MgGraph mg;
+    mg.launches = c->launches - l0;
+    c->launches = l0;
+    if (e != cudaSuccess || !graph || cudaGraphInstantiate(&mg.exec, graph, 0) != cudaSuccess) {
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      c->graphs_off = true;
+      op_mg_apply(c, r, z);
+      return;
+    }
+    cudaGraphDestroy(graph);
+    it = c->mg_graphs.emplace(key, mg).first;
+  }
+  ck(cudaGraphLaunch(it->second.exec, c->stream), "graph launch");
+  c->launches += it->second.launches;
+  c->graph_replays += 1;
+}
+
 // --------------------------------------------------------------- BLAS helpers
 void ensure_krylov(stamg_ctx* c, int restart) {
   if (c->restart_alloc >= restart) return;
@@ -858,7 +1008,7 @@ void upload_coef(stamg_ctx* c, const double* host, int k) {
 
 void apply_precond(stamg_ctx* c, int precond, const double* v, double* z) {
   if (precond == 0) op_sweep(c, c->outer, v, z);
-  else if (precond == 1) op_mg_apply(c, v, z);
+  else if (precond == 1) op_mg_apply_graph(c, v, z);
   else {
     ck(cudaMemcpyAsync(z, v, c->outer.n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream), "copy");
   }
@@ -1183,6 +1333,13 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
       // ncclCommInitRank(comm*, nranks, ncclUniqueId (by value), rank)
       auto init = reinterpret_cast<int (*)(void**, int, UniqueId, int)>(nccl().commInitRank);
       if (init(&c->comm, c->world, uid, c->rank) != 0) throw NcclError("ncclCommInitRank failed");
+      // second communicator for the chunked moment allreduce on its own stream (the dot
+      // products stay on the first, ordered on the compute stream); without ncclCommSplit
+      // the scatter allreduce stays one unchunked call on the compute stream
+      if (nccl().commSplit && !env_is_zero("STAMG_AR_OVERLAP")) {
+        if (nccl().commSplit(c->comm, 0, c->rank, &c->comm_ar, nullptr) != 0) c->comm_ar = nullptr;
+        if (c->comm_ar) ck(cudaStreamCreateWithFlags(&c->ar_stream, cudaStreamNonBlocking), "stream");
+      }
     }
     const auto& s = c->pb.spec;
     c->tree = make_sphere(s.angular_kind, s.angular_level, s.cone_levels, s.cone_half_angle_deg);
@@ -1237,7 +1394,12 @@ int stamg_destroy(stamg_ctx* c) {
       if (e) cudaEventDestroy(e);
     if (c->io_h2d) cudaStreamDestroy(c->io_h2d);
     if (c->io_d2h) cudaStreamDestroy(c->io_d2h);
+    if (c->comm_ar) nccl().commDestroy(c->comm_ar);
     if (c->comm) nccl().commDestroy(c->comm);
+    if (c->ar_stream) cudaStreamDestroy(c->ar_stream);
+    for (cudaEvent_t e : c->ev_d2m) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_ar) cudaEventDestroy(e);
+    for (auto& kv : c->mg_graphs) cudaGraphExecDestroy(kv.second.exec);
     cudaStreamDestroy(c->stream);
     delete c;
   });
@@ -1456,7 +1618,7 @@ int stamg_mg_apply(stamg_ctx* c, const stamg_vec* r, stamg_vec* z) {
     if (!c->have_mg) throw std::invalid_argument("multigrid hierarchy was not built for this context");
     need(r, c->mg.back(), "mg_apply"), need(z, c->mg.back(), "mg_apply");
     if (r->d == z->d) throw std::invalid_argument("mg_apply: z must not alias r");
-    op_mg_apply(c, r->d, z->d);
+    op_mg_apply_graph(c, r->d, z->d);
   });
 }
 int stamg_rhs(stamg_ctx* c, stamg_vec* f) {
@@ -1665,6 +1827,8 @@ int stamg_get_table(stamg_ctx* c, int level, const char* name, double* out, int6
     std::vector<double> v;
     const std::string nm(name);
     if (nm == "fold") v = {double(L.fold_G), double(L.fold_R), double(L.fold_Hf), t.sym_defect, double(t.n_sym_axes)};
+    else if (nm == "ar_chunks") v = {double(c->ar_chunks_used), double(c->comm_ar != nullptr)};
+    else if (nm == "graphs") v = {double(c->mg_graphs.size()), double(c->graph_replays), double(c->graphs_off)};
     else if (nm == "gs_mode")
       v = {double(L.gs_mw), double(L.gs_cluster), double(L.gs_rows), double(L.gs_mb_slots), double(L.gs_mb_credit)};
     else if (nm == "X") v = t.X;

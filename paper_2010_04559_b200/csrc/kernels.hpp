@@ -79,7 +79,8 @@ struct D2MParams {
   const double* X = nullptr;     // [Pk][Hp]   (rows >= P are zero)
   const double* sig = nullptr;   // [n_mat][Hp]
   const int* mat = nullptr;
-  int n_el = 0, P = 0, Hp = 0, Hused = 0;
+  int n_el = 0, P = 0, Hp = 0, Hused = 0;  // n_el: elements of this call, [el_base, el_base + n_el)
+  int el_base = 0;               // first element (element-range chunks of the scatter; global indexing)
   int Hrows = 0;                 // rows of src this call may write (its region; >= Hused)
   double N[16];
 };
@@ -94,7 +95,8 @@ struct M2DParams {
   const double* src = nullptr;   // [n_el][Hp][4]
   double* y = nullptr;
   const double* XT = nullptr;    // [Hp][Pp]
-  int n_el = 0, P = 0, Pp = 0, Hp = 0, Hused = 0;
+  int n_el = 0, P = 0, Pp = 0, Hp = 0, Hused = 0;  // n_el: elements of this call, [el_base, el_base + n_el)
+  int el_base = 0;
   double scale = 1.0, beta = 1.0;
   const double* ext_q = nullptr;  // [n_el] isotropic source density or nullptr
   const double* area = nullptr;   // [P]
@@ -105,11 +107,12 @@ void launch_m2d(const M2DParams& p, cudaStream_t s);
 // reflection-symmetry fold / unfold around the per-class moment GEMMs:
 // Phi[c][el][r][i] = sum_g chi_c(g) phi[el][orbit[r][g]][i];
 // y[el][orbit[r][g]][i] = beta*y + scale*sum_c chi_c(g) Y[c][el][r][i] (+ isotropic source)
-void launch_fold(const double* phi, double* Phi, const int* orbit, int n_el, int P, int R, int G, const WLGeom& wl,
-                 cudaStream_t s);
-void launch_unfold(const double* Y, double* y, const int* orbit, int n_el, int P, int R, int G, double scale,
-                   double beta, const double* ext_q, const double* area, const double* nsum, const WLGeom& wl,
-                   cudaStream_t s);
+// over the elements [el0, el1) of n_el (Phi / Y class stride n_el * R * 4)
+void launch_fold(const double* phi, double* Phi, const int* orbit, int n_el, int el0, int el1, int P, int R, int G,
+                 const WLGeom& wl, cudaStream_t s);
+void launch_unfold(const double* Y, double* y, const int* orbit, int n_el, int el0, int el1, int P, int R, int G,
+                   double scale, double beta, const double* ext_q, const double* area, const double* nsum,
+                   const WLGeom& wl, cudaStream_t s);
 // reference layout [el][q][4] (patch q mapped to internal k = perm[q]) <-> wavefront layout,
 // for elements [el0, el0 + n_el_chunk)
 void launch_to_wl(const double* ref, double* wlv, const int* perm, int el0, int n_el_chunk, int P, const WLGeom& wl,

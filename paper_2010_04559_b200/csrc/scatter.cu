@@ -26,6 +26,9 @@ namespace {
 #ifndef STAMG_GEMM_NSTAGE
 #define STAMG_GEMM_NSTAGE 3
 #endif
+#ifndef STAMG_GEMM_TMA
+#define STAMG_GEMM_TMA 1  // 1: tiles staged by TMA bulk copies (cp.async.bulk + mbarrier); 0: cp.async (LDGSTS)
+#endif
 #ifndef STAMG_GEMM_SWAP
 #define STAMG_GEMM_SWAP 0  // 1: output-row tiles fastest in the grid (Phi / src panel reuse in L2)
 #endif
@@ -39,10 +42,14 @@ constexpr int kThreads = 128;
 // BN = 64 columns. The harmonic parity classes of the folded scatter have 153 /
 // 136 / 120 rows at N = 32: 64-row tiles pad them to 192 (71 % useful work);
 // 24-row warp strips cover them in one CTA tile of 168 / 144 / 120 rows.
+// B tile in shared memory: cp.async path [k][LDB] (k-major, padded); TMA path
+// [e][k][4] (element-major, the panel order of the reference layout, one bulk copy
+// per element; a fragment load covers 2 elements x 128 contiguous bytes: conflict free)
+constexpr int kStageB = STAMG_GEMM_TMA ? BN * BK : BK * LDB;
 template <int MI, int WM>
 struct RowTile {
   static constexpr int kBM = 8 * MI * WM, kLDA = kBM + 4, kThreads = 64 * WM;
-  static constexpr int kStage = BK * (kLDA + LDB);
+  static constexpr int kStage = BK * kLDA + kStageB;
 };
 
 // A tile: sA[k][m] = A_src[(k0+k) * lda + m0 + m]   (rows of k contiguous in m)
@@ -100,11 +107,55 @@ __device__ __forceinline__ void mma_stage(const double* sA, const double* sB, do
 #pragma unroll
     for (int i = 0; i < MI; ++i) a[i] = sA[(kk + t) * TLDA + wm * (8 * MI) + i * 8 + g];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) b[j] = sB[(kk + t) * LDB + wn * 32 + j * 8 + g];
+    for (int j = 0; j < 4; ++j) {
+      if constexpr (STAMG_GEMM_TMA) {
+        const int n = wn * 32 + j * 8 + g;  // column (e, i) = (n / 4, n % 4)
+        b[j] = sB[(n >> 2) * (BK * 4) + (kk + t) * 4 + (n & 3)];
+      } else {
+        b[j] = sB[(kk + t) * LDB + wn * 32 + j * 8 + g];
+      }
+    }
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+}
+
+// ---- TMA staging: warp 0 fills stage `kt % NSTAGE` with bulk copies that complete on
+// that stage's mbarrier (expect_tx set first by lane 0); every thread waits on the
+// barrier's phase parity (kt / NSTAGE) & 1. Stages are zeroed once at kernel start, so
+// the rows a tail tile does not copy hold finite values (multiplied by zero A rows).
+__device__ __forceinline__ void gemm_tma_init(double* smem, int stage_doubles, unsigned long long* bars, int tid,
+                                              int nthreads) {
+  for (int c = tid; c < NSTAGE * stage_doubles / 2; c += nthreads)
+    reinterpret_cast<double2*>(smem)[c] = make_double2(0.0, 0.0);
+  if (tid == 0)
+    for (int st = 0; st < NSTAGE; ++st) mbar_init_cta(bars + st, 1);
+  fence_proxy_async_smem();
+  __syncthreads();
+}
+
+// D2M stage: A = BK rows of X (TBM harmonics each, zero-padded to Pk rows), B = the
+// (k-chunk x 4) panel of each element (reference layout: one run; wavefront layout: one
+// 256-byte run per 8-direction group)
+template <int TBM, int TLDA>
+__device__ __forceinline__ void d2m_tma_issue(const D2MParams& p, double* st, unsigned long long* bar, int kt, int h0,
+                                              int el0, int lane) {
+  const int k0 = kt * BK;
+  const int ne = min(BN / 4, (p.el_base + p.n_el) - el0), kv = min(BK, p.P - k0);
+  if (lane == 0) mbar_expect_tx(bar, unsigned(BK * TBM * 8 + ne * kv * 32));
+  __syncwarp();
+  for (int c = lane; c < BK; c += 32) bulk_g2s(st + c * TLDA, p.X + (size_t)(k0 + c) * p.Hp + h0, TBM * 8, bar);
+  double* sB = st + BK * TLDA;
+  if (p.wl.nd) {
+    for (int c = lane; c < ne * (kv / 8); c += 32) {
+      const int e = c / (kv / 8), gi = c - e * (kv / 8);
+      bulk_g2s(sB + e * (BK * 4) + gi * 32, p.phi + (size_t)wl_block(p.wl, el0 + e, k0 + 8 * gi) * 4, 256, bar);
+    }
+  } else {
+    for (int e = lane; e < ne; e += 32)
+      bulk_g2s(sB + e * (BK * 4), p.phi + ((size_t)(el0 + e) * p.P + k0) * 4, unsigned(kv * 32), bar);
   }
 }
 
@@ -118,7 +169,7 @@ __global__ void __launch_bounds__(RowTile<MI, WM>::kThreads, STAMG_D2M_MINB) d2m
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;
-  const int el0 = (STAMG_GEMM_SWAP ? blockIdx.y : blockIdx.x) * (BN / 4);
+  const int el0 = p.el_base + (STAMG_GEMM_SWAP ? blockIdx.y : blockIdx.x) * (BN / 4);
   const int h0 = (STAMG_GEMM_SWAP ? blockIdx.x : blockIdx.y) * T::kBM;
   double acc[MI][4][2];
 #pragma unroll
@@ -127,13 +178,29 @@ __global__ void __launch_bounds__(RowTile<MI, WM>::kThreads, STAMG_D2M_MINB) d2m
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int nk = (p.P + BK - 1) / BK;
+#if STAMG_GEMM_TMA
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + NSTAGE * T::kStage);
+  gemm_tma_init(smem, T::kStage, bars, tid, T::kThreads);
+  if (warp == 0)
+    for (int s = 0; s < NSTAGE - 1 && s < nk; ++s)
+      d2m_tma_issue<T::kBM, T::kLDA>(p, smem + s * T::kStage, bars + s, s, h0, el0, lane);
+  for (int kt = 0; kt < nk; ++kt) {
+    const int nxt = kt + NSTAGE - 1;  // its stage was released by the barrier closing iteration kt - 1
+    if (warp == 0 && nxt < nk)
+      d2m_tma_issue<T::kBM, T::kLDA>(p, smem + (nxt % NSTAGE) * T::kStage, bars + nxt % NSTAGE, nxt, h0, el0, lane);
+    mbar_wait_parity(bars + kt % NSTAGE, unsigned(kt / NSTAGE) & 1u);
+    const double* st = smem + (kt % NSTAGE) * T::kStage;
+    mma_stage<MI, T::kLDA>(st, st + BK * T::kLDA, acc, wm, wn, g, t);
+    __syncthreads();
+  }
+#else
   const int Pk = nk * BK;  // X has zero rows up to Pk
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
     if (s < nk) {
       double* st = smem + s * T::kStage;
       load_tile_rows<T::kBM, T::kLDA, T::kThreads>(st, p.X, p.Hp, s * BK, h0, Pk, tid);
-      load_phi_tile<T::kThreads>(st + BK * T::kLDA, p.phi, p.P, p.n_el, s * BK, el0, tid, p.wl);
+      load_phi_tile<T::kThreads>(st + BK * T::kLDA, p.phi, p.P, (p.el_base + p.n_el), s * BK, el0, tid, p.wl);
     }
     cp_async_commit();
   }
@@ -142,7 +209,7 @@ __global__ void __launch_bounds__(RowTile<MI, WM>::kThreads, STAMG_D2M_MINB) d2m
     if (nxt < nk) {
       double* st = smem + (nxt % NSTAGE) * T::kStage;
       load_tile_rows<T::kBM, T::kLDA, T::kThreads>(st, p.X, p.Hp, nxt * BK, h0, Pk, tid);
-      load_phi_tile<T::kThreads>(st + BK * T::kLDA, p.phi, p.P, p.n_el, nxt * BK, el0, tid, p.wl);
+      load_phi_tile<T::kThreads>(st + BK * T::kLDA, p.phi, p.P, (p.el_base + p.n_el), nxt * BK, el0, tid, p.wl);
     }
     cp_async_commit();
     cp_async_wait<NSTAGE - 1>();
@@ -152,6 +219,7 @@ __global__ void __launch_bounds__(RowTile<MI, WM>::kThreads, STAMG_D2M_MINB) d2m
     __syncthreads();
   }
   cp_async_wait<0>();
+#endif
 
   // epilogue: complete the element's 4 dofs from the partner lane, apply N and sigma
   // (rows Hused <= h < h0 + BM of the call's region are written as zeros)
@@ -168,7 +236,7 @@ __global__ void __launch_bounds__(RowTile<MI, WM>::kThreads, STAMG_D2M_MINB) d2m
       const int e = (wn * 32 + j * 8) / 4 + (t >> 1);
       const int el = el0 + e;
       const int i0 = (t & 1) * 2;
-      if (el < p.n_el && h < p.Hrows) {
+      if (el < (p.el_base + p.n_el) && h < p.Hrows) {
         double s0 = 0.0, s1 = 0.0;
         if (h < p.Hused) {
           const int mt = p.mat ? p.mat[el] : 0;
@@ -196,7 +264,7 @@ __device__ __forceinline__ double* m2d_out(const M2DParams& p, int el, int q, in
 #define STAMG_M2D_WM 2  // A/B knob: warp rows of the M2D tile (32 patch rows each); c5 A/B: 1 / 2 / 4 = 97.0 / 83.7 / 88.4 ms
 #endif
 constexpr int M2D_BM = 32 * STAMG_M2D_WM, M2D_LDA = M2D_BM + 4, M2D_THREADS = 64 * STAMG_M2D_WM;
-constexpr int M2D_STAGE = BK * (M2D_LDA + LDB);
+constexpr int M2D_STAGE = BK * M2D_LDA + kStageB;
 
 #ifndef STAMG_M2D_MINB
 #define STAMG_M2D_MINB 3  // resident CTAs per SM the beta != 0 M2D registers are sized for (230 -> 168 regs; c4 MG-level M2D 6.97 -> 5.90 ms)
@@ -208,7 +276,7 @@ __global__ void __launch_bounds__(M2D_THREADS, m2d_minb<PRE>()) m2d_kernel(M2DPa
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;
-  const int el0 = (STAMG_GEMM_SWAP ? blockIdx.y : blockIdx.x) * (BN / 4);
+  const int el0 = p.el_base + (STAMG_GEMM_SWAP ? blockIdx.y : blockIdx.x) * (BN / 4);
   const int q0 = (STAMG_GEMM_SWAP ? blockIdx.x : blockIdx.y) * M2D_BM;
   double acc[4][4][2];
 #pragma unroll
@@ -223,19 +291,52 @@ __global__ void __launch_bounds__(M2D_THREADS, m2d_minb<PRE>()) m2d_kernel(M2DPa
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int el = el0 + (wn * 32 + j * 8) / 4 + (t >> 1);
-        oldv[i][j] = (q < p.P && el < p.n_el) ? *reinterpret_cast<const double2*>(m2d_out(p, el, q, (t & 1) * 2))
+        oldv[i][j] = (q < p.P && el < (p.el_base + p.n_el)) ? *reinterpret_cast<const double2*>(m2d_out(p, el, q, (t & 1) * 2))
                                                : make_double2(0.0, 0.0);
       }
     }
   }
 
   const int nk = (p.Hused + BK - 1) / BK;
+#if STAMG_GEMM_TMA
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + NSTAGE * M2D_STAGE);
+  gemm_tma_init(smem, M2D_STAGE, bars, tid, M2D_THREADS);
+  // stage: A = rows h of X^T (M2D_BM patches each), B = the (h-chunk x 4) panel of src per
+  // element; rows h >= Hused are not copied (their A rows are zeroed in the tail tile)
+  auto issue = [&](int kt) {
+    const int k0 = kt * BK, st_i = kt % NSTAGE;
+    double* st = smem + st_i * M2D_STAGE;
+    const int ne = min(BN / 4, (p.el_base + p.n_el) - el0), kv = min(BK, p.Hused - k0);
+    if (lane == 0) mbar_expect_tx(bars + st_i, unsigned(kv * M2D_BM * 8 + ne * kv * 32));
+    __syncwarp();
+    for (int c = lane; c < kv; c += 32)
+      bulk_g2s(st + c * M2D_LDA, p.XT + (size_t)(k0 + c) * p.Pp + q0, M2D_BM * 8, bars + st_i);
+    for (int e = lane; e < ne; e += 32)
+      bulk_g2s(st + BK * M2D_LDA + e * (BK * 4), p.src + ((size_t)(el0 + e) * p.Hp + k0) * 4, unsigned(kv * 32),
+               bars + st_i);
+  };
+  if (warp == 0)
+    for (int s = 0; s < NSTAGE - 1 && s < nk; ++s) issue(s);
+  for (int kt = 0; kt < nk; ++kt) {
+    const int nxt = kt + NSTAGE - 1;
+    if (warp == 0 && nxt < nk) issue(nxt);
+    mbar_wait_parity(bars + kt % NSTAGE, unsigned(kt / NSTAGE) & 1u);
+    double* st = smem + (kt % NSTAGE) * M2D_STAGE;
+    const int kv = p.Hused - kt * BK;
+    if (kv < BK) {  // tail tile (uniform): stale A rows -> 0
+      for (int c = tid; c < (BK - kv) * M2D_LDA; c += M2D_THREADS) st[kv * M2D_LDA + c] = 0.0;
+      __syncthreads();
+    }
+    mma_stage<4, M2D_LDA>(st, st + BK * M2D_LDA, acc, wm, wn, g, t);
+    __syncthreads();
+  }
+#else
 #pragma unroll
   for (int s = 0; s < NSTAGE - 1; ++s) {
     if (s < nk) {
       double* st = smem + s * M2D_STAGE;
       load_tile_rows<M2D_BM, M2D_LDA, M2D_THREADS>(st, p.XT, p.Pp, s * BK, q0, p.Hused, tid);
-      load_src_tile<M2D_THREADS>(st + BK * M2D_LDA, p.src, p.Hp, p.n_el, s * BK, el0, p.Hused, tid);
+      load_src_tile<M2D_THREADS>(st + BK * M2D_LDA, p.src, p.Hp, (p.el_base + p.n_el), s * BK, el0, p.Hused, tid);
     }
     cp_async_commit();
   }
@@ -244,7 +345,7 @@ __global__ void __launch_bounds__(M2D_THREADS, m2d_minb<PRE>()) m2d_kernel(M2DPa
     if (nxt < nk) {
       double* st = smem + (nxt % NSTAGE) * M2D_STAGE;
       load_tile_rows<M2D_BM, M2D_LDA, M2D_THREADS>(st, p.XT, p.Pp, nxt * BK, q0, p.Hused, tid);
-      load_src_tile<M2D_THREADS>(st + BK * M2D_LDA, p.src, p.Hp, p.n_el, nxt * BK, el0, p.Hused, tid);
+      load_src_tile<M2D_THREADS>(st + BK * M2D_LDA, p.src, p.Hp, (p.el_base + p.n_el), nxt * BK, el0, p.Hused, tid);
     }
     cp_async_commit();
     cp_async_wait<NSTAGE - 1>();
@@ -254,6 +355,7 @@ __global__ void __launch_bounds__(M2D_THREADS, m2d_minb<PRE>()) m2d_kernel(M2DPa
     __syncthreads();
   }
   cp_async_wait<0>();
+#endif
 
   constexpr double inv4pi = 0.07957747154594767;  // 1 / (4 pi)
 #pragma unroll
@@ -264,7 +366,7 @@ __global__ void __launch_bounds__(M2D_THREADS, m2d_minb<PRE>()) m2d_kernel(M2DPa
     for (int j = 0; j < 4; ++j) {
       const int e = (wn * 32 + j * 8) / 4 + (t >> 1);
       const int el = el0 + e;
-      if (el >= p.n_el) continue;
+      if (el >= (p.el_base + p.n_el)) continue;
       const int i0 = (t & 1) * 2;
       double* yp = m2d_out(p, el, q, i0);
       double v0 = p.scale * acc[i][j][0], v1 = p.scale * acc[i][j][1];
@@ -283,12 +385,13 @@ __global__ void __launch_bounds__(M2D_THREADS, m2d_minb<PRE>()) m2d_kernel(M2DPa
   }
 }
 
-size_t gemm_smem() { return sizeof(double) * NSTAGE * M2D_STAGE; }
+constexpr size_t kBarBytes = STAMG_GEMM_TMA ? NSTAGE * sizeof(unsigned long long) : 0;  // stage mbarriers
+size_t gemm_smem() { return sizeof(double) * NSTAGE * M2D_STAGE + kBarBytes; }
 
 template <int MI, int WM>
 void launch_d2m_tile(const D2MParams& p, cudaStream_t s) {
   using T = RowTile<MI, WM>;
-  const size_t smem = sizeof(double) * NSTAGE * T::kStage;
+  const size_t smem = sizeof(double) * NSTAGE * T::kStage + kBarBytes;
   // per launch: the attribute is per device (contexts may live on different GPUs)
   cudaFuncSetAttribute(d2m_kernel<MI, WM>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   const unsigned ge = (p.n_el + BN / 4 - 1) / (BN / 4), gh = (p.Hused + T::kBM - 1) / T::kBM;
@@ -318,10 +421,10 @@ __device__ __forceinline__ void wht(double (&v)[G][4]) {
 #endif
 template <int G>
 __global__ void __launch_bounds__(256, STAMG_FOLD_MINB) fold_kernel(const double* __restrict__ phi, double* __restrict__ Phi, const int* __restrict__ orbit,
-                            int n_el, int P, int R, WLGeom wl) {
+                            int n_el, int el0, int el1, int P, int R, WLGeom wl) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)n_el * R) return;
-  const int el = int(idx / R), r = int(idx - (int64_t)el * R);
+  if (idx >= (int64_t)(el1 - el0) * R) return;
+  const int e = int(idx / R), r = int(idx - (int64_t)e * R), el = el0 + e;
   const double* src[G];  // member addresses first, then the G block loads back to back
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -342,11 +445,11 @@ __global__ void __launch_bounds__(256, STAMG_FOLD_MINB) fold_kernel(const double
 // y[el][orbit[r][g]][i] = beta*y + scale * sum_c chi_c(g) Y[c][el][r][i] (+ isotropic source)
 template <int G, bool BETA>
 __global__ void __launch_bounds__(256, STAMG_FOLD_MINB) unfold_kernel(const double* __restrict__ Y, double* __restrict__ y, const int* __restrict__ orbit,
-                              int n_el, int P, int R, double scale, double beta, const double* __restrict__ ext_q,
-                              const double* __restrict__ area, double4 nsum, WLGeom wl) {
+                              int n_el, int el0, int el1, int P, int R, double scale, double beta,
+                              const double* __restrict__ ext_q, const double* __restrict__ area, double4 nsum, WLGeom wl) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)n_el * R) return;
-  const int el = int(idx / R), r = int(idx - (int64_t)el * R);
+  if (idx >= (int64_t)(el1 - el0) * R) return;
+  const int e = int(idx / R), r = int(idx - (int64_t)e * R), el = el0 + e;
   // orbit members and their source weights first: the block stores below are
   // ordered asm (memory clobber), so loads left between them would serialise
   double* o[G];
@@ -422,14 +525,15 @@ void launch_from_wl(const double* wlv, double* ref, const int* perm, int el0, in
   if (n > 0) wl_convert_kernel<false><<<int((n + 255) / 256), 256, 0, s>>>(wlv, ref, perm, el0, n_el_chunk, P, wl);
 }
 
-void launch_fold(const double* phi, double* Phi, const int* orbit, int n_el, int P, int R, int G, const WLGeom& wl,
-                 cudaStream_t s) {
-  const int64_t n = (int64_t)n_el * R;
+void launch_fold(const double* phi, double* Phi, const int* orbit, int n_el, int el0, int el1, int P, int R, int G,
+                 const WLGeom& wl, cudaStream_t s) {
+  const int64_t n = (int64_t)(el1 - el0) * R;
+  if (n <= 0) return;
   const int blocks = int((n + 255) / 256);
   switch (G) {
-    case 2: fold_kernel<2><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, P, R, wl); break;
-    case 4: fold_kernel<4><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, P, R, wl); break;
-    case 8: fold_kernel<8><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, P, R, wl); break;
+    case 2: fold_kernel<2><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, el0, el1, P, R, wl); break;
+    case 4: fold_kernel<4><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, el0, el1, P, R, wl); break;
+    case 8: fold_kernel<8><<<blocks, 256, 0, s>>>(phi, Phi, orbit, n_el, el0, el1, P, R, wl); break;
     default: break;
   }
 }
@@ -441,14 +545,15 @@ void launch_fold(const double* phi, double* Phi, const int* orbit, int n_el, int
 // thread (8 x 2 doubles), the pair still covers each 32-byte block in one access
 template <int G, bool BETA>
 __global__ void __launch_bounds__(256) unfold2_kernel(const double* __restrict__ Y, double* __restrict__ y,
-                                                      const int* __restrict__ orbit, int n_el, int P, int R,
-                                                      double scale, double beta, const double* __restrict__ ext_q,
-                                                      const double* __restrict__ area, double4 nsum, WLGeom wl) {
+                                                      const int* __restrict__ orbit, int n_el, int el0, int el1,
+                                                      int P, int R, double scale, double beta,
+                                                      const double* __restrict__ ext_q, const double* __restrict__ area,
+                                                      double4 nsum, WLGeom wl) {
   const int64_t idx2 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx2 >= (int64_t)n_el * R * 2) return;
+  if (idx2 >= (int64_t)(el1 - el0) * R * 2) return;
   const int half = int(idx2 & 1);
   const int64_t idx = idx2 >> 1;
-  const int el = int(idx / R), r = int(idx - (int64_t)el * R);
+  const int e = int(idx / R), r = int(idx - (int64_t)e * R), el = el0 + e;
   double* o[G];
   double ar[G];
 #pragma unroll
@@ -493,26 +598,27 @@ __global__ void __launch_bounds__(256) unfold2_kernel(const double* __restrict__
   for (int g = 0; g < G; ++g) *reinterpret_cast<double2*>(o[g]) = make_double2(v[g][0], v[g][1]);
 }
 
-void launch_unfold(const double* Y, double* y, const int* orbit, int n_el, int P, int R, int G, double scale,
-                   double beta, const double* ext_q, const double* area, const double* nsum, const WLGeom& wl,
-                   cudaStream_t s) {
-  const int64_t n = (int64_t)n_el * R;
+void launch_unfold(const double* Y, double* y, const int* orbit, int n_el, int el0, int el1, int P, int R, int G,
+                   double scale, double beta, const double* ext_q, const double* area, const double* nsum,
+                   const WLGeom& wl, cudaStream_t s) {
+  const int64_t n = (int64_t)(el1 - el0) * R;
+  if (n <= 0) return;
   const int blocks = int((n + 255) / 256);
   const double4 ns = make_double4(nsum[0], nsum[1], nsum[2], nsum[3]);
   if (STAMG_UNFOLD_SPLIT) {
     const int b2 = int((2 * n + 255) / 256);
     switch (G) {
       case 2:
-        if (beta != 0.0) unfold2_kernel<2, true><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
-        else unfold2_kernel<2, false><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+        if (beta != 0.0) unfold2_kernel<2, true><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, el0, el1, P, R, scale, beta, ext_q, area, ns, wl);
+        else unfold2_kernel<2, false><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, el0, el1, P, R, scale, beta, ext_q, area, ns, wl);
         break;
       case 4:
-        if (beta != 0.0) unfold2_kernel<4, true><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
-        else unfold2_kernel<4, false><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+        if (beta != 0.0) unfold2_kernel<4, true><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, el0, el1, P, R, scale, beta, ext_q, area, ns, wl);
+        else unfold2_kernel<4, false><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, el0, el1, P, R, scale, beta, ext_q, area, ns, wl);
         break;
       case 8:
-        if (beta != 0.0) unfold2_kernel<8, true><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
-        else unfold2_kernel<8, false><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+        if (beta != 0.0) unfold2_kernel<8, true><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, el0, el1, P, R, scale, beta, ext_q, area, ns, wl);
+        else unfold2_kernel<8, false><<<b2, 256, 0, s>>>(Y, y, orbit, n_el, el0, el1, P, R, scale, beta, ext_q, area, ns, wl);
         break;
       default: break;
     }
@@ -520,16 +626,16 @@ void launch_unfold(const double* Y, double* y, const int* orbit, int n_el, int P
   }
   switch (G) {
     case 2:
-      if (beta != 0.0) unfold_kernel<2, true><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
-      else unfold_kernel<2, false><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+      if (beta != 0.0) unfold_kernel<2, true><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, el0, el1, P, R, scale, beta, ext_q, area, ns, wl);
+      else unfold_kernel<2, false><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, el0, el1, P, R, scale, beta, ext_q, area, ns, wl);
       break;
     case 4:
-      if (beta != 0.0) unfold_kernel<4, true><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
-      else unfold_kernel<4, false><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+      if (beta != 0.0) unfold_kernel<4, true><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, el0, el1, P, R, scale, beta, ext_q, area, ns, wl);
+      else unfold_kernel<4, false><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, el0, el1, P, R, scale, beta, ext_q, area, ns, wl);
       break;
     case 8:
-      if (beta != 0.0) unfold_kernel<8, true><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
-      else unfold_kernel<8, false><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, P, R, scale, beta, ext_q, area, ns, wl);
+      if (beta != 0.0) unfold_kernel<8, true><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, el0, el1, P, R, scale, beta, ext_q, area, ns, wl);
+      else unfold_kernel<8, false><<<blocks, 256, 0, s>>>(Y, y, orbit, n_el, el0, el1, P, R, scale, beta, ext_q, area, ns, wl);
       break;
     default: break;
   }

@@ -512,7 +512,11 @@ LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool 
   return L;
 }
 
-std::vector<int> throughput_shard(const SphereTree& t, int rank, int world) {
+// Reflections (axis-aligned mirror maps) that map the leaf set of `t` onto itself:
+// per symmetric axis the leaf position of each leaf's mirror image. With `only`
+// non-empty, just those axes are tried.
+void leaf_mirrors(const SphereTree& t, std::vector<int>& axes, std::vector<std::vector<int>>& mirror,
+                  const std::vector<int>& only) {
   const int Pg = int(t.leaves.size());
   using Key = std::array<std::int64_t, 9>;
   auto key_of = [](std::array<std::int64_t, 9> f) {
@@ -525,9 +529,9 @@ std::vector<int> throughput_shard(const SphereTree& t, int rank, int world) {
   };
   std::map<Key, int> pos;
   for (int q = 0; q < Pg; ++q) pos[key_of(t.flat[t.leaves[q]])] = q;
-  std::vector<int> axes;
-  std::vector<std::vector<int>> mirror;
+  axes.clear(), mirror.clear();
   for (int axis = 0; axis < 3; ++axis) {
+    if (!only.empty() && std::find(only.begin(), only.end(), axis) == only.end()) continue;
     std::vector<int> mq(Pg, -1);
     bool ok = true;
     for (int q = 0; ok && q < Pg; ++q) {
@@ -539,6 +543,13 @@ std::vector<int> throughput_shard(const SphereTree& t, int rank, int world) {
     }
     if (ok) axes.push_back(axis), mirror.push_back(mq);
   }
+}
+
+std::vector<int> throughput_shard(const SphereTree& t, int rank, int world) {
+  const int Pg = int(t.leaves.size());
+  std::vector<int> axes;
+  std::vector<std::vector<int>> mirror;
+  leaf_mirrors(t, axes, mirror, {});
   std::vector<int> reps;  // orbit representatives: octant bits 0 on every symmetric axis
   for (int q = 0; q < Pg; ++q) {
     bool rep = true;
@@ -668,12 +679,50 @@ std::vector<std::vector<int>> partition_levels(const SphereTree& fine, int nlev,
   for (int id : trees.back().leaves) weight[root_of(id)]++;
   long total = 0;
   for (long w : weight) total += w;
-  // contiguous roots, cut where the cumulative weight crosses rank boundaries
+  // units of assignment: whole reflection orbits of roots when the finest mesh is mirror
+  // symmetric (a rank's subtrees are then closed under the reflections at every level and
+  // its scatter folds, as on one GPU), else single roots
+  std::vector<int> axes, axes0;
+  std::vector<std::vector<int>> mf, m0;
+  leaf_mirrors(fine, axes, mf, {});
+  std::vector<std::vector<int>> units;  // roots of each unit, in root order of the unit's first member
+  if (!axes.empty()) {
+    leaf_mirrors(trees[0], axes0, m0, axes);
+    if (axes0 == axes) {
+      std::vector<int> seen(R, 0);
+      for (int c = 0; c < R; ++c) {
+        if (seen[c]) continue;
+        std::vector<int> orb{c};
+        for (size_t k = 0; k < axes0.size(); ++k) {
+          const size_t n = orb.size();
+          for (size_t i = 0; i < n; ++i) orb.push_back(m0[k][orb[i]]);
+        }
+        std::sort(orb.begin(), orb.end());
+        orb.erase(std::unique(orb.begin(), orb.end()), orb.end());
+        for (int q : orb) seen[q] = 1;
+        units.push_back(orb);
+      }
+      if (int(units.size()) < world) units.clear();  // too few orbits to give every rank one
+    }
+  }
+  if (units.empty())
+    for (int c = 0; c < R; ++c) units.push_back({c});
+  // balance the finest-level directions: heaviest unit first onto the least-loaded rank
+  // (deterministic: ties by first root, then by rank); the cone mesh of config 4 has
+  // orbits of very different weight, so contiguous cuts were 1.25x imbalanced at 8 ranks
+  (void)total;
+  std::vector<long> uw(units.size(), 0);
+  for (size_t u = 0; u < units.size(); ++u)
+    for (int c : units[u]) uw[u] += weight[c];
+  std::vector<int> order(units.size());
+  for (size_t u = 0; u < units.size(); ++u) order[u] = int(u);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return uw[a] > uw[b]; });
+  std::vector<long> load(world, 0);
   std::vector<int> owner(R, 0);
-  long acc = 0;
-  for (int c = 0; c < R; ++c) {
-    owner[c] = std::min(world - 1, int((acc + weight[c] / 2) * world / std::max(1L, total)));
-    acc += weight[c];
+  for (int u : order) {
+    const int o = int(std::min_element(load.begin(), load.end()) - load.begin());
+    load[o] += uw[u];
+    for (int c : units[u]) owner[c] = o;
   }
   std::vector<std::vector<int>> parts(nlev);
   for (int i = 0; i < nlev; ++i)

@@ -112,10 +112,18 @@ std::vector<int> range_subset(int q_begin, int q_end);
 // slices of 8 orbit representatives; contiguous slices of 4 patches without symmetry.
 std::vector<int> throughput_shard(const SphereTree& tree, int rank, int world);
 
+// Mirror maps of the reflections (x, y, z; or only the axes in `only`) that map the
+// leaf set onto itself: axes[k] and mirror[k][leaf position] = its mirror's position.
+void leaf_mirrors(const SphereTree& t, std::vector<int>& axes, std::vector<std::vector<int>>& mirror,
+                  const std::vector<int>& only);
 // Direction sharding of a hierarchy: rank r owns whole subtrees rooted at the
-// coarsest used level's patches (contiguous roots, balanced by the number of
-// finest-level descendants). Returns per level (0 = coarsest) the ascending
-// leaf positions held by `rank`; level 0 is replicated (all positions).
+// coarsest used level's patches, assigned in whole reflection orbits of the roots
+// when the finest mesh is mirror symmetric and there are at least `world` orbits (so
+// every rank's levels are closed under the reflections and fold their scatter), else
+// root by root; units balanced by the number of finest-level descendants (heaviest
+// first onto the least-loaded rank), so a rank's roots need not be contiguous.
+// Returns per level (0 = coarsest) the ascending leaf positions held by `rank`;
+// level 0 is replicated (all positions).
 std::vector<std::vector<int>> partition_levels(const SphereTree& fine, int nlev, int rank, int world);
 
 // build_hierarchy: nlev levels, index 0 coarsest; fills up/child maps. With
