@@ -121,6 +121,12 @@ int stamg_partition(const stamg_problem* prob, int rank, int world, int level, i
  * in a context without a hierarchy: whole orbits of the mesh's reflection symmetry, so
  * every rank folds its own scatter (contiguous slices of 4 patches without symmetry). */
 int stamg_shard_patches(const stamg_problem* prob, int rank, int world, int* out, int cap, int* n);
+/* Host only, no device: an outer-level table as the host setup builds it ("X" couplings
+ * [P*D][H], scatter.hpp:32-39; "B" diagonal blocks, transport.hpp:38; "C" inflow blocks;
+ * "M1" patch mass row sums; "octant" per patch; "rhs" assemble_rhs, transport.hpp:62;
+ * "layout" {n_el, P, S, D}).
+ * Call with out = NULL to get the length in *n. */
+int stamg_host_table(const stamg_problem* prob, const char* name, double* out, int64_t cap, int64_t* n);
 int stamg_n_levels(stamg_ctx* ctx, int* n_levels, int* nr);
 /* scatter order of a level's coupling table (ops.kernel.N) */
 int stamg_level_order(stamg_ctx* ctx, int level, int* order);

@@ -19,7 +19,7 @@ CCBIN = "/usr/bin/g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-ccbin", CCBIN, "-I" + os.path.join(HERE, "..", "include")] + os.environ.get("STAMG_NVCC_EXTRA", "").split()
-SOURCES = ["setup.cpp", "sweep.cu", "transport.cu", "scatter.cu", "multigrid.cu", "blas.cu", "couplings.cu", "context.cu"]
+SOURCES = ["setup.cpp", "generic_setup.cpp", "generic.cu", "sweep.cu", "transport.cu", "scatter.cu", "multigrid.cu", "blas.cu", "couplings.cu", "context.cu"]
 
 
 def _obj(src):

@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "generic.hpp"
 #include "kernels.hpp"
 #include "setup.hpp"
 
@@ -103,7 +104,10 @@ struct UniqueId {
 // ------------------------------------------------------------------ device level
 struct DevLevel {
   LevelTables t;
-  int64_t n = 0;  // vector length n_el * P * 4
+  // reference-shape path (generic.hpp): 3D / p0 / Lin levels; t then only carries the sizes
+  gen::Tables gt;
+  gen::Dev* g = nullptr;
+  int64_t n = 0;  // vector length n_el * P * D * S
   bool sharded = false;  // holds only this rank's directions (scatter moments need an allreduce)
   int Hp = 0, Pk = 0, Pp = 0;
   double *X = nullptr, *XT = nullptr, *sig = nullptr, *ones = nullptr, *B = nullptr, *Binv = nullptr;
@@ -125,7 +129,8 @@ struct DevLevel {
   double* src = nullptr;  // scatter moments workspace [n_el][Hp][4]
   double* mom = nullptr;  // coarse GS moments
   int* gs_done = nullptr;
-  double *gs_K = nullptr, *gs_Xo = nullptr, *gs_XoT = nullptr, *gs_G = nullptr;
+  double *gs_K = nullptr, *gs_Xo = nullptr, *gs_XoT = nullptr, *gs_G = nullptr, *gs_Minv = nullptr;
+  int gs_blk = 0;  // blocked patch chain (multi-warp coarse GS)
   int gs_blocks = 0, gs_cpw = 0, gs_kpad = 0, gs_max_np = 0, gs_rows = 0, gs_mw = 0, gs_cluster = 0;
   int gs_mb_slots = 0, gs_mb_credit = 0;
   double *tmp = nullptr, *cf = nullptr, *ce = nullptr;  // V-cycle workspace
@@ -323,6 +328,50 @@ bool env_is_zero(const char* name) {
   return v != nullptr && v[0] == '0' && v[1] == 0;
 }
 
+// Inverses of the coarse-GS chain's diagonal blocks (sweeps.cpp:93-101 restated as a linear
+// system): for block J of an octant (patches a = 4J..4J+3, octant order) and material m,
+// T = I - blockdiag(G_a) (L x I_4) with L[a][b] = K[a][b] for b < a inside the block. T is unit
+// lower block-triangular, so T^-1 = I + S + S^2 + S^3 with S = I - T (formed in long double).
+// Packed per block as column c from row 4 (c / 4): [m][octant][kpad / 4][kGsMinvBlock].
+std::vector<double> gs_minv_table(const LevelTables& t, const std::vector<double>& K, const std::vector<double>& G, int kpad) {
+  const int nb = kpad / 4;
+  std::vector<double> out(size_t(t.n_mat) * 8 * nb * kGsMinvBlock, 0.0);
+  for (int m = 0; m < t.n_mat; ++m)
+    for (int o = 0; o < 8; ++o) {
+      const int pbeg = t.oct_ptr[o], np = t.oct_ptr[o + 1] - pbeg;
+      for (int J = 0; J < nb; ++J) {
+        long double S[16][16] = {}, M[16][16] = {}, Pw[16][16] = {};
+        for (int r = 1; r < 4; ++r) {
+          const int a = 4 * J + r;
+          if (a >= np) continue;
+          const double* Ga = &G[(size_t(m) * t.P + t.oct_patches[pbeg + a]) * 16];
+          for (int r2 = 0; r2 < r; ++r2) {
+            const double k = K[(size_t(m) * t.P + pbeg + a) * kpad + 4 * J + r2];
+            for (int i = 0; i < 4; ++i)
+              for (int j = 0; j < 4; ++j) S[4 * r + i][4 * r2 + j] = (long double)Ga[4 * i + j] * k;
+          }
+        }
+        for (int i = 0; i < 16; ++i) M[i][i] = Pw[i][i] = 1.0L;
+        for (int pw = 1; pw < 4; ++pw) {  // Pw = S^pw, M += Pw
+          long double Nx[16][16] = {};
+          for (int i = 0; i < 16; ++i)
+            for (int k = 0; k < 16; ++k) {
+              if (S[i][k] == 0.0L) continue;
+              for (int j = 0; j < 16; ++j) Nx[i][j] += S[i][k] * Pw[k][j];
+            }
+          for (int i = 0; i < 16; ++i)
+            for (int j = 0; j < 16; ++j) Pw[i][j] = Nx[i][j], M[i][j] += Nx[i][j];
+        }
+        double* dst = &out[((size_t(m) * 8 + o) * nb + J) * kGsMinvBlock];
+        for (int c = 0; c < 16; ++c) {
+          const int cb = c / 4, base = 64 * cb - 8 * cb * (cb - 1) + (c % 4) * (16 - 4 * cb);
+          for (int r = 4 * cb; r < 16; ++r) dst[base + r - 4 * cb] = double(M[r][c]);
+        }
+      }
+    }
+  return out;
+}
+
 void upload_level(stamg_ctx* c, DevLevel& L) {
   cudaStream_t s = c->stream;
   {
@@ -381,17 +430,25 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     L.groups8 = dupload(t.groups8, s), L.group8_oct = dupload(t.group8_oct, s);
     L.sweep_top = dalloc<double2>(t.group8_oct.size() * 8 * size_t(t.nx));
     // fewer groups than SMs (config 5 sharded over 8 GPUs: 128 per rank): two column blocks per
-    // group so the wavefronts cover twice the SMs (STAMG_SWEEP_XBLOCKS=0 keeps one block)
+    // group so the wavefronts cover twice the SMs (STAMG_SWEEP_XBLOCKS=0 keeps one block).
+    // With more groups than CTA slots (config 5 on one GPU: 1024 groups on 296 slots = 3.46
+    // waves run as 4) column blocks would shorten the tail wave, but measured slower:
+    // 23.8 ms with one block, 26.3 with two, 29.2 with four (profiles/r02_sweep_ab.txt);
+    // STAMG_SWEEP_XB forces a block count for A/B runs.
     const int ng = int(t.group8_oct.size());
-    if (c->wl_allowed && ng <= sms && t.nx % 2 == 0 && t.nx / 2 >= kSweep8MinNx && !env_is_zero("STAMG_SWEEP_XBLOCKS")) {
-      L.sweep_xb = 2;
-      if (const char* e = std::getenv("STAMG_SWEEP_XB")) {  // A/B: more blocks (all must stay co-resident)
+    if (c->wl_allowed && !env_is_zero("STAMG_SWEEP_XBLOCKS")) {
+      auto ok = [&](int xb) { return xb >= 1 && t.nx % xb == 0 && t.nx / xb >= kSweep8MinNx; };
+      int best = 1;
+      if (ng <= sms && ok(2)) best = 2;
+      if (const char* e = std::getenv("STAMG_SWEEP_XB")) {  // A/B
         const int xb = std::atoi(e);
-        const int slots = (std::getenv("STAMG_SWEEP_XB_SMEMB") ? 4 : 2) * sms;
-        if (xb >= 1 && t.nx % xb == 0 && t.nx / xb >= kSweep8MinNx && ng * xb <= slots) L.sweep_xb = xb;
+        if (ok(xb)) best = xb;
       }
-      L.sweep_xflag = dalloc<int>(size_t(ng) * L.sweep_xb);
-      L.sweep_xtrace = dalloc<double2>(size_t(ng) * L.sweep_xb * t.ny * 8);
+      if (best > 1) {
+        L.sweep_xb = best;
+        L.sweep_xflag = dalloc<int>(size_t(ng) * L.sweep_xb + 1);  // + the block ticket
+        L.sweep_xtrace = dalloc<double2>(size_t(ng) * L.sweep_xb * t.ny * 8);
+      }
     }
   }
   if (L.wl.nd) {
@@ -406,7 +463,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     L.gs_done = dalloc<int>(size_t(8) * t.n_el);
     // K[m][q][b] = X_q sig_m X_b^T for b in q's octant (coarse GS chain)
     for (int o = 0; o < 8; ++o) L.gs_max_np = std::max(L.gs_max_np, t.oct_ptr[o + 1] - t.oct_ptr[o]);
-    L.gs_kpad = std::max(2, (L.gs_max_np + 1) / 2 * 2);  // even: 16-byte staging chunks
+    L.gs_kpad = std::max(4, round_up(L.gs_max_np, 4));  // whole 4-patch chain blocks, 16-byte staging chunks
     std::vector<double> K(size_t(t.n_mat) * t.P * L.gs_kpad, 0.0);
     for (int m = 0; m < t.n_mat; ++m)
       for (int o = 0; o < 8; ++o)
@@ -431,6 +488,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
             G[b * 16 + i * 4 + j] = acc;
           }
       L.gs_G = dupload(G, s);
+      L.gs_Minv = dupload(gs_minv_table(t, K, G, L.gs_kpad), s);
     }
     std::vector<double> Xo(size_t(t.P) * L.Hp, 0.0), XoT(size_t(L.Hp) * t.P, 0.0);
     for (int a = 0; a < t.P; ++a)
@@ -444,8 +502,20 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     // the neighbouring items beside the chain); measured faster on every BASELINE config
     // (10 passes: c1 12.8 -> 10.4 ms, c2 26.7 -> 20.7, c3 55.7 -> 36.8, c4 640 -> 337).
     // STAMG_GS_MW=0 keeps the one-warp kernels
+    // blocked chain where an octant's patches are one or two blocks (configs 1-2: 4 patches,
+    // 8.6 -> 7.6 and 17.7 -> 15.6 ms per coarse solve); at one patch there is no chain
+    // (config 3), and at 64 patches (config 4) the per-block shared-memory round trips cost
+    // more than the sixteen-fold shorter chain saves (0.314 -> 0.46 s; profiles/r02_gs_c4_chain.txt).
+    // STAMG_GS_CHAIN_BLOCKS=1 / 0 force it on / off.
+    bool want_blk = false;
+    {
+      const char* e = std::getenv("STAMG_GS_CHAIN_BLOCKS");
+      const bool forced_on = e != nullptr && e[0] == '1' && e[1] == 0;
+      want_blk = coarse_gs_chain_blocked() && (forced_on || (L.gs_max_np >= 2 && L.gs_max_np <= 8));
+    }
     L.gs_mw = !env_is_zero("STAMG_GS_MW") &&
-              coarse_gs_mw_ok(L.Hp, t.H, L.gs_kpad, t.n_mat, t.ny, L.gs_max_np);
+              coarse_gs_mw_ok(L.Hp, t.H, L.gs_kpad, t.n_mat, t.ny, L.gs_max_np, want_blk);
+    L.gs_blk = L.gs_mw && want_blk;
     L.gs_rows = (std::getenv("STAMG_GS_SEGMENTS") || t.nx < 64)
                     ? 0
                     : coarse_gs_rows_wpb(L.Hp, L.gs_kpad, t.n_mat, t.nx, t.ny, L.gs_max_np);
@@ -455,7 +525,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
       // mailboxes (STAMG_GS_CLUSTER=0 keeps every hop in global memory)
       const int cl = env_is_zero("STAMG_GS_CLUSTER")
                          ? 0
-                         : coarse_gs_cluster_rows(L.Hp, t.H, L.gs_kpad, t.n_mat, t.nx, t.ny, L.gs_max_np);
+                         : coarse_gs_cluster_rows(L.Hp, t.H, L.gs_kpad, t.n_mat, t.nx, t.ny, L.gs_max_np, L.gs_blk != 0);
       L.gs_cluster = cl & 127, L.gs_mb_credit = (cl >> 7) & 1, L.gs_mb_slots = cl >> 8;
     } else {
       const int max_warps = coarse_gs_max_warps(L.Hp, L.gs_kpad, t.n_mat, L.gs_max_np);
@@ -519,11 +589,51 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
   ck(cudaStreamSynchronize(s), "upload sync");
 }
 
+// reference-shape levels: the dense per-patch tables as they are
+void upload_gen_level(stamg_ctx* c, DevLevel& L) {
+  cudaStream_t s = c->stream;
+  const gen::Tables& t = L.gt;
+  L.t.n_el = t.n_el, L.t.P = t.P, L.t.order = t.order, L.t.H = t.H, L.t.n_mat = 1, L.t.nx = t.nx, L.t.ny = t.ny;
+  L.t.leaf_id = t.leaf_id, L.t.octant = t.octant, L.t.oct_ptr = t.oct_ptr, L.t.oct_patches = t.oct_patches;
+  L.t.up = t.up;
+  L.t.qpos.resize(t.P);
+  for (int q = 0; q < t.P; ++q) L.t.qpos[q] = q;
+  L.t.P_global = t.P;
+  L.n = int64_t(t.n_el) * t.P * t.bs;
+  auto* g = new gen::Dev();
+  L.g = g;
+  g->dim = t.dim, g->nx = t.nx, g->ny = t.ny, g->nz = t.nz, g->n_el = t.n_el, g->S = t.S, g->D = t.D, g->bs = t.bs;
+  g->P = t.P, g->H = t.H, g->order = t.order;
+  g->X = dupload(t.X, s), g->sig = dupload(t.sig, s), g->Bd = dupload(t.Bd, s), g->Binv = dupload(t.Binv, s);
+  g->C = dupload(t.C, s), g->Nmat = dupload(t.Nmat, s);
+  g->octant = dupload(t.octant, s), g->oct_patches = dupload(t.oct_patches, s), g->oct_ptr = dupload(t.oct_ptr, s);
+  g->src = dalloc<double>(size_t(t.n_el) * t.H * t.S);
+  if (!t.BinvGS.empty()) {
+    g->BinvGS = dupload(t.BinvGS, s);
+    g->mom = dalloc<double>(size_t(t.n_el) * t.H * t.S);
+  }
+  if (!t.up.empty()) {
+    g->up = dupload(t.up, s), g->upB = dupload(t.upB, s);
+    g->child_ptr = dupload(t.child_ptr, s), g->child_idx = dupload(t.child_idx, s);
+  }
+  for (int o = 0; o < 8; ++o) g->max_np = std::max(g->max_np, t.oct_ptr[o + 1] - t.oct_ptr[o]);
+  ck(cudaStreamSynchronize(s), "upload sync");
+}
+
 void free_level(DevLevel& L) {
+  if (L.g) {
+    gen::Dev* g = L.g;
+    for (void* p : {(void*)g->X, (void*)g->sig, (void*)g->Bd, (void*)g->Binv, (void*)g->C, (void*)g->BinvGS,
+                    (void*)g->Nmat, (void*)g->upB, (void*)g->src, (void*)g->mom, (void*)g->octant,
+                    (void*)g->oct_patches, (void*)g->oct_ptr, (void*)g->up, (void*)g->child_ptr, (void*)g->child_idx})
+      if (p) cudaFree(p);
+    delete g;
+    L.g = nullptr;
+  }
   for (void* p : {(void*)L.X, (void*)L.XT, (void*)L.sig, (void*)L.ones, (void*)L.B, (void*)L.Binv, (void*)L.cxy,
                   (void*)L.BinvGS, (void*)L.sq, (void*)L.area, (void*)L.up_w, (void*)L.groups, (void*)L.group_oct,
                   (void*)L.oct_patches, (void*)L.oct_ptr, (void*)L.up, (void*)L.child_ptr, (void*)L.child_idx,
-                  (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_K, (void*)L.gs_Xo, (void*)L.gs_XoT, (void*)L.gs_G, (void*)L.Xf, (void*)L.XfT, (void*)L.groups8, (void*)L.group8_oct, (void*)L.sweep_top, (void*)L.sweep_xflag, (void*)L.sweep_xtrace,
+                  (void*)L.src, (void*)L.mom, (void*)L.gs_done, (void*)L.gs_K, (void*)L.gs_Xo, (void*)L.gs_XoT, (void*)L.gs_G, (void*)L.gs_Minv, (void*)L.Xf, (void*)L.XfT, (void*)L.groups8, (void*)L.group8_oct, (void*)L.sweep_top, (void*)L.sweep_xflag, (void*)L.sweep_xtrace,
                   (void*)L.d_ipos, (void*)L.d_iid, (void*)L.stage,
                   (void*)L.sigf, (void*)L.orbit, (void*)L.tmp, (void*)L.cf,
                   (void*)L.ce})
@@ -568,6 +678,12 @@ void op_allreduce(stamg_ctx* c, double* buf, size_t n) {
 void op_apply_L(stamg_ctx* c, DevLevel& L, const double* x, double* y, double alpha = 1.0, double beta = 0.0,
                 const double* f = nullptr) {
   Timed tm(c, "apply_L");
+  if (L.g) {
+    gen::launch_apply_L(*L.g, x, y, alpha, beta, f, c->stream);
+    ck_launch("apply_L");
+    c->launches += 1;
+    return;
+  }
   if (L.wl.nd) {  // wavefront layout: the sweep's skewed schedule, apply_L arithmetic
     SweepParams p;
     p.g = geom(c, L);
@@ -645,6 +761,19 @@ void allreduce_chunk_async(stamg_ctx* c, double* buf, size_t n, int k) {
 void scatter_into(stamg_ctx* c, DevLevel& L, const double* phi, int order, double scale, double beta, double* y,
                   const double* ext) {
   if (order > L.t.order) throw std::invalid_argument("sigma_by_harmonic: max_order exceeds kernel order");
+  if (L.g) {  // reference-shape level: y += scale X sigma (X^T phi) N
+    if (beta != 1.0 || ext) throw std::invalid_argument("the reference-shape path applies the scatter operator only as y += scale * S phi");
+    {
+      Timed tm(c, "d2m");
+      gen::launch_d2m(*L.g, phi, order, true, L.g->src, c->stream);
+      ck_launch("d2m");
+    }
+    Timed tm(c, "m2d");
+    gen::launch_m2d(*L.g, L.g->src, order, scale, y, c->stream);
+    ck_launch("m2d");
+    c->launches += 2;
+    return;
+  }
   const int Hu = (order + 1) * (order + 1);
   const int n_el = L.t.n_el;
   const int K = scatter_chunks(c, L);
@@ -785,6 +914,13 @@ void op_residual(stamg_ctx* c, DevLevel& L, const double* f, const double* phi, 
 
 void op_sweep(stamg_ctx* c, DevLevel& L, const double* rhs, double* z, const double* base = nullptr) {
   Timed tm(c, "sweep");
+  if (L.g) {
+    if (base) throw std::logic_error("reference-shape sweep has no fused base vector");
+    gen::launch_sweep(*L.g, rhs, z, c->stream);
+    ck_launch("sweep");
+    c->launches += 1;
+    return;
+  }
   SweepParams p;
   p.g = geom(c, L);
   if (L.sweep_top) {
@@ -800,7 +936,7 @@ void op_sweep(stamg_ctx* c, DevLevel& L, const double* rhs, double* z, const dou
   if (L.sweep_xb > 1 && !base) {
     p.xb = L.sweep_xb, p.xflag = L.sweep_xflag, p.xtrace = L.sweep_xtrace;
     p.xb_smemb = std::getenv("STAMG_SWEEP_XB_SMEMB") != nullptr;
-    ck(cudaMemsetAsync(L.sweep_xflag, 0, sizeof(int) * L.t.group8_oct.size() * L.sweep_xb, c->stream), "memset");
+    ck(cudaMemsetAsync(L.sweep_xflag, 0, sizeof(int) * (L.t.group8_oct.size() * L.sweep_xb + 1), c->stream), "memset");
   }
   launch_sweep(p, c->stream);
   ck_launch("sweep");
@@ -811,11 +947,25 @@ void op_sweep(stamg_ctx* c, DevLevel& L, const double* rhs, double* z, const dou
 void op_smoother(stamg_ctx* c, DevLevel& L, const double* f, int order, double* phi) {
   if (!L.tmp) L.tmp = dalloc_zero<double>(L.n, c->stream);
   op_residual(c, L, f, phi, order, L.tmp);
+  if (L.g) {  // sweep the residual in place, then add (sweeps.cpp:110-112)
+    op_sweep(c, L, L.tmp, L.tmp);
+    launch_axpy(1.0, L.tmp, phi, L.n, c->stream);
+    c->launches += 1;
+    return;
+  }
   op_sweep(c, L, L.tmp, phi, phi);
 }
 
 void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* phi) {
   if (nu <= 0) return;
+  if (L.g) {
+    if (!L.g->BinvGS) throw std::invalid_argument("coarse_scatter_sweep: not the coarsest level");
+    Timed tm(c, "coarse_gs");
+    gen::launch_coarse_gs(*L.g, rhs, nu, phi, c->stream);
+    ck_launch("coarse_gs");
+    c->launches += 2;
+    return;
+  }
   if (!L.BinvGS) throw std::invalid_argument("coarse_scatter_sweep: not the coarsest level");
   // per-element moments of the current iterate (sweeps.cpp:74-79)
   op_d2m(c, L, phi, L.t.order, L.mom, L.ones, true);
@@ -827,6 +977,7 @@ void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* 
   p.done = L.gs_done, p.K = L.gs_K, p.Xo = L.gs_Xo, p.XoT = L.gs_XoT, p.GS = L.gs_G, p.n_mat = L.t.n_mat;
   p.cells_per_warp = L.gs_cpw, p.kpad = L.gs_kpad, p.grid_blocks = L.gs_blocks, p.rows_mode = L.gs_rows;
   p.multi_warp = L.gs_mw;
+  p.Minv = L.gs_Minv, p.chain_blk = L.gs_blk;
   p.cluster = L.gs_cluster, p.mb_np = L.gs_max_np, p.mb_slots = L.gs_mb_slots, p.mb_credit = L.gs_mb_credit;
   p.mom_stride = L.gs_mb_credit ? (L.t.H + 1) / 2 * 2 : 0;
   p.xreg = std::getenv("STAMG_GS_XGLOBAL") ? 0 : 1;
@@ -843,6 +994,12 @@ void op_prolong(stamg_ctx* c, int l, const double* coarse, double* fine, bool ad
   DevLevel& F = c->mg[l];
   DevLevel& Cl = c->mg[l - 1];
   Timed tm(c, "prolong");
+  if (F.g) {
+    gen::launch_prolong(*F.g, coarse, fine, Cl.t.P, add, c->stream);
+    ck_launch("prolong");
+    c->launches += 1;
+    return;
+  }
   launch_prolong(coarse, fine, F.up, F.up_w, F.t.n_el, F.t.P, Cl.t.P, add, c->stream);
   ck_launch("prolong");
   c->launches += 1;
@@ -852,6 +1009,12 @@ void op_restrict(stamg_ctx* c, int l, const double* fine, double* coarse) {
   DevLevel& F = c->mg[l];
   DevLevel& Cl = c->mg[l - 1];
   Timed tm(c, "restrict");
+  if (F.g) {
+    gen::launch_restrict(*F.g, fine, coarse, Cl.t.P, c->stream);
+    ck_launch("restrict");
+    c->launches += 1;
+    return;
+  }
   launch_restrict(fine, coarse, F.child_ptr, F.child_idx, F.up_w, F.t.n_el, F.t.P, Cl.t.P, c->stream);
   ck_launch("restrict");
   c->launches += 1;
@@ -1197,7 +1360,7 @@ stamg_report op_bicgstab(stamg_ctx* c, int precond, const double* b, double* x, 
 
 // host (reference layout, or internal patch order with `internal`) <-> device vector of a level
 void host_to_vec(stamg_ctx* c, DevLevel& L, const double* host, double* dev, bool internal) {
-  const int64_t nref = int64_t(L.t.n_el) * L.t.P * 4;
+  const int64_t nref = L.g ? L.n : int64_t(L.t.n_el) * L.t.P * 4;
   if (!L.wl.nd) {
     ck(cudaMemcpyAsync(dev, host, nref * sizeof(double), cudaMemcpyHostToDevice, c->stream), "h2d");
     return;
@@ -1218,7 +1381,7 @@ void host_to_vec(stamg_ctx* c, DevLevel& L, const double* host, double* dev, boo
   }
 }
 void vec_to_host(stamg_ctx* c, DevLevel& L, const double* dev, double* host, bool internal) {
-  const int64_t nref = int64_t(L.t.n_el) * L.t.P * 4;
+  const int64_t nref = L.g ? L.n : int64_t(L.t.n_el) * L.t.P * 4;
   if (!L.wl.nd) {
     ck(cudaMemcpyAsync(host, dev, nref * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "d2h");
     return;
@@ -1238,7 +1401,7 @@ void vec_to_host(stamg_ctx* c, DevLevel& L, const double* dev, double* host, boo
        "d2h");
   }
 }
-int64_t ref_size(const DevLevel& L) { return int64_t(L.t.n_el) * L.t.P * 4; }
+int64_t ref_size(const DevLevel& L) { return L.g ? L.n : int64_t(L.t.n_el) * L.t.P * 4; }
 
 template <class F>
 int guard(F&& f) {
@@ -1306,7 +1469,9 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
     if (!prob || !out) throw std::invalid_argument("stamg_create: null argument");
     auto c = std::make_unique<stamg_ctx>();
     c->pb = copy_problem(*prob);
-    validate(c->pb);
+    const bool generic = gen::handles(*prob);
+    if (generic) gen::validate(c->pb);
+    else validate(c->pb);
     c->pb.device_setup = std::getenv("STAMG_HOST_SETUP") == nullptr;  // couplings on the device
     c->device = opt ? opt->device : 0;
     c->rank = opt ? opt->rank : 0;
@@ -1343,6 +1508,24 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
     }
     const auto& s = c->pb.spec;
     c->tree = make_sphere(s.angular_kind, s.angular_level, s.cone_levels, s.cone_half_angle_deg);
+    if (generic) {  // reference-shape path: 3D / p0 / Lin problems on one GPU
+      if (c->world > 1) throw std::invalid_argument("the reference-shape path (3D, p0 or Lin) runs on one GPU");
+      c->wl_allowed = false, c->graphs_off = true;
+      c->outer.gt = gen::build_level(c->pb, c->tree, s.N, false);
+      upload_gen_level(c.get(), c->outer);
+      if (want_mg) {
+        c->nr = s.nr < 0 ? s.N : s.nr;
+        auto lv = gen::build_hierarchy(c->pb, c->tree, c->nr, s.n_levels);
+        c->mg.resize(lv.size());
+        for (size_t i = 0; i < lv.size(); ++i) {
+          c->mg[i].gt = std::move(lv[i]);
+          upload_gen_level(c.get(), c->mg[i]);
+        }
+        c->have_mg = true;
+      }
+      *out = c.release();
+      return;
+    }
     std::vector<std::vector<int>> parts;
     if (c->world > 1 && want_mg) {
       // sharded hierarchy: subtrees of the coarsest level per rank, coarsest replicated
@@ -1408,7 +1591,7 @@ int stamg_destroy(stamg_ctx* c) {
 int stamg_layout(stamg_ctx* c, int level, int out4[4]) {
   return guard_ctx(c, [&] {
     DevLevel& L = level_of(c, level);
-    out4[0] = L.t.n_el, out4[1] = L.t.P, out4[2] = 4, out4[3] = 1;
+    out4[0] = L.t.n_el, out4[1] = L.t.P, out4[2] = L.g ? L.g->S : 4, out4[3] = L.g ? L.g->D : 1;
   });
 }
 int stamg_patch_range(stamg_ctx* c, int level, int* q0, int* q1) {
@@ -1624,6 +1807,12 @@ int stamg_mg_apply(stamg_ctx* c, const stamg_vec* r, stamg_vec* z) {
 int stamg_rhs(stamg_ctx* c, stamg_vec* f) {
   return guard_ctx(c, [&] {
     need(f, c->outer, "assemble_rhs");
+    if (c->outer.g) {
+      const auto v = gen::assemble_rhs(c->pb, c->outer.gt, c->tree);
+      host_to_vec(c, c->outer, v.data(), f->d, true);
+      ck(cudaStreamSynchronize(c->stream), "sync");
+      return;
+    }
     const auto v = assemble_rhs(c->pb, c->outer.t, c->tree);  // tables' (internal) patch order
     host_to_vec(c, c->outer, v.data(), f->d, true);
     ck(cudaStreamSynchronize(c->stream), "sync");
@@ -1783,6 +1972,26 @@ int stamg_scalar_flux(stamg_ctx* c, const stamg_vec* phi, double* out) {
     std::vector<double> h(ref_size(c->outer));
     vec_to_host(c, c->outer, phi->d, h.data(), true);  // tables' (internal) patch order
     ck(cudaStreamSynchronize(c->stream), "sync");
+    if (c->outer.g) {  // harness.cpp:183-205: sum_q (M_q 1)_d phi_{el,q,d,i} (N 1)_i / volume
+      const gen::Tables& gt = c->outer.gt;
+      const auto& sp = c->pb.spec;
+      const double vol = (sp.box / sp.nx) * (sp.box / sp.ny) * (sp.dim == 3 ? sp.box / sp.nz : 1.0);
+      std::vector<double> nsum(gt.S, 0.0);
+      for (int i = 0; i < gt.S; ++i)
+        for (int j = 0; j < gt.S; ++j) nsum[i] += gt.Nmat[i * gt.S + j];
+      for (int el = 0; el < gt.n_el; ++el) {
+        double integral = 0;
+        for (int q = 0; q < gt.P; ++q)
+          for (int d = 0; d < gt.D; ++d) {
+            const double* blk = &h[(size_t(el) * gt.P + q) * gt.bs + d * gt.S];
+            double a = 0;
+            for (int i = 0; i < gt.S; ++i) a += blk[i] * nsum[i];
+            integral += gt.M1[size_t(q) * gt.D + d] * a;
+          }
+        out[el] = integral / vol;
+      }
+      return;
+    }
     const auto& t = c->outer.t;
     const double vol = c->pb.h * c->pb.h;
     for (int el = 0; el < t.n_el; ++el) {
@@ -1812,6 +2021,7 @@ int stamg_source_iteration(stamg_ctx* c, stamg_vec* psi, int n_iter) {
   return guard_ctx(c, [&] {
     DevLevel& O = c->outer;
     need(psi, O, "source_iteration");
+    if (O.g) throw std::invalid_argument("source_iteration is a throughput entry point of the 2D bilinear Const path");
     const int order = c->pb.spec.N;
     for (int it = 0; it < n_iter; ++it) {
       scatter_into(c, O, psi->d, order, 1.0, 0.0, psi->d, c->q_el);  // psi = q + S psi
@@ -1826,11 +2036,18 @@ int stamg_get_table(stamg_ctx* c, int level, const char* name, double* out, int6
     const LevelTables& t = L.t;
     std::vector<double> v;
     const std::string nm(name);
+    if (L.g && (nm == "X" || nm == "B" || nm == "Binv" || nm == "C" || nm == "M1" || nm == "upB")) {
+      const gen::Tables& gt = L.gt;
+      v = nm == "X" ? gt.X : nm == "B" ? gt.Bd : nm == "Binv" ? gt.Binv : nm == "C" ? gt.C : nm == "M1" ? gt.M1 : gt.upB;
+      *n = int64_t(v.size());
+      for (int64_t i = 0; out && i < cap && i < *n; ++i) out[i] = v[i];
+      return;
+    }
     if (nm == "fold") v = {double(L.fold_G), double(L.fold_R), double(L.fold_Hf), t.sym_defect, double(t.n_sym_axes)};
     else if (nm == "ar_chunks") v = {double(c->ar_chunks_used), double(c->comm_ar != nullptr)};
     else if (nm == "graphs") v = {double(c->mg_graphs.size()), double(c->graph_replays), double(c->graphs_off)};
     else if (nm == "gs_mode")
-      v = {double(L.gs_mw), double(L.gs_cluster), double(L.gs_rows), double(L.gs_mb_slots), double(L.gs_mb_credit)};
+      v = {double(L.gs_mw), double(L.gs_cluster), double(L.gs_rows), double(L.gs_mb_slots), double(L.gs_mb_credit), double(L.gs_blk)};
     else if (nm == "X") v = t.X;
     else if (nm == "B") v = t.B;
     else if (nm == "Binv") v = t.Binv;
@@ -1846,6 +2063,44 @@ int stamg_get_table(stamg_ctx* c, int level, const char* name, double* out, int6
     else throw std::invalid_argument("unknown table " + nm);
     *n = int64_t(v.size());
     if (out) std::memcpy(out, v.data(), std::min<int64_t>(cap, *n) * sizeof(double));
+  });
+}
+
+// Host only (no device): outer-level tables as the host setup builds them.
+int stamg_host_table(const stamg_problem* prob, const char* name, double* out, int64_t cap, int64_t* n) {
+  return guard([&] {
+    if (!prob || !name || !n) throw std::invalid_argument("stamg_host_table: null argument");
+    Problem pb = copy_problem(*prob);
+    const bool generic = gen::handles(*prob);
+    if (generic) gen::validate(pb);
+    else validate(pb);
+    const auto& s = pb.spec;
+    const SphereTree tree = make_sphere(s.angular_kind, s.angular_level, s.cone_levels, s.cone_half_angle_deg);
+    const std::string nm(name);
+    std::vector<double> v;
+    if (generic) {
+      const gen::Tables t = gen::build_level(pb, tree, s.N, false);
+      if (nm == "X") v = t.X;
+      else if (nm == "B") v = t.Bd;
+      else if (nm == "C") v = t.C;
+      else if (nm == "M1") v = t.M1;
+      else if (nm == "rhs") v = gen::assemble_rhs(pb, t, tree);
+      else if (nm == "octant") v.assign(t.octant.begin(), t.octant.end());
+      else if (nm == "layout") v = {double(t.n_el), double(t.P), double(t.S), double(t.D)};
+      else throw std::invalid_argument("unknown table");
+    } else {
+      const LevelTables t = build_level(pb, tree, s.N, false);
+      if (nm == "X") v = t.X;
+      else if (nm == "B") v = t.B;
+      else if (nm == "C") v = t.C;
+      else if (nm == "M1") v = t.area;
+      else if (nm == "rhs") v = assemble_rhs(pb, t, tree);
+      else if (nm == "octant") v.assign(t.octant.begin(), t.octant.end());
+      else if (nm == "layout") v = {double(t.n_el), double(t.P), 4.0, 1.0};
+      else throw std::invalid_argument("unknown table");
+    }
+    *n = int64_t(v.size());
+    for (int64_t i = 0; out && i < cap && i < *n; ++i) out[i] = v[i];
   });
 }
 

@@ -1,0 +1,382 @@
+// Kernels of the reference-shape path (generic.hpp): any block size bs = D*S <= 24, 2D or 3D
+// grids. Dense block arithmetic, hyperplane (KBA) ordering for the sweeps: cells with
+// fi + fj + fk = const in the octant's frame are independent (their upwind neighbours lie on
+// the previous plane), which is all the reference's element order (spatial_disc.cpp:90-106)
+// constrains.
+#include "common.cuh"
+#include "generic.hpp"
+
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+
+namespace cg = cooperative_groups;
+
+namespace stamg_b200 {
+namespace gen {
+
+namespace {
+
+struct Frame {  // octant frame <-> grid coordinates
+  int nx, ny, nz;
+  bool xn, yn, zn;
+  __device__ Frame(const Dev& L, int oct) : nx(L.nx), ny(L.ny), nz(L.nz), xn(oct & 1), yn(oct & 2), zn(oct & 4) {}
+  __device__ int el(int fi, int fj, int fk) const {
+    const int ix = xn ? nx - 1 - fi : fi, iy = yn ? ny - 1 - fj : fj, iz = zn ? nz - 1 - fk : fk;
+    return (iz * ny + iy) * nx + ix;
+  }
+};
+
+// upwind neighbour of cell el along axis xi for a patch of octant oct, -1 at the boundary
+// (HexMesh::neighbor with the inflow face, transport.cpp:50-52)
+__device__ __forceinline__ int upwind(const Dev& L, int el, int oct, int xi) {
+  const int ix = el % L.nx, iy = (el / L.nx) % L.ny, iz = el / (L.nx * L.ny);
+  const int dir = (oct >> xi) & 1 ? 1 : -1;  // positive cosine: inflow through the low face
+  int c[3] = {ix, iy, iz};
+  const int n[3] = {L.nx, L.ny, L.nz};
+  c[xi] += dir;
+  if (c[xi] < 0 || c[xi] >= n[xi]) return -1;
+  return (c[2] * L.ny + c[1]) * L.nx + c[0];
+}
+
+__global__ void apply_L_kernel(Dev L, const double* __restrict__ x, double* __restrict__ y, double alpha, double beta,
+                               const double* __restrict__ f) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int bs = L.bs;
+  if (idx >= (int64_t)L.n_el * L.P * bs) return;
+  const int r = int(idx % bs);
+  const int64_t blk = idx / bs;
+  const int q = int(blk % L.P), el = int(blk / L.P);
+  const int oct = L.octant[q];
+  const double* B = L.Bd + ((size_t)q * bs + r) * bs;
+  const double* xb = x + blk * bs;
+  double acc = 0.0;
+  for (int c = 0; c < bs; ++c) acc += B[c] * xb[c];
+  for (int xi = 0; xi < L.dim; ++xi) {
+    const int up = upwind(L, el, oct, xi);
+    if (up < 0) continue;
+    const double* C = L.C + (((size_t)q * 3 + xi) * bs + r) * bs;
+    const double* xu = x + ((size_t)up * L.P + q) * bs;
+    double a2 = 0.0;
+    for (int c = 0; c < bs; ++c) a2 += C[c] * xu[c];
+    acc += a2;
+  }
+  y[idx] = alpha * acc + (beta != 0.0 ? beta * f[idx] : 0.0);
+}
+
+// One CTA per patch; threads take the cells of one hyperplane at a time.
+__global__ void sweep_kernel(Dev L, const double* rhs, double* z) {
+  extern __shared__ __align__(16) double sm[];
+  const int bs = L.bs, q = blockIdx.x, oct = L.octant[q];
+  double* sBi = sm;                 // [bs][bs]
+  double* sC = sm + bs * bs;        // [dim][bs][bs]
+  for (int k = threadIdx.x; k < bs * bs; k += blockDim.x) {
+    sBi[k] = L.Binv[(size_t)q * bs * bs + k];
+    for (int xi = 0; xi < L.dim; ++xi) sC[xi * bs * bs + k] = L.C[((size_t)q * 3 + xi) * bs * bs + k];
+  }
+  __syncthreads();
+  const Frame fr(L, oct);
+  const int nplanes = L.nx + L.ny + L.nz - 2, njk = L.ny * L.nz;
+  for (int pl = 0; pl < nplanes; ++pl) {
+    for (int jk = threadIdx.x; jk < njk; jk += blockDim.x) {
+      const int fj = jk % L.ny, fk = jk / L.ny, fi = pl - fj - fk;
+      if (fi < 0 || fi >= L.nx) continue;
+      const int el = fr.el(fi, fj, fk);
+      double r[kMaxBs];
+      const double* rb = rhs + ((size_t)el * L.P + q) * bs;
+      for (int c = 0; c < bs; ++c) r[c] = rb[c];
+      for (int xi = 0; xi < L.dim; ++xi) {
+        const int fc = xi == 0 ? fi : xi == 1 ? fj : fk;
+        if (fc == 0) continue;
+        const int up = fr.el(fi - (xi == 0), fj - (xi == 1), fk - (xi == 2));
+        const double* zu = z + ((size_t)up * L.P + q) * bs;
+        const double* C = sC + xi * bs * bs;
+        for (int a = 0; a < bs; ++a) {
+          double acc = 0.0;
+          for (int c = 0; c < bs; ++c) acc += C[a * bs + c] * zu[c];
+          r[a] -= acc;
+        }
+      }
+      double* zb = z + ((size_t)el * L.P + q) * bs;
+      for (int a = 0; a < bs; ++a) {
+        double acc = 0.0;
+        for (int c = 0; c < bs; ++c) acc += sBi[a * bs + c] * r[c];
+        zb[a] = acc;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// mom[h][i] = sum_r X[r][h] phi[el][r][i]; with apply_sigma_N: out = sig_h (mom N)[h][i]
+__global__ void d2m_kernel(Dev L, const double* __restrict__ phi, int Hused, bool apply_sigma_N, double* __restrict__ out) {
+  extern __shared__ __align__(16) double sm[];  // [Hused][S]
+  const int el = blockIdx.x, S = L.S, R = L.P * L.D, H = L.H;
+  const double* slab = phi + (size_t)el * R * S;
+  for (int idx = threadIdx.x; idx < Hused * S; idx += blockDim.x) {
+    const int h = idx % Hused, i = idx / Hused;
+    double acc = 0.0;
+    for (int r = 0; r < R; ++r) acc += L.X[(size_t)r * H + h] * slab[(size_t)r * S + i];
+    sm[h * S + i] = acc;
+  }
+  __syncthreads();
+  double* o = out + (size_t)el * H * S;
+  for (int idx = threadIdx.x; idx < Hused * S; idx += blockDim.x) {
+    const int h = idx / S, i = idx % S;
+    double v = sm[idx];
+    if (apply_sigma_N) {
+      double acc = 0.0;
+      for (int j = 0; j < S; ++j) acc += sm[h * S + j] * L.Nmat[j * S + i];
+      v = L.sig[h] * acc;
+    }
+    o[idx] = v;
+  }
+}
+
+// y[el][r][i] += scale sum_h X[r][h] src[el][h][i]
+__global__ void m2d_kernel(Dev L, const double* __restrict__ src, int Hused, double scale, double* __restrict__ y) {
+  extern __shared__ __align__(16) double sm[];  // [Hused][S]
+  const int el = blockIdx.x, S = L.S, R = L.P * L.D, H = L.H;
+  for (int idx = threadIdx.x; idx < Hused * S; idx += blockDim.x) sm[idx] = src[(size_t)el * H * S + idx];
+  __syncthreads();
+  double* slab = y + (size_t)el * R * S;
+  for (int idx = threadIdx.x; idx < R * S; idx += blockDim.x) {
+    const int r = idx / S, i = idx % S;
+    const double* Xr = L.X + (size_t)r * H;
+    double acc = 0.0;
+    for (int h = 0; h < Hused; ++h) acc += Xr[h] * sm[h * S + i];
+    slab[idx] += scale * acc;
+  }
+}
+
+__global__ void prolong_kernel(Dev F, const double* __restrict__ coarse, double* __restrict__ fine, int Pc, bool add) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int S = F.S, D = F.D, bs = F.bs;
+  if (idx >= (int64_t)F.n_el * F.P * bs) return;
+  const int i = int(idx % S), d = int((idx / S) % D);
+  const int64_t blk = idx / bs;
+  const int q = int(blk % F.P), el = int(blk / F.P);
+  const double* B = F.upB + (size_t)q * D * D + d * D;
+  const double* cb = coarse + ((size_t)el * Pc + F.up[q]) * bs;
+  double acc = 0.0;
+  for (int e = 0; e < D; ++e) acc += B[e] * cb[e * S + i];
+  fine[idx] = add ? fine[idx] + acc : acc;
+}
+
+// coarse[el][c] = sum over the children q of c (ascending) of B_q^T fine[el][q]
+__global__ void restrict_kernel(Dev F, const double* __restrict__ fine, double* __restrict__ coarse, int Pc) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int S = F.S, D = F.D, bs = F.bs;
+  if (idx >= (int64_t)F.n_el * Pc * bs) return;
+  const int i = int(idx % S), e = int((idx / S) % D);
+  const int64_t blk = idx / bs;
+  const int c = int(blk % Pc), el = int(blk / Pc);
+  double acc = 0.0;
+  for (int k = F.child_ptr[c]; k < F.child_ptr[c + 1]; ++k) {
+    const int q = F.child_idx[k];
+    const double* B = F.upB + (size_t)q * D * D;
+    const double* fb = fine + ((size_t)el * F.P + q) * bs;
+    double a2 = 0.0;
+    for (int d = 0; d < D; ++d) a2 += B[d * D + e] * fb[d * S + i];
+    acc += a2;
+  }
+  coarse[idx] = acc;
+}
+
+// Scatter-implicit block Gauss-Seidel in the reference's order (sweeps.cpp:83-103):
+// passes, octants, cells in the octant's upwind order, the octant's patches in turn, the
+// cell's moments kept current after every patch. Cells of one hyperplane are independent
+// (a cell's moments are its own; its upwind neighbours are on the previous plane), so one
+// warp takes a cell and the grid synchronises between planes.
+constexpr int GS_WPB = 4;
+
+__host__ __device__ inline size_t gs_warp_doubles(int H, int S, int bs) { return size_t(H) * S + 32 * size_t(bs) + 4 * size_t(bs); }
+
+__global__ void __launch_bounds__(GS_WPB * 32) coarse_gs_kernel(Dev L, const double* __restrict__ rhs, double* phi, int nu) {
+  extern __shared__ __align__(16) double sm[];
+  cg::grid_group grid = cg::this_grid();
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int W = gridDim.x * GS_WPB, gw = blockIdx.x * GS_WPB + wib;
+  const int S = L.S, D = L.D, bs = L.bs, H = L.H, P = L.P;
+  double* smom = sm + wib * gs_warp_doubles(H, S, bs);  // [H][S]
+  double* red = smom + (size_t)H * S;                    // [bs][32]
+  double* sr = red + 32 * bs;                            // [bs] right-hand side
+  double* szo = sr + bs;                                 // [bs] previous iterate
+  double* sdz = szo + bs;                                // [bs] znew - zold
+  double* sv = sdz + bs;                                 // [bs] X sigma (mom - X^T zold)
+  const int nplanes = L.nx + L.ny + L.nz - 2, njk = L.ny * L.nz;
+  for (int pass = 0; pass < nu; ++pass)
+    for (int oct = 0; oct < 8; ++oct) {
+      const int pbeg = L.oct_ptr[oct], np = L.oct_ptr[oct + 1] - pbeg;
+      if (np == 0) continue;
+      const Frame fr(L, oct);
+      for (int pl = 0; pl < nplanes; ++pl) {
+        for (int jk = gw; jk < njk; jk += W) {
+          const int fj = jk % L.ny, fk = jk / L.ny, fi = pl - fj - fk;
+          if (fi < 0 || fi >= L.nx) continue;
+          const int el = fr.el(fi, fj, fk);
+          double* gm = L.mom + (size_t)el * H * S;
+          for (int k = lane; k < H * S; k += 32) smom[k] = __ldcg(gm + k);
+          __syncwarp();
+          for (int a = 0; a < np; ++a) {
+            const int q = L.oct_patches[pbeg + a];
+            const size_t blk = ((size_t)el * P + q) * bs;
+            // r = rhs - sum_xi C phi_up; previous iterate
+            if (lane < bs) {
+              double r = rhs[blk + lane];
+              for (int xi = 0; xi < L.dim; ++xi) {
+                const int fc = xi == 0 ? fi : xi == 1 ? fj : fk;
+                if (fc == 0) continue;
+                const int up = fr.el(fi - (xi == 0), fj - (xi == 1), fk - (xi == 2));
+                const double* C = L.C + (((size_t)q * 3 + xi) * bs + lane) * bs;
+                const double* pu = phi + ((size_t)up * P + q) * bs;
+                double acc = 0.0;
+                for (int c = 0; c < bs; ++c) acc += C[c] * __ldcg(pu + c);
+                r -= acc;
+              }
+              sr[lane] = r;
+              szo[lane] = __ldcg(phi + blk + lane);
+            }
+            __syncwarp();
+            // v[d][j] = sum_h X[(q,d)][h] sig_h (mom[h][j] - sum_e X[(q,e)][h] zold[e][j])
+            {
+              double part[3][8];
+#pragma unroll
+              for (int d = 0; d < 3; ++d)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) part[d][j] = 0.0;
+              for (int h = lane; h < H; h += 32) {
+                double xq[3];
+#pragma unroll
+                for (int d = 0; d < 3; ++d) xq[d] = d < D ? L.X[((size_t)q * D + d) * H + h] : 0.0;
+                const double sg = L.sig[h];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  if (j >= S) break;
+                  double t = 0.0;
+#pragma unroll
+                  for (int e = 0; e < 3; ++e)
+                    if (e < D) t += xq[e] * szo[e * S + j];
+                  const double u = sg * (smom[h * S + j] - t);
+#pragma unroll
+                  for (int d = 0; d < 3; ++d)
+                    if (d < D) part[d][j] += xq[d] * u;
+                }
+              }
+#pragma unroll
+              for (int d = 0; d < 3; ++d)
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  if (d < D && j < S) red[(d * S + j) * 32 + lane] = part[d][j];
+            }
+            __syncwarp();
+            if (lane < bs) {
+              double acc = 0.0;
+              for (int m = 0; m < 32; ++m) acc += red[lane * 32 + m];
+              sv[lane] = acc;
+            }
+            __syncwarp();
+            if (lane < bs) {  // r += v N
+              const int d = lane / S, i = lane - d * S;
+              double acc = 0.0;
+              for (int j = 0; j < S; ++j) acc += sv[d * S + j] * L.Nmat[j * S + i];
+              sr[lane] += acc;
+            }
+            __syncwarp();
+            if (lane < bs) {  // znew = (B - sq N)^-1 r
+              const double* Bi = L.BinvGS + ((size_t)q * bs + lane) * bs;
+              double acc = 0.0;
+              for (int c = 0; c < bs; ++c) acc += Bi[c] * sr[c];
+              __stcg(phi + blk + lane, acc);
+              sdz[lane] = acc - szo[lane];
+            }
+            __syncwarp();
+            // mom += X_q^T (znew - zold)
+            for (int k = lane; k < H * S; k += 32) {
+              const int h = k / S, j = k - h * S;
+              double acc = 0.0;
+              for (int d = 0; d < D; ++d) acc += L.X[((size_t)q * D + d) * H + h] * sdz[d * S + j];
+              smom[k] += acc;
+            }
+            __syncwarp();
+          }
+          for (int k = lane; k < H * S; k += 32) __stcg(gm + k, smom[k]);
+          __syncwarp();
+        }
+        grid.sync();
+      }
+    }
+}
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("cuda: ") + what + ": " + cudaGetErrorString(e));
+}
+
+int blocks_for(int64_t n, int bsz) { return int((n + bsz - 1) / bsz); }
+
+}  // namespace
+
+void launch_apply_L(const Dev& L, const double* x, double* y, double alpha, double beta, const double* f, cudaStream_t s) {
+  const int64_t n = (int64_t)L.n_el * L.P * L.bs;
+  if (n == 0) return;
+  apply_L_kernel<<<blocks_for(n, 256), 256, 0, s>>>(L, x, y, alpha, f ? beta : 0.0, f);
+}
+
+void launch_sweep(const Dev& L, const double* rhs, double* z, cudaStream_t s) {
+  if (L.P == 0 || L.n_el == 0) return;
+  const size_t smem = sizeof(double) * size_t(1 + L.dim) * L.bs * L.bs;
+  const int threads = std::min(256, std::max(32, (L.ny * L.nz + 31) / 32 * 32));
+  sweep_kernel<<<L.P, threads, smem, s>>>(L, rhs, z);
+}
+
+void launch_d2m(const Dev& L, const double* phi, int order, bool apply_sigma_N, double* out, cudaStream_t s) {
+  const int Hused = (order + 1) * (order + 1);
+  const size_t smem = sizeof(double) * size_t(Hused) * L.S;
+  if (smem > 200 * 1024) throw std::invalid_argument("reference-shape scatter: (order+1)^2 * S moments exceed shared memory");
+  if (smem > 48 * 1024) ck(cudaFuncSetAttribute(d2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+  d2m_kernel<<<L.n_el, 128, smem, s>>>(L, phi, Hused, apply_sigma_N, out);
+}
+
+void launch_m2d(const Dev& L, const double* src, int order, double scale, double* y, cudaStream_t s) {
+  const int Hused = (order + 1) * (order + 1);
+  const size_t smem = sizeof(double) * size_t(Hused) * L.S;
+  if (smem > 200 * 1024) throw std::invalid_argument("reference-shape scatter: (order+1)^2 * S moments exceed shared memory");
+  if (smem > 48 * 1024) ck(cudaFuncSetAttribute(m2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+  m2d_kernel<<<L.n_el, 128, smem, s>>>(L, src, Hused, scale, y);
+}
+
+void launch_prolong(const Dev& F, const double* coarse, double* fine, int Pc, bool add, cudaStream_t s) {
+  const int64_t n = (int64_t)F.n_el * F.P * F.bs;
+  if (n == 0) return;
+  prolong_kernel<<<blocks_for(n, 256), 256, 0, s>>>(F, coarse, fine, Pc, add);
+}
+
+void launch_restrict(const Dev& F, const double* fine, double* coarse, int Pc, cudaStream_t s) {
+  const int64_t n = (int64_t)F.n_el * Pc * F.bs;
+  if (n == 0) return;
+  restrict_kernel<<<blocks_for(n, 256), 256, 0, s>>>(F, fine, coarse, Pc);
+}
+
+void launch_coarse_gs(const Dev& L, const double* rhs, int nu, double* phi, cudaStream_t s) {
+  if (nu <= 0 || L.n_el == 0) return;
+  launch_d2m(L, phi, L.order, false, L.mom, s);  // moments of the current iterate (sweeps.cpp:74-79)
+  const size_t smem = sizeof(double) * GS_WPB * gs_warp_doubles(L.H, L.S, L.bs);
+  if (smem > 200 * 1024) throw std::invalid_argument("reference-shape coarse GS: moments exceed shared memory");
+  ck(cudaFuncSetAttribute(coarse_gs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_gs_kernel, GS_WPB * 32, smem), "occupancy");
+  const int want = (L.ny * L.nz + GS_WPB - 1) / GS_WPB;  // at most ny*nz cells per plane
+  const int grid = std::max(1, std::min(want, sms * std::max(per_sm, 1)));
+  Dev Lc = L;
+  const double* r = rhs;
+  void* args[] = {&Lc, &r, &phi, &nu};
+  ck(cudaLaunchCooperativeKernel((const void*)coarse_gs_kernel, dim3(grid), dim3(GS_WPB * 32), args, smem, s),
+     "coarse_gs cooperative launch");
+}
+
+}  // namespace gen
+}  // namespace stamg_b200

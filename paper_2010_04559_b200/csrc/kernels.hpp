@@ -145,6 +145,8 @@ struct CoarseGSParams {
   const double* Xo = nullptr;     // [P][Hp] X rows in octant order (oct_patches)
   const double* XoT = nullptr;    // [Hp][P] its transpose
   const double* K = nullptr;      // [n_mat][P][kpad] X_a sig X_b^T, a = octant-ordered row, b = index in octant
+  const double* Minv = nullptr;   // [n_mat][8][kpad/4][160] packed inverses of the chain's 4-patch diagonal blocks
+  int chain_blk = 0;              // 1: blocked patch chain (multi-warp kernel; kpad a multiple of 4)
   int cells_per_warp = 0, kpad = 0, grid_blocks = 0;  // warp owns a row segment of cells_per_warp cells
   int xreg = 1;       // x-upwind traces inside a segment from registers (0: through global memory)
   int rows_mode = 0;  // > 0: warp owns a whole row, CTA = rows_mode consecutive rows (shared mailbox)
@@ -163,10 +165,14 @@ void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s);
 int coarse_gs_max_warps(int Hp, int kpad, int nmat, int max_np);
 int coarse_gs_warps_per_block(int Hp, int kpad, int nmat);
 int coarse_gs_rows_wpb(int Hp, int kpad, int nmat, int nx, int ny, int max_np);
-int coarse_gs_mw_ok(int Hp, int H, int kpad, int nmat, int ny, int max_np);
+int coarse_gs_mw_ok(int Hp, int H, int kpad, int nmat, int ny, int max_np, bool blk);
+// blocked patch chain of the multi-warp kernel (default; STAMG_GS_CHAIN_BLOCKS=0 keeps the
+// patch-by-patch chain), and the packed size of one 16 x 16 block inverse
+bool coarse_gs_chain_blocked();
+constexpr int kGsMinvBlock = 160;
 // multi-warp rows in clusters: (mailbox slots << 8) | (credit << 7) | rows per cluster (16, 8, 4 or 2)
 // for the largest mailbox whose clusters all fit co-resident, 0 if none
-int coarse_gs_cluster_rows(int Hp, int H, int kpad, int nmat, int nx, int ny, int max_np);
+int coarse_gs_cluster_rows(int Hp, int H, int kpad, int nmat, int nx, int ny, int max_np, bool blk);
 
 // BLAS-1 (deterministic reductions)
 void launch_fill(double* x, double v, int64_t n, cudaStream_t s);

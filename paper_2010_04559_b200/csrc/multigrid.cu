@@ -431,8 +431,20 @@ constexpr int GSW_MW = 4;
 constexpr int MW_BAR = 1;  // named barrier of warps 1..3
 
 __host__ __device__ inline int gs_mw_xs(int H) { return (H % 2 == 0) ? H + 1 : H + 2; }  // odd X row stride
-__host__ __device__ inline size_t gs_mw_doubles(int Hp, int H, int kpad, int nmat, int hs = 0) {
-  return size_t(hs > 0 ? hs : Hp) * 16 + size_t(kpad) * 32 + size_t(nmat) * kpad * kpad + size_t(kpad) * gs_mw_xs(H) +
+// Blocked chain: the chain's K region holds, per material, the K columns right of each 4-patch
+// diagonal block (rows 4J..4J+3 from column 4(J+1): kpad^2/2 - 2 kpad doubles), the diagonal
+// sq_a = K[a][a], and the packed inverses of the diagonal blocks (kGsMinvBlock doubles per
+// block: column c of the 16 x 16 unit lower block-triangular inverse from row 4 (c / 4));
+// then 16 doubles for the block's right-hand side.
+__host__ __device__ inline int gs_koff(int J, int kpad) { return 4 * J * kpad - 8 * J * (J + 1); }
+__host__ __device__ inline size_t gs_blk_mat_doubles(int kpad) {
+  return size_t(gs_koff(kpad / 4, kpad)) + kpad + size_t(kpad / 4) * kGsMinvBlock;
+}
+__host__ __device__ inline size_t gs_mw_kregion(int kpad, int nmat, bool blk) {
+  return blk ? size_t(nmat) * gs_blk_mat_doubles(kpad) + 16 : size_t(nmat) * kpad * kpad;
+}
+__host__ __device__ inline size_t gs_mw_doubles(int Hp, int H, int kpad, int nmat, int hs, bool blk) {
+  return size_t(hs > 0 ? hs : Hp) * 16 + size_t(kpad) * 32 + gs_mw_kregion(kpad, nmat, blk) + size_t(kpad) * gs_mw_xs(H) +
          size_t(nmat) * Hp + 8;  // + oct_ptr
 }
 
@@ -519,7 +531,15 @@ __device__ __forceinline__ void st_relaxed(int* p, int v) {
 // the previous item's flag at the top of each iteration instead (the helpers have slack there)
 template <int NS, bool CL>
 constexpr bool gs_pubw() { return CL && NS == 1; }
-template <int NS, bool CL = false, bool RING = false>
+// BLK: the patch chain in blocks of four patches. With f_a = e_a + G_a t_a the chain solves
+// (I - blockdiag(G_a) (L_K x I_4)) dz = f, L_K the strictly lower part of K: unit lower
+// block-triangular, and a function of (octant, material) only, never of the cell. The host
+// inverts its 16 x 16 diagonal blocks once (gs_minv_table); per block the warp forms f for
+// the block's patches, applies the inverse (one row per lane, four independent FMA chains) and
+// adds the block's dz into the t of the patches to its right (4 x 4 FMAs per lane and slot):
+// np / 4 dependent steps instead of np. Results differ from the patch-by-patch chain at the
+// rounding level (the inverse is formed in extended precision).
+template <int NS, bool CL = false, bool RING = false, bool BLK = true>
 __global__ void __launch_bounds__(GSW_MW * 32 + (gs_pubw<NS, CL>() ? 32 : 0), 2) coarse_gs_mw_kernel(CoarseGSParams p) {
   constexpr bool PUBW = gs_pubw<NS, CL>();
   extern __shared__ __align__(16) double gsm[];
@@ -532,9 +552,12 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (gs_pubw<NS, CL>() ? 32 : 0), 2)
   double* sdz = smom + HS * 16;                   // [2][kpad][4] chain outputs (sweep frame)
   double* st0 = sdz + kpad * 8;                   // [2][kpad][4] projections (physical dofs)
   double* srz = st0 + kpad * 8;                   // [2][kpad][8] warp 0: rhs | iterate of the next item
-  double* sK = srz + kpad * 16;                   // [n_mat][kpad][kpad]
-  double* sX = sK + (size_t)nmat * kpad * kpad;   // [kpad][Hp+1]
+  double* sK = srz + kpad * 16;                   // [n_mat][kpad][kpad]; BLK: [n_mat](Koff | sq | Minv), f[16]
+  double* sX = sK + gs_mw_kregion(kpad, nmat, BLK);  // [kpad][Hp+1]
   const int XS = gs_mw_xs(H);
+  const int matd = int(gs_blk_mat_doubles(kpad));           // BLK: doubles per material
+  const int sq_off = gs_koff(kpad / 4, kpad), minv_off = sq_off + kpad;
+  double* sF = sK + (size_t)nmat * matd;                    // BLK: right-hand side of the current block
   double* sS = sX + (size_t)kpad * XS;            // [n_mat][Hp]
   if (tid < nthr)
     for (int c = tid; c < nmat * Hp; c += nthr) sS[c] = p.sig[c];
@@ -613,9 +636,24 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (gs_pubw<NS, CL>() ? 32 : 0), 2)
   };
   auto stage_octant = [&](int oct) {  // all threads; caller synchronises
     const int pbeg = p.oct_ptr[oct], np = p.oct_ptr[oct + 1] - pbeg;
-    for (int mm = 0; mm < nmat; ++mm)
-      for (int c = tid; c < np * kpad / 2; c += nthr)
-        cp_async16(sK + ((size_t)mm * kpad * kpad) + c * 2, p.K + ((size_t)mm * P + pbeg) * kpad + c * 2, true);
+    if constexpr (BLK) {
+      const int hk = kpad >> 1, nb = (np + 3) >> 2;
+      for (int mm = 0; mm < nmat; ++mm) {
+        double* dm = sK + (size_t)mm * matd;
+        const double* Km = p.K + ((size_t)mm * P + pbeg) * kpad;
+        for (int c = tid; c < np * hk; c += nthr) {  // row a of K from the column after its block
+          const int a = c / hk, col = (c - a * hk) * 2, J = a >> 2, c0 = 4 * (J + 1);
+          if (col >= c0) cp_async16(dm + gs_koff(J, kpad) + (a & 3) * (kpad - c0) + (col - c0), Km + (size_t)a * kpad + col, true);
+        }
+        for (int a = tid; a < np; a += nthr) cp_async8(dm + sq_off + a, Km + (size_t)a * kpad + a, true);
+        const double* Mi = p.Minv + ((size_t)mm * 8 + oct) * (kpad >> 2) * kGsMinvBlock;
+        for (int c = tid; c < nb * (kGsMinvBlock / 2); c += nthr) cp_async16(dm + minv_off + c * 2, Mi + c * 2, true);
+      }
+    } else {
+      for (int mm = 0; mm < nmat; ++mm)
+        for (int c = tid; c < np * kpad / 2; c += nthr)
+          cp_async16(sK + ((size_t)mm * kpad * kpad) + c * 2, p.K + ((size_t)mm * P + pbeg) * kpad + c * 2, true);
+    }
     for (int c = tid; c < np * H; c += nthr) {
       const int a = c / H, h = c - a * H;
       cp_async8(sX + (size_t)a * XS + h, p.Xo + (size_t)(pbeg + a) * Hp + h, true);
@@ -822,7 +860,7 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (gs_pubw<NS, CL>() ? 32 : 0), 2)
           r[sl][1] -= cxy[6] * uy[2] + cxy[7] * uy[3];
         }
       }
-      const double* sKm = sK + (size_t)mt * kpad * kpad;
+      const double* sKm = sK + (size_t)mt * (BLK ? matd : kpad * kpad);
       double e[NS][4];
 #pragma unroll
       for (int sl = 0; sl < NS; ++sl) {
@@ -832,7 +870,7 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (gs_pubw<NS, CL>() ? 32 : 0), 2)
           continue;
         }
         const int a = lane + 32 * sl;
-        const double sq = sKm[(size_t)a * kpad + a];
+        const double sq = BLK ? sKm[sq_off + a] : sKm[(size_t)a * kpad + a];
         double szo[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) szo[i] = sq * zo[sl][i];
@@ -854,6 +892,66 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (gs_pubw<NS, CL>() ? 32 : 0), 2)
         }
       }
       double* dzb = sdz + (it & 1) * kpad * 4;
+      if constexpr (BLK) {
+        const int nblk = (np + 3) >> 2, row = lane & 15;
+        const double* sMi = sKm + minv_off;
+        for (int J = 0; J < nblk; ++J) {
+          const int sl = J >> 3, l0 = (4 * J) & 31;
+          // f of the block's four patches (every lane forms its own slot's candidate)
+          double fb[4];
+#pragma unroll
+          for (int s2 = 0; s2 < NS; ++s2)
+            if (s2 == sl)
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                fb[i] = e[s2][i] + (G[s2][4 * i] * t[s2][0] + G[s2][4 * i + 1] * t[s2][1] +
+                                    G[s2][4 * i + 2] * t[s2][2] + G[s2][4 * i + 3] * t[s2][3]);
+          if (unsigned(lane - l0) < 4u) {
+            reinterpret_cast<double2*>(sF)[2 * (lane - l0)] = make_double2(fb[0], fb[1]);
+            reinterpret_cast<double2*>(sF)[2 * (lane - l0) + 1] = make_double2(fb[2], fb[3]);
+          }
+          __syncwarp();
+          // dz = Minv f: lane = row (lanes 16..31 mirror), column c stored from row 4 (c / 4)
+          {
+            const double* M = sMi + J * kGsMinvBlock;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb) {
+              const double2 fa = reinterpret_cast<const double2*>(sF)[2 * cb], fc = reinterpret_cast<const double2*>(sF)[2 * cb + 1];
+              const int len = 16 - 4 * cb, idx = row - 4 * cb, base = 64 * cb - 8 * cb * (cb - 1);
+              if (idx >= 0) {
+                const double* mc = M + base + idx;
+                a0 += mc[0] * fa.x, a1 += mc[len] * fa.y, a2 += mc[2 * len] * fc.x, a3 += mc[3 * len] * fc.y;
+              }
+            }
+            if (lane < 16) dzb[16 * J + lane] = (a0 + a1) + (a2 + a3);
+          }
+          __syncwarp();
+          // t of the patches right of the block
+          const int c0 = 4 * (J + 1), Lj = kpad - c0, na = min(4, np - 4 * J);
+          if (c0 < np) {
+            const double* Kb = sKm + gs_koff(J, kpad);
+            double2 d[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) d[k] = reinterpret_cast<const double2*>(dzb + 16 * J)[k];
+#pragma unroll
+            for (int s2 = 0; s2 < NS; ++s2) {
+              const int b = lane + 32 * s2;
+              if (32 * s2 + 31 < c0) continue;  // warp-uniform: the whole slot is left of the block's end
+              if (b >= c0) {
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                  if (a < na) {
+                    const double k = Kb[a * Lj + (b - c0)];
+                    t[s2][0] += k * d[2 * a].x, t[s2][1] += k * d[2 * a].y;
+                    t[s2][2] += k * d[2 * a + 1].x, t[s2][3] += k * d[2 * a + 1].y;
+                  }
+                }
+              }
+            }
+          }
+        }
+      } else {
       for (int a = 0; a < np; ++a) {
         const int sl = a >> 5, src = a & 31;
         double dz[4];
@@ -877,6 +975,7 @@ __global__ void __launch_bounds__(GSW_MW * 32 + (gs_pubw<NS, CL>() ? 32 : 0), 2)
           reinterpret_cast<double2*>(dzb)[2 * a] = make_double2(dz[0], dz[1]);
           reinterpret_cast<double2*>(dzb)[2 * a + 1] = make_double2(dz[2], dz[3]);
         }
+      }
       }
       __syncwarp();
 #pragma unroll
@@ -1050,25 +1149,32 @@ int coarse_gs_max_warps(int Hp, int kpad, int nmat, int max_np) {
 int coarse_gs_warps_per_block(int Hp, int kpad, int nmat) { return gs_wpb(Hp, kpad, nmat); }
 
 // multi-warp rows: whether the ny row-CTAs fit co-resident (0 = no)
-int coarse_gs_mw_ok(int Hp, int H, int kpad, int nmat, int ny, int max_np) {
+bool coarse_gs_chain_blocked() {
+  const char* e = std::getenv("STAMG_GS_CHAIN_BLOCKS");
+  return !(e != nullptr && e[0] == '0' && e[1] == 0);
+}
+
+int coarse_gs_mw_ok(int Hp, int H, int kpad, int nmat, int ny, int max_np, bool blk) {
   if (max_np > 64) return 0;
-  const size_t smem = sizeof(double) * gs_mw_doubles(Hp, H, kpad, nmat);
+  if (blk && kpad % 4 != 0) return 0;
+  const size_t smem = sizeof(double) * gs_mw_doubles(Hp, H, kpad, nmat, 0, blk);
   if (smem > 220 * 1024) return 0;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  auto k = max_np > 32 ? coarse_gs_mw_kernel<2> : coarse_gs_mw_kernel<1>;
+  auto k = max_np > 32 ? (blk ? coarse_gs_mw_kernel<2, false, false, true> : coarse_gs_mw_kernel<2, false, false, false>)
+                       : (blk ? coarse_gs_mw_kernel<1, false, false, true> : coarse_gs_mw_kernel<1, false, false, false>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, GSW_MW * 32, smem);
   return per_sm * sms >= ny ? 1 : 0;
 }
 
-size_t gs_mw_cl_smem(int Hp, int H, int kpad, int nmat, int nslots, int mbnp, int hs) {
-  return sizeof(double) * (gs_mw_doubles(Hp, H, kpad, nmat, hs) + gs_mw_cl_doubles(nslots, mbnp));
+size_t gs_mw_cl_smem(int Hp, int H, int kpad, int nmat, int nslots, int mbnp, int hs, bool blk) {
+  return sizeof(double) * (gs_mw_doubles(Hp, H, kpad, nmat, hs, blk) + gs_mw_cl_doubles(nslots, mbnp));
 }
 int gs_ring_hs(int H) { return (H + 1) & ~1; }  // rings: the compact moment ring makes room for the mailbox
 
-template <int NS, bool RING>
+template <int NS, bool RING, bool BLK>
 cudaLaunchConfig_t gs_cl_config(const CoarseGSParams& p, cudaLaunchAttribute* at, size_t smem, int rows, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.ny), cfg.blockDim = dim3((GSW_MW + (gs_pubw<NS, true>() ? 1 : 0)) * 32);
@@ -1076,14 +1182,14 @@ cudaLaunchConfig_t gs_cl_config(const CoarseGSParams& p, cudaLaunchAttribute* at
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = rows, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
   cfg.attrs = at, cfg.numAttrs = 1;
-  auto k = coarse_gs_mw_kernel<NS, true, RING>;
+  auto k = coarse_gs_mw_kernel<NS, true, RING, BLK>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   return cfg;
 }
 
 // rows per cluster and mailbox slots per direction (slots << 8 | credit << 7 | rows), 0 if none
-template <int NS>
+template <int NS, bool BLK>
 int gs_cluster_rows_t(int Hp, int H, int kpad, int nmat, int nx, int ny, int max_np) {
   // rings with credits (for mailboxes of two octants that do not fit) are opt-in: at config 4
   // (64 patches per octant, 4-slot ring) they measured 0.319 s per coarse solve against 0.311 s
@@ -1093,18 +1199,18 @@ int gs_cluster_rows_t(int Hp, int H, int kpad, int nmat, int nx, int ny, int max
     const bool credit = nslots != 2 * nx;
     if (credit && !rings) break;
     if (credit && nslots >= 2 * nx) continue;
-    const size_t smem = gs_mw_cl_smem(Hp, H, kpad, nmat, nslots, max_np, credit ? gs_ring_hs(H) : 0);
+    const size_t smem = gs_mw_cl_smem(Hp, H, kpad, nmat, nslots, max_np, credit ? gs_ring_hs(H) : 0, BLK);
     if (smem > 112 * 1024) continue;  // keep two row-CTAs per SM
     for (int rows : {16, 8, 4, 2}) {
       if (ny % rows != 0 || ny / rows < 2) continue;
       CoarseGSParams p;
       p.ny = ny;
       cudaLaunchAttribute at[1];
-      cudaLaunchConfig_t cfg = credit ? gs_cl_config<NS, true>(p, at, smem, rows, nullptr)
-                                      : gs_cl_config<NS, false>(p, at, smem, rows, nullptr);
+      cudaLaunchConfig_t cfg = credit ? gs_cl_config<NS, true, BLK>(p, at, smem, rows, nullptr)
+                                      : gs_cl_config<NS, false, BLK>(p, at, smem, rows, nullptr);
       int nclusters = 0;
-      const cudaError_t e = credit ? cudaOccupancyMaxActiveClusters(&nclusters, coarse_gs_mw_kernel<NS, true, true>, &cfg)
-                                   : cudaOccupancyMaxActiveClusters(&nclusters, coarse_gs_mw_kernel<NS, true, false>, &cfg);
+      const cudaError_t e = credit ? cudaOccupancyMaxActiveClusters(&nclusters, coarse_gs_mw_kernel<NS, true, true, BLK>, &cfg)
+                                   : cudaOccupancyMaxActiveClusters(&nclusters, coarse_gs_mw_kernel<NS, true, false, BLK>, &cfg);
       if (e != cudaSuccess) {
         cudaGetLastError();
         continue;
@@ -1115,26 +1221,26 @@ int gs_cluster_rows_t(int Hp, int H, int kpad, int nmat, int nx, int ny, int max
   return 0;
 }
 
-template <int NS>
+template <int NS, bool BLK>
 void launch_gs_mw_cluster(const CoarseGSParams& p, cudaStream_t s) {
-  const size_t smem = gs_mw_cl_smem(p.Hp, p.H, p.kpad, p.n_mat, p.mb_slots, p.mb_np, p.mom_stride);
+  const size_t smem = gs_mw_cl_smem(p.Hp, p.H, p.kpad, p.n_mat, p.mb_slots, p.mb_np, p.mom_stride, BLK);
   cudaLaunchAttribute at[1];
   cudaError_t e;
   if (p.mb_credit) {
-    cudaLaunchConfig_t cfg = gs_cl_config<NS, true>(p, at, smem, p.cluster, s);
-    e = cudaLaunchKernelEx(&cfg, coarse_gs_mw_kernel<NS, true, true>, p);
+    cudaLaunchConfig_t cfg = gs_cl_config<NS, true, BLK>(p, at, smem, p.cluster, s);
+    e = cudaLaunchKernelEx(&cfg, coarse_gs_mw_kernel<NS, true, true, BLK>, p);
   } else {
-    cudaLaunchConfig_t cfg = gs_cl_config<NS, false>(p, at, smem, p.cluster, s);
-    e = cudaLaunchKernelEx(&cfg, coarse_gs_mw_kernel<NS, true, false>, p);
+    cudaLaunchConfig_t cfg = gs_cl_config<NS, false, BLK>(p, at, smem, p.cluster, s);
+    e = cudaLaunchKernelEx(&cfg, coarse_gs_mw_kernel<NS, true, false, BLK>, p);
   }
   if (e != cudaSuccess) throw std::runtime_error(std::string("coarse_gs cluster launch: ") + cudaGetErrorString(e));
 }
 
-template <int NS>
+template <int NS, bool BLK>
 void launch_gs_mw(const CoarseGSParams& p, cudaStream_t s) {
-  if (p.cluster > 1) return launch_gs_mw_cluster<NS>(p, s);
-  auto k = coarse_gs_mw_kernel<NS>;
-  const size_t smem = sizeof(double) * gs_mw_doubles(p.Hp, p.H, p.kpad, p.n_mat);
+  if (p.cluster > 1) return launch_gs_mw_cluster<NS, BLK>(p, s);
+  auto k = coarse_gs_mw_kernel<NS, false, false, BLK>;
+  const size_t smem = sizeof(double) * gs_mw_doubles(p.Hp, p.H, p.kpad, p.n_mat, 0, BLK);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   CoarseGSParams q = p;
   void* args[] = {&q};
@@ -1142,17 +1248,26 @@ void launch_gs_mw(const CoarseGSParams& p, cudaStream_t s) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("coarse_gs cooperative launch: ") + cudaGetErrorString(e));
 }
 
-int coarse_gs_cluster_rows(int Hp, int H, int kpad, int nmat, int nx, int ny, int max_np) {
+int coarse_gs_cluster_rows(int Hp, int H, int kpad, int nmat, int nx, int ny, int max_np, bool blk) {
   if (max_np > 64) return 0;
-  return max_np > 32 ? gs_cluster_rows_t<2>(Hp, H, kpad, nmat, nx, ny, max_np)
-                     : gs_cluster_rows_t<1>(Hp, H, kpad, nmat, nx, ny, max_np);
+  if (blk)
+    return max_np > 32 ? gs_cluster_rows_t<2, true>(Hp, H, kpad, nmat, nx, ny, max_np)
+                       : gs_cluster_rows_t<1, true>(Hp, H, kpad, nmat, nx, ny, max_np);
+  return max_np > 32 ? gs_cluster_rows_t<2, false>(Hp, H, kpad, nmat, nx, ny, max_np)
+                     : gs_cluster_rows_t<1, false>(Hp, H, kpad, nmat, nx, ny, max_np);
 }
 
 void launch_coarse_gs(const CoarseGSParams& p, cudaStream_t s) {
   if (p.nu <= 0 || p.n_el == 0) return;
   if (p.multi_warp) {
-    if (p.max_patches_per_octant <= 32) launch_gs_mw<1>(p, s);
-    else launch_gs_mw<2>(p, s);
+    if (p.chain_blk) {
+      if (p.Minv == nullptr || p.kpad % 4 != 0) throw std::logic_error("coarse_scatter_sweep: blocked chain without its tables");
+      if (p.max_patches_per_octant <= 32) launch_gs_mw<1, true>(p, s);
+      else launch_gs_mw<2, true>(p, s);
+    } else {
+      if (p.max_patches_per_octant <= 32) launch_gs_mw<1, false>(p, s);
+      else launch_gs_mw<2, false>(p, s);
+    }
     return;
   }
   if (p.max_patches_per_octant <= 32) launch_gs2<1>(p, s);

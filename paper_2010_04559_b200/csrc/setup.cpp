@@ -260,6 +260,23 @@ void for_each_node(const SphereTree& t, int id, int order, F&& f) {
 
 }  // namespace
 
+// The same rule with its flat-triangle barycentric coordinates (1-u, u(1-v), uv), the nodal
+// Lin basis of angular_disc.cpp:40-59 (quadrature.cpp:84).
+void patch_rule(const SphereTree& t, int id, int order, std::vector<double>& om, std::vector<double>& bary,
+                std::vector<double>& w) {
+  const Rule1D& g = gauss01(order);
+  om.clear(), bary.clear(), w.clear();
+  for_each_node(t, id, order, [&](const double* o, double wt) {
+    om.insert(om.end(), o, o + 3);
+    w.push_back(wt);
+  });
+  for (int iu = 0; iu < order; ++iu)
+    for (int iv = 0; iv < order; ++iv) {
+      const double u = g.x[iu], v = g.x[iv];
+      bary.push_back(1.0 - u), bary.push_back(u * (1.0 - v)), bary.push_back(u * v);
+    }
+}
+
 int patch_order(int level, int base) {  // quadrature.hpp:31-34
   const int bump = level == 0 ? 20 : level == 1 ? 12 : 8;
   return std::max(base, bump);
@@ -306,6 +323,8 @@ inline double kron22(const double* A, const double* B, int r, int c) {
 
 }  // namespace
 
+void real_harmonics(int N, const double* om, double* out) { harmonics(N, om, out); }
+
 void inverse4(const double* A, double* Ainv) {  // partial-pivot Gauss-Jordan
   double m[4][8];
   for (int i = 0; i < 4; ++i)
@@ -335,7 +354,7 @@ Problem copy_problem(const stamg_problem& s) {
   if (s.n_mat < 1 || !s.sigma_t || !s.moments) throw std::invalid_argument("problem: no materials");
   p.sigma_t.assign(s.sigma_t, s.sigma_t + s.n_mat);
   p.moments.assign(s.moments, s.moments + size_t(s.n_mat) * (s.N + 1));
-  p.n_el = s.nx * s.ny;
+  p.n_el = s.nx * s.ny * (s.dim == 3 ? s.nz : 1);
   if (s.mat_of_el) p.mat.assign(s.mat_of_el, s.mat_of_el + p.n_el);
   else p.mat.assign(p.n_el, 0);
   if (s.q_el) p.q_el.assign(s.q_el, s.q_el + p.n_el);

@@ -143,6 +143,12 @@ void gauss_rule01(int n, const double** x, const double** w);
 bool device_couplings_supported(int order);
 void device_couplings(const SphereTree& t, const std::vector<int>& leaf_id, int order, int xorder_base, double* X);
 
+// every node of a patch's Duffy-collapsed rule: unit directions [n][3], flat barycentric
+// coordinates [n][3], weights [n] (quadrature.cpp:59-92); real orthonormal harmonics
+void patch_rule(const SphereTree& t, int id, int order, std::vector<double>& om, std::vector<double>& bary,
+                std::vector<double>& w);
+void real_harmonics(int N, const double* om, double* out);
+
 // 4x4 helpers
 void inverse4(const double* A, double* Ainv);
 

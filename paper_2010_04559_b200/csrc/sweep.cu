@@ -27,6 +27,15 @@ namespace {
 #define STAMG_SWEEP8_BREG 1  // 8-direction kernel keeps B^-1 in registers (2 CTAs/SM); A/B: 82.5 % vs 79 %
 #endif
 constexpr int NST = STAMG_SWEEP_NST;
+#ifndef STAMG_SWEEP_BULK
+// wavefront layout: 1 = a step's rows arrive as one or two TMA bulk copies (cp.async.bulk, one
+// issuing thread, mbarrier completion), 0 = per-thread cp.async. A/B at config 5 (512^2 x 8192,
+// profiles/r02_sweep_ab.txt): cp.async 23.1 ms, bulk copies 23.8 ms with every thread waiting on
+// the stage's mbarrier, 24.6 ms with one waiting thread ahead of the step barrier. The sweep is
+// bandwidth-bound while the waves are full; the bulk path saves address arithmetic but adds an
+// mbarrier round trip per step, so per-thread cp.async stays the default.
+#define STAMG_SWEEP_BULK 0
+#endif
 
 // DIRS directions x R rows per CTA (DIRS*R = 256 threads). thread = (dir, row):
 // dir = tid % DIRS, row = tid / DIRS. With DIRS = 8 a cell's 8 directions are
@@ -47,7 +56,14 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
   constexpr int NT = DIRS * R;
   constexpr int NW = NT / 32;
   constexpr int RPW = 32 / DIRS;  // rows per warp
-  extern __shared__ __align__(16) double smem[];
+  // BULK (wavefront layout): the R rows of a step lie on one anti-diagonal of one strip -- or,
+  // while the wavefront crosses into the next strip, on one diagonal of each -- so the step's
+  // rhs (and base) is one or two contiguous runs of up to R x DIRS x 32 B = 8 KB. Thread 0
+  // issues them as cp.async.bulk copies completing on the stage's mbarrier (UBLKCP); nobody
+  // computes a per-thread source address or issues per-thread LDGSTS for the vector data.
+  constexpr bool BULK = WLAY && TOPG && (STAMG_SWEEP_BULK != 0);
+  __shared__ unsigned long long s_bar[BULK ? NST : 1];
+  extern __shared__ __align__(128) double smem[];
   double* st_rhs = smem;
   double* st_base = st_rhs + NST * NT * 4;
   double* after_base = st_base + (ACCUM ? NST * NT * 4 : 0);
@@ -58,8 +74,18 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
 
   const int tid = threadIdx.x, dir = tid % DIRS, r = tid / DIRS, lane = tid & 31, warp = tid >> 5;
   const int xb = XBLK ? p.xb : 1;
-  const int gb = XBLK ? int(blockIdx.x) / xb : int(blockIdx.x);
-  const int xblk = XBLK ? int(blockIdx.x) - gb * xb : 0;
+  // XBLK: logical block ids come from a ticket, so a block's upwind neighbour (the ticket
+  // before it) is always running or done, whatever order the hardware dispatches CTAs in:
+  // the flag waits below cannot deadlock even when the grid is many waves
+  int bid = int(blockIdx.x);
+  if constexpr (XBLK) {
+    __shared__ int s_bid;
+    if (threadIdx.x == 0) s_bid = atomicAdd(p.xflag + p.g.n_groups * xb, 1);
+    __syncthreads();
+    bid = s_bid;
+  }
+  const int gb = XBLK ? bid / xb : bid;
+  const int xblk = XBLK ? bid - gb * xb : 0;
   const int grp = gb + p.grp0;
   const int q = p.g.groups[grp * DIRS + dir];
   const int oct = p.g.group_oct[grp];
@@ -130,7 +156,35 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
     if constexpr (WLAY) c.off += (size_t)R * DIRS * 4;
     else c.off += (ptrdiff_t)dx * DP * 4;
   };
+  // BULK producer state (thread 0): strip of row 0 at the issue step and the step within it
+  int b_sh = 0, b_rb = 0;
   auto issue = [&](int t, const Cursor& c) {
+    if constexpr (BULK) {
+      if (tid == 0) {
+        // rows 0..rb are in strip sh on diagonal i0 + rb, rows rb+1..R-1 still in strip sh-1
+        // on diagonal i0 + rb + nxl (slot = (strip * nd + diagonal) * R + row)
+        const int nA = b_sh < nstrips ? min(b_rb, R - 1) + 1 : 0;
+        const int nB = (b_sh >= 1 && b_sh - 1 < nstrips && b_rb < R - 1) ? R - 1 - b_rb : 0;
+        if (nA + nB > 0) {
+          const int stg = t % NST;
+          unsigned long long* bar = &s_bar[stg];
+          mbar_expect_tx(bar, unsigned(nA + nB) * DIRS * 32u * (ACCUM ? 2u : 1u));
+          const size_t g0 = (size_t)grp * p.wl.slots;
+          if (nA > 0) {
+            const size_t off = (g0 + ((size_t)b_sh * p.wl.nd + i0 + b_rb) * R) * DIRS * 4;
+            bulk_g2s(st_rhs + (size_t)stg * NT * 4, p.rhs + off, unsigned(nA) * DIRS * 32u, bar);
+            if constexpr (ACCUM) bulk_g2s(st_base + (size_t)stg * NT * 4, p.base + off, unsigned(nA) * DIRS * 32u, bar);
+          }
+          if (nB > 0) {
+            const size_t off = (g0 + ((size_t)(b_sh - 1) * p.wl.nd + i0 + b_rb + nxl) * R + b_rb + 1) * DIRS * 4;
+            const size_t so = ((size_t)stg * NT + (size_t)(b_rb + 1) * DIRS) * 4;
+            bulk_g2s(st_rhs + so, p.rhs + off, unsigned(nB) * DIRS * 32u, bar);
+            if constexpr (ACCUM) bulk_g2s(st_base + so, p.base + off, unsigned(nB) * DIRS * 32u, bar);
+          }
+        }
+        if (++b_rb == nxl) b_rb = 0, ++b_sh;
+      }
+    } else {
     const bool ok = c.ok;
     const size_t off = ok ? c.off : 0;
     const double* src = p.rhs + off;
@@ -142,6 +196,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
       double* db = st_base + ((t % NST) * NT + tid) * 4;
       cp_async16(db, sb, ok);
       cp_async16(db + 2, sb + 2, ok);
+    }
     }
     if constexpr (TOPG) {  // row 0 of strip s >= 1 needs the trace row R-1 left in the scratch
       if (r == 0) {
@@ -168,6 +223,13 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
     __syncthreads();
     ++wait_s, wait_t = wait_s * nxl - (NST - 1);
   };
+  if constexpr (BULK) {
+    if (tid == 0) {
+      for (int k = 0; k < NST; ++k) mbar_init_cta(&s_bar[k], 1);
+      fence_proxy_async_smem();
+    }
+    __syncthreads();
+  }
   if constexpr (XBLK) {
     if (xin) wait_strip();
   }
@@ -192,6 +254,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
     cp_async_commit();
     advance(ci);
     cp_async_wait<NST - 1>();
+    if constexpr (BULK) mbar_wait_parity(&s_bar[t % NST], unsigned(t / NST) & 1u);
     const bool kin = cc.kin;
     const int s = cc.s, i = cc.i;
     double2 ty;

@@ -386,6 +386,16 @@ def partition(spec: ProblemSpec, rank: int, world: int, level: int):
     return qpos, up
 
 
+def host_table(spec: ProblemSpec, name: str) -> np.ndarray:
+    """Host-only: an outer-level table of the host setup (stamg_host_table)."""
+    pr, keep = _problem_struct(spec)
+    n = C.c_int64()
+    _check(lib().stamg_host_table(C.byref(pr), name.encode(), None, C.c_int64(0), C.byref(n)))
+    out = np.empty(n.value)
+    _check(lib().stamg_host_table(C.byref(pr), name.encode(), out.ctypes.data_as(dp), n, C.byref(n)))
+    return out
+
+
 def shard_patches(spec: ProblemSpec, rank: int, world: int) -> np.ndarray:
     """Host-only: global leaf positions (ascending) of `rank`'s directions in a context
     without a hierarchy (whole reflection orbits; stamg_shard_patches)."""

@@ -32,10 +32,20 @@ def test_last_error_is_empty_string_initially(stamg):
 def test_create_rejects_unsupported_problem_without_gpu(stamg):
     # validation runs on the host before any device call
     from paper_2010_04559_b200 import configs as cf
+    # (3D / p0 / Lin problems run on the reference-shape path; a two-material 3D problem and
+    # a 3D cone beam are outside both paths)
     spec = cf.reference_test_problem(2, 1.0, 1, 1, 1, 2, [1.0, 0.5, 0.2], 1.0, dim=3)
+    spec.beam = cf.BEAM_CONE_X0
     try:
         stamg.Context(spec)
     except stamg.InvalidArgument as e:
-        assert "dim" in str(e) or "basis" in str(e)
+        assert "beam" in str(e)
     else:  # pragma: no cover
-        raise AssertionError("3D Lin problem must be rejected by the B200 path")
+        raise AssertionError("a 3D cone beam must be rejected")
+    spec = cf.reference_test_problem(2, 1.0, 1, 0, 2, 2, [1.0, 0.5, 0.2], 1.0, dim=3)
+    try:
+        stamg.Context(spec)
+    except stamg.InvalidArgument as e:
+        assert "p must be 0 or 1" in str(e)
+    else:  # pragma: no cover
+        raise AssertionError("p = 2 must be rejected")

@@ -7,6 +7,7 @@ k = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 nu = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 spec = cf.baseline_config(k)
 g = stamg.Context(spec)
+print("gs_mode (mw, cluster, rows, slots, credit, blocked chain):", [int(v) for v in g.table("gs_mode", 0)], flush=True)
 f = g.vec(0).fill(1e-3)
 phi = g.vec(0)
 for rep in range(2):
