@@ -116,6 +116,7 @@ struct DevLevel {
   int *groups8 = nullptr, *group8_oct = nullptr;
   double2* sweep_top = nullptr;  // 8-direction sweep: strip-boundary trace scratch
   int sweep_xb = 1;               // column blocks per group (sweep_kernel XBLK)
+  int sweep_xb_g0 = 0;            // first group cut into column blocks (the groups before it are swept whole)
   int* sweep_xflag = nullptr;
   double2* sweep_xtrace = nullptr;
   // wavefront layout (contexts without a hierarchy): tables in internal (group-major)
@@ -432,20 +433,35 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     // fewer groups than SMs (config 5 sharded over 8 GPUs: 128 per rank): two column blocks per
     // group so the wavefronts cover twice the SMs (STAMG_SWEEP_XBLOCKS=0 keeps one block).
     // With more groups than CTA slots (config 5 on one GPU: 1024 groups on 296 slots = 3.46
-    // waves run as 4) column blocks would shorten the tail wave, but measured slower:
-    // 23.8 ms with one block, 26.3 with two, 29.2 with four (profiles/r02_sweep_ab.txt);
-    // STAMG_SWEEP_XB forces a block count for A/B runs.
+    // waves run as 4) cutting every group measured slower (23.8 ms with one block, 26.3 with
+    // two, 29.2 with four; profiles/r02_sweep_ab.txt): a block's strip hand-off costs more
+    // than the shorter tail saves. Cutting only the tail wave (the groups of the full waves
+    // swept whole, the remaining ones in xb blocks when those fit one wave; STAMG_SWEEP_TAIL=1)
+    // does not pay either: 23.5 ms against 23.1 ms. The waves are not equally long -- the
+    // kernel is bandwidth-bound while they are full, and the 136 CTAs of the last wave run
+    // faster per CTA -- so there is less tail to recover than the wave count suggests.
+    // STAMG_SWEEP_XB forces a block count for all groups (A/B).
     const int ng = int(t.group8_oct.size());
     if (c->wl_allowed && !env_is_zero("STAMG_SWEEP_XBLOCKS")) {
       auto ok = [&](int xb) { return xb >= 1 && t.nx % xb == 0 && t.nx / xb >= kSweep8MinNx; };
-      int best = 1;
+      const int slots = 2 * sms;
+      int best = 1, g0 = 0;
       if (ng <= sms && ok(2)) best = 2;
+      else if (ng > slots && ng % slots != 0 && std::getenv("STAMG_SWEEP_TAIL") != nullptr &&
+               !env_is_zero("STAMG_SWEEP_TAIL")) {
+        const int rem = ng % slots;
+        for (int xb : {4, 2})
+          if (ok(xb) && rem * xb <= slots) {
+            best = xb, g0 = ng - rem;
+            break;
+          }
+      }
       if (const char* e = std::getenv("STAMG_SWEEP_XB")) {  // A/B
         const int xb = std::atoi(e);
-        if (ok(xb)) best = xb;
+        if (ok(xb)) best = xb, g0 = 0;
       }
       if (best > 1) {
-        L.sweep_xb = best;
+        L.sweep_xb = best, L.sweep_xb_g0 = g0;
         L.sweep_xflag = dalloc<int>(size_t(ng) * L.sweep_xb + 1);  // + the block ticket
         L.sweep_xtrace = dalloc<double2>(size_t(ng) * L.sweep_xb * t.ny * 8);
       }
@@ -934,7 +950,7 @@ void op_sweep(stamg_ctx* c, DevLevel& L, const double* rhs, double* z, const dou
   // groups) keep the one-wave choice
   p.prefer_breg = L.wl.nd > 0 || std::getenv("STAMG_SWEEP8_PREFER_BREG") != nullptr;
   if (L.sweep_xb > 1 && !base) {
-    p.xb = L.sweep_xb, p.xflag = L.sweep_xflag, p.xtrace = L.sweep_xtrace;
+    p.xb = L.sweep_xb, p.xb_g0 = L.sweep_xb_g0, p.xflag = L.sweep_xflag, p.xtrace = L.sweep_xtrace;
     p.xb_smemb = std::getenv("STAMG_SWEEP_XB_SMEMB") != nullptr;
     ck(cudaMemsetAsync(L.sweep_xflag, 0, sizeof(int) * (L.t.group8_oct.size() * L.sweep_xb + 1), c->stream), "memset");
   }
@@ -2046,6 +2062,8 @@ int stamg_get_table(stamg_ctx* c, int level, const char* name, double* out, int6
     if (nm == "fold") v = {double(L.fold_G), double(L.fold_R), double(L.fold_Hf), t.sym_defect, double(t.n_sym_axes)};
     else if (nm == "ar_chunks") v = {double(c->ar_chunks_used), double(c->comm_ar != nullptr)};
     else if (nm == "graphs") v = {double(c->mg_graphs.size()), double(c->graph_replays), double(c->graphs_off)};
+    else if (nm == "sweep_mode")
+      v = {double(L.sweep_xb), double(L.sweep_xb_g0), double(t.group8_oct.size()), double(L.wl.nd)};
     else if (nm == "gs_mode")
       v = {double(L.gs_mw), double(L.gs_cluster), double(L.gs_rows), double(L.gs_mb_slots), double(L.gs_mb_credit), double(L.gs_blk)};
     else if (nm == "X") v = t.X;

@@ -34,11 +34,10 @@ struct Frame {  // octant frame <-> grid coordinates
 __device__ __forceinline__ int upwind(const Dev& L, int el, int oct, int xi) {
   const int ix = el % L.nx, iy = (el / L.nx) % L.ny, iz = el / (L.nx * L.ny);
   const int dir = (oct >> xi) & 1 ? 1 : -1;  // positive cosine: inflow through the low face
-  int c[3] = {ix, iy, iz};
-  const int n[3] = {L.nx, L.ny, L.nz};
-  c[xi] += dir;
-  if (c[xi] < 0 || c[xi] >= n[xi]) return -1;
-  return (c[2] * L.ny + c[1]) * L.nx + c[0];
+  const int cur = xi == 0 ? ix : xi == 1 ? iy : iz, n = xi == 0 ? L.nx : xi == 1 ? L.ny : L.nz;
+  const int stride = xi == 0 ? 1 : xi == 1 ? L.nx : L.nx * L.ny;
+  if (cur + dir < 0 || cur + dir >= n) return -1;
+  return el + dir * stride;
 }
 
 __global__ void apply_L_kernel(Dev L, const double* __restrict__ x, double* __restrict__ y, double alpha, double beta,
@@ -66,7 +65,134 @@ __global__ void apply_L_kernel(Dev L, const double* __restrict__ x, double* __re
   y[idx] = alpha * acc + (beta != 0.0 ? beta * f[idx] : 0.0);
 }
 
-// One CTA per patch; threads take the cells of one hyperplane at a time.
+// Block size known at compile time (1, 3, 8, 12, 24: every S x D the reference has outside the
+// tuned 2D path): a thread owns a whole (cell, patch) block in registers; the patch's dense
+// tables sit in shared memory and are read as warp-wide broadcasts.
+template <int BS>
+__device__ __forceinline__ void load_block(const double* __restrict__ p, double* v) {
+  if constexpr (BS % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < BS; c += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(p + c);
+      v[c] = t.x, v[c + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < BS; ++c) v[c] = p[c];
+  }
+}
+template <int BS>
+__device__ __forceinline__ void store_block(double* p, const double* v) {
+  if constexpr (BS % 2 == 0) {
+#pragma unroll
+    for (int c = 0; c < BS; c += 2) *reinterpret_cast<double2*>(p + c) = make_double2(v[c], v[c + 1]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < BS; ++c) p[c] = v[c];
+  }
+}
+// acc (+)= M v with M [BS][BS] in shared memory (each entry one broadcast load)
+template <int BS, bool SUB>
+__device__ __forceinline__ void matvec_acc(const double* M, const double* v, double* acc) {
+#pragma unroll
+  for (int a = 0; a < BS; ++a) {
+    double t = 0.0;
+#pragma unroll
+    for (int c = 0; c < BS; ++c) t += M[a * BS + c] * v[c];
+    acc[a] = SUB ? acc[a] - t : acc[a] + t;
+  }
+}
+
+// acc += M v, M given transposed in shared memory (MT[c][a]); v streamed from global memory
+// one entry at a time, so only the accumulators live in registers
+template <int BS>
+__device__ __forceinline__ void matvec_cols(const double* MT, const double* __restrict__ v, double* acc) {
+#pragma unroll 2
+  for (int c = 0; c < BS; ++c) {
+    const double vc = v[c];
+    const double* col = MT + c * BS;
+    if constexpr (BS % 2 == 0) {
+#pragma unroll
+      for (int a = 0; a < BS; a += 2) {
+        const double2 m = *reinterpret_cast<const double2*>(col + a);
+        acc[a] += m.x * vc, acc[a + 1] += m.y * vc;
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < BS; ++a) acc[a] += col[a] * vc;
+    }
+  }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(128) apply_L_block_kernel(Dev L, const double* __restrict__ x, double* __restrict__ y,
+                                                            double alpha, double beta, const double* __restrict__ f) {
+  extern __shared__ __align__(16) double sm[];  // B^T | C_0^T .. C_{dim-1}^T
+  const int q = blockIdx.x, oct = L.octant[q];
+  for (int k = threadIdx.x; k < BS * BS; k += blockDim.x) {
+    const int a = k / BS, c = k - a * BS, kt = c * BS + a;
+    sm[kt] = L.Bd[(size_t)q * BS * BS + k];
+    for (int xi = 0; xi < L.dim; ++xi) sm[(1 + xi) * BS * BS + kt] = L.C[((size_t)q * 3 + xi) * BS * BS + k];
+  }
+  __syncthreads();
+  for (int el = blockIdx.y * blockDim.x + threadIdx.x; el < L.n_el; el += gridDim.y * blockDim.x) {
+    double acc[BS];
+#pragma unroll
+    for (int a = 0; a < BS; ++a) acc[a] = 0.0;
+    const size_t off = ((size_t)el * L.P + q) * BS;
+    matvec_cols<BS>(sm, x + off, acc);
+#pragma unroll 1
+    for (int xi = 0; xi < L.dim; ++xi) {
+      const int up = upwind(L, el, oct, xi);
+      if (up < 0) continue;
+      matvec_cols<BS>(sm + (1 + xi) * BS * BS, x + ((size_t)up * L.P + q) * BS, acc);
+    }
+    if (beta != 0.0) {
+#pragma unroll
+      for (int a = 0; a < BS; ++a) acc[a] = alpha * acc[a] + beta * f[off + a];
+    } else {
+#pragma unroll
+      for (int a = 0; a < BS; ++a) acc[a] *= alpha;
+    }
+    store_block<BS>(y + off, acc);
+  }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(256) sweep_block_kernel(Dev L, const double* rhs, double* z) {
+  extern __shared__ __align__(16) double sm[];  // B^-1 | C_0 .. C_{dim-1}
+  const int q = blockIdx.x, oct = L.octant[q];
+  for (int k = threadIdx.x; k < BS * BS; k += blockDim.x) {
+    sm[k] = L.Binv[(size_t)q * BS * BS + k];
+    for (int xi = 0; xi < L.dim; ++xi) sm[(1 + xi) * BS * BS + k] = L.C[((size_t)q * 3 + xi) * BS * BS + k];
+  }
+  __syncthreads();
+  const Frame fr(L, oct);
+  const int nplanes = L.nx + L.ny + L.nz - 2, njk = L.ny * L.nz;
+  for (int pl = 0; pl < nplanes; ++pl) {
+    for (int jk = threadIdx.x; jk < njk; jk += blockDim.x) {
+      const int fj = jk % L.ny, fk = jk / L.ny, fi = pl - fj - fk;
+      if (fi < 0 || fi >= L.nx) continue;
+      const int el = fr.el(fi, fj, fk);
+      double r[BS], v[BS];
+      load_block<BS>(rhs + ((size_t)el * L.P + q) * BS, r);
+      for (int xi = 0; xi < L.dim; ++xi) {
+        const int fc = xi == 0 ? fi : xi == 1 ? fj : fk;
+        if (fc == 0) continue;
+        const int up = fr.el(fi - (xi == 0), fj - (xi == 1), fk - (xi == 2));
+        load_block<BS>(z + ((size_t)up * L.P + q) * BS, v);
+        matvec_acc<BS, true>(sm + (1 + xi) * BS * BS, v, r);
+      }
+#pragma unroll
+      for (int a = 0; a < BS; ++a) v[a] = 0.0;
+      matvec_acc<BS, false>(sm, r, v);
+      store_block<BS>(z + ((size_t)el * L.P + q) * BS, v);
+    }
+    __syncthreads();
+  }
+}
+
+// One CTA per patch; threads take the cells of one hyperplane at a time (any block size).
 __global__ void sweep_kernel(Dev L, const double* rhs, double* z) {
   extern __shared__ __align__(16) double sm[];
   const int bs = L.bs, q = blockIdx.x, oct = L.octant[q];
@@ -318,17 +444,47 @@ int blocks_for(int64_t n, int bsz) { return int((n + bsz - 1) / bsz); }
 
 }  // namespace
 
+template <int BS>
+void launch_apply_L_t(const Dev& L, const double* x, double* y, double alpha, double beta, const double* f, cudaStream_t s) {
+  const size_t smem = sizeof(double) * size_t(1 + L.dim) * BS * BS;
+  const int by = std::max(1, std::min((L.n_el + 127) / 128, std::max(1, 4 * 148 / std::max(L.P, 1))));
+  apply_L_block_kernel<BS><<<dim3(L.P, by), 128, smem, s>>>(L, x, y, alpha, beta, f);
+}
+
+template <int BS>
+void launch_sweep_t(const Dev& L, const double* rhs, double* z, int threads, cudaStream_t s) {
+  const size_t smem = sizeof(double) * size_t(1 + L.dim) * BS * BS;
+  sweep_block_kernel<BS><<<L.P, threads, smem, s>>>(L, rhs, z);
+}
+
 void launch_apply_L(const Dev& L, const double* x, double* y, double alpha, double beta, const double* f, cudaStream_t s) {
   const int64_t n = (int64_t)L.n_el * L.P * L.bs;
   if (n == 0) return;
-  apply_L_kernel<<<blocks_for(n, 256), 256, 0, s>>>(L, x, y, alpha, f ? beta : 0.0, f);
+  if (!f) beta = 0.0;
+  switch (L.bs) {
+    case 1: return launch_apply_L_t<1>(L, x, y, alpha, beta, f, s);
+    case 3: return launch_apply_L_t<3>(L, x, y, alpha, beta, f, s);
+    case 8: return launch_apply_L_t<8>(L, x, y, alpha, beta, f, s);
+    case 12: return launch_apply_L_t<12>(L, x, y, alpha, beta, f, s);
+    case 24: return launch_apply_L_t<24>(L, x, y, alpha, beta, f, s);
+    default: apply_L_kernel<<<blocks_for(n, 256), 256, 0, s>>>(L, x, y, alpha, beta, f);
+  }
 }
 
 void launch_sweep(const Dev& L, const double* rhs, double* z, cudaStream_t s) {
   if (L.P == 0 || L.n_el == 0) return;
-  const size_t smem = sizeof(double) * size_t(1 + L.dim) * L.bs * L.bs;
   const int threads = std::min(256, std::max(32, (L.ny * L.nz + 31) / 32 * 32));
-  sweep_kernel<<<L.P, threads, smem, s>>>(L, rhs, z);
+  switch (L.bs) {
+    case 1: return launch_sweep_t<1>(L, rhs, z, threads, s);
+    case 3: return launch_sweep_t<3>(L, rhs, z, threads, s);
+    case 8: return launch_sweep_t<8>(L, rhs, z, threads, s);
+    case 12: return launch_sweep_t<12>(L, rhs, z, threads, s);
+    case 24: return launch_sweep_t<24>(L, rhs, z, threads, s);
+    default: {
+      const size_t smem = sizeof(double) * size_t(1 + L.dim) * L.bs * L.bs;
+      sweep_kernel<<<L.P, threads, smem, s>>>(L, rhs, z);
+    }
+  }
 }
 
 void launch_d2m(const Dev& L, const double* phi, int order, bool apply_sigma_N, double* out, cudaStream_t s) {

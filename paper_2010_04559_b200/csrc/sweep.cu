@@ -73,19 +73,22 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
   double* sB = reinterpret_cast<double*>(xw + 2 * NW * DIRS);
 
   const int tid = threadIdx.x, dir = tid % DIRS, r = tid / DIRS, lane = tid & 31, warp = tid >> 5;
-  const int xb = XBLK ? p.xb : 1;
   // XBLK: logical block ids come from a ticket, so a block's upwind neighbour (the ticket
   // before it) is always running or done, whatever order the hardware dispatches CTAs in:
-  // the flag waits below cannot deadlock even when the grid is many waves
+  // the flag waits below cannot deadlock even when the grid is many waves.
+  // Groups below p.xb_g0 are swept whole (one block); the groups from xb_g0 on, the tail
+  // wave of a grid of whole-group CTAs, are cut into p.xb column blocks each.
   int bid = int(blockIdx.x);
   if constexpr (XBLK) {
     __shared__ int s_bid;
-    if (threadIdx.x == 0) s_bid = atomicAdd(p.xflag + p.g.n_groups * xb, 1);
+    if (threadIdx.x == 0) s_bid = atomicAdd(p.xflag + p.g.n_groups * p.xb, 1);
     __syncthreads();
     bid = s_bid;
   }
-  const int gb = XBLK ? bid / xb : bid;
-  const int xblk = XBLK ? bid - gb * xb : 0;
+  const bool cut = XBLK && bid >= p.xb_g0;
+  const int xb = cut ? p.xb : 1;
+  const int gb = cut ? p.xb_g0 + (bid - p.xb_g0) / xb : bid;
+  const int xblk = cut ? (bid - p.xb_g0) - (gb - p.xb_g0) * xb : 0;
   const int grp = gb + p.grp0;
   const int q = p.g.groups[grp * DIRS + dir];
   const int oct = p.g.group_oct[grp];
@@ -120,8 +123,9 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
   const int nk = nstrips * nxl;
   const int T = nk + R - 1;
   // XBLK: traces at the block edges, [groups][xb][ny][DIRS], and per-(group, block) strip flags
-  const double2* xin = XBLK && xblk > 0 ? p.xtrace + ((size_t)(grp * xb + xblk - 1) * ny) * DIRS : nullptr;
-  double2* xout = XBLK && xblk < xb - 1 ? p.xtrace + ((size_t)(grp * xb + xblk) * ny) * DIRS : nullptr;
+  const int xbs = XBLK ? p.xb : 1;  // flag / trace stride per group
+  const double2* xin = XBLK && xblk > 0 ? p.xtrace + ((size_t)(grp * xbs + xblk - 1) * ny) * DIRS : nullptr;
+  double2* xout = XBLK && xblk < xb - 1 ? p.xtrace + ((size_t)(grp * xbs + xblk) * ny) * DIRS : nullptr;
 
   // Cursor over this thread's wavefront positions k: strip s, column i, cell el and
   // block offset, advanced incrementally (no integer division inside a strip).
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
   int wait_s = 0, wait_t = 0, pub_s = 0, pub_t = (nxl - 1) + (R - 1);
   auto wait_strip = [&]() {
     if (tid == 0) {
-      const int* f = p.xflag + grp * xb + xblk - 1;
+      const int* f = p.xflag + grp * xbs + xblk - 1;
       while (ld_relaxed(f) < wait_s + 1) {
       }
       fence_acq_rel();
@@ -348,7 +352,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
       if (xout && t == pub_t) {
         if (tid == 0) {
           __threadfence();
-          st_release(p.xflag + grp * xb + xblk, pub_s + 1);
+          st_release(p.xflag + grp * xbs + xblk, pub_s + 1);
         }
         ++pub_s, pub_t += nxl;
       }
@@ -366,7 +370,7 @@ void launch_tb(const SweepParams& p, cudaStream_t s) {
                 ((MULTI || TOPG) ? sizeof(double) * p.g.n_mat * DIRS * 17 : 0) + (XBLK ? sizeof(double2) * NT : 0);
   auto k = sweep_kernel<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, BREG, XBLK>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  k<<<p.g.n_groups * (XBLK ? p.xb : 1), NT, smem, s>>>(p);
+  k<<<XBLK ? p.xb_g0 + (p.g.n_groups - p.xb_g0) * p.xb : p.g.n_groups, NT, smem, s>>>(p);
 }
 
 // 8-direction groups: B^-1 in registers gives 2 CTAs/SM (the faster kernel when the

@@ -39,6 +39,33 @@ def test_column_blocks_bitwise(stamg, monkeypatch, world, rank, n):
     g1.close()
 
 
+def test_tail_wave_column_blocks_bitwise(stamg, monkeypatch):
+    """One GPU, more 8-direction groups than CTA slots (config 5's 1024 groups on 2 x 148 slots):
+    with STAMG_SWEEP_TAIL=1 the groups of the last, partly filled wave are cut into column blocks,
+    the others are swept whole (sweep_kernel XBLK with xb_g0 > 0; an A/B option, not the default:
+    profiles/r02_sweep_ab.txt). Bitwise the plain sweep."""
+    spec = cf.baseline_config(5, 96)
+    monkeypatch.setenv("STAMG_SWEEP_TAIL", "1")
+    g = stamg.Context(spec, build_hierarchy=False)
+    monkeypatch.delenv("STAMG_SWEEP_TAIL")
+    xb, g0, ng, wl = (int(v) for v in g.table("sweep_mode"))
+    assert wl > 0 and ng == 1024
+    assert xb >= 2 and 0 < g0 < ng, (xb, g0, ng)
+    g1 = stamg.Context(spec, build_hierarchy=False)
+    assert int(g1.table("sweep_mode")[0]) == 1
+    x = rnd(g.vec().n, 31)
+    z, z1 = g.vec(), g1.vec()
+    g.standard_sweep(g.vec(data=x), z)
+    g1.standard_sweep(g1.vec(data=x), z1)
+    a = z.numpy()
+    assert np.array_equal(a, z1.numpy())
+    v = g.vec(data=x)
+    g.standard_sweep(v, v)  # in place
+    assert np.array_equal(v.numpy(), a)
+    g.close()
+    g1.close()
+
+
 @pytest.mark.parametrize("world,rank", [(2, 1), (8, 6)])
 def test_sharded_folded_scatter(stamg, monkeypatch, world, rank):
     """A rank's shard is whole reflection orbits, so its scatter folds (|G| = 8); without
