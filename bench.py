@@ -274,6 +274,96 @@ def kernel_rooflines(stamg, cf, dmma_peak):
     return out
 
 
+def reference_shape_cpu(n, box, level, N, m, sigma_t, sigma_a, solve=False):
+    """The reference's OWN sources (oracle/_ref/libstamgref.so: /root/reference/proj/src compiled
+    unchanged against the Eigen-subset shim, OpenMP as the reference has it) on the same 3D problem:
+    standard_sweep / apply_L time and the BiCGSTAB + MG solve. cpu_baseline.kind = "reference"; the
+    shim's dense kernels are plain loops, not Eigen's vectorised ones, which is stated in `note`."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    try:
+        import pyref
+        if not os.path.exists(pyref.LIB_PATH):
+            return {"unavailable": "oracle/_ref/libstamgref.so not built (needs /root/reference at build time)"}
+        r = pyref.Reference(n, box, level, 1, 1, N, m, sigma_t, sigma_a, nr=4)
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+    x = np.ones(r.size())
+    out = {"kind": "reference", "cores": os.cpu_count() or 1, "cpu_model": cpu_model(), "problem": f"{n}^3 cells",
+           "note": "reference sources unchanged; Eigen replaced by oracle/eigen_shim (plain loops)"}
+    if solve:
+        t0 = time.perf_counter()
+        _, rep = r.bicgstab("mg", tol=1e-8, max_iter=100)
+        out["bicgstab_mg"] = {"wall_s": time.perf_counter() - t0, "iterations": rep["iterations"],
+                              "converged": rep["converged"]}
+        return out
+    for name, fn in (("sweep", r.sweep), ("apply_L", r.apply_L)):
+        fn(x)
+        t0 = time.perf_counter()
+        fn(x)
+        out[name + "_ms"] = (time.perf_counter() - t0) * 1e3
+    return out
+
+
+def reference_shape_section(stamg, cf, hbm, with_cpu=True):
+    """The reference-shape path on a problem of the reference's own kind: 3D
+    trilinear cells, Lin angular basis (24 dofs per cell and patch), FP-equivalent moments N = 8,
+    uniform source, all MG levels. Per-operator time with the HBM bandwidth its algorithmic bytes
+    correspond to (apply_L, sweep: one vector in, one out; scatter: two in, one out), and the
+    BiCGSTAB + V(1,1) solve wall time to 1e-8."""
+    n, level, N = 24, 2, 8
+    nn = np.arange(N + 1, dtype=np.float64)
+    m = 0.5 * 0.5 * (N * (N + 1.0) - nn * (nn + 1.0))  # scatter.cpp:9-21, alpha = 0.5
+    spec = cf.reference_test_problem(n, n / 8.0, level, 1, 1, N, m, 0.1 + m[0], dim=3, q_el=np.ones(n ** 3),
+                                     n_levels=0, nr=4)
+    t0 = time.perf_counter()
+    g = stamg.Context(spec)
+    out = {"problem": f"{n}^3 trilinear cells, Lin basis, angular level {level}", "setup_s": time.perf_counter() - t0}
+    n_el, P, S, D = g.layout()
+    vb = n_el * P * S * D * 8
+    out["layout"] = {"n_el": n_el, "patches": P, "S": S, "D": D, "vector_bytes": vb}
+    x, y = g.vec().fill(1.0), g.vec()
+    g.timing(True)
+    reps = 5
+    for _ in range(reps):
+        g.apply_L_into(x, y)
+        g.standard_sweep(x, y)
+        g.apply_scatter_into(x, N, 1.0, y)
+    g.synchronize()
+    rows = {"apply_L": (("apply_L",), 2), "sweep": (("sweep",), 2), "scatter": (("d2m", "m2d"), 3)}
+    for name, (ks, nvec) in rows.items():
+        ms = sum(g.timed(k)[0] for k in ks) / reps
+        out[name] = {"ms": ms, "achieved_gbs": nvec * vb / (ms * 1e-3) * 1e-9, "frac": nvec * vb / (ms * 1e-3) * 1e-9 / hbm,
+                     "bound": "hbm"}
+    out["sweep"]["updates_per_s"] = n_el * P / (out["sweep"]["ms"] * 1e-3)
+    g.timing(False)
+    b = g.rhs()
+    g.solve(b, "bicgstab", "mg", tol=1e-8, max_iter=100)
+    g.synchronize()
+    t0 = time.perf_counter()
+    _, rep = g.solve(b, "bicgstab", "mg", tol=1e-8, max_iter=100)
+    g.synchronize()
+    out["bicgstab_mg"] = {"wall_s": time.perf_counter() - t0, "iterations": rep["iterations"], "converged": rep["converged"]}
+    g.close()
+    # the solve once more on an 8^3 grid, where the reference's own CPU solve takes seconds
+    ns = 8
+    spec8 = cf.reference_test_problem(ns, ns / 8.0, level, 1, 1, N, m, 0.1 + m[0], dim=3, q_el=np.ones(ns ** 3),
+                                      n_levels=0, nr=4)
+    g8 = stamg.Context(spec8)
+    b8 = g8.rhs()
+    g8.solve(b8, "bicgstab", "mg", tol=1e-8, max_iter=100)
+    g8.synchronize()
+    t0 = time.perf_counter()
+    _, rep8 = g8.solve(b8, "bicgstab", "mg", tol=1e-8, max_iter=100)
+    g8.synchronize()
+    out["bicgstab_mg_8cube"] = {"wall_s": time.perf_counter() - t0, "iterations": rep8["iterations"],
+                                "converged": rep8["converged"]}
+    g8.close()
+    if with_cpu:
+        out["cpu"] = reference_shape_cpu(n, n / 8.0, level, N, m, 0.1 + m[0], 0.1)
+        out["cpu_8cube"] = reference_shape_cpu(ns, ns / 8.0, level, N, m, 0.1 + m[0], 0.1, solve=True)
+    return out
+
+
 def make_context(stamg, spec, world, rank, local, dist, build_hierarchy):
     """One context per rank; ranks > 1 share a fresh NCCL communicator (unique id
     from rank 0, broadcast over torch.distributed)."""
@@ -398,6 +488,8 @@ def run_b200(args, world, rank, local, dist):
         extras["kernels"] = kernel_rooflines(stamg, cf, dmma_peak)
         extras["kernels"]["dmma_peak_tflops"] = dmma_peak
         extras["kernels"]["dmma_peak_probe_clocks"] = probe_clk
+    if not args.no_generic and world == 1:
+        extras["reference_shape"] = reference_shape_section(stamg, cf, hbm, with_cpu=not args.no_cpu)
     # ---- extra: GMRES + AMG solve wall time to 1e-8 from a device-resident b
     # (directions sharded over the ranks, coarsest MG level replicated)
     if not args.no_solve:
@@ -488,6 +580,7 @@ def main():
     ap.add_argument("--cpu-solve-configs", type=int, nargs="*", default=[1, 2],
                     help="also time these solves on the CPU oracle (rank 0, N=1); c2 takes ~100 s on 8 cores")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-generic", action="store_true", help="skip the reference-shape (3D trilinear Lin) section")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "generic.hpp"
 #include "kernels.hpp"
 #include "setup.hpp"
@@ -175,6 +177,7 @@ struct stamg_ctx {
   int64_t foldbuf_n = 0;
   int64_t launches = 0;
   bool timing = false;
+  bool nvtx = false;  // STAMG_NVTX=1: NVTX ranges around operator launches and solver phases
   std::map<std::string, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   std::map<std::string, std::pair<double, int64_t>> timed;
   void* comm = nullptr;
@@ -215,6 +218,7 @@ struct Timed {
   const char* name;
   cudaEvent_t e1 = nullptr;
   Timed(stamg_ctx* ctx, const char* nm) : c(ctx), name(nm) {
+    if (c->nvtx) nvtxRangePushA(nm);  // STAMG_NVTX=1: one range per operator launch (nsys / ncu --nvtx)
     if (!c->timing) return;
     cudaEvent_t e0;
     ck(cudaEventCreate(&e0), "event");
@@ -224,6 +228,18 @@ struct Timed {
   }
   ~Timed() {
     if (c->timing && e1) cudaEventRecord(e1, c->stream);
+    if (c->nvtx) nvtxRangePop();
+  }
+};
+
+// NVTX range over a solver phase (V-cycle level, Krylov solve) when STAMG_NVTX=1
+struct NvtxScope {
+  bool on;
+  NvtxScope(const stamg_ctx* c, const std::string& name) : on(c->nvtx) {
+    if (on) nvtxRangePushA(name.c_str());
+  }
+  ~NvtxScope() {
+    if (on) nvtxRangePop();
   }
 };
 
@@ -1043,6 +1059,7 @@ double op_dot(stamg_ctx* c, const double* x, const double* y, int64_t n, bool sh
 
 // lmg_vcycle (multigrid.cpp:138-170)
 void op_vcycle(stamg_ctx* c, int l, const double* f, double* phi) {
+  NvtxScope nv(c, "lmg_vcycle level " + std::to_string(l));
   DevLevel& L = c->mg[l];
   const auto& spec = c->pb.spec;
   if (l == 0) {
@@ -1199,6 +1216,7 @@ stamg_report op_gmres(stamg_ctx* c, int precond, const double* b, double* x, dou
                       std::vector<double>& hist) {
   if (tol <= 0) throw std::invalid_argument("gmres: tol must be positive");
   if (m < 1 || m > 79) throw std::invalid_argument("gmres: restart must be in [1, 79]");
+  NvtxScope nv(c, "gmres");
   const auto t0 = std::chrono::steady_clock::now();
   stamg_report rep{};
   DevLevel& O = c->outer;
@@ -1295,6 +1313,7 @@ stamg_report op_gmres(stamg_ctx* c, int precond, const double* b, double* x, dou
 stamg_report op_bicgstab(stamg_ctx* c, int precond, const double* b, double* x, double tol, int max_iter,
                          std::vector<double>& hist) {
   if (tol <= 0) throw std::invalid_argument("bicgstab: tol must be positive");
+  NvtxScope nv(c, "bicgstab");
   const auto t0 = std::chrono::steady_clock::now();
   stamg_report rep{};
   DevLevel& O = c->outer;
@@ -1489,6 +1508,7 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
     if (generic) gen::validate(c->pb);
     else validate(c->pb);
     c->pb.device_setup = std::getenv("STAMG_HOST_SETUP") == nullptr;  // couplings on the device
+    c->nvtx = std::getenv("STAMG_NVTX") != nullptr && !env_is_zero("STAMG_NVTX");
     c->device = opt ? opt->device : 0;
     c->rank = opt ? opt->rank : 0;
     c->world = opt ? std::max(1, opt->world) : 1;
