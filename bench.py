@@ -304,7 +304,7 @@ def reference_shape_cpu(n, box, level, N, m, sigma_t, sigma_a, solve=False):
     return out
 
 
-def reference_shape_section(stamg, cf, hbm, with_cpu=True):
+def reference_shape_section(stamg, cf, hbm, dfma_peak, with_cpu=True):
     """The reference-shape path on a problem of the reference's own kind: 3D
     trilinear cells, Lin angular basis (24 dofs per cell and patch), FP-equivalent moments N = 8,
     uniform source, all MG levels. Per-operator time with the HBM bandwidth its algorithmic bytes
@@ -329,11 +329,20 @@ def reference_shape_section(stamg, cf, hbm, with_cpu=True):
         g.standard_sweep(x, y)
         g.apply_scatter_into(x, N, 1.0, y)
     g.synchronize()
-    rows = {"apply_L": (("apply_L",), 2), "sweep": (("sweep",), 2), "scatter": (("d2m", "m2d"), 3)}
-    for name, (ks, nvec) in rows.items():
+    # a (cell, patch) block is bs = D*S doubles; apply_L and the sweep do (1 + dim) dense bs x bs
+    # products per block (4.6 kflop per 384 B at bs = 24: above the FP64 ridge, so FP64-bound)
+    bs = S * D
+    blk_flop = 2.0 * bs * bs * 4 * n_el * P
+    rows = {"apply_L": (("apply_L",), 2, blk_flop), "sweep": (("sweep",), 2, blk_flop),
+            "scatter": (("d2m", "m2d"), 3, 4.0 * (N + 1) ** 2 * P * D * S * n_el)}
+    for name, (ks, nvec, flop) in rows.items():
         ms = sum(g.timed(k)[0] for k in ks) / reps
-        out[name] = {"ms": ms, "achieved_gbs": nvec * vb / (ms * 1e-3) * 1e-9, "frac": nvec * vb / (ms * 1e-3) * 1e-9 / hbm,
-                     "bound": "hbm"}
+        gbs, tf = nvec * vb / (ms * 1e-3) * 1e-9, flop / (ms * 1e-3) * 1e-12
+        fp64_bound = flop / (nvec * vb) > dfma_peak * 1e12 / (hbm * 1e9)
+        out[name] = {"ms": ms, "achieved_gbs": gbs, "hbm_frac": gbs / hbm, "achieved_tflops": tf,
+                     "fp64_frac": tf / dfma_peak, "bound": "fp64" if fp64_bound else "hbm",
+                     "frac": tf / dfma_peak if fp64_bound else gbs / hbm}
+    out["fp64_peak_tflops"] = dfma_peak
     out["sweep"]["updates_per_s"] = n_el * P / (out["sweep"]["ms"] * 1e-3)
     g.timing(False)
     b = g.rhs()
@@ -482,14 +491,14 @@ def run_b200(args, world, rank, local, dist):
                "api": "stamg_sweep_host (include/stamg_b200.h), pinned host buffers",
                "pipeline_chunks": g.host_pipeline_chunks()}
         stamg.host_free(host)
-    dmma_peak, _, probe_clk = fp64_peaks_with_clocks(g, local)
+    dmma_peak, dfma_peak_k, probe_clk = fp64_peaks_with_clocks(g, local)
     g.close()
     if not args.no_kernels and world == 1:
         extras["kernels"] = kernel_rooflines(stamg, cf, dmma_peak)
         extras["kernels"]["dmma_peak_tflops"] = dmma_peak
         extras["kernels"]["dmma_peak_probe_clocks"] = probe_clk
     if not args.no_generic and world == 1:
-        extras["reference_shape"] = reference_shape_section(stamg, cf, hbm, with_cpu=not args.no_cpu)
+        extras["reference_shape"] = reference_shape_section(stamg, cf, hbm, dfma_peak_k, with_cpu=not args.no_cpu)
     # ---- extra: GMRES + AMG solve wall time to 1e-8 from a device-resident b
     # (directions sharded over the ranks, coarsest MG level replicated)
     if not args.no_solve:

@@ -636,6 +636,13 @@ void upload_gen_level(stamg_ctx* c, DevLevel& L) {
   L.g = g;
   g->dim = t.dim, g->nx = t.nx, g->ny = t.ny, g->nz = t.nz, g->n_el = t.n_el, g->S = t.S, g->D = t.D, g->bs = t.bs;
   g->P = t.P, g->H = t.H, g->order = t.order;
+  {
+    const int R = t.P * t.D;
+    std::vector<double> XT(size_t(t.H) * R);
+    for (int r = 0; r < R; ++r)
+      for (int h = 0; h < t.H; ++h) XT[size_t(h) * R + r] = t.X[size_t(r) * t.H + h];
+    g->XT = dupload(XT, s);
+  }
   g->X = dupload(t.X, s), g->sig = dupload(t.sig, s), g->Bd = dupload(t.Bd, s), g->Binv = dupload(t.Binv, s);
   g->C = dupload(t.C, s), g->Nmat = dupload(t.Nmat, s);
   g->octant = dupload(t.octant, s), g->oct_patches = dupload(t.oct_patches, s), g->oct_ptr = dupload(t.oct_ptr, s);
@@ -655,7 +662,7 @@ void upload_gen_level(stamg_ctx* c, DevLevel& L) {
 void free_level(DevLevel& L) {
   if (L.g) {
     gen::Dev* g = L.g;
-    for (void* p : {(void*)g->X, (void*)g->sig, (void*)g->Bd, (void*)g->Binv, (void*)g->C, (void*)g->BinvGS,
+    for (void* p : {(void*)g->XT, (void*)g->X, (void*)g->sig, (void*)g->Bd, (void*)g->Binv, (void*)g->C, (void*)g->BinvGS,
                     (void*)g->Nmat, (void*)g->upB, (void*)g->src, (void*)g->mom, (void*)g->octant,
                     (void*)g->oct_patches, (void*)g->oct_ptr, (void*)g->up, (void*)g->child_ptr, (void*)g->child_idx})
       if (p) cudaFree(p);

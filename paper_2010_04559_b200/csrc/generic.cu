@@ -277,6 +277,82 @@ __global__ void m2d_kernel(Dev L, const double* __restrict__ src, int Hused, dou
   }
 }
 
+// Register-blocked scatter kernels, S a template parameter. One CTA per cell; the cell's slab
+// (D2M) or its moments (M2D) are staged in shared memory and read as broadcasts, the coupling
+// table is read coalesced (X[r][h] over h for D2M, XT[h][r] over r for M2D), and a thread keeps
+// the S dofs of its harmonic / row in registers: 1 global + S/2 shared loads per S FMAs.
+constexpr int SC_TILE = 256;  // slab rows staged per step
+
+template <int S>
+__global__ void __launch_bounds__(128) d2m_block_kernel(Dev L, const double* __restrict__ phi, int Hused, bool apply_sigma_N,
+                                                        double* __restrict__ out) {
+  __shared__ __align__(16) double tile[SC_TILE * S];
+  const int el = blockIdx.x, R = L.P * L.D, H = L.H;
+  const double* slab = phi + (size_t)el * R * S;
+  double* o = out + (size_t)el * H * S;
+  for (int h0 = 0; h0 < Hused; h0 += blockDim.x) {
+    const int h = h0 + threadIdx.x;
+    double acc[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) acc[i] = 0.0;
+    for (int r0 = 0; r0 < R; r0 += SC_TILE) {
+      const int nr = min(SC_TILE, R - r0);
+      __syncthreads();
+      for (int k = threadIdx.x; k < nr * S; k += blockDim.x) tile[k] = slab[(size_t)r0 * S + k];
+      __syncthreads();
+      if (h < Hused) {
+        const double* Xc = L.X + (size_t)r0 * H + h;
+        for (int r = 0; r < nr; ++r) {
+          const double x = Xc[(size_t)r * H];
+#pragma unroll
+          for (int i = 0; i < S; ++i) acc[i] += x * tile[r * S + i];
+        }
+      }
+    }
+    if (h < Hused) {
+      if (apply_sigma_N) {
+        double v[S];
+        const double sg = L.sig[h];
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+          double t = 0.0;
+#pragma unroll
+          for (int j = 0; j < S; ++j) t += acc[j] * L.Nmat[j * S + i];
+          v[i] = sg * t;
+        }
+#pragma unroll
+        for (int i = 0; i < S; ++i) o[h * S + i] = v[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < S; ++i) o[h * S + i] = acc[i];
+      }
+    }
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(128) m2d_block_kernel(Dev L, const double* __restrict__ src, int Hused, double scale,
+                                                        double* __restrict__ y) {
+  extern __shared__ __align__(16) double sm[];  // [Hused][S]
+  const int el = blockIdx.x, R = L.P * L.D, H = L.H;
+  for (int idx = threadIdx.x; idx < Hused * S; idx += blockDim.x) sm[idx] = src[(size_t)el * H * S + idx];
+  __syncthreads();
+  double* slab = y + (size_t)el * R * S;
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    double acc[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) acc[i] = 0.0;
+    const double* Xr = L.XT + r;
+    for (int h = 0; h < Hused; ++h) {
+      const double x = Xr[(size_t)h * R];
+#pragma unroll
+      for (int i = 0; i < S; ++i) acc[i] += x * sm[h * S + i];
+    }
+#pragma unroll
+    for (int i = 0; i < S; ++i) slab[(size_t)r * S + i] += scale * acc[i];
+  }
+}
+
 __global__ void prolong_kernel(Dev F, const double* __restrict__ coarse, double* __restrict__ fine, int Pc, bool add) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int S = F.S, D = F.D, bs = F.bs;
@@ -491,6 +567,12 @@ void launch_d2m(const Dev& L, const double* phi, int order, bool apply_sigma_N, 
   const int Hused = (order + 1) * (order + 1);
   const size_t smem = sizeof(double) * size_t(Hused) * L.S;
   if (smem > 200 * 1024) throw std::invalid_argument("reference-shape scatter: (order+1)^2 * S moments exceed shared memory");
+  switch (L.S) {
+    case 1: d2m_block_kernel<1><<<L.n_el, 128, 0, s>>>(L, phi, Hused, apply_sigma_N, out); return;
+    case 4: d2m_block_kernel<4><<<L.n_el, 128, 0, s>>>(L, phi, Hused, apply_sigma_N, out); return;
+    case 8: d2m_block_kernel<8><<<L.n_el, 128, 0, s>>>(L, phi, Hused, apply_sigma_N, out); return;
+    default: break;
+  }
   if (smem > 48 * 1024) ck(cudaFuncSetAttribute(d2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
   d2m_kernel<<<L.n_el, 128, smem, s>>>(L, phi, Hused, apply_sigma_N, out);
 }
@@ -499,6 +581,12 @@ void launch_m2d(const Dev& L, const double* src, int order, double scale, double
   const int Hused = (order + 1) * (order + 1);
   const size_t smem = sizeof(double) * size_t(Hused) * L.S;
   if (smem > 200 * 1024) throw std::invalid_argument("reference-shape scatter: (order+1)^2 * S moments exceed shared memory");
+  if (L.XT && (L.S == 1 || L.S == 4 || L.S == 8)) {
+    auto k = L.S == 1 ? m2d_block_kernel<1> : L.S == 4 ? m2d_block_kernel<4> : m2d_block_kernel<8>;
+    if (smem > 48 * 1024) ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+    k<<<L.n_el, 128, smem, s>>>(L, src, Hused, scale, y);
+    return;
+  }
   if (smem > 48 * 1024) ck(cudaFuncSetAttribute(m2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
   m2d_kernel<<<L.n_el, 128, smem, s>>>(L, src, Hused, scale, y);
 }

@@ -54,6 +54,7 @@ std::vector<double> assemble_rhs(const Problem& pb, const Tables& t, const Spher
 // ---- device side ----
 struct Dev {
   int dim = 3, nx = 0, ny = 0, nz = 1, n_el = 0, S = 1, D = 1, bs = 1, P = 0, H = 0, order = 0;
+  double* XT = nullptr;  // [H][P*D] transposed couplings (M2D reads them coalesced over rows)
   double *X = nullptr, *sig = nullptr, *Bd = nullptr, *Binv = nullptr, *C = nullptr, *BinvGS = nullptr;
   double *Nmat = nullptr, *upB = nullptr, *src = nullptr, *mom = nullptr;
   int *octant = nullptr, *oct_patches = nullptr, *oct_ptr = nullptr, *up = nullptr, *child_ptr = nullptr,
