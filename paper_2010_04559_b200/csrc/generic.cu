@@ -394,7 +394,7 @@ __global__ void restrict_kernel(Dev F, const double* __restrict__ fine, double* 
 // warp takes a cell and the grid synchronises between planes.
 constexpr int GS_WPB = 4;
 
-__host__ __device__ inline size_t gs_warp_doubles(int H, int S, int bs) { return size_t(H) * S + 32 * size_t(bs) + 4 * size_t(bs); }
+__host__ __device__ inline size_t gs_warp_doubles(int H, int S, int bs) { return size_t(H) * S + 32 * size_t(bs) + 7 * size_t(bs); }
 
 __global__ void __launch_bounds__(GS_WPB * 32) coarse_gs_kernel(Dev L, const double* __restrict__ rhs, double* phi, int nu) {
   extern __shared__ __align__(16) double sm[];
@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(GS_WPB * 32) coarse_gs_kernel(Dev L, const dou
   double* szo = sr + bs;                                 // [bs] previous iterate
   double* sdz = szo + bs;                                // [bs] znew - zold
   double* sv = sdz + bs;                                 // [bs] X sigma (mom - X^T zold)
+  double* sup = sv + bs;                                 // [3][bs] upwind iterates of the patch
   const int nplanes = L.nx + L.ny + L.nz - 2, njk = L.ny * L.nz;
   for (int pass = 0; pass < nu; ++pass)
     for (int oct = 0; oct < 8; ++oct) {
@@ -425,21 +426,29 @@ __global__ void __launch_bounds__(GS_WPB * 32) coarse_gs_kernel(Dev L, const dou
           for (int a = 0; a < np; ++a) {
             const int q = L.oct_patches[pbeg + a];
             const size_t blk = ((size_t)el * P + q) * bs;
-            // r = rhs - sum_xi C phi_up; previous iterate
+            // r = rhs - sum_xi C phi_up; previous iterate. The upwind blocks come from other
+            // warps' earlier planes (L2, one coalesced round trip each) and are staged first.
+            if (lane < bs) {
+              for (int xi = 0; xi < L.dim; ++xi) {
+                const int fc = xi == 0 ? fi : xi == 1 ? fj : fk;
+                if (fc == 0) continue;
+                const int up = fr.el(fi - (xi == 0), fj - (xi == 1), fk - (xi == 2));
+                sup[xi * bs + lane] = __ldcg(phi + ((size_t)up * P + q) * bs + lane);
+              }
+              szo[lane] = __ldcg(phi + blk + lane);
+            }
+            __syncwarp();
             if (lane < bs) {
               double r = rhs[blk + lane];
               for (int xi = 0; xi < L.dim; ++xi) {
                 const int fc = xi == 0 ? fi : xi == 1 ? fj : fk;
                 if (fc == 0) continue;
-                const int up = fr.el(fi - (xi == 0), fj - (xi == 1), fk - (xi == 2));
                 const double* C = L.C + (((size_t)q * 3 + xi) * bs + lane) * bs;
-                const double* pu = phi + ((size_t)up * P + q) * bs;
                 double acc = 0.0;
-                for (int c = 0; c < bs; ++c) acc += C[c] * __ldcg(pu + c);
+                for (int c = 0; c < bs; ++c) acc += C[c] * sup[xi * bs + c];
                 r -= acc;
               }
               sr[lane] = r;
-              szo[lane] = __ldcg(phi + blk + lane);
             }
             __syncwarp();
             // v[d][j] = sum_h X[(q,d)][h] sig_h (mom[h][j] - sum_e X[(q,e)][h] zold[e][j])
