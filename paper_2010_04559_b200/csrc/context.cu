@@ -334,9 +334,7 @@ std::vector<int> apply_internal_order(LevelTables& t) {
 // wavefront layout: rank 0's sweep of a 1/N slice on one GPU (tools/shard_probe.py)
 // takes 6.04 / 3.71 ms at N = 4 / 8 against 9.03 / 5.32 ms with 4-direction groups
 // (3.9x / 6.3x instead of 2.6x / 4.4x over one GPU's 23.4 ms).
-// STAMG_SWEEP8_MIN_GROUPS overrides the threshold.
 int sweep8_min_groups(const stamg_ctx* c, int sms) {
-  if (const char* e = std::getenv("STAMG_SWEEP8_MIN_GROUPS")) return std::atoi(e);
   return c->wl_allowed ? 1 : 2 * sms;
 }
 
@@ -396,8 +394,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     const auto& t0 = L.t;
     if (c->wl_allowed && !t0.groups8.empty() && !t0.groups8_padded && t0.nx >= kSweep8MinNx && t0.ny >= kSweep8MinNy &&
-        int(t0.group8_oct.size()) >= sweep8_min_groups(c, sms) && std::getenv("STAMG_SWEEP_DIRS4") == nullptr &&
-        !env_is_zero("STAMG_WAVEFRONT_LAYOUT")) {
+        int(t0.group8_oct.size()) >= sweep8_min_groups(c, sms) && !env_is_zero("STAMG_WAVEFRONT_LAYOUT")) {
       // default for throughput contexts: every sweep step of a group touches one
       // contiguous 8 KB run (90 % of measured HBM bandwidth at 512^2 x 8192 against
       // 82.5 % for the reference layout's 256-byte runs); STAMG_WAVEFRONT_LAYOUT=0
@@ -442,8 +439,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
   // small levels keep the 4-direction kernels (twice the CTAs, latency-bound anyway)
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  if (!t.groups8.empty() && t.nx >= kSweep8MinNx && t.ny >= kSweep8MinNy && int(t.group8_oct.size()) >= sweep8_min_groups(c, sms) &&
-      std::getenv("STAMG_SWEEP_DIRS4") == nullptr) {
+  if (!t.groups8.empty() && t.nx >= kSweep8MinNx && t.ny >= kSweep8MinNy && int(t.group8_oct.size()) >= sweep8_min_groups(c, sms)) {
     L.groups8 = dupload(t.groups8, s), L.group8_oct = dupload(t.group8_oct, s);
     L.sweep_top = dalloc<double2>(t.group8_oct.size() * 8 * size_t(t.nx));
     // fewer groups than SMs (config 5 sharded over 8 GPUs: 128 per rank): two column blocks per
@@ -548,7 +544,7 @@ void upload_level(stamg_ctx* c, DevLevel& L) {
     L.gs_mw = !env_is_zero("STAMG_GS_MW") &&
               coarse_gs_mw_ok(L.Hp, t.H, L.gs_kpad, t.n_mat, t.ny, L.gs_max_np, want_blk);
     L.gs_blk = L.gs_mw && want_blk;
-    L.gs_rows = (std::getenv("STAMG_GS_SEGMENTS") || t.nx < 64)
+    L.gs_rows = t.nx < 64
                     ? 0
                     : coarse_gs_rows_wpb(L.Hp, L.gs_kpad, t.n_mat, t.nx, t.ny, L.gs_max_np);
     if (L.gs_mw) {  // one 4-warp CTA per grid row
@@ -971,10 +967,9 @@ void op_sweep(stamg_ctx* c, DevLevel& L, const double* rhs, double* z, const dou
   // when the groups would fit one wave at four: rank 0 of 2 (512 groups) sweeps in 12.5 ms
   // against 14.6 ms (tools/shard_probe.py); solve contexts (config 4's 364 cone-mesh
   // groups) keep the one-wave choice
-  p.prefer_breg = L.wl.nd > 0 || std::getenv("STAMG_SWEEP8_PREFER_BREG") != nullptr;
+  p.prefer_breg = L.wl.nd > 0;
   if (L.sweep_xb > 1 && !base) {
     p.xb = L.sweep_xb, p.xb_g0 = L.sweep_xb_g0, p.xflag = L.sweep_xflag, p.xtrace = L.sweep_xtrace;
-    p.xb_smemb = std::getenv("STAMG_SWEEP_XB_SMEMB") != nullptr;
     ck(cudaMemsetAsync(L.sweep_xflag, 0, sizeof(int) * (L.t.group8_oct.size() * L.sweep_xb + 1), c->stream), "memset");
   }
   launch_sweep(p, c->stream);
@@ -1019,7 +1014,7 @@ void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* 
   p.Minv = L.gs_Minv, p.chain_blk = L.gs_blk;
   p.cluster = L.gs_cluster, p.mb_np = L.gs_max_np, p.mb_slots = L.gs_mb_slots, p.mb_credit = L.gs_mb_credit;
   p.mom_stride = L.gs_mb_credit ? (L.t.H + 1) / 2 * 2 : 0;
-  p.xreg = std::getenv("STAMG_GS_XGLOBAL") ? 0 : 1;
+  p.xreg = 1;
   p.n_el = L.t.n_el, p.P = L.t.P, p.Hp = L.Hp, p.H = L.t.H, p.nx = L.t.nx, p.ny = L.t.ny, p.nu = nu;
   for (int o = 0; o < 8; ++o)
     p.max_patches_per_octant = std::max(p.max_patches_per_octant, L.t.oct_ptr[o + 1] - L.t.oct_ptr[o]);

@@ -50,7 +50,6 @@ struct SweepParams {
   int grp0 = 0, data_P = 0, data_q0 = 0;
   bool prefer_breg = false;  // 8-direction groups: keep B^-1 in registers (2 CTAs/SM) even for 2-4 CTAs per SM of groups
   int xb = 1;                // > 1: column blocks per group (wavefront layout, plain sweep)
-  bool xb_smemb = false;     // column blocks with B^-1 in shared memory (4 CTAs/SM)
   int xb_g0 = 0;             // groups [0, xb_g0) are swept whole, groups from xb_g0 on in xb column blocks
   int* xflag = nullptr;      // [n_groups][xb] strips published by each block (zeroed per launch)
   double2* xtrace = nullptr; // [n_groups][xb][ny][8] x-traces at the block edges

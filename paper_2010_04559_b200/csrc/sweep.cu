@@ -418,13 +418,9 @@ void launch_sweep(const SweepParams& p, cudaStream_t s) {
       if (p.xb > 1) {  // column blocks (plain sweep, wavefront layout, B^-1 in registers)
         if (p.mode != 0 || p.base || !p.xflag || !p.xtrace || p.g.nx % p.xb || p.g.nx / p.xb < kSweep8MinNx)
           throw std::invalid_argument("sweep: column blocks need a plain sweep and nx / xb >= 38");
-        if (p.xb_smemb) {  // B^-1 in shared memory: 4 CTAs per SM (more blocks co-resident)
-          if (p.g.n_mat > 1) launch_tb<8, 32, true, false, true, true, 0, false, true>(p, s);
-          else launch_tb<8, 32, false, false, true, true, 0, false, true>(p, s);
-        } else {
-          if (p.g.n_mat > 1) launch_tb<8, 32, true, false, true, true, 0, true, true>(p, s);
-          else launch_tb<8, 32, false, false, true, true, 0, true, true>(p, s);
-        }
+        // (B^-1 in shared memory at four CTAs per SM measured slower: 4.77 vs 3.53 ms per rank at N = 8)
+        if (p.g.n_mat > 1) launch_tb<8, 32, true, false, true, true, 0, true, true>(p, s);
+        else launch_tb<8, 32, false, false, true, true, 0, true, true>(p, s);
         return;
       }
       p.mode == 1 ? launch_r<8, 32, true, true, 1>(p, s) : launch_r<8, 32, true, true, 0>(p, s);

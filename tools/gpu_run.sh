@@ -89,11 +89,9 @@ if [ "$MODE" = ramp ]; then
 fi
 if [ "$MODE" = shard ]; then
   timeout 600 python tools/shard_probe.py > gpurun_out/${T}_shard_default.log 2>&1
-  STAMG_SWEEP8_MIN_GROUPS=1 timeout 600 python tools/shard_probe.py 1 2 4 8 > gpurun_out/${T}_shard_8dir.log 2>&1
 fi
 if [ "$MODE" = shard2 ]; then
   timeout 600 python tools/shard_probe.py 1 2 4 8 > gpurun_out/${T}_shard_default.log 2>&1
-  STAMG_SWEEP8_PREFER_BREG=1 timeout 600 python tools/shard_probe.py 2 > gpurun_out/${T}_shard_breg.log 2>&1
 fi
 if [ "$MODE" = xblk ]; then
   timeout 300 python -m pytest tests/test_gpu_shard_sweep.py -m gpu -x -q > gpurun_out/${T}_xtest.log 2>&1; echo "tests rc=$?" >> gpurun_out/${T}_xtest.log
@@ -106,10 +104,6 @@ if [ "$MODE" = orbit ]; then
 fi
 if [ "$MODE" = xbab ]; then
   timeout 300 python tools/shard_probe.py 8 > gpurun_out/${T}_xb2.log 2>&1
-  STAMG_SWEEP_XB_SMEMB=1 timeout 300 python tools/shard_probe.py 8 > gpurun_out/${T}_xb2s.log 2>&1
-  STAMG_SWEEP_XB=4 STAMG_SWEEP_XB_SMEMB=1 timeout 300 python tools/shard_probe.py 8 > gpurun_out/${T}_xb4s.log 2>&1
-  STAMG_SWEEP_XB=4 STAMG_SWEEP_XB_SMEMB=1 timeout 300 python tools/shard_probe.py 4 > gpurun_out/${T}_xb4s_n4.log 2>&1
-  STAMG_SWEEP_XB=4 STAMG_SWEEP_XB_SMEMB=1 STAMG_SHARD_PROBE=1 timeout 300 python -m pytest tests/test_gpu_shard_sweep.py -m gpu -x -q -k column > gpurun_out/${T}_xt.log 2>&1; echo "rc=$?" >> gpurun_out/${T}_xt.log
 fi
 if [ "$MODE" = ab8 ]; then
   for r in 1 2; do for v in old new; do for k in 1 2 3; do
