@@ -106,6 +106,10 @@ int stamg_version(void);
 int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx** out);
 int stamg_destroy(stamg_ctx* ctx);
 int stamg_nccl_unique_id(void* out128);
+/* One-rank round trip through every NCCL call the sharded contexts make (dlopen, unique id,
+ * ncclCommInitRank, ncclCommSplit, ncclAllReduce of n doubles, destroy) on `device`;
+ * *version_out = ncclGetVersion. STAMG_ENCCL if any step fails. */
+int stamg_nccl_selftest(int device, int64_t n, int* version_out);
 
 /* Layout of a level (layout.hpp:16-32): out4 = {n_el, n_patch, S, D}. */
 int stamg_layout(stamg_ctx* ctx, int level, int out4[4]);

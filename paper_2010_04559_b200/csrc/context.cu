@@ -1501,6 +1501,50 @@ int stamg_nccl_unique_id(void* out128) {
   });
 }
 
+// One-rank round trip through the NCCL calls the sharded contexts make: dlopen, unique id,
+// ncclCommInitRank (the id by value), ncclCommSplit (the overlap communicator), two
+// ncclAllReduce of n doubles on a non-blocking stream, destroy. On one GPU the sum over one
+// rank is the identity, which is what is checked; it shows that the library's NCCL (whichever
+// libnccl.so.2 the process already holds, e.g. torch's) loads, matches the call signatures
+// and runs on this device.
+int stamg_nccl_selftest(int device, int64_t n, int* version_out) {
+  return guard([&] {
+    if (n <= 0) throw std::invalid_argument("stamg_nccl_selftest: n must be positive");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    if (!nccl().load()) throw NcclError("libnccl.so.2 not loadable");
+    if (version_out) {
+      *version_out = 0;
+      auto getv = reinterpret_cast<int (*)(int*)>(dlsym(nccl().h, "ncclGetVersion"));
+      if (getv) getv(version_out);
+    }
+    UniqueId uid;
+    if (nccl().getUniqueId(&uid) != 0) throw NcclError("ncclGetUniqueId failed");
+    void *comm = nullptr, *comm2 = nullptr;
+    auto init = reinterpret_cast<int (*)(void**, int, UniqueId, int)>(nccl().commInitRank);
+    if (init(&comm, 1, uid, 0) != 0) throw NcclError("ncclCommInitRank failed");
+    if (nccl().commSplit && nccl().commSplit(comm, 0, 0, &comm2, nullptr) != 0) comm2 = nullptr;
+    cudaStream_t st = nullptr;
+    ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    const size_t nn = static_cast<size_t>(n);
+    std::vector<double> h(nn, 0.0), back(nn, 0.0);
+    for (int64_t i = 0; i < n; ++i) h[size_t(i)] = 0.25 * double(i % 1024) - 7.0;
+    double* d = dalloc<double>(size_t(n));
+    ck(cudaMemcpyAsync(d, h.data(), size_t(n) * sizeof(double), cudaMemcpyHostToDevice, st), "h2d");
+    const int ncclDouble = 8, ncclSum = 0;
+    int rc = nccl().allReduce(d, d, size_t(n), ncclDouble, ncclSum, comm, st);
+    if (rc == 0 && comm2) rc = nccl().allReduce(d, d, size_t(n), ncclDouble, ncclSum, comm2, st);
+    if (rc == 0) ck(cudaMemcpyAsync(back.data(), d, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, st), "d2h");
+    const cudaError_t se = cudaStreamSynchronize(st);
+    cudaFree(d);
+    cudaStreamDestroy(st);
+    if (comm2) nccl().commDestroy(comm2);
+    nccl().commDestroy(comm);
+    if (rc != 0) throw NcclError("ncclAllReduce failed");
+    ck(se, "sync");
+    if (back != h) throw NcclError("one-rank allreduce did not return its input");
+  });
+}
+
 int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx** out) {
   return guard([&] {
     if (!prob || !out) throw std::invalid_argument("stamg_create: null argument");

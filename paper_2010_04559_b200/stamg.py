@@ -407,6 +407,13 @@ def shard_patches(spec: ProblemSpec, rank: int, world: int) -> np.ndarray:
     return out
 
 
+def nccl_selftest(device: int = 0, n: int = 1 << 20) -> int:
+    """One-rank NCCL round trip (stamg_nccl_selftest); returns the NCCL version code."""
+    v = C.c_int()
+    _check(lib().stamg_nccl_selftest(device, C.c_int64(n), C.byref(v)))
+    return v.value
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _check(lib().stamg_nccl_unique_id(buf))
