@@ -646,6 +646,7 @@ void upload_gen_level(stamg_ctx* c, DevLevel& L) {
   if (!t.BinvGS.empty()) {
     g->BinvGS = dupload(t.BinvGS, s);
     g->mom = dalloc<double>(size_t(t.n_el) * t.H * t.S);
+    if (std::getenv("STAMG_GENERIC_GS_BARRIER") == nullptr) g->gs_prog = dalloc<int>(size_t(t.ny) * t.nz);
   }
   if (!t.up.empty()) {
     g->up = dupload(t.up, s), g->upB = dupload(t.upB, s);
@@ -660,7 +661,8 @@ void free_level(DevLevel& L) {
     gen::Dev* g = L.g;
     for (void* p : {(void*)g->XT, (void*)g->X, (void*)g->sig, (void*)g->Bd, (void*)g->Binv, (void*)g->C, (void*)g->BinvGS,
                     (void*)g->Nmat, (void*)g->upB, (void*)g->src, (void*)g->mom, (void*)g->octant,
-                    (void*)g->oct_patches, (void*)g->oct_ptr, (void*)g->up, (void*)g->child_ptr, (void*)g->child_idx})
+                    (void*)g->oct_patches, (void*)g->oct_ptr, (void*)g->up, (void*)g->child_ptr, (void*)g->child_idx,
+                    (void*)g->gs_prog})
       if (p) cudaFree(p);
     delete g;
     L.g = nullptr;

@@ -396,19 +396,154 @@ constexpr int GS_WPB = 4;
 
 __host__ __device__ inline size_t gs_warp_doubles(int H, int S, int bs) { return size_t(H) * S + 32 * size_t(bs) + 7 * size_t(bs); }
 
+// shared-memory scratch of one warp
+struct GsScratch {
+  double *smom, *red, *sr, *szo, *sdz, *sv, *sup;
+  __device__ GsScratch(double* base, int H, int S, int bs) {
+    smom = base;                  // [H][S] moments of the cell
+    red = smom + (size_t)H * S;   // [bs][32]
+    sr = red + 32 * bs;           // [bs] right-hand side
+    szo = sr + bs;                // [bs] previous iterate
+    sdz = szo + bs;               // [bs] znew - zold
+    sv = sdz + bs;                // [bs] X sigma (mom - X^T zold)
+    sup = sv + bs;                // [3][bs] upwind iterates of the patch
+  }
+};
+
+// One cell of one octant by one warp: the octant's patches in turn (sweeps.cpp:86-102).
+__device__ __forceinline__ void gs_cell(const Dev& L, const double* __restrict__ rhs, double* phi, const Frame& fr, int fi,
+                                        int fj, int fk, int pbeg, int np, int lane, const GsScratch& sc) {
+  const int S = L.S, D = L.D, bs = L.bs, H = L.H, P = L.P;
+  double *smom = sc.smom, *red = sc.red, *sr = sc.sr, *szo = sc.szo, *sdz = sc.sdz, *sv = sc.sv, *sup = sc.sup;
+  const int el = fr.el(fi, fj, fk);
+  double* gm = L.mom + (size_t)el * H * S;
+  // every global load of the cell's first patch step is issued together with the
+  // moments (one memory round trip instead of three dependent ones)
+  double pre_r = 0.0, pre_zo = 0.0, pre_up[3] = {0.0, 0.0, 0.0};
+  if (lane < bs) {
+    const int q0 = L.oct_patches[pbeg];
+    const size_t blk0 = ((size_t)el * P + q0) * bs;
+    pre_r = rhs[blk0 + lane];
+    pre_zo = __ldcg(phi + blk0 + lane);
+#pragma unroll
+    for (int xi = 0; xi < 3; ++xi) {
+      const int fc = xi == 0 ? fi : xi == 1 ? fj : fk;
+      if (xi >= L.dim || fc == 0) continue;
+      const int up = fr.el(fi - (xi == 0), fj - (xi == 1), fk - (xi == 2));
+      pre_up[xi] = __ldcg(phi + ((size_t)up * P + q0) * bs + lane);
+    }
+  }
+  for (int k = lane; k < H * S; k += 32) smom[k] = __ldcg(gm + k);
+  __syncwarp();
+  for (int a = 0; a < np; ++a) {
+    const int q = L.oct_patches[pbeg + a];
+    const size_t blk = ((size_t)el * P + q) * bs;
+    // r = rhs - sum_xi C phi_up; previous iterate. The upwind blocks come from other
+    // warps' earlier planes (L2, one coalesced round trip each) and are staged first.
+    double rhs_l = pre_r;
+    if (lane < bs) {
+      if (a == 0) {
+#pragma unroll
+        for (int xi = 0; xi < 3; ++xi)
+          if (xi < L.dim) sup[xi * bs + lane] = pre_up[xi];
+        szo[lane] = pre_zo;
+      } else {
+        for (int xi = 0; xi < L.dim; ++xi) {
+          const int fc = xi == 0 ? fi : xi == 1 ? fj : fk;
+          if (fc == 0) continue;
+          const int up = fr.el(fi - (xi == 0), fj - (xi == 1), fk - (xi == 2));
+          sup[xi * bs + lane] = __ldcg(phi + ((size_t)up * P + q) * bs + lane);
+        }
+        szo[lane] = __ldcg(phi + blk + lane);
+        rhs_l = rhs[blk + lane];
+      }
+    }
+    __syncwarp();
+    if (lane < bs) {
+      double r = rhs_l;
+      for (int xi = 0; xi < L.dim; ++xi) {
+        const int fc = xi == 0 ? fi : xi == 1 ? fj : fk;
+        if (fc == 0) continue;
+        const double* C = L.C + (((size_t)q * 3 + xi) * bs + lane) * bs;
+        double acc = 0.0;
+        for (int c = 0; c < bs; ++c) acc += C[c] * sup[xi * bs + c];
+        r -= acc;
+      }
+      sr[lane] = r;
+    }
+    __syncwarp();
+    // v[d][j] = sum_h X[(q,d)][h] sig_h (mom[h][j] - sum_e X[(q,e)][h] zold[e][j])
+    {
+      double part[3][8];
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) part[d][j] = 0.0;
+      for (int h = lane; h < H; h += 32) {
+        double xq[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) xq[d] = d < D ? L.X[((size_t)q * D + d) * H + h] : 0.0;
+        const double sg = L.sig[h];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j >= S) break;
+          double t = 0.0;
+#pragma unroll
+          for (int e = 0; e < 3; ++e)
+            if (e < D) t += xq[e] * szo[e * S + j];
+          const double u = sg * (smom[h * S + j] - t);
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+            if (d < D) part[d][j] += xq[d] * u;
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (d < D && j < S) red[(d * S + j) * 32 + lane] = part[d][j];
+    }
+    __syncwarp();
+    if (lane < bs) {
+      double acc = 0.0;
+      for (int m = 0; m < 32; ++m) acc += red[lane * 32 + m];
+      sv[lane] = acc;
+    }
+    __syncwarp();
+    if (lane < bs) {  // r += v N
+      const int d = lane / S, i = lane - d * S;
+      double acc = 0.0;
+      for (int j = 0; j < S; ++j) acc += sv[d * S + j] * L.Nmat[j * S + i];
+      sr[lane] += acc;
+    }
+    __syncwarp();
+    if (lane < bs) {  // znew = (B - sq N)^-1 r
+      const double* Bi = L.BinvGS + ((size_t)q * bs + lane) * bs;
+      double acc = 0.0;
+      for (int c = 0; c < bs; ++c) acc += Bi[c] * sr[c];
+      __stcg(phi + blk + lane, acc);
+      sdz[lane] = acc - szo[lane];
+    }
+    __syncwarp();
+    // mom += X_q^T (znew - zold)
+    for (int k = lane; k < H * S; k += 32) {
+      const int h = k / S, j = k - h * S;
+      double acc = 0.0;
+      for (int d = 0; d < D; ++d) acc += L.X[((size_t)q * D + d) * H + h] * sdz[d * S + j];
+      smom[k] += acc;
+    }
+    __syncwarp();
+  }
+  for (int k = lane; k < H * S; k += 32) __stcg(gm + k, smom[k]);
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(GS_WPB * 32) coarse_gs_kernel(Dev L, const double* __restrict__ rhs, double* phi, int nu) {
   extern __shared__ __align__(16) double sm[];
   cg::grid_group grid = cg::this_grid();
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int W = gridDim.x * GS_WPB, gw = blockIdx.x * GS_WPB + wib;
-  const int S = L.S, D = L.D, bs = L.bs, H = L.H, P = L.P;
-  double* smom = sm + wib * gs_warp_doubles(H, S, bs);  // [H][S]
-  double* red = smom + (size_t)H * S;                    // [bs][32]
-  double* sr = red + 32 * bs;                            // [bs] right-hand side
-  double* szo = sr + bs;                                 // [bs] previous iterate
-  double* sdz = szo + bs;                                // [bs] znew - zold
-  double* sv = sdz + bs;                                 // [bs] X sigma (mom - X^T zold)
-  double* sup = sv + bs;                                 // [3][bs] upwind iterates of the patch
+  const GsScratch sc(sm + wib * gs_warp_doubles(L.H, L.S, L.bs), L.H, L.S, L.bs);
   const int nplanes = L.nx + L.ny + L.nz - 2, njk = L.ny * L.nz;
   for (int pass = 0; pass < nu; ++pass)
     for (int oct = 0; oct < 8; ++oct) {
@@ -419,105 +554,59 @@ __global__ void __launch_bounds__(GS_WPB * 32) coarse_gs_kernel(Dev L, const dou
         for (int jk = gw; jk < njk; jk += W) {
           const int fj = jk % L.ny, fk = jk / L.ny, fi = pl - fj - fk;
           if (fi < 0 || fi >= L.nx) continue;
-          const int el = fr.el(fi, fj, fk);
-          double* gm = L.mom + (size_t)el * H * S;
-          for (int k = lane; k < H * S; k += 32) smom[k] = __ldcg(gm + k);
-          __syncwarp();
-          for (int a = 0; a < np; ++a) {
-            const int q = L.oct_patches[pbeg + a];
-            const size_t blk = ((size_t)el * P + q) * bs;
-            // r = rhs - sum_xi C phi_up; previous iterate. The upwind blocks come from other
-            // warps' earlier planes (L2, one coalesced round trip each) and are staged first.
-            if (lane < bs) {
-              for (int xi = 0; xi < L.dim; ++xi) {
-                const int fc = xi == 0 ? fi : xi == 1 ? fj : fk;
-                if (fc == 0) continue;
-                const int up = fr.el(fi - (xi == 0), fj - (xi == 1), fk - (xi == 2));
-                sup[xi * bs + lane] = __ldcg(phi + ((size_t)up * P + q) * bs + lane);
-              }
-              szo[lane] = __ldcg(phi + blk + lane);
-            }
-            __syncwarp();
-            if (lane < bs) {
-              double r = rhs[blk + lane];
-              for (int xi = 0; xi < L.dim; ++xi) {
-                const int fc = xi == 0 ? fi : xi == 1 ? fj : fk;
-                if (fc == 0) continue;
-                const double* C = L.C + (((size_t)q * 3 + xi) * bs + lane) * bs;
-                double acc = 0.0;
-                for (int c = 0; c < bs; ++c) acc += C[c] * sup[xi * bs + c];
-                r -= acc;
-              }
-              sr[lane] = r;
-            }
-            __syncwarp();
-            // v[d][j] = sum_h X[(q,d)][h] sig_h (mom[h][j] - sum_e X[(q,e)][h] zold[e][j])
-            {
-              double part[3][8];
-#pragma unroll
-              for (int d = 0; d < 3; ++d)
-#pragma unroll
-                for (int j = 0; j < 8; ++j) part[d][j] = 0.0;
-              for (int h = lane; h < H; h += 32) {
-                double xq[3];
-#pragma unroll
-                for (int d = 0; d < 3; ++d) xq[d] = d < D ? L.X[((size_t)q * D + d) * H + h] : 0.0;
-                const double sg = L.sig[h];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                  if (j >= S) break;
-                  double t = 0.0;
-#pragma unroll
-                  for (int e = 0; e < 3; ++e)
-                    if (e < D) t += xq[e] * szo[e * S + j];
-                  const double u = sg * (smom[h * S + j] - t);
-#pragma unroll
-                  for (int d = 0; d < 3; ++d)
-                    if (d < D) part[d][j] += xq[d] * u;
-                }
-              }
-#pragma unroll
-              for (int d = 0; d < 3; ++d)
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                  if (d < D && j < S) red[(d * S + j) * 32 + lane] = part[d][j];
-            }
-            __syncwarp();
-            if (lane < bs) {
-              double acc = 0.0;
-              for (int m = 0; m < 32; ++m) acc += red[lane * 32 + m];
-              sv[lane] = acc;
-            }
-            __syncwarp();
-            if (lane < bs) {  // r += v N
-              const int d = lane / S, i = lane - d * S;
-              double acc = 0.0;
-              for (int j = 0; j < S; ++j) acc += sv[d * S + j] * L.Nmat[j * S + i];
-              sr[lane] += acc;
-            }
-            __syncwarp();
-            if (lane < bs) {  // znew = (B - sq N)^-1 r
-              const double* Bi = L.BinvGS + ((size_t)q * bs + lane) * bs;
-              double acc = 0.0;
-              for (int c = 0; c < bs; ++c) acc += Bi[c] * sr[c];
-              __stcg(phi + blk + lane, acc);
-              sdz[lane] = acc - szo[lane];
-            }
-            __syncwarp();
-            // mom += X_q^T (znew - zold)
-            for (int k = lane; k < H * S; k += 32) {
-              const int h = k / S, j = k - h * S;
-              double acc = 0.0;
-              for (int d = 0; d < D; ++d) acc += L.X[((size_t)q * D + d) * H + h] * sdz[d * S + j];
-              smom[k] += acc;
-            }
-            __syncwarp();
-          }
-          for (int k = lane; k < H * S; k += 32) __stcg(gm + k, smom[k]);
-          __syncwarp();
+          gs_cell(L, rhs, phi, fr, fi, fj, fk, pbeg, np, lane, sc);
         }
         grid.sync();
       }
+    }
+}
+
+// Dataflow variant (used when every line of cells along x can have its own co-resident warp):
+// warp w owns the line (iy, iz) = w for the whole call and walks it in each octant's upwind
+// order, so the x-upwind cell and the cell's moments are its own program order. Before a cell
+// it waits until the y- and z-upwind lines have finished the same column of the same octant
+// sweep (their progress counters: cells finished since the start of the call), and -- write
+// after read -- until the downwind lines have finished it in the previous pass. No grid-wide
+// barrier: a hyperplane step costs two flag polls instead of a barrier over all CTAs, and
+// consecutive octants overlap where the reference's order allows it.
+__global__ void __launch_bounds__(GS_WPB * 32) coarse_gs_flow_kernel(Dev L, const double* __restrict__ rhs, double* phi, int nu,
+                                                                    int* prog) {
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int line = blockIdx.x * GS_WPB + wib, njk = L.ny * L.nz;
+  if (line >= njk) return;
+  const GsScratch sc(sm + wib * gs_warp_doubles(L.H, L.S, L.bs), L.H, L.S, L.bs);
+  const int iy = line % L.ny, iz = line / L.ny;
+  int n_active = 0;
+  for (int oct = 0; oct < 8; ++oct) n_active += L.oct_ptr[oct + 1] > L.oct_ptr[oct] ? 1 : 0;
+  int base = 0;  // cells this line has finished before the current octant sweep
+  for (int pass = 0; pass < nu; ++pass)
+    for (int oct = 0; oct < 8; ++oct) {
+      const int pbeg = L.oct_ptr[oct], np = L.oct_ptr[oct + 1] - pbeg;
+      if (np == 0) continue;
+      const Frame fr(L, oct);
+      const int fj = fr.yn ? L.ny - 1 - iy : iy, fk = fr.zn ? L.nz - 1 - iz : iz;
+      // neighbour lines: upwind in y / z (read after write), downwind in y / z (write after read)
+      const int up_y = fj > 0 ? iz * L.ny + (fr.yn ? iy + 1 : iy - 1) : -1;
+      const int up_z = fk > 0 ? (fr.zn ? iz + 1 : iz - 1) * L.ny + iy : -1;
+      const int dn_y = fj < L.ny - 1 ? iz * L.ny + (fr.yn ? iy - 1 : iy + 1) : -1;
+      const int dn_z = fk < L.nz - 1 ? (fr.zn ? iz - 1 : iz + 1) * L.ny + iy : -1;
+      for (int fi = 0; fi < L.nx; ++fi) {
+        const int* f = nullptr;
+        int need = 0;
+        if (lane == 0 && up_y >= 0) f = prog + up_y, need = base + fi + 1;
+        if (lane == 1 && up_z >= 0) f = prog + up_z, need = base + fi + 1;
+        if (lane == 2 && dn_y >= 0 && pass > 0) f = prog + dn_y, need = base - n_active * L.nx + fi + 1;
+        if (lane == 3 && dn_z >= 0 && pass > 0) f = prog + dn_z, need = base - n_active * L.nx + fi + 1;
+        bool ok = f == nullptr || ld_relaxed(f) >= need;
+        while (!__all_sync(0xffffffffu, ok))
+          if (!ok) ok = ld_relaxed(f) >= need;
+        fence_acq_rel();
+        gs_cell(L, rhs, phi, fr, fi, fj, fk, pbeg, np, lane, sc);
+        __syncwarp();
+        if (lane == 0) st_release(prog + line, base + fi + 1);
+      }
+      base += L.nx;
     }
 }
 
@@ -617,15 +706,26 @@ void launch_coarse_gs(const Dev& L, const double* rhs, int nu, double* phi, cuda
   launch_d2m(L, phi, L.order, false, L.mom, s);  // moments of the current iterate (sweeps.cpp:74-79)
   const size_t smem = sizeof(double) * GS_WPB * gs_warp_doubles(L.H, L.S, L.bs);
   if (smem > 200 * 1024) throw std::invalid_argument("reference-shape coarse GS: moments exceed shared memory");
-  ck(cudaFuncSetAttribute(coarse_gs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_gs_kernel, GS_WPB * 32, smem), "occupancy");
-  const int want = (L.ny * L.nz + GS_WPB - 1) / GS_WPB;  // at most ny*nz cells per plane
-  const int grid = std::max(1, std::min(want, sms * std::max(per_sm, 1)));
   Dev Lc = L;
   const double* r = rhs;
+  const int lines = L.ny * L.nz, want = (lines + GS_WPB - 1) / GS_WPB;
+  // dataflow kernel when every line of cells gets its own co-resident warp
+  ck(cudaFuncSetAttribute(coarse_gs_flow_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_gs_flow_kernel, GS_WPB * 32, smem), "occupancy");
+  if (L.gs_prog && want <= sms * per_sm) {
+    ck(cudaMemsetAsync(L.gs_prog, 0, sizeof(int) * size_t(lines), s), "memset");
+    int* prog = L.gs_prog;
+    void* args[] = {&Lc, &r, &phi, &nu, &prog};
+    ck(cudaLaunchCooperativeKernel((const void*)coarse_gs_flow_kernel, dim3(want), dim3(GS_WPB * 32), args, smem, s),
+       "coarse_gs cooperative launch");
+    return;
+  }
+  ck(cudaFuncSetAttribute(coarse_gs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coarse_gs_kernel, GS_WPB * 32, smem), "occupancy");
+  const int grid = std::max(1, std::min(want, sms * std::max(per_sm, 1)));  // at most ny*nz cells per plane
   void* args[] = {&Lc, &r, &phi, &nu};
   ck(cudaLaunchCooperativeKernel((const void*)coarse_gs_kernel, dim3(grid), dim3(GS_WPB * 32), args, smem, s),
      "coarse_gs cooperative launch");

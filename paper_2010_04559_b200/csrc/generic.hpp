@@ -60,6 +60,7 @@ struct Dev {
   int *octant = nullptr, *oct_patches = nullptr, *oct_ptr = nullptr, *up = nullptr, *child_ptr = nullptr,
       *child_idx = nullptr;
   int max_np = 0;
+  int* gs_prog = nullptr;  // [ny*nz] per-line progress counters of the dataflow coarse GS
 };
 
 // y = alpha (B x + sum_xi C_xi x_up) + beta f   (apply_L_into, transport.cpp:66-88)

@@ -276,3 +276,24 @@ def test_2d_reference_shape_matches_oracle(stamg, orc, basis, p):
     assert rep["converged"] and abs(rep["iterations"] - repo["iterations"]) <= 1
     assert rel(g.c.scalar_flux(xs), o.scalar_flux(xo)) <= 1e-7
     g.close()
+
+
+@pytest.mark.parametrize("basis,p,n", [(1, 1, 5), (0, 0, 7)])
+def test_dataflow_coarse_gs_is_bitwise_the_barrier_kernel(stamg, orc, monkeypatch, basis, p, n):
+    """The reference-shape coarse GS runs as a dataflow kernel (one warp per line of cells,
+    progress counters instead of a grid barrier per hyperplane) when the lines fit co-resident;
+    STAMG_GENERIC_GS_BARRIER=1 keeps the hyperplane kernel. Same cell arithmetic, same order of
+    dependent cells: bitwise equal, and repeatable."""
+    m, st = orc.fp_moments(8, 1.0, 0.1)
+    sp = cf.reference_test_problem(n, 1.0, 1, basis, p, 8, m, st, q_el=np.ones(n ** 3), n_levels=0, nr=4)
+    g = Ops(stamg, sp)
+    monkeypatch.setenv("STAMG_GENERIC_GS_BARRIER", "1")
+    gb = Ops(stamg, sp)
+    monkeypatch.delenv("STAMG_GENERIC_GS_BARRIER")
+    f, phi0 = rnd(g.size(0), 51), rnd(g.size(0), 52)
+    a = g.coarse_gs(f, 3, phi0)
+    b = gb.coarse_gs(f, 3, phi0)
+    assert np.array_equal(a, b)
+    assert np.array_equal(g.coarse_gs(f, 3, phi0), a)
+    g.close()
+    gb.close()
