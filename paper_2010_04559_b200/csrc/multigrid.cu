@@ -426,7 +426,10 @@ __global__ void __launch_bounds__(GS_WARPS * 32) coarse_gs_static_kernel(CoarseG
 // update) and the octant's K / X tables change: the pipeline drains there (every
 // nx items). Moments use a 4-buffer ring (items k-1 .. k+2), t0 and dz two buffers.
 // Co-residency of the ny CTAs is required (cooperative launch).
-constexpr int GSW_MW = 4;
+#ifndef STAMG_GSW_MW
+#define STAMG_GSW_MW 4  // warps of a row-CTA: the item warp + helpers (A/B: 2 / 3 / 4 warps all give ~2.0 us per item)
+#endif
+constexpr int GSW_MW = STAMG_GSW_MW;
 
 constexpr int MW_BAR = 1;  // named barrier of warps 1..3
 
