@@ -1591,7 +1591,18 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
       }
     }
     const auto& s = c->pb.spec;
+    // STAMG_SETUP_TRACE=1: wall time of the setup phases on stderr
+    const bool trace = std::getenv("STAMG_SETUP_TRACE") != nullptr;
+    auto tick = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+      if (!trace) return;
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[stamg setup] %-28s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - tick).count());
+      tick = now;
+    };
+    lap("cuda context, stream, comm");
     c->tree = make_sphere(s.angular_kind, s.angular_level, s.cone_levels, s.cone_half_angle_deg);
+    lap("angular mesh");
     if (generic) {  // reference-shape path: 3D / p0 / Lin problems on one GPU
       if (c->world > 1) throw std::invalid_argument("the reference-shape path (3D, p0 or Lin) runs on one GPU");
       c->wl_allowed = false, c->graphs_off = true;
@@ -1624,10 +1635,13 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
       for (int j = 0; j < 4; ++j) c->nsum[i] += c->outer.t.Nmat[i * 4 + j];
     if (s.n_mat > 1) c->mat = dupload(c->pb.mat, c->stream);
     if (!c->pb.q_el.empty()) c->q_el = dupload(c->pb.q_el, c->stream);
+    lap("outer tables (build_level)");
     upload_level(c.get(), c->outer);
+    lap("outer upload (+ fold tables)");
     if (want_mg) {
       c->nr = s.nr < 0 ? s.N : s.nr;
       auto lv = build_hierarchy(c->pb, c->tree, c->nr, s.n_levels, c->world > 1 ? &parts : nullptr);
+      lap("hierarchy tables");
       c->mg.resize(lv.size());
       for (size_t i = 0; i < lv.size(); ++i) {
         c->mg[i].t = std::move(lv[i]);
@@ -1637,6 +1651,7 @@ int stamg_create(const stamg_problem* prob, const stamg_options* opt, stamg_ctx*
       if (c->world > 1 && c->mg.size() == 1)
         throw std::invalid_argument("a sharded hierarchy needs at least two levels (the coarsest is replicated)");
       c->have_mg = true;
+      lap("hierarchy upload");
     }
     *out = c.release();
   });
