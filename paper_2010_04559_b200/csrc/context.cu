@@ -653,6 +653,19 @@ void upload_gen_level(stamg_ctx* c, DevLevel& L) {
     g->child_ptr = dupload(t.child_ptr, s), g->child_idx = dupload(t.child_idx, s);
   }
   for (int o = 0; o < 8; ++o) g->max_np = std::max(g->max_np, t.oct_ptr[o + 1] - t.oct_ptr[o]);
+  if (t.nx < 1024 && t.ny < 1024 && t.nz < 1024 && t.bs % 8 == 0) {  // hyperplane cell lists (tensor-core sweep)
+    const int npl = t.nx + t.ny + t.nz - 2;
+    std::vector<int> ptr(npl + 1, 0), cells(size_t(t.n_el));
+    for (int fk = 0; fk < t.nz; ++fk)
+      for (int fj = 0; fj < t.ny; ++fj)
+        for (int fi = 0; fi < t.nx; ++fi) ptr[fi + fj + fk + 1]++;
+    for (int p = 0; p < npl; ++p) ptr[p + 1] += ptr[p];
+    std::vector<int> fill(ptr.begin(), ptr.end() - 1);
+    for (int fk = 0; fk < t.nz; ++fk)
+      for (int fj = 0; fj < t.ny; ++fj)
+        for (int fi = 0; fi < t.nx; ++fi) cells[size_t(fill[fi + fj + fk]++)] = fi | (fj << 10) | (fk << 20);
+    g->plane_cells = dupload(cells, s), g->plane_ptr = dupload(ptr, s);
+  }
   ck(cudaStreamSynchronize(s), "upload sync");
 }
 
@@ -662,7 +675,7 @@ void free_level(DevLevel& L) {
     for (void* p : {(void*)g->XT, (void*)g->X, (void*)g->sig, (void*)g->Bd, (void*)g->Binv, (void*)g->C, (void*)g->BinvGS,
                     (void*)g->Nmat, (void*)g->upB, (void*)g->src, (void*)g->mom, (void*)g->octant,
                     (void*)g->oct_patches, (void*)g->oct_ptr, (void*)g->up, (void*)g->child_ptr, (void*)g->child_idx,
-                    (void*)g->gs_prog})
+                    (void*)g->gs_prog, (void*)g->plane_cells, (void*)g->plane_ptr})
       if (p) cudaFree(p);
     delete g;
     L.g = nullptr;

@@ -60,6 +60,9 @@ struct Dev {
   int *octant = nullptr, *oct_patches = nullptr, *oct_ptr = nullptr, *up = nullptr, *child_ptr = nullptr,
       *child_idx = nullptr;
   int max_np = 0;
+  // cells listed hyperplane by hyperplane in frame coordinates (fi | fj << 10 | fk << 20), for the
+  // tensor-core sweep; null when a grid side exceeds 1023
+  int *plane_cells = nullptr, *plane_ptr = nullptr;
   int* gs_prog = nullptr;  // [ny*nz] per-line progress counters of the dataflow coarse GS
 };
 
