@@ -50,18 +50,40 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
-// partial[k][b] = sum over block b's contiguous chunk of V_k . w
+// partial[k][b] = sum over block b's contiguous chunk of V_k . w. The chunk is streamed once per
+// group of eight vectors (w read once per group, not once per vector); every partial sum adds its
+// terms in the same order as a one-vector-at-a-time loop, so results are bitwise unchanged.
 __global__ void __launch_bounds__(kBlk) multidot_kernel(VecList vl, int nv, const double* __restrict__ w, int64_t n,
                                                          double* __restrict__ partial) {
   __shared__ double red[kBlk / 32];
+  constexpr int KG = 8;
   const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
   const int64_t lo = blockIdx.x * chunk, hi = std::min<int64_t>(n, lo + chunk);
-  for (int k = 0; k < nv; ++k) {
-    const double* __restrict__ v = vl.v[k];
-    double s = 0.0;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) s += v[i] * w[i];
-    const double tot = block_sum(s, red);
-    if (threadIdx.x == 0) partial[(size_t)k * gridDim.x + blockIdx.x] = tot;
+  for (int k0 = 0; k0 < nv; k0 += KG) {
+    const int kn = min(KG, nv - k0);
+    double s[KG];
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk) s[kk] = 0.0;
+    if (kn == KG) {
+      for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double wi = w[i];
+#pragma unroll
+        for (int kk = 0; kk < KG; ++kk) s[kk] += vl.v[k0 + kk][i] * wi;
+      }
+    } else {
+      for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const double wi = w[i];
+#pragma unroll
+        for (int kk = 0; kk < KG; ++kk)
+          if (kk < kn) s[kk] += vl.v[k0 + kk][i] * wi;
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < KG; ++kk) {
+      if (kk >= kn) break;
+      const double tot = block_sum(s[kk], red);
+      if (threadIdx.x == 0) partial[(size_t)(k0 + kk) * gridDim.x + blockIdx.x] = tot;
+    }
   }
 }
 
