@@ -492,6 +492,117 @@ __global__ void __launch_bounds__(128) m2d_block_kernel(Dev L, const double* __r
   }
 }
 
+// Scatter on the FP64 tensor cores for 8-dof (trilinear) cells: per cell the moment contraction
+// MOM (H x 8) = X^T (H x R) Phi (R x 8) and its transpose Y (R x 8) += X (R x H) SRC (H x 8) are
+// GEMMs whose N dimension is exactly the 8 dofs of a DMMA tile. A warp takes two cells, four
+// 8-row output tiles at a time (accumulators in registers), streaming the coupling table as A
+// fragments and the cell slab / moments as B fragments.
+constexpr int SC_MG = 4;  // output tiles per pass
+constexpr int SC_NC = 2;  // cells per warp
+
+__global__ void __launch_bounds__(128) d2m_mma_kernel(Dev L, const double* __restrict__ phi, int Hused, bool apply_sigma_N,
+                                                      double* __restrict__ out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int R = L.P * L.D, H = L.H;
+  const int el0 = (blockIdx.x * 4 + warp) * SC_NC;
+  if (el0 >= L.n_el) return;
+  const int ncell = min(SC_NC, L.n_el - el0);
+  const int MT = (Hused + 7) / 8;
+  for (int m0 = 0; m0 < MT; m0 += SC_MG) {
+    double acc[SC_MG][SC_NC][2];
+#pragma unroll
+    for (int a = 0; a < SC_MG; ++a)
+#pragma unroll
+      for (int c = 0; c < SC_NC; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+    for (int ks = 0; ks < R / 4; ++ks) {
+      const int r = 4 * ks + t;
+      double af[SC_MG], bf[SC_NC];
+#pragma unroll
+      for (int a = 0; a < SC_MG; ++a) {
+        const int h = 8 * (m0 + a) + g;
+        af[a] = h < Hused ? L.X[(size_t)r * H + h] : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < SC_NC; ++c) bf[c] = c < ncell ? phi[((size_t)(el0 + c) * R + r) * 8 + g] : 0.0;
+#pragma unroll
+      for (int a = 0; a < SC_MG; ++a)
+#pragma unroll
+        for (int c = 0; c < SC_NC; ++c) dmma_8x8x4(acc[a][c][0], acc[a][c][1], af[a], bf[c]);
+    }
+    // epilogue: accumulators hold mom[h = 8 mt + g][i = 2t, 2t + 1]
+#pragma unroll
+    for (int a = 0; a < SC_MG; ++a) {
+      const int h = 8 * (m0 + a) + g;
+#pragma unroll
+      for (int c = 0; c < SC_NC; ++c) {
+        double v0 = acc[a][c][0], v1 = acc[a][c][1];
+        if (apply_sigma_N) {  // row h of mom times N: gather the row's 8 values from the lane quad
+          double row[8];
+          const int qb = lane & ~3;
+#pragma unroll
+          for (int s2 = 0; s2 < 4; ++s2) {
+            row[2 * s2] = __shfl_sync(0xffffffffu, acc[a][c][0], qb + s2);
+            row[2 * s2 + 1] = __shfl_sync(0xffffffffu, acc[a][c][1], qb + s2);
+          }
+          double o0 = 0.0, o1 = 0.0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) o0 += row[j] * L.Nmat[j * 8 + 2 * t], o1 += row[j] * L.Nmat[j * 8 + 2 * t + 1];
+          const double sg = h < Hused ? L.sig[h] : 0.0;
+          v0 = sg * o0, v1 = sg * o1;
+        }
+        if (h < Hused && c < ncell)
+          *reinterpret_cast<double2*>(out + ((size_t)(el0 + c) * H + h) * 8 + 2 * t) = make_double2(v0, v1);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(128) m2d_mma_kernel(Dev L, const double* __restrict__ src, int Hused, double scale,
+                                                      double* __restrict__ y) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int R = L.P * L.D, H = L.H;
+  const int el0 = (blockIdx.x * 4 + warp) * SC_NC;
+  if (el0 >= L.n_el) return;
+  const int ncell = min(SC_NC, L.n_el - el0);
+  const int MT = R / 8, KS = (Hused + 3) / 4;
+  for (int m0 = 0; m0 < MT; m0 += SC_MG) {
+    double acc[SC_MG][SC_NC][2];
+#pragma unroll
+    for (int a = 0; a < SC_MG; ++a)
+#pragma unroll
+      for (int c = 0; c < SC_NC; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+    for (int ks = 0; ks < KS; ++ks) {
+      const int h = 4 * ks + t;
+      const bool hok = h < Hused;
+      double af[SC_MG], bf[SC_NC];
+#pragma unroll
+      for (int a = 0; a < SC_MG; ++a) {
+        const int r = 8 * (m0 + a) + g;
+        af[a] = (hok && m0 + a < MT) ? L.X[(size_t)r * H + h] : 0.0;
+      }
+#pragma unroll
+      for (int c = 0; c < SC_NC; ++c) bf[c] = (hok && c < ncell) ? src[((size_t)(el0 + c) * H + h) * 8 + g] : 0.0;
+#pragma unroll
+      for (int a = 0; a < SC_MG; ++a)
+#pragma unroll
+        for (int c = 0; c < SC_NC; ++c) dmma_8x8x4(acc[a][c][0], acc[a][c][1], af[a], bf[c]);
+    }
+#pragma unroll
+    for (int a = 0; a < SC_MG; ++a) {
+      if (m0 + a >= MT) break;
+      const int r = 8 * (m0 + a) + g;
+#pragma unroll
+      for (int c = 0; c < SC_NC; ++c) {
+        if (c >= ncell) break;
+        double2* yp = reinterpret_cast<double2*>(y + ((size_t)(el0 + c) * R + r) * 8 + 2 * t);
+        double2 v = *yp;
+        v.x += scale * acc[a][c][0], v.y += scale * acc[a][c][1];
+        *yp = v;
+      }
+    }
+  }
+}
+
 __global__ void prolong_kernel(Dev F, const double* __restrict__ coarse, double* __restrict__ fine, int Pc, bool add) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int S = F.S, D = F.D, bs = F.bs;
@@ -821,6 +932,10 @@ void launch_d2m(const Dev& L, const double* phi, int order, bool apply_sigma_N, 
   const int Hused = (order + 1) * (order + 1);
   const size_t smem = sizeof(double) * size_t(Hused) * L.S;
   if (smem > 200 * 1024) throw std::invalid_argument("reference-shape scatter: (order+1)^2 * S moments exceed shared memory");
+  if (L.S == 8 && (L.P * L.D) % 8 == 0) {
+    d2m_mma_kernel<<<(L.n_el + 4 * SC_NC - 1) / (4 * SC_NC), 128, 0, s>>>(L, phi, Hused, apply_sigma_N, out);
+    return;
+  }
   switch (L.S) {
     case 1: d2m_block_kernel<1><<<L.n_el, 128, 0, s>>>(L, phi, Hused, apply_sigma_N, out); return;
     case 4: d2m_block_kernel<4><<<L.n_el, 128, 0, s>>>(L, phi, Hused, apply_sigma_N, out); return;
@@ -835,6 +950,10 @@ void launch_m2d(const Dev& L, const double* src, int order, double scale, double
   const int Hused = (order + 1) * (order + 1);
   const size_t smem = sizeof(double) * size_t(Hused) * L.S;
   if (smem > 200 * 1024) throw std::invalid_argument("reference-shape scatter: (order+1)^2 * S moments exceed shared memory");
+  if (L.S == 8 && (L.P * L.D) % 8 == 0) {
+    m2d_mma_kernel<<<(L.n_el + 4 * SC_NC - 1) / (4 * SC_NC), 128, 0, s>>>(L, src, Hused, scale, y);
+    return;
+  }
   if (L.XT && (L.S == 1 || L.S == 4 || L.S == 8)) {
     auto k = L.S == 1 ? m2d_block_kernel<1> : L.S == 4 ? m2d_block_kernel<4> : m2d_block_kernel<8>;
     if (smem > 48 * 1024) ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), "attr");
