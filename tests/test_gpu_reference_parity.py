@@ -126,3 +126,19 @@ def test_gmres_matches_bicgstab_solution(case):
     assert rel(xs.numpy(), g["bicgstab_mg_x"]) <= 1e-8
     sf = c.scalar_flux(xs)
     assert np.all(np.isfinite(sf)) and sf.shape == (c.layout()[0],)
+
+
+def test_host_buffer_entry_points(case, stamg):
+    """The FFI boundary a reference maintainer binds: host buffers in, host buffers
+    out, for the reference's own discretisations too."""
+    name, c, g, N = case
+    x, _, _ = MGR.inputs(c.vec().n, c.vec(0).n)
+    z = np.empty_like(x)
+    c.sweep_host(np.ascontiguousarray(x), z)
+    assert rel(z, g["sweep"]) <= OP_TOL
+    b = c.rhs().numpy()
+    xs = np.zeros_like(b)
+    rep = c.solve_host(np.ascontiguousarray(b), xs, method="bicgstab", precond="mg", tol=1e-10, max_iter=100)
+    assert rep["converged"]
+    assert abs(rep["iterations"] - int(g["bicgstab_mg_iterations"][0])) <= 1
+    assert rel(xs, g["bicgstab_mg_x"]) <= 1e-9
