@@ -985,6 +985,12 @@ void op_sweep(stamg_ctx* c, DevLevel& L, const double* rhs, double* z, const dou
   p.prefer_breg = L.wl.nd > 0;
   if (L.sweep_xb > 1 && !base) {
     p.xb = L.sweep_xb, p.xb_g0 = L.sweep_xb_g0, p.xflag = L.sweep_xflag, p.xtrace = L.sweep_xtrace;
+    {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+      const int ngr = int(L.t.group8_oct.size());
+      p.xb_ticket = L.sweep_xb_g0 + (ngr - L.sweep_xb_g0) * L.sweep_xb > 2 * sms ? 1 : 0;
+    }
     ck(cudaMemsetAsync(L.sweep_xflag, 0, sizeof(int) * (L.t.group8_oct.size() * L.sweep_xb + 1), c->stream), "memset");
   }
   launch_sweep(p, c->stream);

@@ -51,6 +51,7 @@ struct SweepParams {
   bool prefer_breg = false;  // 8-direction groups: keep B^-1 in registers (2 CTAs/SM) even for 2-4 CTAs per SM of groups
   int xb = 1;                // > 1: column blocks per group (wavefront layout, plain sweep)
   int xb_g0 = 0;             // groups [0, xb_g0) are swept whole, groups from xb_g0 on in xb column blocks
+  int xb_ticket = 0;         // 1: block ids from an atomic ticket (grids larger than the co-resident capacity)
   int* xflag = nullptr;      // [n_groups][xb] strips published by each block (zeroed per launch)
   double2* xtrace = nullptr; // [n_groups][xb][ny][8] x-traces at the block edges
 };

@@ -78,12 +78,15 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
   // the flag waits below cannot deadlock even when the grid is many waves.
   // Groups below p.xb_g0 are swept whole (one block); the groups from xb_g0 on, the tail
   // wave of a grid of whole-group CTAs, are cut into p.xb column blocks each.
+  // (a grid that is co-resident as a whole needs no ticket: p.xb_ticket = 0)
   int bid = int(blockIdx.x);
   if constexpr (XBLK) {
-    __shared__ int s_bid;
-    if (threadIdx.x == 0) s_bid = atomicAdd(p.xflag + p.g.n_groups * p.xb, 1);
-    __syncthreads();
-    bid = s_bid;
+    if (p.xb_ticket) {
+      __shared__ int s_bid;
+      if (threadIdx.x == 0) s_bid = atomicAdd(p.xflag + p.g.n_groups * p.xb, 1);
+      __syncthreads();
+      bid = s_bid;
+    }
   }
   const bool cut = XBLK && bid >= p.xb_g0;
   const int xb = cut ? p.xb : 1;
