@@ -297,3 +297,33 @@ def test_dataflow_coarse_gs_is_bitwise_the_barrier_kernel(stamg, orc, monkeypatc
     assert np.array_equal(g.coarse_gs(f, 3, phi0), a)
     g.close()
     gb.close()
+
+
+def test_krylov_zero_rhs_and_iteration_cap(stamg, orc):  # test_krylov.cpp:29-48,100-116
+    m, st = orc.fp_moments(4, 1.0, 0.2)
+    g = Ops(stamg, cf.reference_test_problem(2, 1.0, 1, 1, 1, 4, m, st, dim=3))  # no source: b = 0
+    for method in ("gmres", "bicgstab"):
+        x, rep = g.c.solve(g.c.rhs(), method, "mg")
+        assert rep["converged"] and rep["iterations"] == 0 and inf(x.numpy()) == 0.0
+    g.close()
+    g2 = Ops(stamg, cf.reference_test_problem(2, 1.0, 1, 1, 1, 4, m, st, dim=3, q_el=np.ones(8)))
+    x, rep = g2.c.solve(g2.c.rhs(), "gmres", "sweep", tol=1e-14, max_iter=3)
+    assert rep["iterations"] == 3 and not rep["converged"]
+    x, rep = g2.c.solve(g2.c.rhs(), "bicgstab", "sweep", tol=1e-14, max_iter=2)
+    assert rep["iterations"] == 2 and not rep["converged"]
+    g2.close()
+
+
+def test_scatter_orders(stamg, orc):  # scatter.cpp:101-135: order 0 keeps only the isotropic moment, order < 0 is a no-op
+    sp = spec_ref(orc, 2, 1.0, 1, 1, 1, N=4)
+    o = orc.Oracle(sp)
+    g = Ops(stamg, sp)
+    x, y0 = rnd(o.size(), 61), rnd(o.size(), 62)
+    for order in (0, 2, 4):
+        yv = g.c.vec(data=y0)
+        g.c.apply_scatter_into(g.c.vec(data=x), order, 1.5, yv)
+        assert rel(yv.numpy(), o.apply_scatter(x, order, 1.5, y=y0)) <= 1e-12
+    yv = g.c.vec(data=y0)
+    g.c.apply_scatter_into(g.c.vec(data=x), -1, 1.0, yv)
+    assert np.array_equal(yv.numpy(), y0)
+    g.close()
