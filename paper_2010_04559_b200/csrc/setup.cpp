@@ -436,7 +436,20 @@ LevelTables build_level(const Problem& pb, const SphereTree& t, int order, bool 
   // the couplings are ~all of the setup time (1e9 harmonic evaluations at config 5): on the device
   const bool device_X = pb.device_setup && device_couplings_supported(order);
   if (device_X) device_couplings(t, L.leaf_id, order, xorder_base, L.X.data());
-  for (int q = 0; q < P; ++q) {
+  for (int q = 0; q < P; ++q) L.octant[q] = t.octant[L.leaf_id[q]];
+  // operator blocks on the device too (build_operators, transport.cpp:43-57); the host loop below
+  // is the STAMG_HOST_SETUP=1 path and the test oracle for the kernel
+  const bool device_blocks = pb.device_setup;
+  if (device_blocks) {
+    double el16[176];
+    std::copy(Nm, Nm + 16, el16);
+    std::copy(&V[0][0], &V[0][0] + 32, el16 + 16);
+    std::copy(&Fs[0][0], &Fs[0][0] + 64, el16 + 48);
+    std::copy(&Fn[0][0], &Fn[0][0] + 64, el16 + 112);
+    device_patch_blocks(t, L.leaf_id, pb.sigma_t, el16, L.area.data(), L.Aflow.data(), L.B.data(), L.Binv.data(),
+                        L.C.data(), L.cxy.data());
+  }
+  for (int q = 0; q < P && !(device_blocks && device_X); ++q) {
     const int id = L.leaf_id[q];
     L.octant[q] = t.octant[id];
     // Const patch operators: M = sum w, A^xi = sum w Omega_xi (angular_disc.cpp:40-59)

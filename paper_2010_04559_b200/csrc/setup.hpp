@@ -142,6 +142,10 @@ void gauss_rule01(int n, const double** x, const double** w);
 // the given leaves, written to host memory; orders up to 32
 bool device_couplings_supported(int order);
 void device_couplings(const SphereTree& t, const std::vector<int>& leaf_id, int order, int xorder_base, double* X);
+// build_operators (transport.cpp:43-57) on the current CUDA device: patch mass and Jacobians by
+// quadrature, fused blocks, their inverses, inflow blocks; el16 = N | V0 | V1 | F_self[4] | F_neigh[4]
+void device_patch_blocks(const SphereTree& t, const std::vector<int>& leaf_id, const std::vector<double>& sigma_t,
+                         const double* el16, double* area, double* Aflow, double* B, double* Binv, double* C, double* cxy);
 
 // every node of a patch's Duffy-collapsed rule: unit directions [n][3], flat barycentric
 // coordinates [n][3], weights [n] (quadrature.cpp:59-92); real orthonormal harmonics

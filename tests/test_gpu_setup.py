@@ -1,8 +1,9 @@
-"""Device-side setup: build_couplings (scatter.cpp:74-99)
-runs on the GPU (csrc/couplings.cu). Its table must match the host loop
-(STAMG_HOST_SETUP=1, the same quadrature and recurrence on one core) at the
-full BASELINE sizes, including config 4's mixed-level cone mesh and every MG
-level, and the device path must be much faster."""
+"""Device-side setup: build_couplings (scatter.cpp:74-99) and
+build_operators (transport.cpp:43-57: patch mass / Jacobians by quadrature, fused blocks,
+their inverses, inflow blocks) run on the GPU (csrc/couplings.cu). The tables must match
+the host loops (STAMG_HOST_SETUP=1, the same quadrature, recurrence and block algebra on
+one core) at the full BASELINE angular meshes, including config 4's mixed-level cone mesh,
+config 3's two materials and every MG level, and the device path must be much faster."""
 import os
 import time
 
@@ -36,6 +37,10 @@ def test_device_couplings_match_host(stamg, k, mg):
             a, b = d.table("X", l), h.table("X", l)
             assert a.shape == b.shape
             assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max(), l
+            for name in ("B", "Binv", "C", "area"):  # build_operators on the device
+                a, b = d.table(name, l), h.table(name, l)
+                assert a.shape == b.shape
+                assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max(), (name, l)
         print(f"c{k}: setup device {td:.3f} s, host {th:.3f} s")
         if k == 5:
             assert td < th
