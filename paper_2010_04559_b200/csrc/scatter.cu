@@ -122,6 +122,27 @@ __device__ __forceinline__ void mma_stage(const double* sA, const double* sB, do
   }
 }
 
+// the first `steps` k-steps (of 4 rows) of a stage: the tail tile of a short k-loop
+template <int MI, int TLDA>
+__device__ __forceinline__ void mma_steps(const double* sA, const double* sB, double (&acc)[MI][4][2], int wm, int wn,
+                                          int g, int t, int steps) {
+#pragma unroll 1
+  for (int kk = 0; kk < steps * 4; kk += 4) {
+    double a[MI], b[4];
+#pragma unroll
+    for (int i = 0; i < MI; ++i) a[i] = sA[(kk + t) * TLDA + wm * (8 * MI) + i * 8 + g];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = wn * 32 + j * 8 + g;
+      b[j] = sB[(n >> 2) * (BK * 4) + (kk + t) * 4 + (n & 3)];
+    }
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+}
+
 // ---- TMA staging: warp 0 fills stage `kt % NSTAGE` with bulk copies that complete on
 // that stage's mbarrier (expect_tx set first by lane 0); every thread waits on the
 // barrier's phase parity (kt / NSTAGE) & 1. Stages are zeroed once at kernel start, so
@@ -269,15 +290,28 @@ constexpr int M2D_STAGE = BK * M2D_LDA + kStageB;
 #ifndef STAMG_M2D_MINB
 #define STAMG_M2D_MINB 3  // resident CTAs per SM the beta != 0 M2D registers are sized for (230 -> 168 regs; c4 MG-level M2D 6.97 -> 5.90 ms)
 #endif
+#ifndef STAMG_M2D_PATCH_FASTEST
+// 1: CTAs of one element tile are consecutive (1D grid, patch tiles fastest), so the tile's
+// src panel comes from DRAM once and from L2 for the other patch tiles; X^T (a few MB) stays
+// L2-resident. With element tiles fastest the whole src array (268 MB at config 4's MG level,
+// more than L2) was streamed from DRAM once per patch tile: 14.2 GB read per launch against
+// 6.3 GB algorithmic (ncu, profiles/r02_c4_kernels.txt).
+#define STAMG_M2D_PATCH_FASTEST 1
+#endif
 template <bool PRE_>
-constexpr int m2d_minb() { return PRE_ ? STAMG_M2D_MINB : 1; }
+constexpr int m2d_minb() { return PRE_ ? STAMG_M2D_MINB : 4; }  // beta == 0: 4 CTAs/SM (<= 128 registers)
 template <bool PRE>
 __global__ void __launch_bounds__(M2D_THREADS, m2d_minb<PRE>()) m2d_kernel(M2DParams p) {
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3, wm = warp >> 1, wn = warp & 1;
+#if STAMG_M2D_PATCH_FASTEST
+  const unsigned gq = (p.P + M2D_BM - 1) / M2D_BM, te = blockIdx.x / gq, tq = blockIdx.x - te * gq;
+  const int el0 = p.el_base + int(te) * (BN / 4), q0 = int(tq) * M2D_BM;
+#else
   const int el0 = p.el_base + (STAMG_GEMM_SWAP ? blockIdx.y : blockIdx.x) * (BN / 4);
   const int q0 = (STAMG_GEMM_SWAP ? blockIdx.x : blockIdx.y) * M2D_BM;
+#endif
   double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -300,7 +334,12 @@ __global__ void __launch_bounds__(M2D_THREADS, m2d_minb<PRE>()) m2d_kernel(M2DPa
   const int nk = (p.Hused + BK - 1) / BK;
 #if STAMG_GEMM_TMA
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + NSTAGE * M2D_STAGE);
-  gemm_tma_init(smem, M2D_STAGE, bars, tid, M2D_THREADS);
+  // no zero fill: every A row and B row a k-step reads is copied or zeroed by the tail code, and
+  // B columns of elements past the end only feed accumulators that are never stored
+  if (tid == 0)
+    for (int st = 0; st < NSTAGE; ++st) mbar_init_cta(bars + st, 1);
+  fence_proxy_async_smem();
+  __syncthreads();
   // stage: A = rows h of X^T (M2D_BM patches each), B = the (h-chunk x 4) panel of src per
   // element; rows h >= Hused are not copied (their A rows are zeroed in the tail tile)
   auto issue = [&](int kt) {
@@ -323,11 +362,21 @@ __global__ void __launch_bounds__(M2D_THREADS, m2d_minb<PRE>()) m2d_kernel(M2DPa
     mbar_wait_parity(bars + kt % NSTAGE, unsigned(kt / NSTAGE) & 1u);
     double* st = smem + (kt % NSTAGE) * M2D_STAGE;
     const int kv = p.Hused - kt * BK;
-    if (kv < BK) {  // tail tile (uniform): stale A rows -> 0
-      for (int c = tid; c < (BK - kv) * M2D_LDA; c += M2D_THREADS) st[kv * M2D_LDA + c] = 0.0;
+    if (kv < BK) {
+      // tail tile (CTA-uniform): only the k-steps that hold copied rows run; the rows that pad
+      // the last step to 4 are zeroed in A and in B (a stage is never zero-filled as a whole)
+      const int kv4 = (kv + 3) & ~3, pad = kv4 - kv;
+      for (int c = tid; c < pad * M2D_LDA; c += M2D_THREADS) st[kv * M2D_LDA + c] = 0.0;
+      double* sB = st + BK * M2D_LDA;
+      for (int c = tid; c < (BN / 4) * pad * 4; c += M2D_THREADS) {
+        const int e = c / (pad * 4), w = c - e * (pad * 4);
+        sB[e * (BK * 4) + kv * 4 + w] = 0.0;
+      }
       __syncthreads();
+      mma_steps<4, M2D_LDA>(st, sB, acc, wm, wn, g, t, kv4 / 4);
+    } else {
+      mma_stage<4, M2D_LDA>(st, st + BK * M2D_LDA, acc, wm, wn, g, t);
     }
-    mma_stage<4, M2D_LDA>(st, st + BK * M2D_LDA, acc, wm, wn, g, t);
     __syncthreads();
   }
 #else
@@ -682,6 +731,7 @@ void launch_m2d(const M2DParams& p, cudaStream_t s) {
   if (p.Pp % M2D_BM != 0) throw std::invalid_argument("m2d: X^T row pitch is not a multiple of the patch tile");
   const unsigned ge = (p.n_el + BN / 4 - 1) / (BN / 4), gq = (p.P + M2D_BM - 1) / M2D_BM;
   dim3 grid = STAMG_GEMM_SWAP ? dim3(gq, ge) : dim3(ge, gq);
+  if (STAMG_M2D_PATCH_FASTEST) grid = dim3(ge * gq);
   if (p.beta != 0.0) m2d_kernel<true><<<grid, M2D_THREADS, gemm_smem(), s>>>(p);
   else m2d_kernel<false><<<grid, M2D_THREADS, gemm_smem(), s>>>(p);
 }

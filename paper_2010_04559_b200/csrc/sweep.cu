@@ -17,8 +17,10 @@
 #include "common.cuh"
 #include "kernels.hpp"
 
+#include <algorithm>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 namespace stamg_b200 {
 namespace {
@@ -26,7 +28,10 @@ namespace {
 #ifndef STAMG_SWEEP8_BREG
 #define STAMG_SWEEP8_BREG 1  // 8-direction kernel keeps B^-1 in registers (2 CTAs/SM); A/B: 82.5 % vs 79 %
 #endif
-constexpr int NST = STAMG_SWEEP_NST;
+constexpr int kNST = STAMG_SWEEP_NST;
+#ifndef STAMG_SWEEP_ONE_WAVE4
+#define STAMG_SWEEP_ONE_WAVE4 1  // A/B: 0 = always the 2-per-SM kernel (B^-1 in registers)
+#endif
 #ifndef STAMG_SWEEP_BULK
 // wavefront layout: 1 = a step's rows arrive as one or two TMA bulk copies (cp.async.bulk, one
 // issuing thread, mbarrier completion), 0 = per-thread cp.async. A/B at config 5 (512^2 x 8192,
@@ -47,9 +52,13 @@ constexpr int NST = STAMG_SWEEP_NST;
 // x-traces at their common edge (global scratch + one flag per strip), so a group's
 // wavefront runs on xb SMs. Used when there are fewer groups than SMs (config 5
 // sharded over 8 GPUs: 128 groups per rank); all CTAs are co-resident.
-template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY = false, int MODE = 0, bool BREG = true,
-          bool XBLK = false>
-__global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_kernel(SweepParams p) {
+// BPS: resident CTAs per SM the registers are sized for (8-direction kernels): 2 or 3 keep B^-1 in
+// registers (112 / 80 registers), 4 reads it from shared memory (64 registers).
+template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY = false, int MODE = 0, int BPS = 2,
+          bool XBLK = false, int NST_ = kNST>
+__global__ void __launch_bounds__(DIRS * R, (TOPG ? BPS : 1)) sweep_kernel(SweepParams p) {
+  constexpr bool BREG = BPS < 4;
+  constexpr int NST = NST_;  // rhs staging depth of this instantiation
   // WLAY: vectors in the wavefront layout (a step's R rows are consecutive slots).
   // MODE 1: apply_L on the same skewed schedule (y = alpha*(B x + C x_up) + beta*f, traces of x).
   // TOPG (8-direction) variant: 4 CTAs/SM (<= 64 registers), B^-1 read from shared memory
@@ -62,7 +71,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
   // issues them as cp.async.bulk copies completing on the stage's mbarrier (UBLKCP); nobody
   // computes a per-thread source address or issues per-thread LDGSTS for the vector data.
   constexpr bool BULK = WLAY && TOPG && (STAMG_SWEEP_BULK != 0);
-  __shared__ unsigned long long s_bar[BULK ? NST : 1];
+  __shared__ unsigned long long s_bar[BULK ? NST_ : 1];
   extern __shared__ __align__(128) double smem[];
   double* st_rhs = smem;
   double* st_base = st_rhs + NST * NT * 4;
@@ -130,42 +139,47 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
   const double2* xin = XBLK && xblk > 0 ? p.xtrace + ((size_t)(grp * xbs + xblk - 1) * ny) * DIRS : nullptr;
   double2* xout = XBLK && xblk < xb - 1 ? p.xtrace + ((size_t)(grp * xbs + xblk) * ny) * DIRS : nullptr;
 
-  // Cursor over this thread's wavefront positions k: strip s, column i, cell el and
-  // block offset, advanced incrementally (no integer division inside a strip).
+  // Cursor over this thread's wavefront positions k = (strip s, column i): advanced by one
+  // add per field; the block offset (and the row's validity) is recomputed only when the
+  // cursor enters a strip. Positions k < 0 (this row's ramp-in) count i up from -r on the
+  // virtual columns left of strip 0; positions k >= nk run past the last strip. Neither is
+  // dereferenced (kin() is false).
   struct Cursor {
     int k, s, i, el;
-    bool ok, kin;
+    bool rowok;
     size_t off;
   };
   const int dx = xneg ? -1 : 1;
-  auto fresh = [&](Cursor& c, int k) {
-    c.k = k;
-    c.kin = k >= 0 && k < nk;
-    if (!c.kin) {
-      c.ok = false, c.s = 0, c.i = 0, c.el = 0, c.off = 0;
-      return;
-    }
-    c.s = k / nxl, c.i = k - c.s * nxl;
-    const int j = c.s * R + r, fi = i0 + c.i;
-    c.ok = qok && j < ny;
-    const int gx = xneg ? nx - 1 - fi : fi, gy = yneg ? ny - 1 - j : (j < ny ? j : 0);
+  const ptrdiff_t cstride = WLAY ? (ptrdiff_t)R * DIRS * 4 : (ptrdiff_t)dx * DP * 4;
+  auto enter = [&](Cursor& c) {  // column 0 of strip c.s
+    const int j = c.s * R + r;
+    c.rowok = qok && j < ny;
+    const int jj = j < ny ? j : 0;
+    const int gx = xneg ? nx - 1 - i0 : i0, gy = yneg ? ny - 1 - jj : jj;
     c.el = gy * nx + gx;
-    if constexpr (WLAY) c.off = (((size_t)grp * p.wl.slots + wl_slot_frame(p.wl, fi, j)) * DIRS + dir) * 4;
+    if constexpr (WLAY) c.off = (((size_t)grp * p.wl.slots + wl_slot_frame(p.wl, i0, jj)) * DIRS + dir) * 4;
     else c.off = ((size_t)c.el * DP + (qq - DQ0)) * 4;
   };
-  auto advance = [&](Cursor& c) {
-    const int k = c.k + 1;
-    if (k <= 0 || k >= nk || c.i + 1 == nxl) {
-      fresh(c, k);
-      return;
-    }
-    c.k = k, c.i += 1, c.el += dx;
-    if constexpr (WLAY) c.off += (size_t)R * DIRS * 4;
-    else c.off += (ptrdiff_t)dx * DP * 4;
+  auto start = [&](Cursor& c) {  // position k = -r
+    c.s = 0;
+    enter(c);
+    c.k = c.i = -r;
+    c.off -= (size_t)((ptrdiff_t)r * cstride);
+    c.el -= r * dx;
   };
+  auto advance = [&](Cursor& c) {
+    ++c.k, ++c.i, c.off += (size_t)cstride;
+    if constexpr (MULTI) c.el += dx;
+    if (c.i == nxl) {
+      c.i = 0, ++c.s;
+      enter(c);
+    }
+  };
+  auto kin_of = [&](const Cursor& c) { return (unsigned)c.k < (unsigned)nk; };
   // BULK producer state (thread 0): strip of row 0 at the issue step and the step within it
   int b_sh = 0, b_rb = 0;
-  auto issue = [&](int t, const Cursor& c) {
+  auto issue = [&](int t, int stg, const Cursor& c) {
+    const bool c_kin = kin_of(c), c_ok = c_kin && c.rowok;
     if constexpr (BULK) {
       if (tid == 0) {
         // rows 0..rb are in strip sh on diagonal i0 + rb, rows rb+1..R-1 still in strip sh-1
@@ -173,7 +187,6 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
         const int nA = b_sh < nstrips ? min(b_rb, R - 1) + 1 : 0;
         const int nB = (b_sh >= 1 && b_sh - 1 < nstrips && b_rb < R - 1) ? R - 1 - b_rb : 0;
         if (nA + nB > 0) {
-          const int stg = t % NST;
           unsigned long long* bar = &s_bar[stg];
           mbar_expect_tx(bar, unsigned(nA + nB) * DIRS * 32u * (ACCUM ? 2u : 1u));
           const size_t g0 = (size_t)grp * p.wl.slots;
@@ -192,27 +205,27 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
         if (++b_rb == nxl) b_rb = 0, ++b_sh;
       }
     } else {
-    const bool ok = c.ok;
+    const bool ok = c_ok;
     const size_t off = ok ? c.off : 0;
     const double* src = p.rhs + off;
-    double* dst = st_rhs + ((t % NST) * NT + tid) * 4;
+    double* dst = st_rhs + (stg * NT + tid) * 4;
     cp_async16(dst, src, ok);
     cp_async16(dst + 2, src + 2, ok);
     if constexpr (ACCUM) {
       const double* sb = p.base + off;
-      double* db = st_base + ((t % NST) * NT + tid) * 4;
+      double* db = st_base + (stg * NT + tid) * 4;
       cp_async16(db, sb, ok);
       cp_async16(db + 2, sb + 2, ok);
     }
     }
     if constexpr (TOPG) {  // row 0 of strip s >= 1 needs the trace row R-1 left in the scratch
       if (r == 0) {
-        const bool tk = c.kin && c.s >= 1;
-        cp_async16(st_top + (t % NST) * DIRS + dir, gtop + (size_t)dir * nx + (tk ? i0 + c.i : 0), tk);
+        const bool tk = c_kin && c.s >= 1;
+        cp_async16(st_top + stg * DIRS + dir, gtop + (size_t)dir * nx + (tk ? i0 + c.i : 0), tk);
       }
     }
     if constexpr (XBLK) {  // the block's first column of a strip: x-trace from the upwind block
-      if (xin && c.kin && c.i == 0) {
+      if (xin && c_kin && c.i == 0) {
         const int j = c.s * R + r;
         cp_async16(sxin + tid, xin + (size_t)(j < ny ? j : 0) * DIRS + dir, j < ny);
       }
@@ -241,28 +254,32 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
     if (xin) wait_strip();
   }
   Cursor ci, cc;  // issue cursor (k = t + NST - 1 - r) and compute cursor (k = t - r)
-  fresh(ci, -r);
-  fresh(cc, -r);
+  start(ci);
+  start(cc);
 #pragma unroll
   for (int t = 0; t < NST - 1; ++t) {
-    issue(t, ci);
+    issue(t, t, ci);
     cp_async_commit();
     advance(ci);
   }
   __syncthreads();
 
-  const int m = (xneg ? 1 : 0) | (yneg ? 2 : 0);
+  // The step loop is instantiated per octant reflection m (CTA-uniform), so the
+  // physical <-> sweep-frame dof permutations are register renames, not selects.
+  auto steps = [&](auto mtag) {
+  constexpr int m = decltype(mtag)::value;
   double2 tx = make_double2(0.0, 0.0), typrev = make_double2(0.0, 0.0);
+  int stg = 0, stg_issue = NST - 1;  // stage of step t, stage filled during step t (= t + NST - 1 mod NST)
   for (int t = 0; t < T; ++t) {
     if constexpr (XBLK) {
       if (xin && wait_s < nstrips && t == wait_t) wait_strip();
     }
-    issue(t + NST - 1, ci);
+    issue(t + NST - 1, stg_issue, ci);
     cp_async_commit();
     advance(ci);
     cp_async_wait<NST - 1>();
-    if constexpr (BULK) mbar_wait_parity(&s_bar[t % NST], unsigned(t / NST) & 1u);
-    const bool kin = cc.kin;
+    if constexpr (BULK) mbar_wait_parity(&s_bar[stg], unsigned(t / NST) & 1u);
+    const bool kin = kin_of(cc);
     const int s = cc.s, i = cc.i;
     double2 ty;
     ty.x = __shfl_up_sync(0xffffffffu, typrev.x, DIRS);
@@ -270,23 +287,23 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
     if (lane < DIRS) {
       if (warp == 0) {
         if (s == 0 || !kin) ty = make_double2(0.0, 0.0);
-        else if constexpr (TOPG) ty = st_top[(t % NST) * DIRS + dir];
+        else if constexpr (TOPG) ty = st_top[stg * DIRS + dir];
         else ty = top[dir * nx + i];
       } else {
         ty = xw[((t - 1) & 1) * NW * DIRS + (warp - 1) * DIRS + dir];
       }
     }
     double2 tyout = make_double2(0.0, 0.0);
-    const int el = cc.el;
-    if (cc.ok) {
-      const double* rs = st_rhs + ((t % NST) * NT + tid) * 4;
+    [[maybe_unused]] const int el = cc.el;
+    if (kin && cc.rowok) {
+      const double* rs = st_rhs + (stg * NT + tid) * 4;
       double r0 = rs[0], r1 = rs[1], r2 = rs[2], r3 = rs[3];
       // physical -> sweep frame (dof i -> i ^ m)
       if (m & 1) { double u = r0; r0 = r1; r1 = u; u = r2; r2 = r3; r3 = u; }
       if (m & 2) { double u = r0; r0 = r2; r2 = u; u = r1; r1 = r3; r3 = u; }
       if (i == 0) tx = (XBLK && xin) ? sxin[tid] : make_double2(0.0, 0.0);
       const double* B = Bi;
-      double Bm[16];
+      [[maybe_unused]] double Bm[16];
       if constexpr (BSMEM) {
         const int mt = MULTI ? p.g.mat[el] : 0;
 #pragma unroll
@@ -329,7 +346,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
       if (m & 2) { double u = z0; z0 = z2; z2 = u; u = z1; z1 = z3; z3 = u; }
       if (m & 1) { double u = z0; z0 = z1; z1 = u; u = z2; z2 = z3; z3 = u; }
       if constexpr (ACCUM) {
-        const double* bs = st_base + ((t % NST) * NT + tid) * 4;
+        const double* bs = st_base + (stg * NT + tid) * 4;
         if constexpr (MODE == 0) {
           z0 += bs[0], z1 += bs[1], z2 += bs[2], z3 += bs[3];
         } else {
@@ -350,6 +367,8 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
     }
     typrev = tyout;
     advance(cc);
+    stg_issue = stg;
+    stg = stg + 1 == NST ? 0 : stg + 1;
     __syncthreads();
     if constexpr (XBLK) {  // strip pub_s's last column is done by every row: publish its edge traces
       if (xout && t == pub_t) {
@@ -361,35 +380,77 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? (BREG ? 2 : 4) : 1)) sweep_k
       }
     }
   }
+  };
+  switch ((xneg ? 1 : 0) | (yneg ? 2 : 0)) {
+    case 0: steps(std::integral_constant<int, 0>{}); break;
+    case 1: steps(std::integral_constant<int, 1>{}); break;
+    case 2: steps(std::integral_constant<int, 2>{}); break;
+    default: steps(std::integral_constant<int, 3>{}); break;
+  }
   cp_async_wait<0>();
   (void)RPW;
 }
 
-template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY, int MODE, bool BREG, bool XBLK = false>
+template <int DIRS, int R, bool ACCUM, bool TOPG>
+size_t sweep_smem(const SweepParams& p, int NST, bool bsmem, bool xblk) {
+  constexpr int NT = DIRS * R;
+  return sizeof(double) * NST * NT * 4 * (ACCUM ? 2 : 1) +
+         sizeof(double2) * ((TOPG ? NST * DIRS : DIRS * p.g.nx) + 2 * (NT / 32) * DIRS) +
+         (bsmem ? sizeof(double) * p.g.n_mat * DIRS * 17 : 0) + (xblk ? sizeof(double2) * NT : 0);
+}
+
+template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY, int MODE, int BPS, bool XBLK = false,
+          int NST = kNST>
 void launch_tb(const SweepParams& p, cudaStream_t s) {
   constexpr int NT = DIRS * R;
-  size_t smem = sizeof(double) * NST * NT * 4 * (ACCUM ? 2 : 1) +
-                sizeof(double2) * ((TOPG ? NST * DIRS : DIRS * p.g.nx) + 2 * (NT / 32) * DIRS) +
-                ((MULTI || TOPG) ? sizeof(double) * p.g.n_mat * DIRS * 17 : 0) + (XBLK ? sizeof(double2) * NT : 0);
-  auto k = sweep_kernel<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, BREG, XBLK>;
+  const size_t smem = sweep_smem<DIRS, R, ACCUM, TOPG>(p, NST, MULTI || (TOPG && BPS == 4), XBLK);
+  auto k = sweep_kernel<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, BPS, XBLK, NST>;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   k<<<XBLK ? p.xb_g0 + (p.g.n_groups - p.xb_g0) * p.xb : p.g.n_groups, NT, smem, s>>>(p);
 }
 
-// 8-direction groups: B^-1 in registers gives 2 CTAs/SM (the faster kernel when the
-// grid is many waves, 82.5 % vs 79 % of HBM at config 5), B^-1 in shared memory 4.
-// A group count just above one 2-per-SM wave (config 4's cone mesh: 364 groups
-// for 296 slots) would leave a second, mostly empty wave of whole-grid sweeps:
-// there the 4-per-SM kernel runs everything in one wave.
+// 8-direction groups, by how the grid fills the SMs:
+//  * many waves (config 5: 1024 groups) or at most two CTAs per SM: B^-1 in registers at
+//    112 registers, 2 CTAs/SM (82.5 % vs 79 % of HBM for the shared-memory B^-1 at config 5);
+//  * a grid that fits one wave at 3 CTAs per SM (config 4's cone mesh: 364 groups on 444
+//    slots): B^-1 still in registers, capped at 80 registers;
+//  * one wave only at 4 CTAs per SM: B^-1 in shared memory (64 registers).
+// The one-wave kernels only pay when the whole grid is resident, so the rhs staging depth
+// drops from 6 to 4 or 3 steps where shared memory would otherwise limit residency (a base
+// vector doubles the staging: config 4's smoother sweep, 5.60 -> 4.17 ms at depth 4).
+#ifndef STAMG_SWEEP_BPS
+#define STAMG_SWEEP_BPS 2  // A/B: CTAs per SM of the many-wave kernel
+#endif
+template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY, int MODE, int BPS>
+void launch_resident(const SweepParams& p, int sms, cudaStream_t s) {
+  auto resident = [&](int nst) {
+    const size_t smem = sweep_smem<DIRS, R, ACCUM, TOPG>(p, nst, MULTI || BPS == 4, false) + 1024;
+    return int(std::min<size_t>(BPS, (227 * 1024) / smem)) * sms >= p.g.n_groups;
+  };
+  if (kNST > 4 && !resident(kNST)) {
+    if (resident(4)) launch_tb<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, BPS, false, 4>(p, s);
+    else launch_tb<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, BPS, false, 3>(p, s);
+    return;
+  }
+  launch_tb<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, BPS>(p, s);
+}
+
 template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY = false, int MODE = 0>
 void launch_t(const SweepParams& p, cudaStream_t s) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const bool one_wave4 = TOPG && p.g.n_groups > 2 * sms && p.g.n_groups <= 4 * sms && !p.prefer_breg;
-  const bool breg = STAMG_SWEEP8_BREG && !one_wave4;
-  if (breg) launch_tb<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, true>(p, s);
-  else launch_tb<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, false>(p, s);
+  if constexpr (TOPG) {
+    const int ng = p.g.n_groups;
+    if (STAMG_SWEEP_ONE_WAVE4 && !p.prefer_breg && ng > 2 * sms && ng <= 4 * sms) {
+      if (ng <= 3 * sms) launch_resident<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, 3>(p, sms, s);
+      else launch_resident<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, 4>(p, sms, s);
+      return;
+    }
+    launch_tb<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, STAMG_SWEEP8_BREG ? STAMG_SWEEP_BPS : 4>(p, s);
+  } else {
+    launch_tb<DIRS, R, MULTI, ACCUM, TOPG, WLAY, MODE, 2>(p, s);
+  }
 }
 
 template <int DIRS, int R, bool TOPG, bool WLAY = false, int MODE = 0>
@@ -422,8 +483,8 @@ void launch_sweep(const SweepParams& p, cudaStream_t s) {
         if (p.mode != 0 || p.base || !p.xflag || !p.xtrace || p.g.nx % p.xb || p.g.nx / p.xb < kSweep8MinNx)
           throw std::invalid_argument("sweep: column blocks need a plain sweep and nx / xb >= 38");
         // (B^-1 in shared memory at four CTAs per SM measured slower: 4.77 vs 3.53 ms per rank at N = 8)
-        if (p.g.n_mat > 1) launch_tb<8, 32, true, false, true, true, 0, true, true>(p, s);
-        else launch_tb<8, 32, false, false, true, true, 0, true, true>(p, s);
+        if (p.g.n_mat > 1) launch_tb<8, 32, true, false, true, true, 0, 2, true>(p, s);
+        else launch_tb<8, 32, false, false, true, true, 0, 2, true>(p, s);
         return;
       }
       p.mode == 1 ? launch_r<8, 32, true, true, 1>(p, s) : launch_r<8, 32, true, true, 0>(p, s);
