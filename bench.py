@@ -268,6 +268,22 @@ def kernel_rooflines(stamg, cf, dmma_peak):
             out[f"{kname}_mg_nr{nr}"] = {"ms": t * 1e3, "algorithmic_flop": flop, "achieved_tflops": flop / t * 1e-12,
                                         "frac": flop / t * 1e-12 / dmma_peak, "bound": "fp64_tensor"}
         g.timing(False)
+        # the forms the V-cycle runs: one smoother step on the finest MG level = residual
+        # apply_L (y = f - L x: reads x and f, writes y) + reduced-order scatter + accumulating
+        # sweep (reads rhs and the base vector, writes z): 96 B per cell-direction each
+        ff, ph = g.vec(lf).fill(1.0), g.vec(lf).fill(0.5)
+        g.smoother_step(ff, nr, ph, level=lf)
+        g.synchronize()
+        g.timing(True)
+        g.smoother_step(ff, nr, ph, level=lf)
+        g.synchronize()
+        for name, kname in (("smoother_apply_L", "apply_L"), ("smoother_sweep", "sweep")):
+            ms, n = g.timed(kname)
+            t = ms / max(n, 1) * 1e-3
+            nbytes = n_el * Pf * 96
+            out[name] = {"ms": t * 1e3, "bytes": nbytes, "achieved_gbs": nbytes / t * 1e-9, "frac": nbytes / t * 1e-9 / hbm,
+                         "bound": "hbm", "level": lf}
+        g.timing(False)
         out["config"] = f"c4 full: {n_el} cells, outer P={P} (N={spec.N}), MG levels {lf}->{lf - 1}: P {Pf}->{Pc} (nr={nr})"
     finally:
         g.close()

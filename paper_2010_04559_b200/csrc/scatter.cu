@@ -298,6 +298,11 @@ constexpr int M2D_STAGE = BK * M2D_LDA + kStageB;
 // 6.3 GB algorithmic (ncu, profiles/r02_c4_kernels.txt).
 #define STAMG_M2D_PATCH_FASTEST 1
 #endif
+// Measured and not kept (profiles/r02_c4_kernels.txt): one CTA walking 4 / 8 / 16 element tiles
+// with a single TMA pipeline over the (tile, k-tile) pairs -- no pipeline refill or barrier
+// setup per tile -- ran the K = 81 M2D in 7.5 / 7.5 / 7.6 ms against 6.4 ms for one tile per
+// CTA, and 8.4 ms with two instead of three resident CTAs: what hides a tile's epilogue and
+// first-copy latency is other CTAs' tensor work, so more, shorter CTAs win.
 template <bool PRE_>
 constexpr int m2d_minb() { return PRE_ ? STAMG_M2D_MINB : 4; }  // beta == 0: 4 CTAs/SM (<= 128 registers)
 template <bool PRE>
