@@ -1011,7 +1011,9 @@ void op_smoother(stamg_ctx* c, DevLevel& L, const double* f, int order, double* 
   op_sweep(c, L, L.tmp, phi, phi);
 }
 
-void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* phi) {
+// phi_zero: the caller has just zero-filled phi (the V-cycle's coarse correction), so its
+// moments are zero without a D2M
+void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* phi, bool phi_zero = false) {
   if (nu <= 0) return;
   if (L.g) {
     if (!L.g->BinvGS) throw std::invalid_argument("coarse_scatter_sweep: not the coarsest level");
@@ -1023,7 +1025,8 @@ void op_coarse_gs(stamg_ctx* c, DevLevel& L, const double* rhs, int nu, double* 
   }
   if (!L.BinvGS) throw std::invalid_argument("coarse_scatter_sweep: not the coarsest level");
   // per-element moments of the current iterate (sweeps.cpp:74-79)
-  op_d2m(c, L, phi, L.t.order, L.mom, L.ones, true);
+  if (phi_zero) ck(cudaMemsetAsync(L.mom, 0, sizeof(double) * size_t(L.t.n_el) * L.Hp * 4, c->stream), "memset");
+  else op_d2m(c, L, phi, L.t.order, L.mom, L.ones, true);
   ck(cudaMemsetAsync(L.gs_done, 0, sizeof(int) * 8 * size_t(L.t.n_el), c->stream), "memset");
   Timed tm(c, "coarse_gs");
   CoarseGSParams p;
@@ -1081,42 +1084,58 @@ void op_restrict(stamg_ctx* c, int l, const double* fine, double* coarse) {
 double op_dot(stamg_ctx* c, const double* x, const double* y, int64_t n, bool sharded);
 
 // lmg_vcycle (multigrid.cpp:138-170)
-void op_vcycle(stamg_ctx* c, int l, const double* f, double* phi) {
+// zero_guess: phi is to be taken as zero whatever it holds (mg_apply's z and every coarse
+// correction, multigrid.cpp:138-176 start from zero). The first pre-smoothing step is then
+// phi = L^-1 f -- its residual f - A*0 is f itself, so the apply_L, the D2M / M2D pair and
+// the base-vector read of the sweep are skipped; the results are those of the full sequence
+// (0 * x and f - 0 are exact), only the sign of a zero can differ. A third of the MG levels'
+// operator applications (STAMG_MG_ZERO_GUESS=0 runs the full sequence).
+void op_vcycle(stamg_ctx* c, int l, const double* f, double* phi, bool zero_guess = false) {
   NvtxScope nv(c, "lmg_vcycle level " + std::to_string(l));
   DevLevel& L = c->mg[l];
   const auto& spec = c->pb.spec;
+  auto zero_fill = [&]() {
+    launch_fill(phi, 0.0, L.n, c->stream);
+    c->launches += 1;
+  };
+  if (zero_guess && env_is_zero("STAMG_MG_ZERO_GUESS")) {  // A/B: fill and run the full sequence
+    zero_fill();
+    zero_guess = false;
+  }
   if (l == 0) {
+    if (zero_guess) zero_fill();
     if (spec.coarse_tol > 0) {
       if (!L.tmp) L.tmp = dalloc_zero<double>(L.n, c->stream);
       const double fnorm = std::sqrt(op_dot(c, f, f, L.n, L.sharded));
       for (int s = 0; s < 200; ++s) {
-        op_coarse_gs(c, L, f, 1, phi);
+        op_coarse_gs(c, L, f, 1, phi, zero_guess && s == 0);
         op_residual(c, L, f, phi, L.t.order, L.tmp);
         if (std::sqrt(op_dot(c, L.tmp, L.tmp, L.n, L.sharded)) <= spec.coarse_tol * fnorm) break;
       }
     } else {
-      op_coarse_gs(c, L, f, spec.coarse_sweeps, phi);
+      op_coarse_gs(c, L, f, spec.coarse_sweeps, phi, zero_guess);
     }
     return;
   }
   DevLevel& Cl = c->mg[l - 1];
   if (!L.tmp) L.tmp = dalloc_zero<double>(L.n, c->stream);
   if (!Cl.cf) Cl.cf = dalloc_zero<double>(Cl.n, c->stream), Cl.ce = dalloc_zero<double>(Cl.n, c->stream);
-  for (int s = 0; s < spec.nu_pre; ++s) op_smoother(c, L, f, c->nr, phi);
+  int s0 = 0;
+  if (zero_guess) {
+    if (spec.nu_pre > 0) op_sweep(c, L, f, phi), s0 = 1;
+    else zero_fill();
+  }
+  for (int s = s0; s < spec.nu_pre; ++s) op_smoother(c, L, f, c->nr, phi);
   op_residual(c, L, f, phi, c->nr, L.tmp);
   op_restrict(c, l, L.tmp, Cl.cf);
-  launch_fill(Cl.ce, 0.0, Cl.n, c->stream);
-  c->launches += 1;
-  op_vcycle(c, l - 1, Cl.cf, Cl.ce);
+  op_vcycle(c, l - 1, Cl.cf, Cl.ce, true);
   op_prolong(c, l, Cl.ce, phi, true);
   for (int s = 0; s < spec.nu_post; ++s) op_smoother(c, L, f, c->nr, phi);
 }
 
 void op_mg_apply(stamg_ctx* c, const double* r, double* z) {
   const int top = int(c->mg.size()) - 1;
-  launch_fill(z, 0.0, c->mg[top].n, c->stream);
-  c->launches += 1;
-  op_vcycle(c, top, r, z);
+  op_vcycle(c, top, r, z, true);
 }
 
 // mg_apply through a CUDA graph: the V-cycle is a fixed sequence of
