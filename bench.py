@@ -42,16 +42,50 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region: through NVML every 5 ms
+    when pynvml can load it (the timed region of the default run is a quarter of a second),
+    otherwise one nvidia-smi query per 0.2 s."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []       # nvidia-smi rows
+        self.samples = []    # NVML samples: (sm_mhz, reasons bitmask, power_w, mem_mhz)
         self._stop = threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
+        self._nvml = None
+        self._h = None
+        self._max = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self._max = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+            self._nvml = pynvml
+        except Exception:
+            self._nvml = None
+        self._t = threading.Thread(target=self._run_nvml if self._nvml else self._run, daemon=True)
+
+    def _run_nvml(self):
+        nv, h = self._nvml, self._h
+        reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                try:
+                    mem = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_MEM))
+                except Exception:
+                    mem = None
+                try:
+                    pw = nv.nvmlDeviceGetPowerUsage(h) * 1e-3
+                except Exception:
+                    pw = None
+                self.samples.append((sm, int(reasons(h)), pw, mem))
+            except Exception:
+                pass
+            self._stop.wait(0.005)
 
     def _run(self):
         while not self._stop.is_set():
@@ -74,15 +108,32 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
+        if self._nvml and self.samples:
+            nv = self._nvml
+            bits = {"hw_slowdown": nv.nvmlClocksThrottleReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksThrottleReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksThrottleReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksThrottleReasonSwPowerCap}
+            seen = sorted(n for n, b in bits.items() if any(s[1] & b for s in self.samples))
+            out = {"sm_mhz": statistics.median(s[0] for s in self.samples), "sm_max_mhz": self._max, "reasons": seen,
+                   "samples": len(self.samples), "source": "nvml, 5 ms period",
+                   "sm_mhz_min": min(s[0] for s in self.samples)}
+            pw = [s[2] for s in self.samples if s[2] is not None]
+            mem = [s[3] for s in self.samples if s[3] is not None]
+            if pw:
+                out["power_w"] = statistics.median(pw)
+            if mem:
+                out["mem_mhz"] = statistics.median(mem)
+            return out
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        names = self.NAMES
         reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
                           and "Not" not in r[2 + i]})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "source": "nvidia-smi, 0.2 s period"}
 
 
 def fp64_peaks_with_clocks(g, local):

@@ -38,3 +38,25 @@ def test_graphs_off_matches(stamg, monkeypatch):
     assert np.array_equal(x0.numpy(), x1.numpy())
     c0.close()
     c1.close()
+
+
+@pytest.mark.parametrize("k,n", [(1, 16), (2, 32), (3, 16), (4, 16)])
+def test_zero_guess_vcycle_is_the_full_sequence(stamg, monkeypatch, k, n):
+    """mg_apply starts every level from zero (multigrid.cpp:138-176), so the first pre-smoothing
+    step is phi = L^-1 f; STAMG_MG_ZERO_GUESS=0 computes that step's residual f - A*0 in full.
+    Both are the same arithmetic on the same values (0*x and f - 0 are exact): equal iterates,
+    equal GMRES iteration counts."""
+    spec = cf.baseline_config(k, n)
+    monkeypatch.setenv("STAMG_GRAPHS", "0")  # a captured graph would replay the mode it was captured in
+    c = stamg.Context(spec)
+    x = np.random.default_rng(5).uniform(-1, 1, c.vec().n)
+    r = c.vec(data=x)
+    fast = c.mg_apply(r).numpy()
+    xs, rep_fast = c.solve(c.rhs(), "gmres", "mg")
+    monkeypatch.setenv("STAMG_MG_ZERO_GUESS", "0")
+    full = c.mg_apply(r).numpy()
+    xf, rep_full = c.solve(c.rhs(), "gmres", "mg")
+    assert np.array_equal(fast, full)  # -0.0 == +0.0
+    assert rep_fast["iterations"] == rep_full["iterations"]
+    assert np.array_equal(xs.numpy(), xf.numpy())
+    c.close()
