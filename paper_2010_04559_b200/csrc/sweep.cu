@@ -28,18 +28,24 @@ namespace {
 #ifndef STAMG_SWEEP8_BREG
 #define STAMG_SWEEP8_BREG 1  // 8-direction kernel keeps B^-1 in registers (2 CTAs/SM); A/B: 82.5 % vs 79 %
 #endif
+#ifndef STAMG_SWEEP_UNROLL
+#define STAMG_SWEEP_UNROLL 2  // step-loop unroll: the loop-carried traces alternate registers instead of being moved
+#endif
 constexpr int kNST = STAMG_SWEEP_NST;
+constexpr int kSweepUnroll = STAMG_SWEEP_UNROLL;
 #ifndef STAMG_SWEEP_ONE_WAVE4
 #define STAMG_SWEEP_ONE_WAVE4 1  // A/B: 0 = always the 2-per-SM kernel (B^-1 in registers)
 #endif
 #ifndef STAMG_SWEEP_BULK
 // wavefront layout: 1 = a step's rows arrive as one or two TMA bulk copies (cp.async.bulk, one
-// issuing thread, mbarrier completion), 0 = per-thread cp.async. A/B at config 5 (512^2 x 8192,
-// profiles/r02_sweep_ab.txt): cp.async 23.1 ms, bulk copies 23.8 ms with every thread waiting on
-// the stage's mbarrier, 24.6 ms with one waiting thread ahead of the step barrier. The sweep is
-// bandwidth-bound while the waves are full; the bulk path saves address arithmetic but adds an
-// mbarrier round trip per step, so per-thread cp.async stays the default.
-#define STAMG_SWEEP_BULK 0
+// issuing thread, mbarrier completion), 0 = per-thread cp.async. The bulk path removes the
+// per-thread source addressing and LDGSTS issue from every step and draws less power, and the
+// sweep runs against the board's power cap: with the lean step loop it measures
+// 22.6 ms against 22.9 ms per config-5 sweep over 10 back-to-back sweeps (0.928 vs 0.916 of the
+// copy bandwidth) and 23.2 against 23.7 ms over 40 (SM clock 1710 vs 1610 MHz under
+// sw_power_cap); profiles/r02_sweep_ab.txt. With the earlier, heavier step loop it had been
+// slower (23.8 vs 23.1 ms), which is why it was off until the last session of round 2.
+#define STAMG_SWEEP_BULK 1
 #endif
 
 // DIRS directions x R rows per CTA (DIRS*R = 256 threads). thread = (dir, row):
@@ -70,7 +76,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? BPS : 1)) sweep_kernel(Sweep
   // rhs (and base) is one or two contiguous runs of up to R x DIRS x 32 B = 8 KB. Thread 0
   // issues them as cp.async.bulk copies completing on the stage's mbarrier (UBLKCP); nobody
   // computes a per-thread source address or issues per-thread LDGSTS for the vector data.
-  constexpr bool BULK = WLAY && TOPG && (STAMG_SWEEP_BULK != 0);
+  constexpr bool BULK = WLAY && TOPG && !XBLK && (STAMG_SWEEP_BULK != 0);  // column blocks: cp.async measured faster (3.23 vs 3.36 ms per rank at N = 8)
   __shared__ unsigned long long s_bar[BULK ? NST_ : 1];
   extern __shared__ __align__(128) double smem[];
   double* st_rhs = smem;
@@ -219,7 +225,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? BPS : 1)) sweep_kernel(Sweep
     }
     }
     if constexpr (TOPG) {  // row 0 of strip s >= 1 needs the trace row R-1 left in the scratch
-      if (r == 0) {
+      if (warp == 0 && r == 0) {  // (warp-uniform outer test: the other warps branch over the address math)
         const bool tk = c_kin && c.s >= 1;
         cp_async16(st_top + stg * DIRS + dir, gtop + (size_t)dir * nx + (tk ? i0 + c.i : 0), tk);
       }
@@ -254,13 +260,16 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? BPS : 1)) sweep_kernel(Sweep
     if (xin) wait_strip();
   }
   Cursor ci, cc;  // issue cursor (k = t + NST - 1 - r) and compute cursor (k = t - r)
+  // with bulk copies only warp 0 (the producer thread and the strip-scratch loads of row 0)
+  // reads the issue cursor
+  const bool ci_used = !BULK || warp == 0;
   start(ci);
   start(cc);
 #pragma unroll
   for (int t = 0; t < NST - 1; ++t) {
     issue(t, t, ci);
     cp_async_commit();
-    advance(ci);
+    if (ci_used) advance(ci);
   }
   __syncthreads();
 
@@ -270,13 +279,14 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? BPS : 1)) sweep_kernel(Sweep
   constexpr int m = decltype(mtag)::value;
   double2 tx = make_double2(0.0, 0.0), typrev = make_double2(0.0, 0.0);
   int stg = 0, stg_issue = NST - 1;  // stage of step t, stage filled during step t (= t + NST - 1 mod NST)
+#pragma unroll kSweepUnroll
   for (int t = 0; t < T; ++t) {
     if constexpr (XBLK) {
       if (xin && wait_s < nstrips && t == wait_t) wait_strip();
     }
     issue(t + NST - 1, stg_issue, ci);
     cp_async_commit();
-    advance(ci);
+    if (ci_used) advance(ci);
     cp_async_wait<NST - 1>();
     if constexpr (BULK) mbar_wait_parity(&s_bar[stg], unsigned(t / NST) & 1u);
     const bool kin = kin_of(cc);
@@ -361,7 +371,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? BPS : 1)) sweep_kernel(Sweep
       reinterpret_cast<double2*>(out)[1] = make_double2(z2, z3);
     }
     if (lane >= 32 - DIRS) xw[(t & 1) * NW * DIRS + warp * DIRS + dir] = tyout;
-    if (r == R - 1 && kin) {
+    if (warp == NW - 1 && r == R - 1 && kin) {
       if constexpr (TOPG) reinterpret_cast<double2*>(gtop)[(size_t)dir * nx + i0 + i] = tyout;
       else top[dir * nx + i] = tyout;
     }
