@@ -64,6 +64,10 @@ template <int DIRS, int R, bool MULTI, bool ACCUM, bool TOPG, bool WLAY = false,
           bool XBLK = false, int NST_ = kNST>
 __global__ void __launch_bounds__(DIRS * R, (TOPG ? BPS : 1)) sweep_kernel(SweepParams p) {
   constexpr bool BREG = BPS < 4;
+  // step-loop unroll only where the register budget has room (112 registers at 2 CTAs/SM): the
+  // 80- and 64-register variants spill with it (config 4's plain sweep 3.10 -> 3.39 ms)
+  constexpr int UNR = (TOPG && BPS == 2) ? kSweepUnroll : 1;
+  constexpr bool WG = TOPG && BPS == 2;  // likewise the warp-uniform guards (8 bytes of spill, 3 % at config 4)
   constexpr int NST = NST_;  // rhs staging depth of this instantiation
   // WLAY: vectors in the wavefront layout (a step's R rows are consecutive slots).
   // MODE 1: apply_L on the same skewed schedule (y = alpha*(B x + C x_up) + beta*f, traces of x).
@@ -225,7 +229,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? BPS : 1)) sweep_kernel(Sweep
     }
     }
     if constexpr (TOPG) {  // row 0 of strip s >= 1 needs the trace row R-1 left in the scratch
-      if (warp == 0 && r == 0) {  // (warp-uniform outer test: the other warps branch over the address math)
+      if ((!WG || warp == 0) && r == 0) {  // (WG: warp-uniform outer test, the other warps branch over the address math)
         const bool tk = c_kin && c.s >= 1;
         cp_async16(st_top + stg * DIRS + dir, gtop + (size_t)dir * nx + (tk ? i0 + c.i : 0), tk);
       }
@@ -260,16 +264,13 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? BPS : 1)) sweep_kernel(Sweep
     if (xin) wait_strip();
   }
   Cursor ci, cc;  // issue cursor (k = t + NST - 1 - r) and compute cursor (k = t - r)
-  // with bulk copies only warp 0 (the producer thread and the strip-scratch loads of row 0)
-  // reads the issue cursor
-  const bool ci_used = !BULK || warp == 0;
   start(ci);
   start(cc);
 #pragma unroll
   for (int t = 0; t < NST - 1; ++t) {
     issue(t, t, ci);
     cp_async_commit();
-    if (ci_used) advance(ci);
+    advance(ci);
   }
   __syncthreads();
 
@@ -279,14 +280,13 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? BPS : 1)) sweep_kernel(Sweep
   constexpr int m = decltype(mtag)::value;
   double2 tx = make_double2(0.0, 0.0), typrev = make_double2(0.0, 0.0);
   int stg = 0, stg_issue = NST - 1;  // stage of step t, stage filled during step t (= t + NST - 1 mod NST)
-#pragma unroll kSweepUnroll
-  for (int t = 0; t < T; ++t) {
+  auto step = [&](int t) {
     if constexpr (XBLK) {
       if (xin && wait_s < nstrips && t == wait_t) wait_strip();
     }
     issue(t + NST - 1, stg_issue, ci);
     cp_async_commit();
-    if (ci_used) advance(ci);
+    advance(ci);
     cp_async_wait<NST - 1>();
     if constexpr (BULK) mbar_wait_parity(&s_bar[stg], unsigned(t / NST) & 1u);
     const bool kin = kin_of(cc);
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? BPS : 1)) sweep_kernel(Sweep
       reinterpret_cast<double2*>(out)[1] = make_double2(z2, z3);
     }
     if (lane >= 32 - DIRS) xw[(t & 1) * NW * DIRS + warp * DIRS + dir] = tyout;
-    if (warp == NW - 1 && r == R - 1 && kin) {
+    if ((!WG || warp == NW - 1) && r == R - 1 && kin) {
       if constexpr (TOPG) reinterpret_cast<double2*>(gtop)[(size_t)dir * nx + i0 + i] = tyout;
       else top[dir * nx + i] = tyout;
     }
@@ -389,6 +389,12 @@ __global__ void __launch_bounds__(DIRS * R, (TOPG ? BPS : 1)) sweep_kernel(Sweep
         ++pub_s, pub_t += nxl;
       }
     }
+  };
+  if constexpr (UNR > 1) {
+#pragma unroll UNR
+    for (int t = 0; t < T; ++t) step(t);
+  } else {  // no pragma: the register-capped variants keep the compiler's own schedule
+    for (int t = 0; t < T; ++t) step(t);
   }
   };
   switch ((xneg ? 1 : 0) | (yneg ? 2 : 0)) {
